@@ -1,0 +1,343 @@
+"""TEST INFRASTRUCTURE ONLY — CPU checkers for the B200 hot path.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline leg
+and ``--impl reference`` arm) may import this package, and only as the checker
+or the timed CPU baseline — never as the product path.
+
+Two interchangeable backends with one Python surface:
+
+* ``port()``  — ``oracle/liboracle_port.so``, the plain-C restatement in
+  ``oracle/skr_oracle.c`` (every function cites the reference file:line).
+* ``ref()``   — ``oracle/_ref/libskridge_ref.so``, the UNMODIFIED reference
+  library compiled from /root/reference/proj/src plus the extern "C" shim
+  ``oracle/ref_capi.cpp``.  Present wherever it was built (it travels to the GPU
+  box with the repo snapshot); ``ref_available()`` says whether it loaded.
+
+Array conventions: X is (n, d) C-contiguous float64 (== the reference's d x n
+column-major DenseMatrix); U is returned as (d, k) with Fortran order, i.e.
+column j is basis vector j exactly as DenseMatrix stores it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_PATH = os.path.join(_HERE, "liboracle_port.so")
+REF_PATH = os.path.join(_HERE, "_ref", "libskridge_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_up = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+i64, u64, f64, cint = C.c_int64, C.c_uint64, C.c_double, C.c_int
+vp = C.c_void_p
+P = C.POINTER
+
+ERRORS = {1: "DimensionError", 2: "ParameterError", 3: "InputError", 4: "ScaleGuardError",
+          5: "DivergenceError", 8: "EmptyBasisError", 10: "InternalError"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERRORS.get(code, str(code))
+
+
+@dataclass
+class Sketch:
+    U: np.ndarray          # (d, k) column-major basis
+    sigma: np.ndarray      # (k,)
+    V: np.ndarray | None   # (n, k) or None
+    k: int
+    q: int
+    rank_reduced: bool
+
+
+@dataclass
+class SvrgOut:
+    iterate: np.ndarray
+    trace: np.ndarray
+    diverged: bool = False
+    error: str = ""
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class _Backend:
+    """Common wrapper; `prefix` is "skro_" (port) or "ref_" (reference shim)."""
+
+    def __init__(self, path: str, prefix: str):
+        self.path = path
+        self.lib = C.CDLL(path)
+        self.prefix = prefix
+        self.name = "port" if prefix == "skro_" else "reference"
+        self._err = self._fn("last_error", C.c_char_p, [])
+
+    def _fn(self, name, res, args):
+        f = getattr(self.lib, self.prefix + name)
+        f.restype = res
+        f.argtypes = args
+        return f
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OracleError(rc, self._err().decode())
+
+    # -- random.cpp --------------------------------------------------------
+    def uniforms(self, seed: int, count: int) -> np.ndarray:
+        out = np.empty(count)
+        self._check(self._fn("uniforms", cint, [u64, i64, _dp])(seed, count, out))
+        return out
+
+    def gaussian_matrix(self, rows: int, cols: int, seed: int) -> np.ndarray:
+        """(rows, cols) array whose Fortran-order bytes equal the reference DenseMatrix."""
+        out = np.empty(rows * cols)
+        self._check(self._fn("gaussian_matrix", cint, [i64, i64, u64, _dp])(rows, cols, seed, out))
+        return out.reshape(cols, rows).T
+
+    def sym_eigs(self, a: np.ndarray):
+        n = a.shape[0]
+        vals = np.empty(n)
+        vecs = np.empty(n * n)
+        self._check(self._fn("sym_eigs", cint, [_dp, i64, _dp, _dp])(
+            _c64(np.asfortranarray(a).ravel(order="F")), n, vals, vecs))
+        return vals, vecs.reshape(n, n).T
+
+    # -- sketch.cpp --------------------------------------------------------
+    def block_lanczos(self, x, k, q=0, seed=0, scale=None, eps_prime=0.5, want_right=True):
+        x = _c64(x)
+        n, d = x.shape
+        if scale is None:
+            scale = 1.0 / math.sqrt(n)
+        U = np.zeros(d * k)
+        sig = np.zeros(k)
+        V = np.zeros(n * k) if want_right else None
+        ku, qu = i64(), i64()
+        rr = cint()
+        if self.prefix == "skro_":
+            f = self._fn("block_lanczos", cint, [_dp, i64, i64, f64, i64, i64, f64, u64, _dp, _dp,
+                                                  vp, P(i64), P(i64), P(cint), P(i64)])
+            rc = f(x, n, d, scale, k, q, eps_prime, seed, U, sig,
+                   V.ctypes.data if V is not None else None, C.byref(ku), C.byref(qu),
+                   C.byref(rr), None)
+        else:
+            f = self._fn("block_lanczos", cint, [_dp, i64, i64, f64, i64, i64, f64, u64, _dp, _dp,
+                                                  vp, P(i64), P(i64), P(cint)])
+            rc = f(x, n, d, scale, k, q, eps_prime, seed, U, sig,
+                   V.ctypes.data if V is not None else None, C.byref(ku), C.byref(qu), C.byref(rr))
+        self._check(rc)
+        kk = ku.value
+        Um = U[: d * kk].reshape(kk, d).T
+        Vm = V[: n * kk].reshape(kk, n).T if V is not None else None
+        return Sketch(Um, sig[:kk].copy(), Vm, kk, qu.value, bool(rr.value))
+
+    # -- ridge.cpp / bench.cpp / precond.cpp -----------------------------------
+    def objective(self, x, y, lam, w) -> float:
+        x = _c64(x)
+        n, d = x.shape
+        out = f64()
+        self._check(self._fn("objective", cint, [_dp, i64, i64, _dp, f64, _dp, P(f64)])(
+            x, n, d, _c64(y), lam, _c64(w), C.byref(out)))
+        return out.value
+
+    def reference_minimum(self, x, y, lam):
+        x = _c64(x)
+        n, d = x.shape
+        w = np.empty(d)
+        mn = f64()
+        self._check(self._fn("reference_minimum", cint, [_dp, i64, i64, _dp, f64, _dp, P(f64)])(
+            x, n, d, _c64(y), lam, w, C.byref(mn)))
+        return w, mn.value
+
+    def conditioned_cond(self, x, lam, U, sigma, unguarded=False) -> float:
+        x = _c64(x)
+        n, d = x.shape
+        k = 0 if U is None else U.shape[1]
+        Uf = _c64(np.asarray(U).ravel(order="F")) if k else np.zeros(1)
+        out = f64()
+        if self.prefix == "skro_":
+            D, c = self.build_sketched(sigma, lam) if k else (np.zeros(1), 1.0)
+            self._check(self._fn("conditioned_cond", cint, [_dp, i64, i64, f64, _dp, _dp, i64, f64,
+                                                             cint, P(f64)])(
+                x, n, d, lam, Uf, _c64(D), k, c, int(unguarded), C.byref(out)))
+        else:
+            s = _c64(sigma) if k else np.zeros(1)
+            self._check(self._fn("conditioned_cond", cint, [_dp, i64, i64, f64, _dp, _dp, i64, cint,
+                                                             P(f64)])(
+                x, n, d, lam, Uf, s, k, int(unguarded), C.byref(out)))
+        return out.value
+
+    def build_sketched(self, sigma, lam):
+        sigma = _c64(sigma)
+        return build_sketched(sigma, lam)
+
+    def apply_inv_sqrt(self, U, sigma, lam, v):
+        d = len(v)
+        k = 0 if U is None else U.shape[1]
+        Uf = _c64(np.asarray(U).ravel(order="F")) if k else np.zeros(1)
+        out = np.empty(d)
+        if self.prefix == "skro_":
+            D, c = build_sketched(sigma, lam) if k else (np.zeros(1), 1.0)
+            self._check(self._fn("apply_inv_sqrt", cint, [i64, _dp, _dp, i64, f64, _dp, _dp])(
+                d, Uf, _c64(D), k, c, _c64(v), out))
+        else:
+            s = _c64(sigma) if k else np.zeros(1)
+            self._check(self._fn("apply_inv_sqrt", cint, [i64, _dp, _dp, i64, f64, _dp, _dp])(
+                d, Uf, s, k, lam, _c64(v), out))
+        return out
+
+    def problem(self, x, y, lam, U=None, sigma=None, mode=0) -> "Problem":
+        return Problem(self, x, y, lam, U, sigma, mode)
+
+    def index_stream(self, betas, seed, count) -> np.ndarray:
+        b = _c64(betas)
+        out = np.empty(count, dtype=np.int64)
+        self._check(self._fn("index_stream", cint, [_dp, i64, u64, i64, _ip])(
+            b, len(b), seed, count, out))
+        return out
+
+    def cumulative_weights(self, betas) -> np.ndarray:
+        b = _c64(betas)
+        out = np.empty(len(b))
+        self._check(self._fn("cumulative_weights", cint, [_dp, i64, _dp])(b, len(b), out))
+        return out
+
+
+def build_sketched(sigma, lam):
+    """precond.cpp:120-136 restated on the host (k scalars)."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    D = 1.0 / np.sqrt(sigma * sigma + lam)
+    return D, float(D[-1])
+
+
+class Problem:
+    """PreconditionedRidge (Dense mode for the port; any mode for the reference)."""
+
+    def __init__(self, be: _Backend, x, y, lam, U, sigma, mode):
+        self.be = be
+        x = _c64(x)
+        self.n, self.d = x.shape
+        self.k = 0 if U is None else U.shape[1]
+        self.lam = lam
+        Uf = _c64(np.asarray(U).ravel(order="F")) if self.k else np.zeros(1)
+        h = vp()
+        if be.prefix == "skro_":
+            D, c = build_sketched(sigma, lam) if self.k else (np.zeros(1), 1.0)
+            be._check(be._fn("problem_create", cint, [_dp, i64, i64, _dp, f64, _dp, _dp, i64, f64,
+                                                      P(vp)])(
+                x, self.n, self.d, _c64(y), lam, Uf, _c64(D), self.k, c, C.byref(h)))
+            self._destroy = be._fn("problem_destroy", None, [vp])
+        else:
+            s = _c64(sigma) if self.k else np.zeros(1)
+            be._check(be._fn("problem_create", cint, [_dp, i64, i64, _dp, f64, _dp, _dp, i64, cint,
+                                                      P(vp)])(
+                x, self.n, self.d, _c64(y), lam, Uf, s, self.k, mode, C.byref(h)))
+            self._destroy = be._fn("problem_destroy", cint, [vp])
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._destroy(self.h)
+            self.h = None
+
+    @property
+    def N(self):
+        return self.n + self.d
+
+    def betas(self):
+        out = np.empty(self.N)
+        self.be._check(self.be._fn("problem_betas", cint, [vp, _dp])(self.h, out))
+        return out
+
+    def objective(self, w) -> float:
+        out = f64()
+        self.be._check(self.be._fn("problem_objective", cint, [vp, _dp, P(f64)])(
+            self.h, _c64(w), C.byref(out)))
+        return out.value
+
+    def full_gradient(self, w):
+        out = np.empty(self.d)
+        self.be._check(self.be._fn("problem_full_gradient", cint, [vp, _dp, _dp])(
+            self.h, _c64(w), out))
+        return out
+
+    def component_gradient(self, i, w):
+        out = np.empty(self.d)
+        self.be._check(self.be._fn("problem_component_gradient", cint, [vp, i64, _dp, _dp])(
+            self.h, i, _c64(w), out))
+        return out
+
+    def scalars(self):
+        a, b = f64(), f64()
+        if self.be.prefix == "skro_":
+            m = f64()
+            self.be._check(self.be._fn("problem_scalars", cint, [vp, P(f64), P(f64), P(f64)])(
+                self.h, C.byref(a), C.byref(b), C.byref(m)))
+            return a.value, b.value, m.value
+        self.be._check(self.be._fn("problem_scalars", cint, [vp, P(f64), P(f64)])(
+            self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value, None
+
+    def transformed(self):
+        out = np.empty(self.n * self.d)
+        self.be._check(self.be._fn("problem_transformed", cint, [vp, _dp])(self.h, out))
+        return out.reshape(self.n, self.d)
+
+    def svrg(self, epochs, m, eta, seed, w0=None, reference=float("nan")) -> SvrgOut:
+        w0 = np.zeros(self.d) if w0 is None else _c64(w0)
+        w = np.empty(self.d)
+        tr = np.full(epochs, np.nan)
+        done = i64()
+        if self.be.prefix == "skro_":
+            f = self.be._fn("svrg_solve", cint, [vp, i64, i64, f64, u64, _dp, f64, _dp, _dp, P(i64)])
+            rc = f(self.h, epochs, m, eta, seed, w0, reference, w, tr, C.byref(done))
+        else:
+            f = self.be._fn("svrg_solve", cint, [vp, i64, i64, f64, u64, _dp, f64, _dp, _dp, vp,
+                                                 P(i64)])
+            rc = f(self.h, epochs, m, eta, seed, w0, reference, w, tr, None, C.byref(done))
+        if rc == 5:
+            return SvrgOut(w, tr[: done.value], True, self.be._err().decode())
+        self.be._check(rc)
+        return SvrgOut(w, tr[: done.value])
+
+
+_port = None
+_ref = None
+
+
+def port() -> _Backend:
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_PATH):
+            raise RuntimeError(f"oracle port not built: {PORT_PATH} (run `make -C oracle port`)")
+        _port = _Backend(PORT_PATH, "skro_")
+    return _port
+
+
+def ref_available() -> bool:
+    try:
+        ref()
+        return True
+    except Exception:
+        return False
+
+
+def ref() -> _Backend:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_PATH):
+            raise RuntimeError(f"reference library not built: {REF_PATH}")
+        _ref = _Backend(REF_PATH, "ref_")
+    return _ref
+
+
+def best() -> _Backend:
+    """The real reference when it is available, else the restatement."""
+    return ref() if ref_available() else port()

@@ -1,0 +1,321 @@
+// TEST INFRASTRUCTURE ONLY — never linked into or called by the product path.
+//
+// extern "C" shim over the UNMODIFIED reference library (skridge, built from
+// /root/reference/proj/src/*.cpp by oracle/Makefile into oracle/_ref/).  It lets
+// the Python tests, tests/golden/make_golden.py and bench.py's reference arm /
+// cpu_baseline call the reference's own public C++ API through ctypes.
+//
+// Layout convention at this boundary: the data matrix is passed as n x d
+// ROW-major doubles, which is byte-identical to the reference's d x n
+// column-major DenseMatrix (dense_matrix.hpp:12-15).  Dense
+// results (U, V) are returned column-major exactly as DenseMatrix stores them.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+
+#include "skridge/bench.hpp"
+#include "skridge/data_matrix.hpp"
+#include "skridge/errors.hpp"
+#include "skridge/factorize.hpp"
+#include "skridge/kernels.hpp"
+#include "skridge/precond.hpp"
+#include "skridge/random.hpp"
+#include "skridge/ridge.hpp"
+#include "skridge/sketch.hpp"
+#include "skridge/svrg.hpp"
+
+using namespace skridge;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Error codes mirror include/skr.h so tests can compare error behaviour.
+int classify(const std::exception& e) {
+  if (dynamic_cast<const DimensionError*>(&e)) return 1;
+  if (dynamic_cast<const ParameterError*>(&e)) return 2;
+  if (dynamic_cast<const InputError*>(&e)) return 3;
+  if (dynamic_cast<const ScaleGuardError*>(&e)) return 4;
+  if (dynamic_cast<const DivergenceError*>(&e)) return 5;
+  if (dynamic_cast<const EmptyBasisError*>(&e)) return 8;
+  return 10;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
+DenseMatrix colmajor(const double* p, std::size_t rows, std::size_t cols) {
+  return DenseMatrix(rows, cols, Vector(p, p + rows * cols));
+}
+
+struct RefProblem {
+  RidgeProblem problem;
+  Preconditioner precond;
+  std::shared_ptr<PreconditionedRidge> pre;
+};
+
+Preconditioner make_precond(std::size_t d, const double* U, const double* sigma, std::size_t k,
+                            double lambda) {
+  if (k == 0) return Preconditioner::identity(d, lambda);
+  SketchedSvd sv;
+  sv.left = colmajor(U, d, k);
+  sv.singular_values = Vector(sigma, sigma + k);
+  sv.right = DenseMatrix(1, k);
+  sv.k = k;
+  return build_sketched(sv, lambda);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_set_threads_serial(int serial) {
+  kernels::set_execution(serial ? kernels::Execution::Serial : kernels::Execution::Auto);
+  return 0;
+}
+
+// NormalSampler(seed).uniform() x count  (random.cpp:10-12)
+int ref_uniforms(std::uint64_t seed, std::int64_t count, double* out) {
+  return guard([&] {
+    NormalSampler s(seed);
+    for (std::int64_t i = 0; i < count; ++i) out[i] = s.uniform();
+  });
+}
+
+// gaussian_matrix(rows, cols, seed), column-major (random.cpp:28-41)
+int ref_gaussian_matrix(std::int64_t rows, std::int64_t cols, std::uint64_t seed, double* out) {
+  return guard([&] {
+    DenseMatrix m = gaussian_matrix(rows, cols, seed);
+    std::memcpy(out, m.data(), sizeof(double) * m.size());
+  });
+}
+
+// sym_eigs (factorize.cpp:87-165); a is n x n column-major.
+int ref_sym_eigs(const double* a, std::int64_t n, double* values, double* vectors) {
+  return guard([&] {
+    EigResult r = sym_eigs(colmajor(a, n, n));
+    std::memcpy(values, r.values.data(), sizeof(double) * n);
+    std::memcpy(vectors, r.vectors.data(), sizeof(double) * n * n);
+  });
+}
+
+// krylov_block width only (sketch.cpp:18-39), used to probe rank drop.
+int ref_krylov_width(const double* x, std::int64_t n, std::int64_t d, double scale,
+                     std::int64_t k, std::int64_t q, std::uint64_t seed, std::int64_t* width) {
+  return guard([&] {
+    DataMatrix a(colmajor(x, d, n), scale);
+    DenseMatrix pi = gaussian_matrix(n, k, seed);
+    *width = static_cast<std::int64_t>(krylov_block(a, pi, q).cols());
+  });
+}
+
+// block_lanczos (sketch.cpp:41-90).  q <= 0 -> lanczos_iterations(n, eps').
+int ref_block_lanczos(const double* x, std::int64_t n, std::int64_t d, double scale,
+                      std::int64_t k, std::int64_t q, double eps_prime, std::uint64_t seed,
+                      double* U, double* sigma, double* V, std::int64_t* k_used,
+                      std::int64_t* q_used, int* rank_reduced) {
+  return guard([&] {
+    DataMatrix a(colmajor(x, d, n), scale);
+    LanczosConfig cfg;
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.eps_prime = eps_prime;
+    cfg.seed = seed;
+    if (q > 0) cfg.q_override = static_cast<std::size_t>(q);
+    SketchedSvd sv = block_lanczos(a, cfg);
+    std::memcpy(U, sv.left.data(), sizeof(double) * sv.left.size());
+    std::memcpy(sigma, sv.singular_values.data(), sizeof(double) * sv.k);
+    if (V) std::memcpy(V, sv.right.data(), sizeof(double) * sv.right.size());
+    *k_used = static_cast<std::int64_t>(sv.k);
+    *q_used = static_cast<std::int64_t>(sv.q);
+    *rank_reduced = sv.rank_reduced ? 1 : 0;
+  });
+}
+
+// objective(p, w) on the ORIGINAL problem (ridge.cpp:33-43).
+int ref_objective(const double* x, std::int64_t n, std::int64_t d, const double* y,
+                  double lambda, const double* w, double* out) {
+  return guard([&] {
+    RidgeProblem p(DataMatrix(colmajor(x, d, n)), Vector(y, y + n), lambda);
+    *out = objective(p, Vector(w, w + d));
+  });
+}
+
+// reference_minimum (bench.cpp:84-94).
+int ref_reference_minimum(const double* x, std::int64_t n, std::int64_t d, const double* y,
+                          double lambda, double* w_out, double* min_out) {
+  return guard([&] {
+    RidgeProblem p(DataMatrix(colmajor(x, d, n)), Vector(y, y + n), lambda);
+    ReferenceSolution r = reference_minimum(p);
+    std::memcpy(w_out, r.minimizer.data(), sizeof(double) * d);
+    *min_out = r.minimum;
+  });
+}
+
+// conditioned_condition_number on scaled_design(p) (precond.cpp:196-206);
+// unguarded=1 composes conditioned_matrix + sym_eigs directly (d > 2000).
+int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double lambda,
+                         const double* U, const double* sigma, std::int64_t k, int unguarded,
+                         double* out) {
+  return guard([&] {
+    DataMatrix a(colmajor(x, d, n), 1.0 / std::sqrt(static_cast<double>(n)));
+    Preconditioner pc = make_precond(d, U, sigma, k, lambda);
+    if (!unguarded) {
+      *out = conditioned_condition_number(a, lambda, pc);
+    } else {
+      DenseMatrix m = conditioned_matrix(a, lambda, pc);
+      EigResult eig = sym_eigs(m);
+      double tr = 0.0;
+      for (std::size_t i = 0; i < m.rows(); ++i) tr += m(i, i);
+      *out = tr / eig.values.back();
+    }
+  });
+}
+
+// Preconditioner::apply_inv_sqrt (precond.cpp:67-80).
+int ref_apply_inv_sqrt(std::int64_t d, const double* U, const double* sigma, std::int64_t k,
+                       double lambda, const double* v, double* out) {
+  return guard([&] {
+    Preconditioner pc = make_precond(d, U, sigma, k, lambda);
+    Vector r = pc.apply_inv_sqrt(Vector(v, v + d));
+    std::memcpy(out, r.data(), sizeof(double) * d);
+  });
+}
+
+// preconditioned_components(p, build_sketched(sv, lambda), mode) (ridge.cpp:93-150).
+// k == 0 -> Preconditioner::identity.  mode: 0 Dense, 1 Lazy, 2 Auto.
+int ref_problem_create(const double* x, std::int64_t n, std::int64_t d, const double* y,
+                       double lambda, const double* U, const double* sigma, std::int64_t k,
+                       int mode, void** out) {
+  return guard([&] {
+    RidgeProblem p(DataMatrix(colmajor(x, d, n)), Vector(y, y + n), lambda);
+    Preconditioner pc = make_precond(d, U, sigma, k, lambda);
+    ApplyMode m = mode == 0 ? ApplyMode::Dense : mode == 1 ? ApplyMode::Lazy : ApplyMode::Auto;
+    auto pre = preconditioned_components(p, pc, m);
+    *out = new RefProblem{std::move(p), std::move(pc), std::move(pre)};
+  });
+}
+
+int ref_problem_destroy(void* h) {
+  delete static_cast<RefProblem*>(h);
+  return 0;
+}
+
+int ref_problem_mode(void* h) {
+  return static_cast<RefProblem*>(h)->pre->mode() == ApplyMode::Dense ? 0 : 1;
+}
+
+int ref_problem_betas(void* h, double* out) {
+  return guard([&] {
+    const Vector& b = static_cast<RefProblem*>(h)->pre->betas();
+    std::memcpy(out, b.data(), sizeof(double) * b.size());
+  });
+}
+
+int ref_problem_scalars(void* h, double* alpha, double* beta_hat) {
+  return guard([&] {
+    auto& pre = *static_cast<RefProblem*>(h)->pre;
+    *alpha = pre.strong_convexity();
+    *beta_hat = mean_beta(pre);
+  });
+}
+
+int ref_problem_objective(void* h, const double* w, double* out) {
+  return guard([&] {
+    auto& pre = *static_cast<RefProblem*>(h)->pre;
+    *out = pre.objective(Vector(w, w + pre.dimension()));
+  });
+}
+
+int ref_problem_full_gradient(void* h, const double* w, double* out) {
+  return guard([&] {
+    auto& pre = *static_cast<RefProblem*>(h)->pre;
+    Vector g;
+    pre.full_gradient(Vector(w, w + pre.dimension()), g);
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+  });
+}
+
+int ref_problem_component_gradient(void* h, std::int64_t i, const double* w, double* out) {
+  return guard([&] {
+    auto& pre = *static_cast<RefProblem*>(h)->pre;
+    Vector g;
+    pre.component_gradient(static_cast<std::size_t>(i), Vector(w, w + pre.dimension()), g);
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+  });
+}
+
+// svrg_solve (svrg.cpp:152-211).  reference = NaN -> no suboptimality.
+// trace_obj/trace_ms sized `epochs`; *done = number of records (partial on divergence).
+int ref_svrg_solve(void* h, std::int64_t epochs, std::int64_t m, double eta, std::uint64_t seed,
+                   const double* w0, double reference, double* w_out, double* trace_obj,
+                   double* trace_ms, std::int64_t* done) {
+  auto& pre = *static_cast<RefProblem*>(h)->pre;
+  try {
+    SvrgConfig cfg;
+    cfg.epochs = static_cast<std::size_t>(epochs);
+    cfg.epoch_length = static_cast<std::size_t>(m);
+    cfg.step_size = eta;
+    cfg.seed = seed;
+    std::optional<double> ref;
+    if (!std::isnan(reference)) ref = reference;
+    SvrgResult r = svrg_solve(pre, cfg, Vector(w0, w0 + pre.dimension()), ref);
+    std::memcpy(w_out, r.iterate.data(), sizeof(double) * r.iterate.size());
+    for (std::size_t s = 0; s < r.trace.size(); ++s) {
+      trace_obj[s] = r.trace[s].objective;
+      if (trace_ms) trace_ms[s] = r.trace[s].elapsed_ms;
+    }
+    *done = static_cast<std::int64_t>(r.trace.size());
+    return 0;
+  } catch (const DivergenceError& e) {
+    for (std::size_t s = 0; s < e.trace().size(); ++s) {
+      trace_obj[s] = e.trace()[s].objective;
+      if (trace_ms) trace_ms[s] = e.trace()[s].elapsed_ms;
+    }
+    *done = static_cast<std::int64_t>(e.trace().size());
+    g_err = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
+// Index stream svrg_solve draws: lookup_index(make_cumulative_weights(beta),
+// NormalSampler(seed).uniform()) for `count` steps (svrg.cpp:90-126,165,174,192).
+int ref_index_stream(const double* betas, std::int64_t N, std::uint64_t seed, std::int64_t count,
+                     std::int64_t* out) {
+  return guard([&] {
+    Vector cum = make_cumulative_weights(Vector(betas, betas + N));
+    NormalSampler rng(seed);
+    (void)sample_index(cum, 0.5);  // validates the table once, as svrg_solve does
+    for (std::int64_t t = 0; t < count; ++t) {
+      // lookup_index (svrg.cpp:122-126) is file-local; same std::lower_bound + clamp.
+      auto it = std::lower_bound(cum.begin(), cum.end(), rng.uniform());
+      if (it == cum.end()) --it;
+      out[t] = static_cast<std::int64_t>(it - cum.begin());
+    }
+  });
+}
+
+int ref_cumulative_weights(const double* betas, std::int64_t N, double* out) {
+  return guard([&] {
+    Vector cum = make_cumulative_weights(Vector(betas, betas + N));
+    std::memcpy(out, cum.data(), sizeof(double) * N);
+  });
+}
+
+}  // extern "C"
