@@ -1,0 +1,88 @@
+"""The five BASELINE.json configurations and their synthetic data.
+
+X = G diag(sigma) V^T with G iid N(0,1) (n x d), V Haar (QR of an iid N(0,1)
+d x d matrix, V = Q diag(sign diag R)), optional |Student-t(3)| row scaling,
+w* ~ N(0, I/d), y = X w* + tau N(0,1).  fp32 configs round X and y to fp32 and
+the oracle consumes exactly those values promoted to fp64.
+
+Two generators implement this spec:
+  * ``host_instance`` (numpy, Philox bit generator; draw order G, V-Gaussian,
+    t-scales, w*, noise) — used for parity instances small enough for the CPU
+    oracle and for the reference arm of bench.py;
+  * ``skridge.DataMatrix.generate`` (device, Philox4x32-10 streams 1..5) — used
+    at benchmark scale.  The two are statistically identical, not bitwise; any
+    parity check hands the SAME arrays to both sides.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    dtype: str          # "f64" | "f32"
+    n: int
+    d: int
+    seed: int
+    spectrum: int       # 0: 1/j, 1: r^j, 2: j^-p, 3: 1/j (j<=50), 0.02/j beyond
+    spectrum_param: float
+    t_scale: bool
+    tau: float
+    lam: float
+    k: int
+    q: int
+    epochs: int
+
+    def sigma(self, d: int | None = None) -> np.ndarray:
+        j = np.arange(1, (d or self.d) + 1, dtype=np.float64)
+        if self.spectrum == 0:
+            return 1.0 / j
+        if self.spectrum == 1:
+            return self.spectrum_param ** j
+        if self.spectrum == 2:
+            return j ** (-self.spectrum_param)
+        return np.where(j <= 50, 1.0 / j, 0.02 / j)
+
+    def scaled(self, n: int) -> "Config":
+        """Same config at n rows (row-subsampled parity instances)."""
+        return Config(**{**self.__dict__, "n": n})
+
+
+CONFIGS = {
+    "c1": Config("c1", "f64", 8192, 256, 0, 0, 0.0, False, 0.1, 1e-3, 16, 3, 20),
+    "c2": Config("c2", "f64", 65536, 1024, 1, 1, 0.97, False, 0.05, 1e-5, 64, 4, 30),
+    "c3": Config("c3", "f32", 1 << 20, 2048, 2, 2, 1.5, False, 0.1, 1e-6, 128, 3, 20),
+    "c4": Config("c4", "f32", 1 << 22, 4096, 3, 3, 0.0, True, 0.1, 1e-6, 256, 3, 60),
+    "c5": Config("c5", "f32", 1 << 24, 1024, 4, 1, 0.99, False, 0.2, 1e-6, 64, 2, 20),
+}
+
+
+def host_instance(cfg: Config):
+    """(X, y) as numpy arrays: float64, or float32 for fp32 configs."""
+    rng = np.random.Generator(np.random.Philox(cfg.seed))
+    n, d = cfg.n, cfg.d
+    G = rng.standard_normal((n, d))
+    A = rng.standard_normal((d, d))
+    Q, R = np.linalg.qr(A)
+    V = Q * np.sign(np.diag(R))
+    X = (G * cfg.sigma()) @ V.T
+    if cfg.t_scale:
+        t = np.abs(rng.standard_t(3, size=n))
+        X *= t[:, None]
+    wstar = rng.standard_normal(d) / math.sqrt(d)
+    noise = rng.standard_normal(n)
+    if cfg.dtype == "f32":
+        X = X.astype(np.float32)
+        y = (X.astype(np.float64) @ wstar + cfg.tau * noise).astype(np.float32)
+        return X, y
+    y = X @ wstar + cfg.tau * noise
+    return np.ascontiguousarray(X), y
+
+
+def step_size(max_row_sq: float) -> float:
+    """BASELINE c1 rule, applied to every config: eta = 1 / (4 max_i ||x~_i||^2)."""
+    return 1.0 / (4.0 * max_row_sq)

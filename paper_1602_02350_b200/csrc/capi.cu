@@ -1,0 +1,1523 @@
+// C-ABI implementation (include/skr.h): the host runtime that orders the
+// hot-path kernels on the context stream, owns device memory, and runs the
+// row-sharded collectives.  All reference citations are relative to proj/.
+#include <cmath>
+#include <chrono>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "fullgrad.cuh"
+#include "gemm.cuh"
+#include "lanczos.cuh"
+#include "rng.cuh"
+#include "svrg.cuh"
+
+using namespace skr;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SKR_OK;
+  } catch (const skr::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return SKR_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SKR_EINTERNAL;
+  }
+}
+
+#define DISPATCH_DTYPE(dtype, T, ...)        \
+  do {                                       \
+    if ((dtype) == SKR_F32) {                \
+      using T = float;                       \
+      __VA_ARGS__;                           \
+    } else {                                 \
+      using T = double;                      \
+      __VA_ARGS__;                           \
+    }                                        \
+  } while (0)
+
+void check_dtype(int dtype) {
+  if (dtype != SKR_F32 && dtype != SKR_F64) raise(SKR_EPARAM, "dtype must be SKR_F64 or SKR_F32");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Handles
+struct skr_ctx {
+  Ctx c;
+};
+
+struct Storage {
+  int dtype = SKR_F64;
+  int64_t n = 0, d = 0, ld = 0;
+  void* ptr = nullptr;  // device rows, n x ld
+  bool owns = true;
+  cudaStream_t stream = nullptr;
+  DBuf<double> labels;  // synthetic generator output (local rows)
+  ~Storage() {
+    if (owns && ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+struct skr_data {
+  skr_ctx* ctx = nullptr;
+  std::shared_ptr<Storage> st;
+  double scale = 1.0;
+  int64_t n_global = 0, row0 = 0;
+};
+
+struct skr_problem {
+  skr_ctx* ctx = nullptr;
+  int dtype = SKR_F64;
+  int64_t n = 0, n_global = 0, row0 = 0, d = 0, ld = 0, k = 0;
+  double lambda = 0, c = 1, data_coef = 0, reg_coef = 0;
+  double alpha = 0, beta_hat = 0, max_row_sq = 0;
+  std::shared_ptr<Storage> xt;  // local X~ rows (aliases X for the identity preconditioner)
+  DBuf<unsigned char> xt_all_buf;  // all rows (distributed contexts only)
+  const void* xt_all = nullptr;
+  DBuf<double> B, y, y_all_buf, Ut, D, betas, cum, inv_nq, total;
+  const double* y_all = nullptr;
+  bool tables = false;
+  // full-gradient workspace
+  int fg_grid = 0;
+  DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
+  DBuf<MtState> mt;
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+namespace {
+
+Ctx& C_(skr_ctx* x) {
+  if (!x) raise(SKR_EPARAM, "null context");
+  return x->c;
+}
+
+void upload_padded(Ctx& c, double* dst, const double* src, int64_t d, int64_t ld) {
+  SKR_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * ld, c.stream));
+  SKR_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
+}
+
+// host U (d x k col-major) -> device Ut (k x ld rows, zero padded)
+void upload_rows(Ctx& c, double* dst, const double* src, int64_t rows, int64_t d, int64_t ld) {
+  SKR_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * rows * ld, c.stream));
+  if (rows)
+    SKR_CUDA(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, d * sizeof(double), d * sizeof(double),
+                               rows, cudaMemcpyHostToDevice, c.stream));
+}
+
+void download_rows(Ctx& c, double* dst, const double* src, int64_t rows, int64_t d, int64_t ld) {
+  if (rows)
+    SKR_CUDA(cudaMemcpy2DAsync(dst, d * sizeof(double), src, ld * sizeof(double), d * sizeof(double),
+                               rows, cudaMemcpyDeviceToHost, c.stream));
+}
+
+// Shard layout across ranks: gather every rank's local row count.
+void shard_layout(Ctx& c, int64_t n_local, int64_t* n_global, int64_t* row0,
+                  std::vector<int64_t>* counts = nullptr) {
+  std::vector<int64_t> all(c.world, n_local);
+  if (c.world > 1) {
+    DBuf<int64_t> send(1, c.stream), recv(c.world, c.stream);
+    SKR_CUDA(cudaMemcpyAsync(send.get(), &n_local, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+    c.allgather_bytes(send.get(), recv.get(), sizeof(int64_t));
+    SKR_CUDA(cudaMemcpyAsync(all.data(), recv.get(), sizeof(int64_t) * c.world, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  }
+  int64_t tot = 0, r0 = 0;
+  for (int r = 0; r < c.world; ++r) {
+    if (r == c.rank) r0 = tot;
+    tot += all[r];
+  }
+  *n_global = tot;
+  *row0 = r0;
+  if (counts) *counts = all;
+}
+
+std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d) {
+  auto st = std::make_shared<Storage>();
+  st->dtype = dtype;
+  st->n = n;
+  st->d = d;
+  st->ld = padded_ld(d);
+  st->stream = c.stream;
+  const size_t bytes = (size_t)std::max<int64_t>(n, 1) * st->ld * dtype_size(dtype);
+  SKR_CUDA(cudaMallocAsync(&st->ptr, bytes, c.stream));
+  SKR_CUDA(cudaMemsetAsync(st->ptr, 0, bytes, c.stream));
+  return st;
+}
+
+// ---- K9 dispatch -----------------------------------------------------------
+template <class T, int VEC, int TR>
+void launch_fullgrad_t(Ctx& c, int nt, int grid, const T* X, int64_t ld, int64_t n, const double* y,
+                       const double* w, double* part_g, double* part_loss) {
+  switch (nt / 32) {
+#define FG_CASE(NW)                                                                              \
+  case NW:                                                                                       \
+    fullgrad_kernel<T, VEC, TR, NW * 32><<<grid, NW * 32, 0, c.stream>>>(X, ld, n, y, w, part_g,  \
+                                                                         part_loss);             \
+    break;
+    FG_CASE(2) FG_CASE(4) FG_CASE(8) FG_CASE(16)
+#undef FG_CASE
+    default:
+      raise(SKR_EINTERNAL, "fullgrad: unsupported block size");
+  }
+  SKR_LAUNCHED(&c);
+}
+
+struct FgPlan {
+  int vec = 0, nt = 0, tr = 0, grid = 0;
+};
+
+// Choose columns-per-thread so each row costs every thread 16-64 B of vector
+// loads, keep the block <= 512 threads, and size the grid to fill the SMs.
+template <class T>
+FgPlan plan_fullgrad(Ctx& c, int64_t ld, int64_t n) {
+  FgPlan p;
+  const int cand[] = {2, 4, 8, 16};
+  for (int v : cand) {
+    if (v * (int)sizeof(T) < 16) continue;
+    int nt = (int)((ld + v - 1) / v);
+    nt = (nt + 31) / 32 * 32;
+    if (nt < 64) nt = 64;
+    if (nt <= 512) {
+      p.vec = v;
+      p.nt = 1;
+      while (p.nt < nt) p.nt *= 2;
+      break;
+    }
+  }
+  if (!p.vec) raise(SKR_EDIM, "full gradient: dimension too large for the fused pass");
+  p.tr = std::max(2, std::min(8, 32 / p.vec));
+  const int64_t tiles = (n + p.tr - 1) / p.tr;
+  const int per_sm = std::max(1, 2048 / p.nt);
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sm_count * per_sm));
+  return p;
+}
+
+template <class T>
+void run_fullgrad_main(Ctx& c, const FgPlan& p, const T* X, int64_t ld, int64_t n, const double* y,
+                       const double* w, double* part_g, double* part_loss) {
+  if (p.vec == 2) {
+    if constexpr (sizeof(T) == 8) launch_fullgrad_t<T, 2, 8>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
+    else raise(SKR_EINTERNAL, "plan");
+  } else if (p.vec == 4) {
+    launch_fullgrad_t<T, 4, 8>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
+  } else if (p.vec == 8) {
+    launch_fullgrad_t<T, 8, 4>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
+  } else {
+    launch_fullgrad_t<T, 16, 2>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
+  }
+}
+
+// raw sums[0..ld) = sum_i r_i x_i, sums[ld] = sum_i r_i^2 over ALL ranks' rows
+void fullgrad_sums(Ctx& c, int dtype, const void* X, int64_t ld, int64_t n, const double* y,
+                   const double* w, DBuf<double>& part_g, DBuf<double>& part_loss,
+                   DBuf<double>& sums) {
+  FgPlan plan;
+  DISPATCH_DTYPE(dtype, T, plan = plan_fullgrad<T>(c, ld, n));
+  if (part_g.n < (size_t)plan.grid * ld) part_g.alloc((size_t)plan.grid * ld, c.stream);
+  if (part_loss.n < (size_t)plan.grid) part_loss.alloc(plan.grid, c.stream);
+  if (sums.n < (size_t)ld + 1) sums.alloc(ld + 1, c.stream);
+  if (n > 0) {
+    DISPATCH_DTYPE(dtype, T,
+                   run_fullgrad_main<T>(c, plan, static_cast<const T*>(X), ld, n, y, w,
+                                        part_g.get(), part_loss.get()));
+    fullgrad_reduce_kernel<<<ceil_div(ld + 1, 256), 256, 0, c.stream>>>(part_g.get(), part_loss.get(),
+                                                                        ld, plan.grid, sums.get());
+    SKR_LAUNCHED(&c);
+  } else {
+    sums.zero();
+  }
+  c.allreduce_sum(sums.get(), ld + 1);
+}
+
+// out = P^{-1/2} v through the low-rank form; proj gets U^T v (k) and v.v (index k).
+void apply_inv_sqrt_dev(Ctx& c, const skr_problem* p, const double* v, double* proj, double* out) {
+  const int64_t k = p->k;
+  lowrank_proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), p->ld, p->d, k, v, proj);
+  SKR_LAUNCHED(&c);
+  lowrank_apply_kernel<<<ceil_div(p->ld, 256), 256, 0, c.stream>>>(p->Ut.get(), p->ld, p->d, k, p->D.get(),
+                                                                   p->c, v, proj, out);
+  SKR_LAUNCHED(&c);
+}
+
+// K9 on the problem: mu (ld, device) and optional obj (device scalar) at w (device, ld).
+void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) {
+  Ctx& c = p->ctx->c;
+  // regulariser: lambda P^{-1} w = lambda P^{-1/2}(P^{-1/2} w)  (ridge.cpp:232-235)
+  apply_inv_sqrt_dev(c, p, w, p->uw.get(), p->half.get());
+  apply_inv_sqrt_dev(c, p, p->half.get(), p->uh.get(), p->pinv.get());
+  fullgrad_sums(c, p->dtype, p->xt->ptr, p->ld, p->n, p->y.get(), w, p->part_g, p->part_loss, p->sums);
+  fullgrad_finalize_kernel<<<ceil_div(p->ld, 256), 256, 0, c.stream>>>(
+      p->sums.get(), p->ld, p->d, (double)p->n_global, p->lambda, p->pinv.get(), p->uw.get(), p->k,
+      p->D.get(), p->c, mu, obj);
+  SKR_LAUNCHED(&c);
+}
+
+// Exact sampling tables (svrg.cpp:90-106, :165-172), built once per problem.
+void ensure_tables(skr_problem* p) {
+  if (p->tables) return;
+  Ctx& c = p->ctx->c;
+  const int64_t N = p->n_global + p->d;
+  p->cum.alloc(N, c.stream);
+  p->inv_nq.alloc(N, c.stream);
+  p->total.alloc(1, c.stream);
+  cumulative_kernel<<<1, 1, 0, c.stream>>>(p->betas.get(), N, p->cum.get(), p->total.get());
+  SKR_LAUNCHED(&c);
+  inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.stream>>>(p->betas.get(), N, p->total.get(),
+                                                                                  p->inv_nq.get());
+  SKR_LAUNCHED(&c);
+  p->tables = true;
+}
+
+void seed_mt(Ctx& c, DBuf<MtState>& mt, uint64_t seed) {
+  MtState h;
+  mt_seed_host(h, seed);
+  if (!mt.p) mt.alloc(1, c.stream);
+  SKR_CUDA(cudaMemcpyAsync(mt.get(), &h, sizeof(MtState), cudaMemcpyHostToDevice, c.stream));
+}
+
+void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
+  if (count <= 0) return;
+  mt_generate_kernel<false><<<1, 320, 0, c.stream>>>(st, out, count);
+  SKR_LAUNCHED(&c);
+}
+
+// indices for `m` steps continuing the problem's stream
+void draw_indices(skr_problem* p, DBuf<double>& u, DBuf<int64_t>& idx, int64_t m) {
+  Ctx& c = p->ctx->c;
+  if (u.n < (size_t)m) u.alloc(m, c.stream);
+  if (idx.n < (size_t)m) idx.alloc(m, c.stream);
+  mt_uniforms_dev(c, p->mt.get(), u.get(), m);
+  lower_bound_kernel<<<std::min<unsigned>(ceil_div(m, 256), 8 * c.sm_count), 256, 0, c.stream>>>(
+      p->cum.get(), p->n_global + p->d, u.get(), m, idx.get());
+  SKR_LAUNCHED(&c);
+}
+
+// MgsBasis::append_block (factorize.cpp:53-71): BCGS2 against the accepted
+// basis Qt[0..W), Householder QR of the block, drop |R_jj| < 1e-12 * ref.
+// V (a rows x ld) is overwritten.  Returns the number of rows appended.
+int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap, double* V, int a) {
+  DBuf<double> ref(1, c.stream), rdiag(a, c.stream), tau(a, c.stream);
+  row_norm_max_kernel<<<1, 1024, 0, c.stream>>>(V, ld, d, a, ref.get());
+  SKR_LAUNCHED(&c);
+  if (W > 0) {
+    DBuf<double> C((size_t)a * W, c.stream);
+    for (int pass = 0; pass < 2; ++pass) {
+      gemm<double, double, false, true>(&c, a, W, d, V, ld, Qt, ld, EpiStore{C.get(), W, 1.0, 0.0});
+      gemm<double, double, false, false>(&c, a, d, W, C.get(), W, Qt, ld, EpiStore{V, ld, -1.0, 1.0});
+    }
+  }
+  int lwork = 0, lwork2 = 0;
+  SKR_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, (int)d, a, V, (int)ld, &lwork));
+  SKR_SOLVER(cusolverDnDorgqr_bufferSize(c.solver, (int)d, a, a, V, (int)ld, tau.get(), &lwork2));
+  DBuf<double> work(std::max(std::max(lwork, lwork2), 1), c.stream);
+  DBuf<int> info(3, c.stream);
+  SKR_SOLVER(cusolverDnDgeqrf(c.solver, (int)d, a, V, (int)ld, tau.get(), work.get(), lwork, info.get()));
+  qr_diag_kernel<<<ceil_div(a, 256), 256, 0, c.stream>>>(V, ld, a, rdiag.get());
+  SKR_LAUNCHED(&c);
+  SKR_SOLVER(cusolverDnDorgqr(c.solver, (int)d, a, a, V, (int)ld, tau.get(), work.get(), std::max(lwork, lwork2),
+                              info.get()));
+  int hc[2] = {W, 0};
+  SKR_CUDA(cudaMemcpyAsync(info.get() + 1, hc, sizeof(hc), cudaMemcpyHostToDevice, c.stream));
+  qr_select_kernel<<<1, 1024, 0, c.stream>>>(Qt, ld, d, info.get() + 1, (int)cap, V, rdiag.get(), ref.get(), a);
+  SKR_LAUNCHED(&c);
+  SKR_CUDA(cudaMemcpyAsync(hc, info.get() + 1, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  W = hc[0];
+  return hc[1];
+}
+
+// ---- K10 dispatch ----------------------------------------------------------
+template <class T, int VEC, int NT>
+void launch_epoch_t(Ctx& c, const EpochArgs& a) {
+  const size_t smem = svrg_epoch_smem<T, VEC, NT>();
+  static bool configured = false;
+  if (!configured) {
+    SKR_CUDA(cudaFuncSetAttribute(svrg_epoch_kernel<T, VEC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    configured = true;
+  }
+  svrg_epoch_kernel<T, VEC, NT><<<1, NT, smem, c.stream>>>(a);
+  SKR_LAUNCHED(&c);
+}
+
+template <class T>
+void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
+  // block of 128..512 threads with 4/8 (fp32: 8/16) columns each
+  if (sizeof(T) == 8) {
+    if (ld <= 512) launch_epoch_t<T, 4, 128>(c, a);
+    else if (ld <= 1024) launch_epoch_t<T, 4, 256>(c, a);
+    else if (ld <= 2048) launch_epoch_t<T, 8, 256>(c, a);
+    else if (ld <= 4096) launch_epoch_t<T, 8, 512>(c, a);
+    else raise(SKR_EDIM, "svrg: dimension too large for the inner-loop kernel");
+  } else {
+    if (ld <= 1024) launch_epoch_t<T, 8, 128>(c, a);
+    else if (ld <= 2048) launch_epoch_t<T, 8, 256>(c, a);
+    else if (ld <= 4096) launch_epoch_t<T, 8, 512>(c, a);
+    else raise(SKR_EDIM, "svrg: dimension too large for the inner-loop kernel");
+  }
+}
+
+void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m,
+               double eta, double* w_avg) {
+  ensure_tables(p);
+  EpochArgs a;
+  a.Xt = p->xt_all;
+  a.B = p->B.get();
+  a.ld = p->ld;
+  a.n = p->n_global;
+  a.N = p->n_global + p->d;
+  a.y = p->y_all;
+  a.inv_nq = p->inv_nq.get();
+  a.data_coef = p->data_coef;
+  a.reg_coef = p->reg_coef;
+  a.idx = idx;
+  a.m = m;
+  a.eta = eta;
+  a.snapshot = snap;
+  a.mu = mu;
+  a.w_avg = w_avg;
+  DISPATCH_DTYPE(p->dtype, T, run_epoch_t<T>(p->ctx->c, p->ld, a));
+}
+
+// ---- elementwise helpers ----------------------------------------------------
+__global__ void scale_cols_kernel(double* __restrict__ P, int64_t rows, int64_t k,
+                                  const double* __restrict__ D, double c) {
+  const int64_t total = rows * k;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    P[e] *= D[e % k] - c;
+}
+__global__ void scale_rows_kernel(double* __restrict__ Ut, int64_t k, int64_t ld, const double* __restrict__ D,
+                                  double c) {
+  const int64_t total = k * ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    Ut[e] *= D[e / ld] - c;
+}
+
+// beta_i = data_coef (c^2 ||x_i||^2 + sum_j (D_j^2 - c^2) P_ij^2) (ridge.cpp:124-127,
+// precond.cpp:110-118); one warp per row.  rowsq_out gets the unscaled ||x~_i||^2.
+template <class T>
+__global__ void data_betas_kernel(const T* __restrict__ X, int64_t ld, int64_t d, int64_t n,
+                                  const double* __restrict__ P, int64_t k, const double* __restrict__ D,
+                                  double c, double data_coef, double* __restrict__ beta,
+                                  double* __restrict__ rowmax) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double mymax = 0.0;
+  for (int64_t i = warp; i < n; i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int64_t j = lane; j < d; j += 32) {
+      const double x = (double)X[i * ld + j];
+      s = fma(x, x, s);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    double t = 0.0;
+    for (int64_t j = lane; j < k; j += 32) {
+      const double pj = P[i * k + j];
+      t = fma((D[j] * D[j] - c * c) * pj, pj, t);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    const double nrm = c * c * s + t;
+    if (lane == 0) beta[i] = data_coef * nrm;
+    mymax = fmax(mymax, nrm);
+  }
+  if (lane == 0) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(rowmax), __double_as_longlong(mymax));
+  }
+}
+
+// beta_{n+j} = reg_coef (c^2 + sum_l (D_l^2 - c^2) U_jl^2) (ridge.cpp:128-130)
+__global__ void reg_betas_kernel(const double* __restrict__ Ut, int64_t ld, int64_t d, int64_t k,
+                                 const double* __restrict__ D, double c, double reg_coef,
+                                 double* __restrict__ beta) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  double s = c * c;
+  for (int64_t l = 0; l < k; ++l) {
+    const double u = Ut[l * ld + j];
+    s = fma((D[l] * D[l] - c * c) * u, u, s);
+  }
+  beta[j] = reg_coef * s;
+}
+
+__global__ void max_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, v[i]);
+  m = block_max(m, scratch);
+  if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(m));
+}
+
+// floor_betas (ridge.cpp:16-21)
+__global__ void floor_kernel(double* __restrict__ b, int64_t n, const double* __restrict__ top) {
+  const double fl = *top * 1e-12;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = fmax(b[i], fl);
+}
+
+__global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  // deterministic single-CTA sum (fixed thread/stride order)
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// epilogues for the preconditioner build
+template <class T>
+struct EpiXtilde {  // X~[m,n] = T(c X[m,n] + acc)   (ridge.cpp:133-149)
+  const T* X;
+  T* Xt;
+  int64_t ld;
+  double c;
+  __device__ void operator()(int64_t m, int64_t n, double acc) const {
+    Xt[m * ld + n] = (T)fma(c, (double)X[m * ld + n], acc);
+  }
+};
+struct EpiBmat {  // B[m,n] = acc + c [m == n]   (P^{-1/2} = c I + U (D - c) U^T)
+  double* B;
+  int64_t ld;
+  double c;
+  __device__ void operator()(int64_t m, int64_t n, double acc) const { B[m * ld + n] = acc + (m == n ? c : 0.0); }
+};
+template <class T>
+struct EpiStoreT {  // C[m,n] = T(alpha acc)
+  T* C;
+  int64_t ldc;
+  double alpha;
+  __device__ void operator()(int64_t m, int64_t n, double acc) const { C[m * ldc + n] = (T)(alpha * acc); }
+};
+
+// component_gradient (ridge.cpp:238-278) on the stacked rows, one CTA.
+template <class T>
+__global__ void component_gradient_kernel(const T* __restrict__ Xt, const double* __restrict__ B, int64_t ld,
+                                          int64_t d, int64_t n, const double* __restrict__ y, double data_coef,
+                                          double reg_coef, int64_t i, const double* __restrict__ w,
+                                          double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    const double x = i < n ? (double)Xt[i * ld + j] : B[(i - n) * ld + j];
+    s = fma(x, w[j], s);
+  }
+  s = block_sum(s, scratch);
+  const double g = i < n ? data_coef * (s - y[i]) : reg_coef * s;
+  for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) {
+    const double x = j < d ? (i < n ? (double)Xt[i * ld + j] : B[(i - n) * ld + j]) : 0.0;
+    out[j] = g * x;
+  }
+}
+
+__global__ void add_diag_kernel(double* __restrict__ G, int64_t d, int64_t ld, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) G[i * ld + i] += v;
+}
+
+__global__ void symmetrize_kernel(double* __restrict__ M, int64_t d, int64_t ld) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d * d) return;
+  const int64_t i = e / d, j = e % d;
+  if (i > j) {
+    const double v = 0.5 * (M[i * ld + j] + M[j * ld + i]);
+    M[i * ld + j] = v;
+    M[j * ld + i] = v;
+  }
+}
+
+__global__ void trace_kernel(const double* __restrict__ M, int64_t d, int64_t ld, double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s += M[i * ld + i];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// compact an ld-strided d x d block to a dense d x d (column-major == row-major, symmetric)
+__global__ void compact_kernel(const double* __restrict__ src, int64_t d, int64_t ld, double* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < d * d) dst[e] = src[(e / d) * ld + e % d];
+}
+
+// synthetic data: G[i,j] = sigma_j * z, z from Philox stream 1 at global element (row0+i)*d+j
+__global__ void synth_g_kernel(uint64_t seed, int64_t row0, int64_t rows, int64_t d, int64_t ld,
+                               const double* __restrict__ sigma, double* __restrict__ G) {
+  const int64_t total = rows * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d, j = e % d;
+    const uint64_t ge = (uint64_t)(row0 + i) * (uint64_t)d + (uint64_t)j;
+    const double2 z = philox_normal2(seed, 1u, ge >> 1);
+    G[i * ld + j] = sigma[j] * ((ge & 1) ? z.y : z.x);
+  }
+}
+
+// |Student-t(3)| row factors: t = Z0 / sqrt((Z1^2+Z2^2+Z3^2)/3), stream 3 at global row.
+template <class T>
+__global__ void synth_tscale_kernel(uint64_t seed, int64_t row0, int64_t rows, int64_t d, int64_t ld,
+                                    T* __restrict__ X) {
+  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+    const double2 a = philox_normal2(seed, 3u, 2 * (uint64_t)(row0 + i));
+    const double2 b = philox_normal2(seed, 3u, 2 * (uint64_t)(row0 + i) + 1);
+    const double t = fabs(a.x / sqrt((a.y * a.y + b.x * b.x + b.y * b.y) / 3.0));
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) X[i * ld + j] = (T)((double)X[i * ld + j] * t);
+  }
+}
+
+// y_i = T(x_i . w* + tau z_i) widened back to double (fp32 configs store fp32 labels)
+template <class T>
+__global__ void synth_labels_kernel(const T* __restrict__ X, int64_t ld, int64_t d, int64_t rows, int64_t row0,
+                                    const double* __restrict__ wstar, double tau, uint64_t seed,
+                                    double* __restrict__ y) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = warp; i < rows; i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int64_t j = lane; j < d; j += 32) s = fma((double)X[i * ld + j], wstar[j], s);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) {
+      const uint64_t g = (uint64_t)(row0 + i);
+      const double2 z = philox_normal2(seed, 5u, g >> 1);
+      y[i] = (double)(T)(s + tau * ((g & 1) ? z.y : z.x));
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+extern "C" {
+
+const char* skr_last_error(void) { return g_err.c_str(); }
+int skr_abi_version(void) { return SKR_ABI_VERSION; }
+
+static void ctx_init(Ctx& c, int device) {
+  c.device = device;
+  SKR_CUDA(cudaSetDevice(device));
+  SKR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  SKR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
+  cudaMemPool_t pool;
+  SKR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = std::numeric_limits<uint64_t>::max();
+  SKR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  SKR_SOLVER(cusolverDnCreate(&c.solver));
+  SKR_SOLVER(cusolverDnSetStream(c.solver, c.stream));
+}
+
+int skr_ctx_create(int device, skr_ctx** out) {
+  return guard([&] {
+    if (!out) raise(SKR_EPARAM, "null output");
+    auto x = std::make_unique<skr_ctx>();
+    ctx_init(x->c, device);
+    *out = x.release();
+  });
+}
+
+int skr_nccl_unique_id(char id_out[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    SKR_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(id_out, &id, 128);
+  });
+}
+
+int skr_ctx_create_dist(int device, int rank, int world, const char id[128], skr_ctx** out) {
+  return guard([&] {
+    if (!out || world < 1 || rank < 0 || rank >= world) raise(SKR_EPARAM, "bad rank/world");
+    auto x = std::make_unique<skr_ctx>();
+    ctx_init(x->c, device);
+    x->c.rank = rank;
+    x->c.world = world;
+    if (world > 1) {
+      ncclUniqueId uid;
+      std::memcpy(&uid, id, 128);
+      SKR_NCCL(ncclCommInitRank(&x->c.comm, world, uid, rank));
+    }
+    *out = x.release();
+  });
+}
+
+int skr_ctx_destroy(skr_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+    if (ctx->c.solver) cusolverDnDestroy(ctx->c.solver);
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+  });
+}
+
+int skr_ctx_synchronize(skr_ctx* ctx) { return guard([&] { C_(ctx).sync(); }); }
+void* skr_ctx_stream(skr_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+int64_t skr_ctx_kernel_launches(const skr_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+// ---- data --------------------------------------------------------------------
+int skr_data_create(skr_ctx* ctx, const void* rows, int64_t n, int64_t d, int dtype, skr_data** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    check_dtype(dtype);
+    if (n < 0 || d < 1) raise(SKR_EDIM, "data matrix: bad shape");
+    if (n > 0 && !rows) raise(SKR_EPARAM, "null rows");
+    auto st = new_storage(c, dtype, n, d);
+    const size_t s = dtype_size(dtype);
+    if (n > 0)
+      SKR_CUDA(cudaMemcpy2DAsync(st->ptr, st->ld * s, rows, d * s, d * s, n, cudaMemcpyHostToDevice, c.stream));
+    auto x = std::make_unique<skr_data>();
+    x->ctx = ctx;
+    x->st = st;
+    shard_layout(c, n, &x->n_global, &x->row0);
+    c.sync();
+    *out = x.release();
+  });
+}
+
+int skr_data_create_device(skr_ctx* ctx, const void* dev_rows, int64_t ld, int64_t n, int64_t d, int dtype,
+                           skr_data** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    check_dtype(dtype);
+    if (n < 0 || d < 1 || ld < d) raise(SKR_EDIM, "data matrix: bad shape");
+    auto st = new_storage(c, dtype, n, d);
+    const size_t s = dtype_size(dtype);
+    if (n > 0)
+      SKR_CUDA(cudaMemcpy2DAsync(st->ptr, st->ld * s, dev_rows, ld * s, d * s, n, cudaMemcpyDeviceToDevice, c.stream));
+    auto x = std::make_unique<skr_data>();
+    x->ctx = ctx;
+    x->st = st;
+    shard_layout(c, n, &x->n_global, &x->row0);
+    c.sync();
+    *out = x.release();
+  });
+}
+
+int skr_data_scaled(const skr_data* src, double factor, skr_data** out) {
+  return guard([&] {
+    if (!src || !out) raise(SKR_EPARAM, "null handle");
+    if (!(factor > 0.0) || !std::isfinite(factor)) raise(SKR_EPARAM, "data matrix: scale must be positive and finite");
+    auto x = std::make_unique<skr_data>(*src);
+    x->scale = src->scale * factor;
+    *out = x.release();
+  });
+}
+
+int skr_data_info(const skr_data* x, int64_t* n, int64_t* d, int* dtype, double* scale, int64_t* n_global,
+                  int64_t* row0) {
+  return guard([&] {
+    if (!x) raise(SKR_EPARAM, "null handle");
+    if (n) *n = x->st->n;
+    if (d) *d = x->st->d;
+    if (dtype) *dtype = x->st->dtype;
+    if (scale) *scale = x->scale;
+    if (n_global) *n_global = x->n_global;
+    if (row0) *row0 = x->row0;
+  });
+}
+
+int skr_data_download(const skr_data* x, void* rows_out) {
+  return guard([&] {
+    if (!x) raise(SKR_EPARAM, "null handle");
+    Ctx& c = x->ctx->c;
+    const size_t s = dtype_size(x->st->dtype);
+    if (x->st->n > 0)
+      SKR_CUDA(cudaMemcpy2DAsync(rows_out, x->st->d * s, x->st->ptr, x->st->ld * s, x->st->d * s, x->st->n,
+                                 cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_data_destroy(skr_data* x) {
+  return guard([&] { delete x; });
+}
+
+int skr_data_labels(const skr_data* x, double* y_out) {
+  return guard([&] {
+    if (!x) raise(SKR_EPARAM, "null handle");
+    if (!x->st->labels.p) raise(SKR_EINPUT, "data handle carries no generated labels");
+    Ctx& c = x->ctx->c;
+    SKR_CUDA(cudaMemcpyAsync(y_out, x->st->labels.get(), sizeof(double) * x->st->n, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_data_generate(skr_ctx* ctx, const skr_synth_spec* spec, skr_data** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!spec || !out) raise(SKR_EPARAM, "null argument");
+    check_dtype(spec->dtype);
+    const int64_t n = spec->n, d = spec->d, ld = padded_ld(d);
+    if (n < 1 || d < 1) raise(SKR_EDIM, "synthetic: bad shape");
+    // spectrum
+    std::vector<double> sig(d);
+    for (int64_t j = 0; j < d; ++j) {
+      const double q = (double)(j + 1);
+      switch (spec->spectrum) {
+        case 0: sig[j] = 1.0 / q; break;
+        case 1: sig[j] = std::pow(spec->spectrum_param, q); break;
+        case 2: sig[j] = std::pow(q, -spec->spectrum_param); break;
+        case 3: sig[j] = q <= 50 ? 1.0 / q : 0.02 / q; break;
+        default: raise(SKR_EPARAM, "synthetic: unknown spectrum");
+      }
+    }
+    DBuf<double> sigma(d, c.stream);
+    SKR_CUDA(cudaMemcpyAsync(sigma.get(), sig.data(), sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
+    // V: Gram-Schmidt of the rows of a d x d Gaussian (stream 2) -> Haar orthogonal
+    DBuf<double> A((size_t)d * ld, c.stream), Qt((size_t)d * ld, c.stream);
+    DBuf<double> Araw((size_t)d * d, c.stream);
+    philox_normal_kernel<<<std::min<unsigned>(ceil_div(d * d / 2 + 1, 256), 8192), 256, 0, c.stream>>>(
+        spec->seed, 2u, d * d, 1.0, Araw.get());
+    SKR_LAUNCHED(&c);
+    A.zero();
+    SKR_CUDA(cudaMemcpy2DAsync(A.get(), ld * 8, Araw.get(), d * 8, d * 8, d, cudaMemcpyDeviceToDevice, c.stream));
+    {  // Haar V = Q diag(sign diag R) from QR of the Gaussian (rows of A are columns of
+       // the column-major d x d view); Qt row j = column j of V
+      DBuf<double> tau(d, c.stream), rdiag(d, c.stream);
+      int lw1 = 0, lw2 = 0;
+      SKR_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, (int)d, (int)d, A.get(), (int)ld, &lw1));
+      SKR_SOLVER(cusolverDnDorgqr_bufferSize(c.solver, (int)d, (int)d, (int)d, A.get(), (int)ld, tau.get(), &lw2));
+      DBuf<double> work(std::max(std::max(lw1, lw2), 1), c.stream);
+      DBuf<int> info(1, c.stream);
+      SKR_SOLVER(cusolverDnDgeqrf(c.solver, (int)d, (int)d, A.get(), (int)ld, tau.get(), work.get(), lw1, info.get()));
+      qr_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(A.get(), ld, (int)d, rdiag.get());
+      SKR_LAUNCHED(&c);
+      SKR_SOLVER(cusolverDnDorgqr(c.solver, (int)d, (int)d, (int)d, A.get(), (int)ld, tau.get(), work.get(),
+                                  std::max(lw1, lw2), info.get()));
+      qr_sign_rows_kernel<<<(unsigned)d, 256, 0, c.stream>>>(A.get(), ld, d, rdiag.get(), (int)d);
+      SKR_LAUNCHED(&c);
+      SKR_CUDA(cudaMemcpyAsync(Qt.get(), A.get(), sizeof(double) * d * ld, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    // shard
+    int64_t n_local = n / c.world + (c.rank < n % c.world ? 1 : 0);
+    int64_t row0 = c.rank * (n / c.world) + std::min<int64_t>(c.rank, n % c.world);
+    auto st = new_storage(c, spec->dtype, n_local, d);
+    // X = (G diag sigma) V^T in row chunks: X_chunk = G_chunk Qt
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_local, (int64_t)(1 << 30) / ld));
+    DBuf<double> G((size_t)chunk * ld, c.stream);
+    for (int64_t r = 0; r < n_local; r += chunk) {
+      const int64_t rows = std::min(chunk, n_local - r);
+      G.zero();
+      synth_g_kernel<<<std::min<unsigned>(ceil_div(rows * d, 256), 16384), 256, 0, c.stream>>>(
+          spec->seed, row0 + r, rows, d, ld, sigma.get(), G.get());
+      SKR_LAUNCHED(&c);
+      DISPATCH_DTYPE(spec->dtype, T, {
+        T* Xc = static_cast<T*>(st->ptr) + r * ld;
+        gemm<double, double, false, false>(&c, rows, d, d, G.get(), ld, Qt.get(), ld, EpiStoreT<T>{Xc, ld, 1.0}, 1);
+        if (spec->t_scale) {
+          synth_tscale_kernel<T><<<std::min<unsigned>((unsigned)rows, 65535u), 256, 0, c.stream>>>(
+              spec->seed, row0 + r, rows, d, ld, Xc);
+          SKR_LAUNCHED(&c);
+        }
+      });
+    }
+    // w* ~ N(0, I/d) (stream 4), y = X w* + tau z (stream 5)
+    DBuf<double> wstar(d, c.stream);
+    philox_normal_kernel<<<ceil_div(d / 2 + 1, 256), 256, 0, c.stream>>>(spec->seed, 4u, d, 1.0 / std::sqrt((double)d),
+                                                                        wstar.get());
+    SKR_LAUNCHED(&c);
+    st->labels.alloc(std::max<int64_t>(n_local, 1), c.stream);
+    DISPATCH_DTYPE(spec->dtype, T, {
+      synth_labels_kernel<T><<<std::min<unsigned>(ceil_div(n_local * 32, 256), 65535u), 256, 0, c.stream>>>(
+          static_cast<const T*>(st->ptr), ld, d, n_local, row0, wstar.get(), spec->tau, spec->seed, st->labels.get());
+      SKR_LAUNCHED(&c);
+    });
+    auto x = std::make_unique<skr_data>();
+    x->ctx = ctx;
+    x->st = st;
+    x->n_global = n;
+    x->row0 = row0;
+    c.sync();
+    *out = x.release();
+  });
+}
+
+// ---- block_lanczos -------------------------------------------------------------
+int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double eps_prime, uint64_t seed, double* U,
+                double* sigma, double* V, int64_t* k_used, int64_t* q_used, int* rank_reduced) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!A) raise(SKR_EPARAM, "null data");
+    const Storage& S = *A->st;
+    const int64_t n = S.n, ng = A->n_global, d = S.d, ld = S.ld;
+    const double scale = A->scale;
+    if (k < 1 || k > std::min(d, ng)) raise(SKR_EPARAM, "block_lanczos: k must satisfy 1 <= k <= min(d, n)");
+    if (!(eps_prime > 0.0 && eps_prime < 1.0)) raise(SKR_EPARAM, "block_lanczos: eps_prime must lie in (0, 1)");
+    if (q <= 0) {  // lanczos_iterations (sketch.cpp:13-16)
+      const double qq = std::ceil(std::log((double)ng) / std::sqrt(eps_prime));
+      q = std::max<int64_t>(2, (int64_t)qq);
+    }
+    const int64_t cap = q * k;
+    // Pi = gaussian_matrix(n, k, seed): the reference stream, local rows (random.cpp:28-41)
+    const int64_t total_normals = ng * k;
+    const int64_t nu = (total_normals + 1) / 2 * 2;
+    DBuf<MtState> mt(1, c.stream);
+    seed_mt(c, mt, seed);
+    DBuf<double> u(nu, c.stream);
+    mt_uniforms_dev(c, mt.get(), u.get(), nu);
+    DBuf<double> Pt((size_t)k * std::max<int64_t>(n, 1), c.stream);
+    box_muller_kernel<<<std::min<unsigned>(ceil_div(n * k, 256), 65535u), 256, 0, c.stream>>>(
+        u.get(), ng, k, A->row0, n, Pt.get());
+    SKR_LAUNCHED(&c);
+    u.release();
+
+    DBuf<double> Qt((size_t)cap * ld, c.stream), Vt((size_t)k * ld, c.stream);
+    Qt.zero();
+    int Wb = 0;
+    // block = A Pi  -> Vt (k x ld) = scale * Pi^T X   (sketch.cpp:25)
+    DISPATCH_DTYPE(S.dtype, T, {
+      const T* X = static_cast<const T*>(S.ptr);
+      Vt.zero();
+      gemm<double, T, false, false>(&c, k, d, n, Pt.get(), n, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
+    });
+    c.allreduce_sum(Vt.get(), (size_t)k * ld);
+    int appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), (int)k);
+    if (Wb == 0) raise(SKR_EEMPTY, "krylov_block: A * Pi is numerically zero");
+    DBuf<double> Tm((size_t)std::max<int64_t>(n, 1) * k, c.stream);
+    for (int64_t j = 1; j < q && appended > 0; ++j) {
+      const int64_t W = Wb;
+      const double* prev = Qt.get() + (W - appended) * ld;
+      DISPATCH_DTYPE(S.dtype, T, {
+        const T* X = static_cast<const T*>(S.ptr);
+        // T = scale * X prev^T (n x a);   block^T = scale * T^T X (a x d)   (sketch.cpp:35)
+        gemm<T, double, false, true>(&c, n, appended, d, X, ld, prev, ld, EpiStore{Tm.get(), appended, scale, 0.0});
+        Vt.zero();
+        gemm<double, T, true, false>(&c, appended, d, n, Tm.get(), appended, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
+      });
+      c.allreduce_sum(Vt.get(), (size_t)appended * ld);
+      appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), appended);
+    }
+    Tm.release();
+    Pt.release();
+    const int64_t W = Wb;
+    const int64_t kk = std::min<int64_t>(k, W);
+    // Rayleigh-Ritz: G = (X Q)^T (X Q) scale^2 over row chunks (sketch.cpp:59-61)
+    DBuf<double> G((size_t)W * W, c.stream);
+    G.zero();
+    {
+      const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
+      DBuf<double> Z((size_t)chunk * W, c.stream);
+      for (int64_t r = 0; r < n; r += chunk) {
+        const int64_t rows = std::min(chunk, n - r);
+        DISPATCH_DTYPE(S.dtype, T, {
+          const T* X = static_cast<const T*>(S.ptr) + r * ld;
+          gemm<T, double, false, true>(&c, rows, W, d, X, ld, Qt.get(), ld, EpiStore{Z.get(), W, scale, 0.0});
+        });
+        gemm<double, double, true, false>(&c, W, W, rows, Z.get(), W, Z.get(), W, EpiStore{G.get(), W, 1.0, 1.0});
+      }
+    }
+    c.allreduce_sum(G.get(), (size_t)W * W);
+    // eigendecomposition on the device (cuSOLVER syevd), reference ordering/sign rules
+    DBuf<double> evals(W, c.stream), vals_desc(W, c.stream), Wt((size_t)kk * W, c.stream);
+    {
+      int lwork = 0;
+      SKR_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)W,
+                                             G.get(), (int)W, evals.get(), &lwork));
+      DBuf<double> work(std::max(lwork, 1), c.stream);
+      DBuf<int> info(1, c.stream);
+      SKR_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)W, G.get(),
+                                  (int)W, evals.get(), work.get(), lwork, info.get()));
+      int hinfo = 0;
+      SKR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (hinfo != 0) raise(SKR_EINTERNAL, "sym_eigs: eigensolver did not converge");
+    }
+    eig_post_kernel<<<(unsigned)W, 256, 0, c.stream>>>(G.get(), evals.get(), (int)W, (int)kk, Wt.get(),
+                                                        vals_desc.get());
+    SKR_LAUNCHED(&c);
+    // U = Q W_k  -> Ut (kk x ld) = Wt Qt   (sketch.cpp:74-76)
+    DBuf<double> Ut((size_t)kk * ld, c.stream);
+    Ut.zero();
+    gemm<double, double, false, false>(&c, kk, d, W, Wt.get(), W, Qt.get(), ld, EpiStore{Ut.get(), ld, 1.0, 0.0});
+    DBuf<double> flip(kk, c.stream);
+    svd_sign_kernel<<<(unsigned)kk, 256, 0, c.stream>>>(Ut.get(), ld, d, flip.get());
+    SKR_LAUNCHED(&c);
+    std::vector<double> hv(W);
+    SKR_CUDA(cudaMemcpyAsync(hv.data(), vals_desc.get(), sizeof(double) * W, cudaMemcpyDeviceToHost, c.stream));
+    download_rows(c, U, Ut.get(), kk, d, ld);
+    if (V) {
+      // V_j = (Q^T A)^T w_j / ||.|| = scale X u_j / ||.||  (sketch.cpp:78-86); u_j after the sign flip,
+      // so V carries the same flip as normalize_svd_signs applies (factorize.cpp:167-178)
+      DBuf<double> Vm((size_t)std::max<int64_t>(n, 1) * kk, c.stream), sq(kk, c.stream), ones(kk, c.stream);
+      DISPATCH_DTYPE(S.dtype, T, {
+        const T* X = static_cast<const T*>(S.ptr);
+        gemm<T, double, false, true>(&c, n, kk, d, X, ld, Ut.get(), ld, EpiStore{Vm.get(), kk, scale, 0.0});
+      });
+      sq.zero();
+      if (n > 0) {
+        col_sq_norms_kernel<<<std::min<unsigned>((unsigned)n, 1024u), (unsigned)((kk + 31) / 32 * 32), 0, c.stream>>>(
+            Vm.get(), n, (int)kk, sq.get());
+        SKR_LAUNCHED(&c);
+      }
+      c.allreduce_sum(sq.get(), kk);
+      std::vector<double> one(kk, 1.0);
+      SKR_CUDA(cudaMemcpyAsync(ones.get(), one.data(), sizeof(double) * kk, cudaMemcpyHostToDevice, c.stream));
+      col_normalize_kernel<<<std::min<unsigned>(ceil_div(n * kk, 256), 65535u), 256, 0, c.stream>>>(
+          Vm.get(), n, (int)kk, sq.get(), ones.get());
+      SKR_LAUNCHED(&c);
+      // host V is n x kk column-major; Vm is n x kk row-major -> transpose on copy-out
+      std::vector<double> tmp((size_t)n * kk);
+      SKR_CUDA(cudaMemcpyAsync(tmp.data(), Vm.get(), sizeof(double) * n * kk, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < kk; ++j) V[j * n + i] = tmp[i * kk + j];
+    }
+    c.sync();
+    for (int64_t j = 0; j < kk; ++j) sigma[j] = std::sqrt(std::max(hv[j], 0.0));
+    *k_used = kk;
+    *q_used = q;
+    *rank_reduced = kk < k ? 1 : 0;
+  });
+}
+
+// ---- preconditioned components -------------------------------------------------
+int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
+                       const double* sigma, int64_t k, skr_problem** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X || !out) raise(SKR_EPARAM, "null argument");
+    if (X->scale != 1.0) raise(SKR_EPARAM, "preconditioned components expect the unscaled data handle");
+    if (!(lambda > 0.0) || !std::isfinite(lambda)) raise(SKR_EPARAM, "ridge problem: lambda must be positive");
+    if (k < 0) raise(SKR_EPARAM, "k must be >= 0");
+    const Storage& S = *X->st;
+    auto p = std::make_unique<skr_problem>();
+    p->ctx = ctx;
+    p->dtype = S.dtype;
+    p->n = S.n;
+    p->n_global = X->n_global;
+    p->row0 = X->row0;
+    p->d = S.d;
+    p->ld = S.ld;
+    p->k = k;
+    p->lambda = lambda;
+    const int64_t n = p->n, ng = p->n_global, d = p->d, ld = p->ld;
+    if (k > std::min(d, ng)) raise(SKR_EPARAM, "preconditioner: rank exceeds min(d, n)");
+    // build_sketched (precond.cpp:120-136) + validate (:34-49)
+    std::vector<double> D(std::max<int64_t>(k, 1), 1.0);
+    if (k > 0) {
+      for (int64_t j = 0; j < k; ++j) D[j] = 1.0 / std::sqrt(sigma[j] * sigma[j] + lambda);
+      p->c = D[k - 1];
+      const double cap = 1.0 / std::sqrt(lambda) * (1.0 + 1e-12);
+      double prev = 0.0;
+      for (int64_t j = 0; j < k; ++j) {
+        if (!(D[j] > 0.0) || D[j] > cap) raise(SKR_EINPUT, "preconditioner: coefficient out of range");
+        if (D[j] < prev) raise(SKR_EINPUT, "preconditioner: coefficients must be non-decreasing");
+        prev = D[j];
+      }
+    } else {
+      p->c = 1.0;
+    }
+    p->data_coef = (double)(ng + d) / (double)ng;
+    p->reg_coef = lambda * (double)(ng + d);
+    p->alpha = lambda * (k > 0 ? D[0] * D[0] : 1.0);  // ridge.cpp:152-157, precond.cpp:62-65
+    p->D.alloc(std::max<int64_t>(k, 1), c.stream);
+    SKR_CUDA(cudaMemcpyAsync(p->D.get(), D.data(), sizeof(double) * D.size(), cudaMemcpyHostToDevice, c.stream));
+    p->Ut.alloc((size_t)std::max<int64_t>(k, 1) * ld, c.stream);
+    p->Ut.zero();
+    if (k > 0) upload_rows(c, p->Ut.get(), U, k, d, ld);
+    p->y.alloc(std::max<int64_t>(n, 1), c.stream);
+    if (n > 0) SKR_CUDA(cudaMemcpyAsync(p->y.get(), y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+
+    const int64_t N = ng + d;
+    p->betas.alloc(N, c.stream);
+    p->betas.zero();
+    DBuf<double> rowmax(1, c.stream);
+    rowmax.zero();
+    // P = X U (n x k) with ||x_i||^2 -> data betas; X~ = c X + (P o (D - c)) U^T
+    DBuf<double> P((size_t)std::max<int64_t>(n, 1) * std::max<int64_t>(k, 1), c.stream);
+    DISPATCH_DTYPE(S.dtype, T, {
+      const T* Xp = static_cast<const T*>(S.ptr);
+      if (k > 0) gemm<T, double, false, true>(&c, n, k, d, Xp, ld, p->Ut.get(), ld, EpiStore{P.get(), k, 1.0, 0.0});
+      if (n > 0) {
+        data_betas_kernel<T><<<std::min<unsigned>(ceil_div(n * 32, 256), 8u * c.sm_count), 256, 0, c.stream>>>(
+            Xp, ld, d, n, P.get(), k, p->D.get(), p->c, p->data_coef, p->betas.get() + p->row0, rowmax.get());
+        SKR_LAUNCHED(&c);
+      }
+      if (k > 0) {
+        auto xt = new_storage(c, S.dtype, n, d);
+        scale_cols_kernel<<<std::min<unsigned>(ceil_div(n * k, 256), 65535u), 256, 0, c.stream>>>(
+            P.get(), n, k, p->D.get(), p->c);
+        SKR_LAUNCHED(&c);
+        gemm<double, double, false, false>(&c, n, d, k, P.get(), k, p->Ut.get(), ld,
+                                           EpiXtilde<T>{Xp, static_cast<T*>(xt->ptr), ld, p->c}, 1);
+        p->xt = xt;
+      } else {
+        p->xt = X->st;  // identity: X~ = X exactly (c = 1)
+      }
+    });
+    P.release();
+    // B = P^{-1/2} = c I + U (D - c) U^T  (d x ld); regulariser betas on rank 0 only (summed below)
+    p->B.alloc((size_t)d * ld, c.stream);
+    p->B.zero();
+    if (k > 0) {
+      DBuf<double> Us((size_t)k * ld, c.stream);
+      SKR_CUDA(cudaMemcpyAsync(Us.get(), p->Ut.get(), sizeof(double) * k * ld, cudaMemcpyDeviceToDevice, c.stream));
+      scale_rows_kernel<<<std::min<unsigned>(ceil_div(k * ld, 256), 65535u), 256, 0, c.stream>>>(Us.get(), k, ld,
+                                                                                                 p->D.get(), p->c);
+      SKR_LAUNCHED(&c);
+      gemm<double, double, true, false>(&c, d, d, k, Us.get(), ld, p->Ut.get(), ld, EpiBmat{p->B.get(), ld, p->c}, 1);
+    } else {
+      add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(p->B.get(), d, ld, 1.0);
+      SKR_LAUNCHED(&c);
+    }
+    if (c.rank == 0) {
+      reg_betas_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, p->D.get(), p->c, p->reg_coef,
+                                                              p->betas.get() + ng);
+      SKR_LAUNCHED(&c);
+    }
+    c.allreduce_sum(p->betas.get(), N);
+    c.allreduce_max(rowmax.get(), 1);
+    DBuf<double> top(1, c.stream);
+    top.zero();
+    max_kernel<<<std::min<unsigned>(ceil_div(N, 256), 1024u), 256, 0, c.stream>>>(p->betas.get(), N, top.get());
+    SKR_LAUNCHED(&c);
+    floor_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096u), 256, 0, c.stream>>>(p->betas.get(), N, top.get());
+    SKR_LAUNCHED(&c);
+    DBuf<double> bsum(1, c.stream);
+    sum_kernel<<<1, 1024, 0, c.stream>>>(p->betas.get(), N, bsum.get());
+    SKR_LAUNCHED(&c);
+    double hsum = 0.0;
+    SKR_CUDA(cudaMemcpyAsync(&hsum, bsum.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(&p->max_row_sq, rowmax.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    // all rows of X~ and y on every rank for the (sequential, replicated) inner loop
+    if (c.world == 1) {
+      p->xt_all = p->xt->ptr;
+      p->y_all = p->y.get();
+    } else {
+      std::vector<int64_t> counts;
+      int64_t ngl = 0, r0 = 0;
+      shard_layout(c, n, &ngl, &r0, &counts);
+      const int64_t mx = *std::max_element(counts.begin(), counts.end());
+      const size_t s = dtype_size(S.dtype), row_bytes = (size_t)ld * s;
+      DBuf<unsigned char> send((size_t)mx * row_bytes, c.stream), recv((size_t)mx * row_bytes * c.world, c.stream);
+      SKR_CUDA(cudaMemcpyAsync(send.get(), p->xt->ptr, (size_t)n * row_bytes, cudaMemcpyDeviceToDevice, c.stream));
+      c.allgather_bytes(send.get(), recv.get(), (size_t)mx * row_bytes);
+      p->xt_all_buf.alloc((size_t)ng * row_bytes, c.stream);
+      DBuf<double> ysend(mx, c.stream), yrecv((size_t)mx * c.world, c.stream);
+      SKR_CUDA(cudaMemcpyAsync(ysend.get(), p->y.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+      c.allgather_bytes(ysend.get(), yrecv.get(), sizeof(double) * mx);
+      p->y_all_buf.alloc(ng, c.stream);
+      int64_t off = 0;
+      for (int r = 0; r < c.world; ++r) {
+        SKR_CUDA(cudaMemcpyAsync(p->xt_all_buf.get() + off * row_bytes, recv.get() + (size_t)r * mx * row_bytes,
+                                 (size_t)counts[r] * row_bytes, cudaMemcpyDeviceToDevice, c.stream));
+        SKR_CUDA(cudaMemcpyAsync(p->y_all_buf.get() + off, yrecv.get() + (size_t)r * mx, sizeof(double) * counts[r],
+                                 cudaMemcpyDeviceToDevice, c.stream));
+        off += counts[r];
+      }
+      p->xt_all = p->xt_all_buf.get();
+      p->y_all = p->y_all_buf.get();
+    }
+    // workspaces
+    p->uw.alloc(std::max<int64_t>(k, 1) + 1, c.stream);
+    p->uh.alloc(std::max<int64_t>(k, 1) + 1, c.stream);
+    p->half.alloc(ld, c.stream);
+    p->pinv.alloc(ld, c.stream);
+    p->wv.alloc(ld, c.stream);
+    p->muv.alloc(ld, c.stream);
+    p->objv.alloc(1, c.stream);
+    p->wv.zero();
+    c.sync();
+    p->beta_hat = hsum / (double)N;
+    *out = p.release();
+  });
+}
+
+int skr_problem_destroy(skr_problem* p) {
+  return guard([&] {
+    if (!p) return;
+    cudaStreamSynchronize(p->ctx->c.stream);
+    delete p;
+  });
+}
+
+int skr_problem_info(const skr_problem* p, int64_t* n, int64_t* d, int64_t* k, double* alpha, double* beta_hat,
+                     double* max_row_sq) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    if (n) *n = p->n_global;
+    if (d) *d = p->d;
+    if (k) *k = p->k;
+    if (alpha) *alpha = p->alpha;
+    if (beta_hat) *beta_hat = p->beta_hat;
+    if (max_row_sq) *max_row_sq = p->max_row_sq;
+  });
+}
+
+int skr_problem_betas(const skr_problem* p, double* out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    Ctx& c = p->ctx->c;
+    SKR_CUDA(cudaMemcpyAsync(out, p->betas.get(), sizeof(double) * (p->n_global + p->d), cudaMemcpyDeviceToHost,
+                             c.stream));
+    c.sync();
+  });
+}
+
+int skr_problem_transformed(const skr_problem* p, void* rows_out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    Ctx& c = p->ctx->c;
+    const size_t s = dtype_size(p->dtype);
+    if (p->n > 0)
+      SKR_CUDA(cudaMemcpy2DAsync(rows_out, p->d * s, p->xt->ptr, p->ld * s, p->d * s, p->n, cudaMemcpyDeviceToHost,
+                                 c.stream));
+    c.sync();
+  });
+}
+
+static void check_vec(const double* v, const char* what) {
+  if (!v) raise(SKR_EPARAM, std::string("null ") + what);
+}
+
+int skr_full_gradient_device(skr_problem* p, const double* w_dev, double* mu_dev, double* obj_dev) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    problem_fullgrad(p, w_dev, mu_dev, obj_dev);
+  });
+}
+
+int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    check_vec(w, "w");
+    Ctx& c = p->ctx->c;
+    upload_padded(c, p->wv.get(), w, p->d, p->ld);
+    problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->objv.get() : nullptr);
+    if (mu) SKR_CUDA(cudaMemcpyAsync(mu, p->muv.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+    if (obj) SKR_CUDA(cudaMemcpyAsync(obj, p->objv.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_objective(skr_problem* p, const double* w, double* out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    check_vec(w, "w");
+    Ctx& c = p->ctx->c;
+    upload_padded(c, p->wv.get(), w, p->d, p->ld);
+    problem_fullgrad(p, p->wv.get(), p->muv.get(), p->objv.get());
+    SKR_CUDA(cudaMemcpyAsync(out, p->objv.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_component_gradient(skr_problem* p, int64_t i, const double* w, double* out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    if (i < 0 || i >= p->n_global + p->d) raise(SKR_EINPUT, "component_gradient: index out of range");
+    Ctx& c = p->ctx->c;
+    upload_padded(c, p->wv.get(), w, p->d, p->ld);
+    DISPATCH_DTYPE(p->dtype, T, {
+      component_gradient_kernel<T><<<1, 256, 0, c.stream>>>(static_cast<const T*>(p->xt_all), p->B.get(), p->ld, p->d,
+                                                            p->n_global, p->y_all, p->data_coef, p->reg_coef, i,
+                                                            p->wv.get(), p->muv.get());
+      SKR_LAUNCHED(&c);
+    });
+    SKR_CUDA(cudaMemcpyAsync(out, p->muv.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_apply_inv_sqrt(skr_problem* p, const double* v, double* out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    Ctx& c = p->ctx->c;
+    upload_padded(c, p->wv.get(), v, p->d, p->ld);
+    apply_inv_sqrt_dev(c, p, p->wv.get(), p->uw.get(), p->half.get());
+    SKR_CUDA(cudaMemcpyAsync(out, p->half.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_epoch(skr_problem* p, const double* snapshot, const double* mu, const int64_t* idx, int64_t m, double eta,
+              double* w_avg) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    if (m < 1) raise(SKR_EPARAM, "svrg: epochs and epoch length must be >= 1");
+    Ctx& c = p->ctx->c;
+    const int64_t N = p->n_global + p->d;
+    for (int64_t t = 0; t < m; ++t)
+      if (idx[t] < 0 || idx[t] >= N) raise(SKR_EINPUT, "component_gradient: index out of range");
+    DBuf<double> snap(p->ld, c.stream), muv(p->ld, c.stream), out(p->ld, c.stream);
+    DBuf<int64_t> di(m, c.stream);
+    upload_padded(c, snap.get(), snapshot, p->d, p->ld);
+    upload_padded(c, muv.get(), mu, p->d, p->ld);
+    SKR_CUDA(cudaMemcpyAsync(di.get(), idx, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c.stream));
+    run_epoch(p, snap.get(), muv.get(), di.get(), m, eta, out.get());
+    SKR_CUDA(cudaMemcpyAsync(w_avg, out.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_svrg(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double* w_out,
+             skr_epoch_record* trace, int64_t* epochs_done) {
+  return guard([&] {
+    if (!p || !cfg) raise(SKR_EPARAM, "null argument");
+    if (cfg->epochs < 1 || cfg->epoch_length < 1) raise(SKR_EPARAM, "svrg: epochs and epoch length must be >= 1");
+    if (!(cfg->step_size > 0.0)) raise(SKR_EPARAM, "svrg: step size must be positive");
+    for (int64_t j = 0; j < p->d; ++j)
+      if (!std::isfinite(w0[j])) raise(SKR_EINPUT, "svrg: start point must be finite");
+    Ctx& c = p->ctx->c;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    ensure_tables(p);
+    seed_mt(c, p->mt, cfg->seed);
+    const int64_t m = cfg->epoch_length, ld = p->ld;
+    DBuf<double> w(ld, c.stream), mu(ld, c.stream), obj(1, c.stream), u(m, c.stream);
+    DBuf<int64_t> idx(m, c.stream);
+    upload_padded(c, w.get(), w0, p->d, ld);
+    // initial objective and the first full gradient share one pass (same w)
+    problem_fullgrad(p, w.get(), mu.get(), obj.get());
+    double initial = 0.0;
+    SKR_CUDA(cudaMemcpyAsync(&initial, obj.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    *epochs_done = 0;
+    DBuf<double> wnext(ld, c.stream);
+    for (int64_t s = 1; s <= cfg->epochs; ++s) {
+      draw_indices(p, u, idx, m);
+      run_epoch(p, w.get(), mu.get(), idx.get(), m, cfg->step_size, wnext.get());
+      std::swap(w.p, wnext.p);
+      // objective at w_s; its pass also yields mu for epoch s+1 (svrg.cpp:189,196)
+      problem_fullgrad(p, w.get(), mu.get(), obj.get());
+      double ho = 0.0;
+      SKR_CUDA(cudaMemcpyAsync(&ho, obj.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      skr_epoch_record& r = trace[s - 1];
+      r.epoch = s;
+      r.objective = ho;
+      r.suboptimality = std::isnan(reference) ? std::numeric_limits<double>::quiet_NaN() : ho - reference;
+      r.elapsed_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+      *epochs_done = s;
+      if (!std::isfinite(ho) || (initial > 0.0 && ho > 1e6 * initial)) {
+        SKR_CUDA(cudaMemcpyAsync(w_out, w.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        raise(SKR_EDIVERGED, "svrg: objective diverged at epoch " + std::to_string(s));
+      }
+    }
+    SKR_CUDA(cudaMemcpyAsync(w_out, w.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out) {
+  return guard([&] {
+    if (!p) raise(SKR_EPARAM, "null problem");
+    Ctx& c = p->ctx->c;
+    ensure_tables(p);
+    DBuf<MtState> mt(1, c.stream);
+    seed_mt(c, mt, seed);
+    DBuf<double> u(std::max<int64_t>(count, 1), c.stream);
+    DBuf<int64_t> idx(std::max<int64_t>(count, 1), c.stream);
+    mt_uniforms_dev(c, mt.get(), u.get(), count);
+    if (count > 0) {
+      lower_bound_kernel<<<std::min<unsigned>(ceil_div(count, 256), 8 * c.sm_count), 256, 0, c.stream>>>(
+          p->cum.get(), p->n_global + p->d, u.get(), count, idx.get());
+      SKR_LAUNCHED(&c);
+      SKR_CUDA(cudaMemcpyAsync(out, idx.get(), sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c.stream));
+    }
+    c.sync();
+  });
+}
+
+int skr_mt_uniforms(skr_ctx* ctx, uint64_t seed, int64_t count, double* out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    DBuf<MtState> mt(1, c.stream);
+    seed_mt(c, mt, seed);
+    DBuf<double> u(std::max<int64_t>(count, 1), c.stream);
+    mt_uniforms_dev(c, mt.get(), u.get(), count);
+    if (count > 0) SKR_CUDA(cudaMemcpyAsync(out, u.get(), sizeof(double) * count, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_gaussian_matrix(skr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (rows < 1 || cols < 1) raise(SKR_EDIM, "gaussian_matrix: rows and cols must be at least 1");
+    const int64_t nu = (rows * cols + 1) / 2 * 2;
+    DBuf<MtState> mt(1, c.stream);
+    seed_mt(c, mt, seed);
+    DBuf<double> u(nu, c.stream), Pt((size_t)rows * cols, c.stream);
+    mt_uniforms_dev(c, mt.get(), u.get(), nu);
+    box_muller_kernel<<<std::min<unsigned>(ceil_div(rows * cols, 256), 65535u), 256, 0, c.stream>>>(
+        u.get(), rows, cols, 0, rows, Pt.get());
+    SKR_LAUNCHED(&c);
+    // Pt is cols x rows row-major == rows x cols column-major
+    SKR_CUDA(cudaMemcpyAsync(out, Pt.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+// ---- diagnostics ------------------------------------------------------------------
+static double ridge_objective_dev(Ctx& c, const skr_data* X, const double* y_dev, double lambda, const double* w_dev,
+                                  DBuf<double>& pg, DBuf<double>& pl, DBuf<double>& sums) {
+  const Storage& S = *X->st;
+  fullgrad_sums(c, S.dtype, S.ptr, S.ld, S.n, y_dev, w_dev, pg, pl, sums);
+  std::vector<double> hs(S.ld + 1), hw(S.ld);
+  SKR_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), sizeof(double) * (S.ld + 1), cudaMemcpyDeviceToHost, c.stream));
+  SKR_CUDA(cudaMemcpyAsync(hw.data(), w_dev, sizeof(double) * S.ld, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  double sq = 0.0;
+  for (int64_t j = 0; j < S.d; ++j) sq += hw[j] * hw[j];
+  return hs[S.ld] / (2.0 * (double)X->n_global) + 0.5 * lambda * sq;
+}
+
+int skr_ridge_objective(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* w,
+                        double* out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X) raise(SKR_EPARAM, "null data");
+    const Storage& S = *X->st;
+    DBuf<double> yd(std::max<int64_t>(S.n, 1), c.stream), wd(S.ld, c.stream), pg, pl, sums;
+    if (S.n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * S.n, cudaMemcpyHostToDevice, c.stream));
+    upload_padded(c, wd.get(), w, S.d, S.ld);
+    *out = ridge_objective_dev(c, X, yd.get(), lambda, wd.get(), pg, pl, sums);
+  });
+}
+
+// DataMatrix::gram (data_matrix.cpp:111-119) of the handle scaled by `factor`:
+// G = (scale*factor)^2 X^T X, d x ld
+static void scaled_gram_dev(Ctx& c, const skr_data* X, double factor, DBuf<double>& G) {
+  const Storage& S = *X->st;
+  const int64_t d = S.d, ld = S.ld;
+  const double s = X->scale * factor;
+  G.alloc((size_t)d * ld, c.stream);
+  G.zero();
+  DISPATCH_DTYPE(S.dtype, T, {
+    const T* Xp = static_cast<const T*>(S.ptr);
+    gemm<T, T, true, false>(&c, d, d, S.n, Xp, ld, Xp, ld, EpiStore{G.get(), ld, s * s, 0.0});
+  });
+  c.allreduce_sum(G.get(), (size_t)d * ld);
+}
+
+int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, double* w_out,
+                          double* min_out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X) raise(SKR_EPARAM, "null data");
+    if (!(lambda > 0.0)) raise(SKR_EPARAM, "ridge problem: lambda must be positive");
+    const Storage& S = *X->st;
+    const int64_t d = S.d, ld = S.ld, n = S.n;
+    DBuf<double> G;
+    scaled_gram_dev(c, X, 1.0 / std::sqrt((double)X->n_global), G);  // scaled_design(p).gram()
+    add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(G.get(), d, ld, lambda);
+    SKR_LAUNCHED(&c);
+    // rhs = X^T y / n  (bench.cpp:50-54)
+    DBuf<double> yd(std::max<int64_t>(n, 1), c.stream), rhs(ld, c.stream);
+    if (n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    rhs.zero();
+    DISPATCH_DTYPE(S.dtype, T, {
+      gemm<T, double, true, false>(&c, d, 1, n, static_cast<const T*>(S.ptr), ld, yd.get(), 1,
+                                   EpiStore{rhs.get(), 1, 1.0 / (double)X->n_global, 0.0});
+    });
+    c.allreduce_sum(rhs.get(), d);
+    // Cholesky on the device (bench.cpp:22-48)
+    DBuf<double> Gd((size_t)d * d, c.stream);
+    compact_kernel<<<ceil_div(d * d, 256), 256, 0, c.stream>>>(G.get(), d, ld, Gd.get());
+    SKR_LAUNCHED(&c);
+    G.release();
+    int lwork = 0;
+    SKR_SOLVER(cusolverDnDpotrf_bufferSize(c.solver, CUBLAS_FILL_MODE_LOWER, (int)d, Gd.get(), (int)d, &lwork));
+    DBuf<double> work(std::max(lwork, 1), c.stream);
+    DBuf<int> info(1, c.stream);
+    SKR_SOLVER(cusolverDnDpotrf(c.solver, CUBLAS_FILL_MODE_LOWER, (int)d, Gd.get(), (int)d, work.get(), lwork,
+                                info.get()));
+    SKR_SOLVER(cusolverDnDpotrs(c.solver, CUBLAS_FILL_MODE_LOWER, (int)d, 1, Gd.get(), (int)d, rhs.get(), (int)d,
+                                info.get()));
+    int hinfo = 0;
+    SKR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hinfo != 0) raise(SKR_EINPUT, "cholesky: matrix not positive definite");
+    SKR_CUDA(cudaMemsetAsync(rhs.get() + d, 0, sizeof(double) * (ld - d), c.stream));
+    DBuf<double> pg, pl, sums;
+    *min_out = ridge_objective_dev(c, X, yd.get(), lambda, rhs.get(), pg, pl, sums);
+    SKR_CUDA(cudaMemcpyAsync(w_out, rhs.get(), sizeof(double) * d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+
+int skr_conditioned_cond(skr_ctx* ctx, const skr_data* X, double lambda, const double* U, const double* sigma,
+                         int64_t k, double* out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X) raise(SKR_EPARAM, "null data");
+    if (!(lambda > 0.0)) raise(SKR_EPARAM, "preconditioner: lambda must be positive");
+    const Storage& S = *X->st;
+    const int64_t d = S.d, ld = S.ld;
+    DBuf<double> G;
+    scaled_gram_dev(c, X, 1.0, G);  // data.gram() of the (scaled) handle passed in
+    add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(G.get(), d, ld, lambda);
+    SKR_LAUNCHED(&c);
+    // B = P^{-1/2} (d x ld)
+    std::vector<double> D(std::max<int64_t>(k, 1), 1.0);
+    double cc = 1.0;
+    for (int64_t j = 0; j < k; ++j) D[j] = 1.0 / std::sqrt(sigma[j] * sigma[j] + lambda);
+    if (k > 0) cc = D[k - 1];
+    DBuf<double> B((size_t)d * ld, c.stream), Dd(D.size(), c.stream);
+    B.zero();
+    SKR_CUDA(cudaMemcpyAsync(Dd.get(), D.data(), sizeof(double) * D.size(), cudaMemcpyHostToDevice, c.stream));
+    if (k > 0) {
+      DBuf<double> Ut((size_t)k * ld, c.stream), Us((size_t)k * ld, c.stream);
+      upload_rows(c, Ut.get(), U, k, d, ld);
+      SKR_CUDA(cudaMemcpyAsync(Us.get(), Ut.get(), sizeof(double) * k * ld, cudaMemcpyDeviceToDevice, c.stream));
+      scale_rows_kernel<<<std::min<unsigned>(ceil_div(k * ld, 256), 65535u), 256, 0, c.stream>>>(Us.get(), k, ld,
+                                                                                                 Dd.get(), cc);
+      SKR_LAUNCHED(&c);
+      gemm<double, double, true, false>(&c, d, d, k, Us.get(), ld, Ut.get(), ld, EpiBmat{B.get(), ld, cc}, 1);
+    } else {
+      add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(B.get(), d, ld, 1.0);
+      SKR_LAUNCHED(&c);
+    }
+    // M = B (G + lambda I) B  (precond.cpp:174-194), symmetrised
+    DBuf<double> H((size_t)d * ld, c.stream), M((size_t)d * ld, c.stream);
+    H.zero();
+    M.zero();
+    gemm<double, double, false, false>(&c, d, d, d, B.get(), ld, G.get(), ld, EpiStore{H.get(), ld, 1.0, 0.0}, 1);
+    gemm<double, double, false, false>(&c, d, d, d, H.get(), ld, B.get(), ld, EpiStore{M.get(), ld, 1.0, 0.0}, 1);
+    symmetrize_kernel<<<ceil_div(d * d, 256), 256, 0, c.stream>>>(M.get(), d, ld);
+    SKR_LAUNCHED(&c);
+    DBuf<double> tr(1, c.stream), Md((size_t)d * d, c.stream), ev(d, c.stream);
+    trace_kernel<<<1, 1024, 0, c.stream>>>(M.get(), d, ld, tr.get());
+    SKR_LAUNCHED(&c);
+    compact_kernel<<<ceil_div(d * d, 256), 256, 0, c.stream>>>(M.get(), d, ld, Md.get());
+    SKR_LAUNCHED(&c);
+    int lwork = 0;
+    SKR_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)d,
+                                           Md.get(), (int)d, ev.get(), &lwork));
+    DBuf<double> work(std::max(lwork, 1), c.stream);
+    DBuf<int> info(1, c.stream);
+    SKR_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, Md.get(),
+                                (int)d, ev.get(), work.get(), lwork, info.get()));
+    double htr = 0.0, hmin = 0.0;
+    int hinfo = 0;
+    SKR_CUDA(cudaMemcpyAsync(&htr, tr.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(&hmin, ev.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hinfo != 0) raise(SKR_EINTERNAL, "sym_eigs: eigensolver did not converge");
+    *out = htr / hmin;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// Shared runtime pieces: status/exception plumbing, the context, device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/skr.h"
+
+namespace skr {
+
+// Internal exceptions carry an skr_status; the C-ABI layer converts them.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define SKR_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      ::skr::raise(e_ == cudaErrorMemoryAllocation ? SKR_ENOMEM : SKR_ECUDA,            \
+                   std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+#define SKR_SOLVER(call)                                                                \
+  do {                                                                                  \
+    cusolverStatus_t s_ = (call);                                                       \
+    if (s_ != CUSOLVER_STATUS_SUCCESS)                                                  \
+      ::skr::raise(SKR_ECUDA, std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
+  } while (0)
+
+#define SKR_NCCL(call)                                                                  \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      ::skr::raise(SKR_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+// Check the last launch and count it (gpu_launches evidence in bench.py).
+#define SKR_LAUNCHED(ctx)                                                               \
+  do {                                                                                  \
+    SKR_CUDA(cudaGetLastError());                                                       \
+    (ctx)->launches++;                                                                  \
+  } while (0)
+
+// Device buffer with RAII; allocation through the stream-ordered pool.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) SKR_CUDA(cudaMallocAsync(&p, count * sizeof(T), stream));
+  }
+  void zero() {
+    if (n) SKR_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+struct Ctx {
+  int device = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  ncclComm_t comm = nullptr;
+  int sm_count = 148;
+  int64_t launches = 0;
+
+  // Row-sharded collectives (no-ops on one GPU).  Sum of doubles in place.
+  void allreduce_sum(double* buf, size_t count) {
+    if (world > 1 && count) SKR_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+  }
+  void allreduce_max(double* buf, size_t count) {
+    if (world > 1 && count) SKR_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, comm, stream));
+  }
+  void allgather_bytes(const void* send, void* recv, size_t bytes_per_rank) {
+    if (world > 1) SKR_NCCL(ncclAllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
+  }
+  void sync() { SKR_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+inline size_t dtype_size(int dtype) { return dtype == SKR_F32 ? 4 : 8; }
+
+// Device row stride: rows padded to 16 elements so every row starts on a
+// 64 B (fp32) / 128 B (fp64) boundary and vector loads never straddle rows.
+inline int64_t padded_ld(int64_t d) { return (d + 15) / 16 * 16; }
+
+inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace skr

@@ -1,0 +1,248 @@
+// K8 — sampling tables and the index stream; K10 — the sequential SVRG inner loop.
+//
+// Reference: svrg_solve + DenseEpochState (svrg.cpp:18-54, :90-211) over the
+// (n+d)-component preconditioned ridge (ridge.cpp:238-278).  Device layout is
+// the stacked-row form R = [X~ ; B]: component i < n is
+// data row x~_i with coefficient (n+d)/n and label y_i; component n+j is row j
+// of B = P^{-1/2} (materialised, symmetric) with coefficient lambda(n+d) and
+// label 0.  Every step is then "one row, two dots, one axpy".
+#pragma once
+
+#include "common.cuh"
+
+namespace skr {
+
+// make_cumulative_weights (svrg.cpp:90-106) bit-exactly: the sequential fp64
+// sum and running prefix in index order (one thread; a parallel scan would
+// reassociate and could flip indices at table boundaries).  Also writes
+// total to *total_out.
+__global__ void cumulative_kernel(const double* __restrict__ beta, int64_t N,
+                                  double* __restrict__ cum, double* __restrict__ total_out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double total = 0.0;
+  for (int64_t i = 0; i < N; ++i) total = __dadd_rn(total, beta[i]);
+  double run = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    run = __dadd_rn(run, __ddiv_rn(beta[i], total));
+    cum[i] = run;
+  }
+  cum[N - 1] = 1.0;
+  *total_out = total;
+}
+
+// inv_nq_i = total / (N * beta_i)  (svrg.cpp:167-172)
+__global__ void inv_nq_kernel(const double* __restrict__ beta, int64_t N,
+                              const double* __restrict__ total, double* __restrict__ inv_nq) {
+  const double t = *total;
+  const double Nd = (double)N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv_nq[i] = __ddiv_rn(t, __dmul_rn(Nd, beta[i]));
+}
+
+// lookup_index (svrg.cpp:122-126): std::lower_bound, clamped to N-1.
+__global__ void lower_bound_kernel(const double* __restrict__ cum, int64_t N,
+                                   const double* __restrict__ u, int64_t count,
+                                   int64_t* __restrict__ idx) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double x = u[t];
+    int64_t lo = 0, len = N;
+    while (len > 0) {
+      const int64_t half = len >> 1;
+      if (cum[lo + half] < x) {
+        lo += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    idx[t] = lo == N ? N - 1 : lo;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K10: one epoch of the inner loop in ONE persistent CTA.
+//
+// Thread t owns columns [t*VEC, t*VEC+VEC) of w, the snapshot, mu and the
+// running sum, all in registers.  The epoch's indices are known in advance,
+// so rows are prefetched DEPTH steps ahead with cp.async into a per-thread
+// shared-memory ring (each thread copies and later reads only its own
+// columns, so the ring needs no barrier); per-step scalars (index, inv_nq,
+// label) are gathered in chunks.  Per step: two dots (w, snapshot) -> one
+// block reduction (shuffles + one __syncthreads) -> the update
+//   dir = (g(w) - g(snap)) * inv_nq + mu,  w -= eta * dir,  sum += w
+// (svrg.cpp:37-43, :142-150).
+constexpr int K10_DEPTH = 8;
+constexpr int K10_CHUNK = 512;
+
+__device__ __forceinline__ void cp_async_bytes16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_bytes8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_bytes4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_span(void* smem, const void* gmem) {
+  if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 16; ++c)
+      cp_async_bytes16(static_cast<char*>(smem) + 16 * c, static_cast<const char*>(gmem) + 16 * c);
+  } else if constexpr (BYTES % 8 == 0) {
+#pragma unroll
+    for (int c = 0; c < BYTES / 8; ++c)
+      cp_async_bytes8(static_cast<char*>(smem) + 8 * c, static_cast<const char*>(gmem) + 8 * c);
+  } else {
+#pragma unroll
+    for (int c = 0; c < BYTES / 4; ++c)
+      cp_async_bytes4(static_cast<char*>(smem) + 4 * c, static_cast<const char*>(gmem) + 4 * c);
+  }
+}
+
+struct EpochArgs {
+  const void* Xt;            // n_total x ld rows of dtype T (data components)
+  const double* B;           // d x ld rows (regulariser components)
+  int64_t ld, n, N;
+  const double* y;           // n labels
+  const double* inv_nq;      // N
+  double data_coef, reg_coef;
+  const int64_t* idx;        // m indices
+  int64_t m;
+  double eta;
+  const double* snapshot;    // ld
+  const double* mu;          // ld
+  double* w_avg;             // ld
+};
+
+template <class T, int VEC, int NT>
+__global__ void __launch_bounds__(NT, 1) svrg_epoch_kernel(EpochArgs a) {
+  constexpr int NW = NT / 32;
+  constexpr int SLOT = NT * VEC;  // doubles per ring slot (fits an fp64 B row)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);                      // DEPTH * SLOT
+  int64_t* s_idx = reinterpret_cast<int64_t*>(ring + K10_DEPTH * SLOT);     // CHUNK + DEPTH
+  double* s_q = reinterpret_cast<double*>(s_idx + K10_CHUNK + K10_DEPTH);  // CHUNK
+  double* s_y = s_q + K10_CHUNK;                                            // CHUNK
+  __shared__ double2 red[2][NW];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)tid * VEC;
+  const bool active = c0 < a.ld;
+  const T* Xt = static_cast<const T*>(a.Xt);
+
+  double w[VEC], ws[VEC], mu[VEC], sum[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    ws[v] = active ? a.snapshot[c0 + v] : 0.0;
+    w[v] = ws[v];
+    mu[v] = active ? a.mu[c0 + v] : 0.0;
+    sum[v] = 0.0;
+  }
+
+  auto issue = [&](int64_t step, int64_t i) {  // prefetch row of component i into slot
+    double* slot = ring + (step % K10_DEPTH) * SLOT + (int64_t)tid * VEC;
+    if (active) {
+      if (i < a.n) cp_async_span<VEC * (int)sizeof(T)>(slot, Xt + i * a.ld + c0);
+      else cp_async_span<VEC * 8>(slot, a.B + (i - a.n) * a.ld + c0);
+    }
+    cp_async_commit();
+  };
+  auto load_chunk = [&](int64_t t0) {  // indices [t0, t0+CHUNK+DEPTH), scalars [t0, t0+CHUNK)
+    __syncthreads();
+    for (int e = tid; e < K10_CHUNK + K10_DEPTH; e += NT) {
+      const int64_t t = t0 + e;
+      s_idx[e] = t < a.m ? a.idx[t] : 0;
+    }
+    __syncthreads();
+    for (int e = tid; e < K10_CHUNK; e += NT) {
+      const int64_t i = s_idx[e];
+      s_q[e] = a.inv_nq[i];
+      s_y[e] = i < a.n ? a.y[i] : 0.0;
+    }
+    __syncthreads();
+  };
+
+  load_chunk(0);
+  for (int s = 0; s < K10_DEPTH; ++s) {
+    if (s < a.m) issue(s, s_idx[s]);
+    else cp_async_commit();
+  }
+  int par = 0;
+  for (int64_t t = 0; t < a.m; ++t) {
+    const int e = (int)(t % K10_CHUNK);
+    if (e == 0 && t > 0) load_chunk(t);
+    const int64_t i = s_idx[e];
+    cp_async_wait<K10_DEPTH - 1>();  // this thread's copy for step t has landed
+    const double* slot = ring + (t % K10_DEPTH) * SLOT + (int64_t)tid * VEC;
+    double x[VEC];
+    if (i < a.n) {
+      const T* xs = reinterpret_cast<const T*>(slot);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) x[v] = active ? (double)xs[v] : 0.0;
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) x[v] = active ? slot[v] : 0.0;
+    }
+    double p1 = 0.0, p2 = 0.0;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      p1 = fma(x[v], w[v], p1);
+      p2 = fma(x[v], ws[v], p2);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      p1 += __shfl_xor_sync(0xffffffffu, p1, off);
+      p2 += __shfl_xor_sync(0xffffffffu, p2, off);
+    }
+    if (lane == 0) red[par][warp] = make_double2(p1, p2);
+    // refill the ring slot consumed DEPTH steps from now (slot of step t is
+    // reused for step t+DEPTH; this thread has already read its part into x[])
+    {
+      const int64_t tn = t + K10_DEPTH;
+      if (tn < a.m) issue(tn, s_idx[e + K10_DEPTH]);
+      else cp_async_commit();
+    }
+    __syncthreads();
+    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      const double2 r = red[par][q];
+      d1 += r.x;
+      d2 += r.y;
+    }
+    par ^= 1;
+    const double coef = i < a.n ? a.data_coef : a.reg_coef;
+    const double yi = s_y[e];
+    const double q = s_q[e];
+    const double g1 = coef * (d1 - yi), g2 = coef * (d2 - yi);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const double dir = (g1 * x[v] - g2 * x[v]) * q + mu[v];
+      w[v] = fma(-a.eta, dir, w[v]);
+      sum[v] += w[v];
+    }
+  }
+  cp_async_wait<0>();
+  if (active) {
+    const double inv_m = 1.0 / (double)a.m;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) a.w_avg[c0 + v] = sum[v] * inv_m;
+  }
+}
+
+template <class T, int VEC, int NT>
+size_t svrg_epoch_smem() {
+  return (size_t)K10_DEPTH * NT * VEC * 8 + (K10_CHUNK + K10_DEPTH) * 8 + 2 * K10_CHUNK * 8;
+}
+
+}  // namespace skr

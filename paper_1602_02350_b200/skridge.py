@@ -1,0 +1,662 @@
+"""Python mirror of the reference's public C++ interface for the hot path.
+
+Names, argument meaning and error behaviour follow proj/include/skridge/
+(sketch.hpp, precond.hpp, svrg.hpp, ridge.hpp, bench.hpp); every call runs on
+the B200 through the C-ABI in include/skr.h.  There is no CPU fallback: the
+CUDA library must load or the first call raises.
+
+Orientation: data is handed over as an (n, d) row-major array — byte-identical
+to the reference's d x n column-major DenseMatrix — and factors come back as
+(d, k) arrays whose column j is basis vector j (``left[:, j]``), as in
+SketchedSvd::left.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import EpochRecordC, SvrgConfigC, SynthSpecC, f64, i64, cint, vp
+
+# ---------------------------------------------------------------------------
+# errors.hpp:10-60, svrg.hpp:27-35 (+ DeviceError for CUDA/NCCL failures)
+
+
+class SkridgeError(Exception):
+    pass
+
+
+class DimensionError(SkridgeError, ValueError):
+    pass
+
+
+class ParameterError(SkridgeError, ValueError):
+    pass
+
+
+class InputError(SkridgeError, ValueError):
+    pass
+
+
+class EmptyBasisError(SkridgeError, ValueError):
+    pass
+
+
+class ScaleGuardError(SkridgeError, RuntimeError):
+    pass
+
+
+class DeviceError(SkridgeError, RuntimeError):
+    pass
+
+
+class DivergenceError(SkridgeError, RuntimeError):
+    def __init__(self, what: str, trace: list):
+        super().__init__(what)
+        self.trace = trace
+
+
+_ERR = {1: DimensionError, 2: ParameterError, 3: InputError, 4: ScaleGuardError, 6: DeviceError,
+        7: DeviceError, 8: EmptyBasisError, 9: DeviceError, 10: DeviceError}
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = _lib.last_error()
+        raise _ERR.get(rc, DeviceError)(msg)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One per process and GPU (the C-ABI's skr_ctx)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        lib = _lib.load()
+        h = vp()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ParameterError("distributed context needs the 128-byte NCCL id")
+            _check(lib.skr_ctx_create_dist(device, rank, world, nccl_id, C.byref(h)))
+        else:
+            _check(lib.skr_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.load().skr_nccl_unique_id(buf))
+        return buf.raw
+
+    def synchronize(self):
+        _check(_lib.load().skr_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        return _lib.load().skr_ctx_stream(self.h) or 0
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.load().skr_ctx_kernel_launches(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.load().skr_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ---------------------------------------------------------------------------
+class DataMatrix:
+    """DataMatrix (data_matrix.hpp:18-61): immutable device storage + uniform scale.
+
+    ``rows()`` is the dimension d and ``cols()`` the point count n, as in the
+    reference (points are its columns).
+    """
+
+    def __init__(self, x=None, scale: float = 1.0, ctx: Context | None = None, _handle=None,
+                 _owner=None):
+        self.ctx = ctx or default_context()
+        self._owner = _owner
+        if _handle is not None:
+            self.h = _handle
+        else:
+            x = np.asarray(x)
+            if x.ndim != 2:
+                raise DimensionError("data matrix: expected an (n, d) array")
+            if x.dtype == np.float32:
+                dt, arr = 1, np.ascontiguousarray(x)
+            else:
+                dt, arr = 0, _f64(x)
+            if not np.all(np.isfinite(arr)):
+                raise InputError("data matrix: entries must be finite")
+            h = vp()
+            _check(_lib.load().skr_data_create(self.ctx.h, arr.ctypes.data, arr.shape[0], arr.shape[1],
+                                               dt, C.byref(h)))
+            self.h = h
+            if scale != 1.0:
+                h2 = vp()
+                _check(_lib.load().skr_data_scaled(self.h, float(scale), C.byref(h2)))
+                _lib.load().skr_data_destroy(self.h)
+                self.h = h2
+        n, d, dt, sc, ng, r0 = i64(), i64(), cint(), f64(), i64(), i64()
+        _check(_lib.load().skr_data_info(self.h, C.byref(n), C.byref(d), C.byref(dt), C.byref(sc),
+                                         C.byref(ng), C.byref(r0)))
+        self.n_local, self.d, self.dtype = n.value, d.value, dt.value
+        self._scale, self.n_global, self.row0 = sc.value, ng.value, r0.value
+
+    @classmethod
+    def generate(cls, spec: "SynthSpec", ctx: Context | None = None) -> "DataMatrix":
+        ctx = ctx or default_context()
+        c = SynthSpecC(spec.n, spec.d, 1 if spec.dtype == "f32" else 0, spec.seed, spec.spectrum,
+                       spec.spectrum_param, int(spec.t_scale), spec.tau)
+        h = vp()
+        _check(_lib.load().skr_data_generate(ctx.h, C.byref(c), C.byref(h)))
+        return cls(ctx=ctx, _handle=h)
+
+    def rows(self) -> int:
+        return self.d
+
+    def cols(self) -> int:
+        return self.n_global
+
+    def scale(self) -> float:
+        return self._scale
+
+    def scaled(self, factor: float) -> "DataMatrix":
+        h = vp()
+        _check(_lib.load().skr_data_scaled(self.h, float(factor), C.byref(h)))
+        return DataMatrix(ctx=self.ctx, _handle=h, _owner=self)
+
+    def download(self) -> np.ndarray:
+        out = np.empty((self.n_local, self.d), dtype=np.float32 if self.dtype == 1 else np.float64)
+        _check(_lib.load().skr_data_download(self.h, out.ctypes.data))
+        return out
+
+    def labels(self) -> np.ndarray:
+        out = np.empty(self.n_local)
+        _check(_lib.load().skr_data_labels(self.h, out))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                _lib.load().skr_data_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+
+@dataclass
+class SynthSpec:
+    n: int
+    d: int
+    dtype: str = "f64"
+    seed: int = 0
+    spectrum: int = 0          # 0: 1/j, 1: r^j, 2: j^-p, 3: 1/j (j<=50), 0.02/j beyond
+    spectrum_param: float = 0.0
+    t_scale: bool = False
+    tau: float = 0.1
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class RidgeProblem:
+    """RidgeProblem (ridge.hpp:17-27)."""
+    data: DataMatrix
+    labels: np.ndarray
+    lam: float
+
+    def __post_init__(self):
+        self.labels = _f64(self.labels)
+        if len(self.labels) != self.data.n_local:
+            raise DimensionError("ridge problem: label count must equal point count")
+        if not (self.lam > 0.0):
+            raise ParameterError("ridge problem: lambda must be positive")
+
+    def dim(self) -> int:
+        return self.data.d
+
+    def count(self) -> int:
+        return self.data.n_global
+
+
+def scaled_design(p: RidgeProblem) -> DataMatrix:
+    """ridge.cpp:54-56: the data scaled by 1/sqrt(n), storage shared."""
+    return p.data.scaled(1.0 / math.sqrt(p.count()))
+
+
+def objective(p: RidgeProblem, w) -> float:
+    """ridge.cpp:33-43 on the device."""
+    w = _f64(w)
+    if len(w) != p.dim():
+        raise DimensionError("objective: vector length mismatch")
+    out = f64()
+    _check(_lib.load().skr_ridge_objective(p.data.ctx.h, p.data.h, p.labels, p.lam, w, C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class LanczosConfig:
+    """sketch.hpp:27-32."""
+    k: int = 0
+    eps_prime: float = 0.5
+    seed: int = 0
+    q_override: Optional[int] = None
+
+
+@dataclass
+class SketchedSvd:
+    """sketch.hpp:18-25.  left is (d, k); right is (n_local, k) or None."""
+    left: np.ndarray
+    singular_values: np.ndarray
+    right: Optional[np.ndarray]
+    k: int
+    q: int
+    rank_reduced: bool = False
+
+
+def lanczos_iterations(n: int, eps_prime: float) -> int:
+    """sketch.cpp:13-16."""
+    return max(2, int(math.ceil(math.log(n) / math.sqrt(eps_prime))))
+
+
+def block_lanczos(a: DataMatrix, cfg: LanczosConfig, want_right: bool = True) -> SketchedSvd:
+    """sketch.cpp:41-90 on the device (Pi from the reference's mt19937_64 stream)."""
+    k, d, n = int(cfg.k), a.d, a.n_local
+    U = np.zeros(d * max(k, 1))
+    sig = np.zeros(max(k, 1))
+    V = np.zeros(n * max(k, 1)) if want_right else None
+    ku, qu, rr = i64(), i64(), cint()
+    q = int(cfg.q_override) if cfg.q_override else 0
+    _check(_lib.load().skr_lanczos(a.ctx.h, a.h, k, q, float(cfg.eps_prime), int(cfg.seed), U, sig,
+                                   V.ctypes.data if V is not None else None, C.byref(ku), C.byref(qu),
+                                   C.byref(rr)))
+    kk = ku.value
+    left = U[: d * kk].reshape(kk, d).T
+    right = V[: n * kk].reshape(kk, n).T if V is not None else None
+    return SketchedSvd(left, sig[:kk].copy(), right, kk, qu.value, bool(rr.value))
+
+
+# ---------------------------------------------------------------------------
+class PreconditionerKind(Enum):
+    Sketched = 0
+    Exact = 1
+    Identity = 2
+
+
+class Preconditioner:
+    """precond.hpp:28-67: P^{-1/2} v = c v + U (diag(inv_sqrt) - c) U^T v (a host value type)."""
+
+    def __init__(self, kind, dim, basis, inv_sqrt, tail, lam):
+        self._kind, self._dim, self._basis = kind, dim, basis
+        self._inv_sqrt, self._tail, self._lambda = inv_sqrt, tail, lam
+
+    @staticmethod
+    def identity(dim: int, lam: float) -> "Preconditioner":
+        _check_lambda(lam)
+        return Preconditioner(PreconditionerKind.Identity, dim, np.zeros((dim, 0)), np.zeros(0), 1.0, lam)
+
+    def kind(self):
+        return self._kind
+
+    def dim(self) -> int:
+        return self._dim
+
+    def rank(self) -> int:
+        return len(self._inv_sqrt)
+
+    def lam(self) -> float:
+        return self._lambda
+
+    def tail_coeff(self) -> float:
+        return self._tail
+
+    def inv_sqrt_diag(self) -> np.ndarray:
+        return self._inv_sqrt
+
+    def basis(self) -> np.ndarray:
+        return self._basis
+
+    def min_inv_eigenvalue(self) -> float:
+        lead = self._inv_sqrt[0] if self.rank() else self._tail
+        return lead * lead
+
+    def singular_values(self) -> np.ndarray:
+        """sigma~ recovered from the coefficients (what the C-ABI takes)."""
+        return self._sigma
+
+
+def _check_lambda(lam):
+    if not (lam > 0.0) or not math.isfinite(lam):
+        raise ParameterError("preconditioner: lambda must be positive")
+
+
+def build_sketched(sv: SketchedSvd, lam: float) -> Preconditioner:
+    """precond.cpp:120-136 (+ validate, :34-49)."""
+    _check_lambda(lam)
+    if sv.k < 1:
+        raise ParameterError("build_sketched: factors must have rank >= 1")
+    s = np.asarray(sv.singular_values[: sv.k], dtype=np.float64)
+    inv = 1.0 / np.sqrt(s * s + lam)
+    cap = 1.0 / math.sqrt(lam) * (1.0 + 1e-12)
+    if np.any(~(inv > 0.0)) or np.any(inv > cap):
+        raise InputError("preconditioner: coefficient out of range")
+    if np.any(np.diff(inv) < 0):
+        raise InputError("preconditioner: coefficients must be non-decreasing")
+    p = Preconditioner(PreconditionerKind.Sketched, sv.left.shape[0], np.asarray(sv.left), inv,
+                       float(inv[-1]), lam)
+    p._sigma = s
+    return p
+
+
+class ApplyMode(Enum):
+    Dense = 0
+    Lazy = 1
+    Auto = 2
+
+
+kDenseModeMaxEntries = 200_000_000  # ridge.hpp:65 (the GPU has no lazy path)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class SvrgConfig:
+    """svrg.hpp:39-45."""
+    epochs: int = 1
+    epoch_length: int = 1
+    step_size: float = 0.1
+    seed: int = 0
+
+
+@dataclass
+class EpochRecord:
+    """svrg.hpp:16-21."""
+    epoch: int
+    objective: float
+    suboptimality: Optional[float]
+    elapsed_ms: float
+
+
+@dataclass
+class SvrgResult:
+    iterate: np.ndarray
+    trace: list
+
+
+class GpuEpochState:
+    """EpochState (svrg.hpp:53-62) for an external engine: step() only records
+    (index, inv_nq); epoch_average() runs the whole epoch as one K10 launch."""
+
+    def __init__(self, p: "PreconditionedRidge"):
+        self.p = p
+        self._idx: list[int] = []
+
+    def begin_epoch(self, snapshot, full_grad):
+        self._snap, self._mu = _f64(snapshot), _f64(full_grad)
+        self._idx = []
+
+    def step(self, index: int, eta: float, inv_nq: float = 0.0):
+        self._eta = eta
+        self._idx.append(int(index))
+
+    def epoch_average(self) -> np.ndarray:
+        out = np.empty(self.p.d)
+        idx = np.asarray(self._idx, dtype=np.int64)
+        _check(_lib.load().skr_epoch(self.p.h, self._snap, self._mu, idx, len(idx), float(self._eta), out))
+        return out
+
+
+class PreconditionedRidge:
+    """PreconditionedRidge (ridge.hpp:78-119) — the FiniteSumProblem plugin on the B200.
+
+    Dense mode only: X~ is materialised in HBM (180 GB holds every BASELINE
+    config), so the reference's Lazy mode (ridge.cpp:283-400) has no GPU
+    counterpart; mode() reports Dense.
+    """
+
+    def __init__(self, p: RidgeProblem, precond: Preconditioner, mode: ApplyMode = ApplyMode.Auto):
+        if precond.dim() != p.dim():
+            raise DimensionError("preconditioned components: dimension mismatch")
+        self.problem_ = p
+        self.precond_ = precond
+        k = precond.rank()
+        self.k = k
+        U = np.ascontiguousarray(np.asarray(precond.basis()).T) if k else None  # (k, d): row j = u_j
+        sig = _f64(precond._sigma) if k else None
+        h = vp()
+        _check(_lib.load().skr_problem_create(p.data.ctx.h, p.data.h, p.labels, float(p.lam),
+                                              U.ctypes.data if k else None,
+                                              sig.ctypes.data if k else None, k, C.byref(h)))
+        self.h = h
+        n, d, kk, a, b, m = i64(), i64(), i64(), f64(), f64(), f64()
+        _check(_lib.load().skr_problem_info(self.h, C.byref(n), C.byref(d), C.byref(kk), C.byref(a),
+                                            C.byref(b), C.byref(m)))
+        self.n, self.d = n.value, d.value
+        self._alpha, self._beta_hat, self._max_row_sq = a.value, b.value, m.value
+        self._betas = None
+
+    # FiniteSumProblem (svrg.hpp:67-80)
+    def component_count(self) -> int:
+        return self.n + self.d
+
+    def dimension(self) -> int:
+        return self.d
+
+    def betas(self) -> np.ndarray:
+        if self._betas is None:
+            out = np.empty(self.n + self.d)
+            _check(_lib.load().skr_problem_betas(self.h, out))
+            self._betas = out
+        return self._betas
+
+    def strong_convexity(self) -> float:
+        return self._alpha
+
+    def objective(self, w) -> float:
+        out = f64()
+        _check(_lib.load().skr_objective(self.h, _f64(w), C.byref(out)))
+        return out.value
+
+    def full_gradient(self, w, with_objective: bool = False):
+        mu = np.empty(self.d)
+        obj = f64()
+        _check(_lib.load().skr_full_gradient(self.h, _f64(w), mu, C.byref(obj) if with_objective else None))
+        return (mu, obj.value) if with_objective else mu
+
+    def component_gradient(self, i: int, w) -> np.ndarray:
+        out = np.empty(self.d)
+        _check(_lib.load().skr_component_gradient(self.h, int(i), _f64(w), out))
+        return out
+
+    def make_epoch_state(self) -> GpuEpochState:
+        return GpuEpochState(self)
+
+    # PreconditionedRidge extras
+    def mode(self) -> ApplyMode:
+        return ApplyMode.Dense
+
+    def preconditioner(self) -> Preconditioner:
+        return self.precond_
+
+    def problem(self) -> RidgeProblem:
+        return self.problem_
+
+    def max_row_sq(self) -> float:
+        """max_i ||x~_i||^2 over the data rows (the BASELINE step-size rule)."""
+        return self._max_row_sq
+
+    def mean_beta(self) -> float:
+        return self._beta_hat
+
+    def apply_inv_sqrt(self, v) -> np.ndarray:
+        out = np.empty(self.d)
+        _check(_lib.load().skr_apply_inv_sqrt(self.h, _f64(v), out))
+        return out
+
+    def transformed(self) -> np.ndarray:
+        out = np.empty((self.problem_.data.n_local, self.d),
+                       dtype=np.float32 if self.problem_.data.dtype == 1 else np.float64)
+        _check(_lib.load().skr_problem_transformed(self.h, out.ctypes.data))
+        return out
+
+    def index_stream(self, seed: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.int64)
+        _check(_lib.load().skr_index_stream(self.h, int(seed), int(count), out))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                _lib.load().skr_problem_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+
+def preconditioned_components(p: RidgeProblem, precond: Preconditioner,
+                              mode: ApplyMode = ApplyMode.Auto) -> PreconditionedRidge:
+    """ridge.hpp:121-123."""
+    return PreconditionedRidge(p, precond, mode)
+
+
+def mean_beta(p: PreconditionedRidge) -> float:
+    """svrg.cpp:213-217."""
+    return p.mean_beta()
+
+
+def svrg_solve(p: PreconditionedRidge, cfg: SvrgConfig, w0=None,
+               reference_value: Optional[float] = None) -> SvrgResult:
+    """svrg.cpp:152-211 — GPU-native: the index stream is the reference's
+    NormalSampler(cfg.seed) stream, drawn on the device."""
+    w0 = np.zeros(p.d) if w0 is None else _f64(w0)
+    if len(w0) != p.d:
+        raise DimensionError("svrg: start point length mismatch")
+    c = SvrgConfigC(int(cfg.epochs), int(cfg.epoch_length), float(cfg.step_size), int(cfg.seed))
+    tr = (EpochRecordC * max(1, int(cfg.epochs)))()
+    w = np.empty(p.d)
+    done = i64()
+    ref = float("nan") if reference_value is None else float(reference_value)
+    rc = _lib.load().skr_svrg(p.h, C.byref(c), w0, ref, w, tr, C.byref(done))
+    trace = [EpochRecord(int(r.epoch), float(r.objective),
+                         None if math.isnan(r.suboptimality) else float(r.suboptimality),
+                         float(r.elapsed_ms)) for r in tr[: done.value]]
+    if rc == 5:
+        raise DivergenceError(_lib.last_error(), trace)
+    _check(rc)
+    return SvrgResult(w, trace)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class SketchedSolveDiagnostics:
+    """ridge.hpp:125-136."""
+    singular_values: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    k_used: int = 0
+    q_used: int = 0
+    rank_reduced: bool = False
+    mode: ApplyMode = ApplyMode.Dense
+    beta_hat: float = 0.0
+    sketch_ms: float = 0.0
+    precompute_ms: float = 0.0
+    solve_ms: float = 0.0
+    max_projection_drift: float = 0.0
+
+
+@dataclass
+class SketchedSolveResult:
+    iterate: np.ndarray
+    trace: list
+    diagnostics: SketchedSolveDiagnostics
+
+
+def sketched_preconditioned_svrg(p: RidgeProblem, k: int, cfg: SvrgConfig, sketch_seed: int,
+                                 mode: ApplyMode = ApplyMode.Auto,
+                                 reference_value: Optional[float] = None,
+                                 q_override: Optional[int] = None) -> SketchedSolveResult:
+    """ridge.cpp:413-454.  q_override lets the BASELINE configs fix q (the
+    reference's pipeline hard-codes eps' = 0.5)."""
+    if k < 1 or k > min(p.dim(), p.count()):
+        raise ParameterError("sketched svrg: k must satisfy 1 <= k <= min(d, n)")
+    diag = SketchedSolveDiagnostics()
+    t0 = time.perf_counter()
+    sv = block_lanczos(scaled_design(p), LanczosConfig(k, 0.5, sketch_seed, q_override), want_right=False)
+    diag.sketch_ms = (time.perf_counter() - t0) * 1e3
+    diag.singular_values, diag.k_used, diag.q_used, diag.rank_reduced = sv.singular_values, sv.k, sv.q, sv.rank_reduced
+    t0 = time.perf_counter()
+    pc = build_sketched(sv, p.lam)
+    comp = preconditioned_components(p, pc, mode)
+    diag.precompute_ms = (time.perf_counter() - t0) * 1e3
+    diag.mode = comp.mode()
+    diag.beta_hat = comp.mean_beta()
+    t0 = time.perf_counter()
+    res = svrg_solve(comp, cfg, np.zeros(p.dim()), reference_value)
+    diag.solve_ms = (time.perf_counter() - t0) * 1e3
+    return SketchedSolveResult(comp.apply_inv_sqrt(res.iterate), res.trace, diag)
+
+
+@dataclass
+class ReferenceSolution:
+    minimizer: np.ndarray
+    minimum: float
+
+
+def reference_minimum(p: RidgeProblem) -> ReferenceSolution:
+    """bench.cpp:84-94 on the device (SYRK + Cholesky)."""
+    w = np.empty(p.dim())
+    mn = f64()
+    _check(_lib.load().skr_reference_minimum(p.data.ctx.h, p.data.h, p.labels, float(p.lam), w, C.byref(mn)))
+    return ReferenceSolution(w, mn.value)
+
+
+def conditioned_condition_number(data: DataMatrix, lam: float, precond: Preconditioner) -> float:
+    """precond.cpp:196-206 without the d <= 2000 guard (the device has the memory)."""
+    k = precond.rank()
+    U = np.ascontiguousarray(np.asarray(precond.basis()).T) if k else None
+    sig = _f64(precond._sigma) if k else None
+    out = f64()
+    _check(_lib.load().skr_conditioned_cond(data.ctx.h, data.h, float(lam), U.ctypes.data if k else None,
+                                            sig.ctypes.data if k else None, k, C.byref(out)))
+    return out.value
+
+
+# test hooks for the reference streams
+def mt_uniforms(seed: int, count: int, ctx: Context | None = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    out = np.empty(count)
+    _check(_lib.load().skr_mt_uniforms(ctx.h, int(seed), int(count), out))
+    return out
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int, ctx: Context | None = None) -> np.ndarray:
+    """random.cpp:28-41 on the device; returns (rows, cols)."""
+    ctx = ctx or default_context()
+    out = np.empty(rows * cols)
+    _check(_lib.load().skr_gaussian_matrix(ctx.h, int(rows), int(cols), int(seed), out))
+    return out.reshape(cols, rows).T

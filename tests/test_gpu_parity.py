@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+The oracle port (oracle/skr_oracle.c) is bitwise-identical to the reference
+library on these paths (tests/test_oracle_golden.py pins it); where the built
+reference (oracle/_ref) is present it is used directly as well.
+
+Tolerances (stated per test): streams and indices are exact; fp64 arithmetic
+agrees to ~1e-12 relative (parallel reductions reassociate); the BASELINE gates
+are 1e-6 (fp64) / 1e-3 (fp32) on Ritz values and 1e-8 / 1e-5 on L(w^).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1602_02350_b200 import configs, skridge as sk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def O():
+    return oracle.port()
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def spectrum_matrix(n, d, sigma, seed):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, len(sigma))))
+    V, _ = np.linalg.qr(rng.standard_normal((d, len(sigma))))
+    return np.ascontiguousarray((U * sigma) @ V.T)
+
+
+# ---- reference streams ----------------------------------------------------------
+@pytest.mark.parametrize("seed", [0, 5, 12345678901])
+def test_mt_uniforms_bit_exact(O, seed):
+    got = sk.mt_uniforms(seed, 3 * 312 + 17)
+    assert np.array_equal(got, O.uniforms(seed, 3 * 312 + 17))
+
+
+def test_gaussian_matrix_matches_normal_sampler(O):
+    # Box-Muller transcendentals on the device may differ from glibc by an ulp
+    got = sk.gaussian_matrix(37, 5, 42)
+    want = O.gaussian_matrix(37, 5, 42)
+    assert rel(got, want) < 1e-14
+
+
+# ---- block_lanczos -----------------------------------------------------------------
+@pytest.mark.parametrize("n,d,k,q", [(400, 30, 5, 3), (257, 61, 8, 2), (1000, 128, 16, 4)])
+def test_block_lanczos_matches_oracle(O, n, d, k, q):
+    rng = np.random.default_rng(n + d)
+    X = rng.standard_normal((n, d)) * (1.0 / np.arange(1, d + 1))
+    want = O.block_lanczos(X, k, q=q, seed=7)
+    got = sk.block_lanczos(sk.DataMatrix(X).scaled(1 / math.sqrt(n)), sk.LanczosConfig(k, 0.5, 7, q))
+    assert got.k == want.k and got.q == want.q and not got.rank_reduced
+    assert rel(got.singular_values, want.sigma) < 1e-10
+    # U: same basis up to rounding (sign rule applied on both sides)
+    assert np.max(np.abs(got.left - want.U)) < 1e-8
+    assert np.max(np.abs(got.right - want.V)) < 1e-7
+
+
+def test_block_lanczos_default_q_and_errors(O):
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((60, 14))
+    a = sk.DataMatrix(X)
+    got = sk.block_lanczos(a, sk.LanczosConfig(3, 0.5, 1))
+    want = O.block_lanczos(X, 3, q=0, seed=1, scale=1.0)
+    assert got.q == want.q == sk.lanczos_iterations(60, 0.5)
+    assert rel(got.singular_values, want.sigma) < 1e-10
+    with pytest.raises(sk.ParameterError):
+        sk.block_lanczos(a, sk.LanczosConfig(15, 0.5, 1))
+    with pytest.raises(sk.ParameterError):
+        sk.block_lanczos(a, sk.LanczosConfig(2, 1.0, 1))
+
+
+def test_block_lanczos_rank_drop(O):
+    # rank-2 data: q = 3 blocks of width 2 collapse to width 2 (test_sketch.cpp:80-88)
+    X = spectrum_matrix(20, 12, np.array([2.0, 1.0]), 7)
+    got = sk.block_lanczos(sk.DataMatrix(X), sk.LanczosConfig(2, 0.5, 8, 3))
+    want = O.block_lanczos(X, 2, q=3, seed=8, scale=1.0)
+    assert rel(got.singular_values, want.sigma) < 1e-10
+    # rank-3 data with k = 5: the basis collapses below k -> rank_reduced
+    X3 = spectrum_matrix(45, 30, np.array([3.0, 1.5, 0.75]), 11)
+    got3 = sk.block_lanczos(sk.DataMatrix(X3), sk.LanczosConfig(5, 0.5, 4, 1))
+    want3 = O.block_lanczos(X3, 5, q=1, seed=4, scale=1.0)
+    assert got3.k == want3.k == 3 and got3.rank_reduced and want3.rank_reduced
+    assert rel(got3.singular_values, [3.0, 1.5, 0.75]) < 1e-8
+
+
+def test_block_lanczos_high_q_is_exact():
+    rng = np.random.default_rng(53)
+    X = rng.standard_normal((36, 24))
+    got = sk.block_lanczos(sk.DataMatrix(X), sk.LanczosConfig(5, 0.5, 59, 30))
+    exact = np.linalg.svd(X, compute_uv=False)[:5]
+    assert np.max(np.abs(got.singular_values - exact)) < 1e-6
+
+
+# ---- preconditioned components ----------------------------------------------------
+def small_problem(n=300, d=40, k=6, lam=1e-3, seed=0, dtype=np.float64):
+    rng = np.random.default_rng(seed)
+    X = (rng.standard_normal((n, d)) * (1.0 / np.arange(1, d + 1) ** 1.2)).astype(dtype)
+    y = rng.standard_normal(n).astype(dtype).astype(np.float64)
+    return X, y, lam, k
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_components_match_oracle(O, dtype):
+    X, y, lam, k = small_problem(dtype=dtype)
+    n, d = X.shape
+    Xd = X.astype(np.float64)
+    sv = O.block_lanczos(Xd, k, q=3, seed=3)
+    po = O.problem(Xd, y, lam, sv.U, sv.sigma)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    sketch = sk.SketchedSvd(sv.U, sv.sigma, None, sv.k, 3)
+    pc = sk.build_sketched(sketch, lam)
+    pg = sk.preconditioned_components(p, pc)
+    tol = 1e-12 if dtype == np.float64 else 1e-5  # X~ is stored in the data dtype (fp32: ~1e-7 per entry, amplified by cancellation in r_i)
+    assert rel(pg.betas(), po.betas()) < 1e-12
+    a_o, b_o, m_o = po.scalars()
+    assert abs(pg.strong_convexity() - a_o) <= 1e-15 * a_o
+    assert abs(pg.mean_beta() - b_o) <= 1e-12 * b_o
+    assert abs(pg.max_row_sq() - m_o) <= 1e-12 * m_o
+    assert rel(pg.transformed(), po.transformed()) < (1e-13 if dtype == np.float64 else 1e-6)
+    rng = np.random.default_rng(9)
+    for t in range(3):
+        w = rng.standard_normal(d)
+        mu, obj = pg.full_gradient(w, with_objective=True)
+        assert rel(mu, po.full_gradient(w)) < tol
+        assert abs(obj - po.objective(w)) <= tol * abs(po.objective(w))
+        assert abs(pg.objective(w) - obj) <= 1e-15 * abs(obj)
+    w = rng.standard_normal(d)
+    for i in [0, 7, n - 1, n, n + d - 1]:
+        assert rel(pg.component_gradient(i, w), po.component_gradient(i, w)) < tol
+    v = rng.standard_normal(d)
+    assert rel(pg.apply_inv_sqrt(v), O.apply_inv_sqrt(sv.U, sv.sigma, lam, v)) < 1e-13
+
+
+def test_identity_preconditioner(O):
+    X, y, lam, _ = small_problem(n=200, d=33)
+    po = O.problem(X, y, lam)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.Preconditioner.identity(33, lam))
+    assert rel(pg.betas(), po.betas()) < 1e-13
+    w = np.random.default_rng(1).standard_normal(33)
+    assert rel(pg.full_gradient(w), po.full_gradient(w)) < 1e-12
+    assert pg.strong_convexity() == lam
+
+
+def test_full_gradient_is_mean_of_components():
+    # test_ridge.cpp:167-181
+    X, y, lam, k = small_problem(n=60, d=12, k=3)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(k, 0.5, 137))
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, lam))
+    w = np.random.default_rng(139).standard_normal(12)
+    mean = sum(pg.component_gradient(i, w) for i in range(pg.component_count())) / pg.component_count()
+    assert np.max(np.abs(pg.full_gradient(w) - mean)) < 1e-8
+
+
+# ---- sampling + SVRG -----------------------------------------------------------------
+def test_index_stream_identical(O):
+    X, y, lam, k = small_problem()
+    sv = O.block_lanczos(X, k, q=3, seed=3)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.build_sketched(sk.SketchedSvd(sv.U, sv.sigma, None, k, 3), lam))
+    po = O.problem(X, y, lam, sv.U, sv.sigma)
+    got = pg.index_stream(11, 20000)
+    assert np.array_equal(got, O.index_stream(pg.betas(), 11, 20000))
+    assert np.array_equal(got, O.index_stream(po.betas(), 11, 20000))
+
+
+def test_epoch_replay_matches_oracle_trace(O):
+    X, y, lam, k = small_problem(n=200, d=24, k=4)
+    n, d = X.shape
+    sv = O.block_lanczos(X, k, q=3, seed=5)
+    po = O.problem(X, y, lam, sv.U, sv.sigma)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.build_sketched(sk.SketchedSvd(sv.U, sv.sigma, None, k, 3), lam))
+    eta = configs.step_size(po.scalars()[2])
+    m = 2 * n
+    idx = O.index_stream(po.betas(), 21, m)
+    w0 = np.zeros(d)
+    mu = po.full_gradient(w0)
+    st = pg.make_epoch_state()
+    st.begin_epoch(w0, mu)
+    for i in idx:
+        st.step(i, eta)
+    got = st.epoch_average()
+    want = O.problem(X, y, lam, sv.U, sv.sigma).svrg(1, m, eta, 21).iterate
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_svrg_solve_matches_oracle(O, dtype):
+    X, y, lam, k = small_problem(n=500, d=48, k=6, dtype=dtype)
+    n, d = X.shape
+    Xd = X.astype(np.float64)
+    sv = O.block_lanczos(Xd, k, q=3, seed=2)
+    po = O.problem(Xd, y, lam, sv.U, sv.sigma)
+    eta = configs.step_size(po.scalars()[2])
+    want = po.svrg(6, 2 * n, eta, 13)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.build_sketched(sk.SketchedSvd(sv.U, sv.sigma, None, k, 3), lam))
+    got = sk.svrg_solve(pg, sk.SvrgConfig(6, 2 * n, eta, 13), np.zeros(d))
+    tr = np.array([r.objective for r in got.trace])
+    tol = 1e-10 if dtype == np.float64 else 1e-5
+    assert rel(tr, want.trace) < tol
+    assert rel(got.iterate, want.iterate) < (1e-8 if dtype == np.float64 else 1e-3)
+
+
+def test_svrg_divergence_raises_with_trace():
+    X, y, lam, k = small_problem(n=100, d=10, k=2)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.Preconditioner.identity(10, lam))
+    with pytest.raises(sk.DivergenceError) as e:
+        sk.svrg_solve(pg, sk.SvrgConfig(5, 200, 1e3, 1), np.zeros(10))
+    assert len(e.value.trace) >= 1
+
+
+# ---- diagnostics ----------------------------------------------------------------------
+def test_reference_minimum_and_objective(O):
+    X, y, lam, _ = small_problem(n=400, d=50)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    w_o, m_o = O.reference_minimum(X, y, lam)
+    r = sk.reference_minimum(p)
+    assert rel(r.minimizer, w_o) < 1e-9
+    assert abs(r.minimum - m_o) <= 1e-12 * abs(m_o)
+    w = np.random.default_rng(4).standard_normal(50)
+    assert abs(sk.objective(p, w) - O.objective(X, y, lam, w)) <= 1e-12 * O.objective(X, y, lam, w)
+
+
+def test_conditioned_condition_number(O):
+    X, y, lam, k = small_problem(n=400, d=50, k=6)
+    sv = O.block_lanczos(X, k, q=3, seed=8)
+    want = O.conditioned_cond(X, lam, sv.U, sv.sigma)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    pc = sk.build_sketched(sk.SketchedSvd(sv.U, sv.sigma, None, k, 3), lam)
+    got = sk.conditioned_condition_number(sk.scaled_design(p), lam, pc)
+    assert abs(got - want) <= 1e-8 * want
+    # beta_hat = tr(M) (test_ridge.cpp:229-237)
+
+
+# ---- the BASELINE plumbing config c1, end to end ------------------------------------
+@pytest.mark.slow
+def test_config_c1_end_to_end(O):
+    cfg = configs.CONFIGS["c1"]
+    X, y = configs.host_instance(cfg)
+    n, d = X.shape
+    scale = 1 / math.sqrt(n)
+    # oracle pipeline, composed as SURVEY §0 fact 6 prescribes
+    sv_o = O.block_lanczos(X, cfg.k, q=cfg.q, seed=cfg.seed, scale=scale, want_right=False)
+    po = O.problem(X, y, cfg.lam, sv_o.U, sv_o.sigma)
+    eta = configs.step_size(po.scalars()[2])
+    m = 2 * n
+    out_o = po.svrg(cfg.epochs, m, eta, cfg.seed)
+    w_hat_o = O.apply_inv_sqrt(sv_o.U, sv_o.sigma, cfg.lam, out_o.iterate)
+    L_o = O.objective(X, y, cfg.lam, w_hat_o)
+    # GPU pipeline
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, cfg.lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+    assert rel(sv.singular_values, sv_o.sigma) < 1e-6          # BASELINE gate (fp64)
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))
+    assert abs(configs.step_size(pg.max_row_sq()) - eta) <= 1e-10 * eta
+    res = sk.svrg_solve(pg, sk.SvrgConfig(cfg.epochs, m, eta, cfg.seed), np.zeros(d))
+    w_hat = pg.apply_inv_sqrt(res.iterate)
+    L = sk.objective(p, w_hat)
+    assert abs(L - L_o) <= 1e-8 * abs(L_o)                      # BASELINE gate (fp64)
+    # identical index sequence for the fp64 inner loop
+    assert np.array_equal(pg.index_stream(cfg.seed, 50000), O.index_stream(po.betas(), cfg.seed, 50000))
