@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path.
+
+A step is ONE full-gradient pass (the fused K9 pass of
+PreconditionedRidge::full_gradient + objective, ridge.cpp:174-236) over the
+preconditioned rows X~ of the configs[1] workload (c2: fp64, n = 65,536 rows
+per GPU, d = 1024).  `value` is the whole-job HBM throughput of that pass in
+algorithmic GB/s (n*d*8 bytes of X~ per pass per GPU, all GPUs); `e2e` is the
+same metric through the reference-facing C-ABI call with host buffers
+(skr_full_gradient: w uploaded, mu and the objective read back every step).
+
+Multi-GPU (torchrun): rows are sharded, each rank owns a c2-sized shard (weak
+scaling) and the pass ends in one NCCL allreduce of d+1 doubles.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref: the unmodified skridge library, OpenMP on all host cores) on the
+same metric; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SVRG full-gradient pass throughput (HBM GB/s)"
+CLOCK_QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the workload runs."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={CLOCK_QUERY}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+def cpu_full_gradient_sample(X, y, lam, U, sigma, budget_s: float, max_passes: int):
+    """The reference's PreconditionedRidge::full_gradient (oracle/_ref, OpenMP) on the
+    same instance; returns (seconds per pass, passes timed, threads)."""
+    import oracle
+    R = oracle.ref() if oracle.ref_available() else oracle.port()
+    prob = R.problem(X, y, lam, U, sigma, 0)
+    w = np.random.default_rng(1).standard_normal(X.shape[1]) * 1e-2
+    prob.full_gradient(w)  # warm-up
+    t0 = time.perf_counter()
+    k = 0
+    while k < max_passes and (k == 0 or time.perf_counter() - t0 < budget_s):
+        prob.full_gradient(w)
+        k += 1
+    dt = (time.perf_counter() - t0) / k
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return dt, k, threads, R.name
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference CPU path on the same workload (rank 0 only)."""
+    import oracle
+    from paper_1602_02350_b200 import configs
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libskridge_ref.so not built"}))
+        return
+    R = oracle.ref()
+    X, y = configs.host_instance(cfg)
+    X = X.astype(np.float64)
+    y = y.astype(np.float64)
+    n, d = X.shape
+    sv = R.block_lanczos(X, cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
+    prob = R.problem(X, y, cfg.lam, sv.U, sv.sigma, 0)
+    w = np.random.default_rng(1).standard_normal(d) * 1e-2
+    for _ in range(args.warmup):
+        prob.full_gradient(w)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prob.full_gradient(w)
+        prob.objective(w)  # the GPU step also yields the objective
+    dt = (time.perf_counter() - t0) / args.steps
+    bytes_per_step = n * d * 8
+    val = bytes_per_step / dt / 1e9
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    print(json.dumps({
+        "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (configs.host_instance, numpy Philox)",
+        "impl": "reference",
+        "config": {"workload": f"{cfg.name}: full-gradient + objective pass over X~ (n={n}, d={d}, k={cfg.k})",
+                   "n": n, "d": d, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full_gradient+objective calls of skridge::PreconditionedRidge "
+                                   f"(Dense) on the {cfg.name} instance"},
+        "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    from paper_1602_02350_b200 import configs, skridge as sk
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nid = [sk.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        ctx = sk.Context(local, rank, world, nid[0])
+    else:
+        ctx = sk.Context(local)
+    sk._default_ctx = ctx
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- workload: c2-shaped shard per GPU, generated on the device
+    n_total = cfg.n * world
+    spec = sk.SynthSpec(n_total, cfg.d, cfg.dtype, cfg.seed, cfg.spectrum, cfg.spectrum_param, cfg.t_scale, cfg.tau)
+    data = sk.DataMatrix.generate(spec, ctx)
+    y = data.labels()
+    p = sk.RidgeProblem(data, y, cfg.lam)
+    n_loc, d = data.n_local, data.d
+    s_bytes = 4 if cfg.dtype == "f32" else 8
+    ld = (d + 15) // 16 * 16
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+    ctx.synchronize()
+    lanczos_s = max_over_ranks(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    pc = sk.build_sketched(sv, cfg.lam)
+    prob = sk.preconditioned_components(p, pc)
+    ctx.synchronize()
+    precompute_s = max_over_ranks(time.perf_counter() - t0)
+
+    # ---- device-resident timed loop: K9 through skr_full_gradient_device
+    lib = sk._lib.load()
+    w = torch.zeros(ld, dtype=torch.float64, device="cuda")
+    w[:d] = torch.randn(d, dtype=torch.float64, device="cuda") * 1e-2
+    mu = torch.zeros(ld, dtype=torch.float64, device="cuda")
+    obj = torch.zeros(1, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+
+    def step():
+        rc = lib.skr_full_gradient_device(prob.h, w.data_ptr(), mu.data_ptr(), obj.data_ptr())
+        if rc:
+            raise RuntimeError(sk._lib.last_error())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    ctx.synchronize()
+    ctx.profile(True)
+    launches0 = ctx.kernel_launches
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ctx.synchronize()
+        launches = ctx.kernel_launches - launches0
+        # keep the same loop running ~0.4 s more so the clock sampler sees load
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 0.4:
+            for _ in range(20):
+                step()
+            ctx.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    barrier()
+    ms = max_over_ranks(ms)
+    k9_ms, k9_n = ctx.profile_read("fullgrad")
+    ctx.profile(False)
+    ms_step = ms / args.steps
+    bytes_per_gpu = n_loc * d * s_bytes
+    value = world * bytes_per_gpu / (ms_step * 1e-3) / 1e9
+    # the dominant kernel: K9's streaming pass (average over the timed + soak launches)
+    k9_avg = k9_ms / max(k9_n, 1)
+    hbm, bf16, src = peaks()
+    achieved = bytes_per_gpu / (k9_avg * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k9_traffic.json")) as f:
+            tj = json.load(f).get(cfg.name)
+            traffic = tj.get("traffic_bytes") if tj else None
+    except Exception:
+        pass
+
+    # ---- e2e: the reference-facing call with host buffers (w in, mu + objective out)
+    wh = w[:d].double().cpu().numpy().copy()
+    for _ in range(3):
+        prob.full_gradient(wh, with_objective=True)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prob.full_gradient(wh, with_objective=True)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    e2e_value = world * bytes_per_gpu / e2e_s / 1e9
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic (device Philox4x32-10 generator, BASELINE spectrum)",
+        "config": {"workload": f"{cfg.name}: fused full-gradient + objective pass over X~ "
+                               f"(n={cfg.n} rows/GPU, d={d}, {cfg.dtype}, k={cfg.k}, q={cfg.q})",
+                   "n_per_gpu": cfg.n, "n_total": n_total, "d": d, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam,
+                   "parallelism": f"rows sharded dp{world}",
+                   "l2": f"inputs larger than L2 (X~ {bytes_per_gpu / 1e6:.0f} MB/GPU vs 126 MB L2)"},
+        "passes_per_s": round(1e3 / ms_step, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "kernel": "fullgrad_kernel (K9)", "kernel_ms": round(k9_avg, 5), "peak_source": src,
+                     "bytes_per_launch": bytes_per_gpu},
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": d * 8,
+                "d2h_bytes_per_step": d * 8 + 8, "ms_per_step": round(e2e_s * 1e3, 4)},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": round(launches / max(1, args.steps), 2),
+        "clocks": clk.summary(),
+        "lanczos": {"seconds": round(lanczos_s, 4),
+                    "tflops": round(lanczos_flops(cfg, n_total) / lanczos_s / 1e12 / world, 4),
+                    "note": "whole block_lanczos call incl. Pi stream, ortho, RR, eigensolve"},
+        "precompute_s": round(precompute_s, 4),
+    }
+
+    if not args.no_extras:
+        out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
+    if world == 1 and not args.no_cpu_baseline and rank == 0:
+        X = data.download().astype(np.float64)
+        dt, kk, thr, kind = cpu_full_gradient_sample(X, y, cfg.lam, sv.left, sv.singular_values,
+                                                     budget_s=10.0, max_passes=max(3, args.steps))
+        out["cpu_baseline"] = {"value": round(bytes_per_gpu / dt / 1e9, 3), "unit": "GB/s", "cores": thr,
+                               "kind": kind,
+                               "sample": f"{kk} PreconditionedRidge::full_gradient calls (reference, Dense, "
+                                         f"OpenMP) on the same {cfg.name} instance"}
+    if rank == 0:
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def lanczos_flops(cfg, n):
+    """2ndk + 4ndk(q-1) + 2nd*qk + n(qk)^2 algorithmic flops."""
+    d, k, q = cfg.d, cfg.k, cfg.q
+    return 2 * n * d * k + 4 * n * d * k * (q - 1) + 2 * n * d * q * k + n * (q * k) ** 2
+
+
+def solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx):
+    """Epoch time and time-to-eps (eps = 1e-6 absolute suboptimality) of the full solve."""
+    from paper_1602_02350_b200 import configs
+    ref = sk.reference_minimum(p)
+    eta = configs.step_size(prob.max_row_sq())
+    m = 2 * p.count()
+    ctx.profile(True)
+    res = sk.svrg_solve(prob, sk.SvrgConfig(cfg.epochs, m, eta, cfg.seed), None, ref.minimum)
+    k10_ms, k10_n = ctx.profile_read("svrg_epoch")
+    ctx.profile(False)
+    eps = 1e-6
+    hit = next((r for r in res.trace if r.suboptimality is not None and r.suboptimality <= eps), None)
+    w_hat = prob.apply_inv_sqrt(res.iterate)
+    L = sk.objective(p, w_hat)
+    return {"svrg": {
+        "epochs": len(res.trace), "m": m, "eta": eta, "L_star": ref.minimum, "L_final": L,
+        "suboptimality_final": L - ref.minimum,
+        "epoch_ms": round(res.trace[-1].elapsed_ms / len(res.trace), 3),
+        "inner_loop_ms_per_epoch": round(k10_ms / max(k10_n, 1), 3),
+        "inner_loop_ns_per_step": round(k10_ms / max(k10_n, 1) * 1e6 / m, 2),
+        "time_to_eps_s": None if hit is None else round(lanczos_s + precompute_s + hit.elapsed_ms / 1e3, 4),
+        "epochs_to_eps": None if hit is None else hit.epoch,
+        "trace": [r.objective for r in res.trace][:10]}}
+
+
+def run_sweep(args):
+    """K9 alone at every BASELINE shape (identity preconditioner: X~ = X, no copy)."""
+    import torch
+    from paper_1602_02350_b200 import configs, skridge as sk
+    ctx = sk.Context(0)
+    sk._default_ctx = ctx
+    hbm, _, src = peaks()
+    rows = []
+    for name in args.sweep.split(","):
+        cfg = configs.CONFIGS[name]
+        spec = sk.SynthSpec(cfg.n, cfg.d, cfg.dtype, cfg.seed, cfg.spectrum, cfg.spectrum_param, cfg.t_scale, cfg.tau)
+        t0 = time.perf_counter()
+        data = sk.DataMatrix.generate(spec, ctx)
+        gen_s = time.perf_counter() - t0
+        p = sk.RidgeProblem(data, data.labels(), cfg.lam)
+        prob = sk.preconditioned_components(p, sk.Preconditioner.identity(cfg.d, cfg.lam))
+        ld = (cfg.d + 15) // 16 * 16
+        w = torch.zeros(ld, dtype=torch.float64, device="cuda")
+        w[: cfg.d] = 1e-2
+        mu = torch.zeros(ld, dtype=torch.float64, device="cuda")
+        obj = torch.zeros(1, dtype=torch.float64, device="cuda")
+        lib = sk._lib.load()
+        for _ in range(3):
+            lib.skr_full_gradient_device(prob.h, w.data_ptr(), mu.data_ptr(), obj.data_ptr())
+        ctx.profile(True)
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, min(50, int(2e10 // (cfg.n * cfg.d * (4 if cfg.dtype == "f32" else 8)))))
+        e0.record(stream)
+        for _ in range(reps):
+            lib.skr_full_gradient_device(prob.h, w.data_ptr(), mu.data_ptr(), obj.data_ptr())
+        e1.record(stream)
+        ctx.synchronize()
+        k_ms, k_n = ctx.profile_read("fullgrad")
+        ctx.profile(False)
+        byts = cfg.n * cfg.d * (4 if cfg.dtype == "f32" else 8)
+        step_ms = e0.elapsed_time(e1) / reps
+        kern_ms = k_ms / max(k_n, 1)
+        rows.append({"config": name, "bytes": byts, "kernel_ms": round(kern_ms, 4), "step_ms": round(step_ms, 4),
+                     "kernel_GBps": round(byts / kern_ms / 1e6, 1), "step_GBps": round(byts / step_ms / 1e6, 1),
+                     "frac": round(byts / kern_ms / 1e6 / hbm, 4), "gen_s": round(gen_s, 2)})
+        print(json.dumps(rows[-1]), flush=True)
+        del prob, p, data
+    print(json.dumps({"k9_sweep": rows, "peak_GBps": hbm, "peak_source": src}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sweep", default="", help="comma list of configs: K9 alone at each shape")
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_1602_02350_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    if args.sweep:
+        run_sweep(args)
+        return
+    if args.impl == "reference":
+        rank, world, _ = dist_env()
+        if rank != 0:
+            return
+        run_reference(args, cfg)
+        return
+    run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

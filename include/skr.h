@@ -67,6 +67,11 @@ int skr_ctx_synchronize(skr_ctx* ctx);
 void* skr_ctx_stream(skr_ctx* ctx); /* cudaStream_t the context orders work on */
 /* number of this library's kernel launches so far on the context */
 int64_t skr_ctx_kernel_launches(const skr_ctx* ctx);
+/* CUDA-event timing of the hot kernels on the context stream: enable (resets
+ * the counters) and read the summed device time of a key ("fullgrad": the K9
+ * streaming kernel; "svrg_epoch": the K10 inner loop). */
+int skr_ctx_profile(skr_ctx* ctx, int enable);
+int skr_ctx_profile_read(skr_ctx* ctx, const char* key, double* total_ms, int64_t* launches);
 
 /* ---- data: DataMatrix (data_matrix.hpp:18-61) -------------------------- */
 /* rows: n x d row-major host array of `dtype`.  On a distributed context the

@@ -161,88 +161,206 @@ std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d) {
 }
 
 // ---- K9 dispatch -----------------------------------------------------------
-template <class T, int VEC, int TR>
-void launch_fullgrad_t(Ctx& c, int nt, int grid, const T* X, int64_t ld, int64_t n, const double* y,
-                       const double* w, double* part_g, double* part_loss) {
-  switch (nt / 32) {
-#define FG_CASE(NW)                                                                              \
-  case NW:                                                                                       \
-    fullgrad_kernel<T, VEC, TR, NW * 32><<<grid, NW * 32, 0, c.stream>>>(X, ld, n, y, w, part_g,  \
-                                                                         part_loss);             \
-    break;
-    FG_CASE(2) FG_CASE(4) FG_CASE(8) FG_CASE(16)
-#undef FG_CASE
-    default:
-      raise(SKR_EINTERNAL, "fullgrad: unsupported block size");
+// Each thread owns VEC = 8 columns of every row, so a row is covered by
+// ceil(ld / 8) threads (<= 512: d <= 4096); TR rows per tile.  Grid =
+// resident CTAs per SM (occupancy API) x SM count.
+struct FgPlan {
+  int bytes = 64, nt = 0, grid = 0;
+};
+
+struct K9Knobs {
+  int impl = 3;       // 3: bulk-copy staged (TMA ring), 2: register-direct loads
+  int smem_kb = 96;   // stage-ring budget per CTA (v3)
+  K9Knobs() {
+    if (const char* e = getenv("SKR_K9_IMPL")) impl = atoi(e);
+    if (const char* e = getenv("SKR_K9_SMEM_KB")) smem_kb = atoi(e);
   }
+};
+inline const K9Knobs& k9_knobs() {
+  static K9Knobs k;
+  return k;
+}
+
+template <class T, int VEC, int TR, int NT>
+void launch_fullgrad_nt(Ctx& c, FgPlan& p, int64_t ntiles, const T* X, int64_t ld, int64_t n, const double* y,
+                        const double* w, double* part_g, double* part_loss, bool plan_only) {
+  const K9Knobs& kn = k9_knobs();
+  if (kn.impl != 2) {
+    auto kern = fullgrad_tma_kernel<T, VEC, TR, NT>;
+    const size_t tile = (size_t)ld * sizeof(T) * TR;
+    // 2 CTAs/SM at <= 256 threads (96 KB rings), 1 CTA/SM with a ~200 KB ring at 512
+    const size_t budget = (size_t)(getenv("SKR_K9_SMEM_KB") ? kn.smem_kb : (NT >= 512 ? 200 : 96)) * 1024;
+    const int stages = (int)std::max<size_t>(2, std::min<size_t>(16, budget / tile));
+    const size_t smem = tile * stages;
+    static int per_sm = 0;
+    static size_t configured = 0;
+    if (configured != smem) {
+      SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+      per_sm = std::max(per_sm, 1);
+      configured = smem;
+    }
+    p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * c.sm_count));
+    if (plan_only) return;
+    if (getenv("SKR_DEBUG"))
+      fprintf(stderr, "[skr] K9 tma: NT=%d VEC=%d TR=%d stages=%d smem=%zu per_sm=%d grid=%d\n", NT, VEC, TR, stages,
+              smem, per_sm, p.grid);
+    kern<<<p.grid, NT, smem, c.stream>>>(X, ld, n, y, w, part_g, part_loss, stages);
+    SKR_LAUNCHED(&c);
+    return;
+  }
+  auto kern = fullgrad_kernel<T, VEC, TR, NT>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * c.sm_count));
+  if (plan_only) return;
+  kern<<<p.grid, NT, 0, c.stream>>>(X, ld, n, y, w, part_g, part_loss);
   SKR_LAUNCHED(&c);
 }
 
-struct FgPlan {
-  int vec = 0, nt = 0, tr = 0, grid = 0;
-};
-
-// Choose columns-per-thread so each row costs every thread 16-64 B of vector
-// loads, keep the block <= 512 threads, and size the grid to fill the SMs.
-template <class T>
-FgPlan plan_fullgrad(Ctx& c, int64_t ld, int64_t n) {
-  FgPlan p;
-  const int cand[] = {2, 4, 8, 16};
-  for (int v : cand) {
-    if (v * (int)sizeof(T) < 16) continue;
-    int nt = (int)((ld + v - 1) / v);
-    nt = (nt + 31) / 32 * 32;
-    if (nt < 64) nt = 64;
-    if (nt <= 512) {
-      p.vec = v;
-      p.nt = 1;
-      while (p.nt < nt) p.nt *= 2;
-      break;
-    }
+template <class T, int VEC, int TR>
+void launch_fullgrad_v(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
+                       double* part_g, double* part_loss, bool plan_only) {
+  const int64_t ntiles = (n + TR - 1) / TR;
+  switch (p.nt) {
+#define FG_CASE(NTV) \
+  case NTV: launch_fullgrad_nt<T, VEC, TR, NTV>(c, p, ntiles, X, ld, n, y, w, part_g, part_loss, plan_only); break;
+    FG_CASE(32) FG_CASE(64) FG_CASE(128) FG_CASE(256) FG_CASE(512)
+#undef FG_CASE
+    default: raise(SKR_EINTERNAL, "fullgrad: unsupported block size");
   }
-  if (!p.vec) raise(SKR_EDIM, "full gradient: dimension too large for the fused pass");
-  p.tr = std::max(2, std::min(8, 32 / p.vec));
-  const int64_t tiles = (n + p.tr - 1) / p.tr;
-  const int per_sm = std::max(1, 2048 / p.nt);
-  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c.sm_count * per_sm));
+}
+
+template <class T>
+FgPlan run_fullgrad_tiles(Ctx& c, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
+                         double* part_g, double* part_loss, bool plan_only) {
+  // VEC = 8 columns per thread (64 B of fp64 / 32 B of fp32 per row), TR = 4 rows
+  // per tile (SKR_K9_TR=8 selects 8: a tuning knob).
+  FgPlan p;
+  static int env_tr = [] {
+    const char* e = getenv("SKR_K9_TR");
+    return e ? atoi(e) : 0;
+  }();
+  static int env_vec = [] {
+    const char* e = getenv("SKR_K9_VEC");
+    return e ? atoi(e) : 0;
+  }();
+  // 8 columns per thread when that still gives >= 256 threads per row, else 4
+  // (d <= 1024: keeps 8 warps per CTA); TR = 32 / VEC rows per tile.
+  const int vec = env_vec == 4 || env_vec == 8 ? env_vec : ((ld / 8 >= 256) ? 8 : 4);
+  int nt = (int)((ld + vec - 1) / vec);
+  int pow2 = 32;
+  while (pow2 < nt) pow2 *= 2;
+  if (pow2 > 512) raise(SKR_EDIM, "full gradient: dimension too large for the fused pass (d > 4096)");
+  p.nt = pow2;
+  p.bytes = vec * (int)sizeof(T);
+  if (vec == 8) launch_fullgrad_v<T, 8, 4>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);
+  else if (env_tr == 4) launch_fullgrad_v<T, 4, 4>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);
+  else launch_fullgrad_v<T, 4, 8>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);
   return p;
 }
 
-template <class T>
-void run_fullgrad_main(Ctx& c, const FgPlan& p, const T* X, int64_t ld, int64_t n, const double* y,
-                       const double* w, double* part_g, double* part_loss) {
-  if (p.vec == 2) {
-    if constexpr (sizeof(T) == 8) launch_fullgrad_t<T, 2, 8>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
-    else raise(SKR_EINTERNAL, "plan");
-  } else if (p.vec == 4) {
-    launch_fullgrad_t<T, 4, 8>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
-  } else if (p.vec == 8) {
-    launch_fullgrad_t<T, 8, 4>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
-  } else {
-    launch_fullgrad_t<T, 16, 2>(c, p.nt, p.grid, X, ld, n, y, w, part_g, part_loss);
+template <class T, int CH, int RPI>
+void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
+                    double* part_g, double* part_loss, bool plan_only) {
+  auto kern = fullgrad_rowwarp_kernel<T, CH, RPI>;
+  const size_t smem = 2 * ld * sizeof(double);
+  static int per_sm = 0;
+  static size_t configured = 0;
+  if (configured != smem) {
+    if (smem > 48 * 1024) SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowwarpThreads, smem));
+    per_sm = std::max(per_sm, 1);
+    configured = smem;
   }
+  constexpr int NWR = kRowwarpThreads / 32;
+  const int64_t warps_needed = (n + RPI - 1) / RPI;
+  p.nt = kRowwarpThreads;
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps_needed + NWR - 1) / NWR, (int64_t)per_sm * c.sm_count));
+  if (plan_only) return;
+  if (getenv("SKR_DEBUG"))
+    fprintf(stderr, "[skr] K9 rowwarp: CH=%d RPI=%d smem=%zu per_sm=%d grid=%d\n", CH, RPI, smem, per_sm, p.grid);
+  kern<<<p.grid, kRowwarpThreads, smem, c.stream>>>(X, ld, n, y, w, part_g, part_loss);
+  SKR_LAUNCHED(&c);
 }
 
-// raw sums[0..ld) = sum_i r_i x_i, sums[ld] = sum_i r_i^2 over ALL ranks' rows
+// K9 dispatch: warp-per-row (v4) for d <= 1024 (<= 32 elements per lane), else the
+// bulk-copy staged tile kernel (v3).  SKR_K9_IMPL=2/3 forces the tile variants.
+template <class T>
+FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
+                         double* part_g, double* part_loss, bool plan_only) {
+  static int env_impl = [] {
+    const char* e = getenv("SKR_K9_IMPL");
+    return e ? atoi(e) : 0;
+  }();
+  static int env_rpi = [] {
+    const char* e = getenv("SKR_K9_RPI");
+    return e ? atoi(e) : 1;
+  }();
+  const int64_t row_bytes = ld * (int64_t)sizeof(T);
+  if ((env_impl == 0 || env_impl == 4) && ld <= 1024) {  // <= 32 elements per lane
+    FgPlan p;
+    p.bytes = (int)row_bytes;
+    const int ch = (int)((row_bytes + 511) / 512);  // 16-byte chunks per lane
+#define RW(CHV)                                                                                         \
+  if (ch <= CHV) {                                                                                      \
+    if (env_rpi == 2) launch_rowwarp<T, CHV, 2>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);  \
+    else launch_rowwarp<T, CHV, 1>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);               \
+    return p;                                                                                           \
+  }
+    RW(2) RW(4) RW(8)
+    if (sizeof(T) == 8) { RW(16) }
+#undef RW
+  }
+  return run_fullgrad_tiles<T>(c, ld, n, X, y, w, part_g, part_loss, plan_only);
+}
+
+struct FinalizeArgs {  // set when the pass should end in mu / obj directly
+  double n = 1, lambda = 0, c = 1;
+  const double *w = nullptr, *Ut = nullptr, *uw = nullptr, *D = nullptr;
+  int64_t d = 0, k = 0;
+  double *mu = nullptr, *obj = nullptr;
+};
+
+// K9 main pass + fused reduction.  With `fin` on one GPU the launch pair ends
+// in mu/obj; otherwise it produces the raw sums[0..ld] (sum_i r_i x_i, sum_i r_i^2)
+// allreduced across ranks.
 void fullgrad_sums(Ctx& c, int dtype, const void* X, int64_t ld, int64_t n, const double* y,
                    const double* w, DBuf<double>& part_g, DBuf<double>& part_loss,
-                   DBuf<double>& sums) {
+                   DBuf<double>& sums, const FinalizeArgs* fin = nullptr) {
   FgPlan plan;
-  DISPATCH_DTYPE(dtype, T, plan = plan_fullgrad<T>(c, ld, n));
-  if (part_g.n < (size_t)plan.grid * ld) part_g.alloc((size_t)plan.grid * ld, c.stream);
+  DISPATCH_DTYPE(dtype, T, plan = run_fullgrad_main<T>(c, ld, std::max<int64_t>(n, 1), (const T*)X, y, w, nullptr,
+                                                        nullptr, true));
+  const size_t need_g = (size_t)plan.grid * ld;
+  if (part_g.n < need_g) part_g.alloc(need_g, c.stream);
   if (part_loss.n < (size_t)plan.grid) part_loss.alloc(plan.grid, c.stream);
   if (sums.n < (size_t)ld + 1) sums.alloc(ld + 1, c.stream);
+  const bool direct = fin && c.world == 1;
   if (n > 0) {
-    DISPATCH_DTYPE(dtype, T,
-                   run_fullgrad_main<T>(c, plan, static_cast<const T*>(X), ld, n, y, w,
-                                        part_g.get(), part_loss.get()));
-    fullgrad_reduce_kernel<<<ceil_div(ld + 1, 256), 256, 0, c.stream>>>(part_g.get(), part_loss.get(),
-                                                                        ld, plan.grid, sums.get());
+    if (c.prof_on) c.prof_mark("fullgrad");
+    DISPATCH_DTYPE(dtype, T, run_fullgrad_main<T>(c, ld, n, static_cast<const T*>(X), y, w, part_g.get(),
+                                                  part_loss.get(), false));
+    if (c.prof_on) c.prof_mark("fullgrad");
+    fullgrad_colreduce_kernel<<<ceil_div(ld + 1, 32), 256, 0, c.stream>>>(
+        part_g.get(), part_loss.get(), ld, plan.grid, direct ? fin->d : 0, direct ? fin->n : 1.0,
+        direct ? fin->lambda : 0.0, direct ? fin->w : nullptr, direct ? fin->Ut : nullptr, direct ? fin->uw : nullptr,
+        direct ? fin->k : 0, direct ? fin->D : nullptr, direct ? fin->c : 1.0, direct ? fin->mu : nullptr,
+        direct ? fin->obj : nullptr, direct ? nullptr : sums.get());
     SKR_LAUNCHED(&c);
+    if (direct) return;
   } else {
     sums.zero();
   }
   c.allreduce_sum(sums.get(), ld + 1);
+  if (fin) {
+    fullgrad_finalize_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(sums.get(), ld, fin->d, fin->n, fin->lambda,
+                                                                     fin->w, fin->Ut, fin->uw, fin->k, fin->D, fin->c,
+                                                                     fin->mu, fin->obj);
+    SKR_LAUNCHED(&c);
+  }
 }
 
 // out = P^{-1/2} v through the low-rank form; proj gets U^T v (k) and v.v (index k).
@@ -258,14 +376,23 @@ void apply_inv_sqrt_dev(Ctx& c, const skr_problem* p, const double* v, double* p
 // K9 on the problem: mu (ld, device) and optional obj (device scalar) at w (device, ld).
 void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) {
   Ctx& c = p->ctx->c;
-  // regulariser: lambda P^{-1} w = lambda P^{-1/2}(P^{-1/2} w)  (ridge.cpp:232-235)
-  apply_inv_sqrt_dev(c, p, w, p->uw.get(), p->half.get());
-  apply_inv_sqrt_dev(c, p, p->half.get(), p->uh.get(), p->pinv.get());
-  fullgrad_sums(c, p->dtype, p->xt->ptr, p->ld, p->n, p->y.get(), w, p->part_g, p->part_loss, p->sums);
-  fullgrad_finalize_kernel<<<ceil_div(p->ld, 256), 256, 0, c.stream>>>(
-      p->sums.get(), p->ld, p->d, (double)p->n_global, p->lambda, p->pinv.get(), p->uw.get(), p->k,
-      p->D.get(), p->c, mu, obj);
+  // U^T w and w.w for lambda P^{-1} w and the regulariser norm (applied in the
+  // fused reduction); a few small CTAs ordered before the streaming pass
+  proj_kernel<<<ceil_div((p->k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), p->ld, p->d, p->k, w, p->uw.get());
   SKR_LAUNCHED(&c);
+  FinalizeArgs fin;
+  fin.n = (double)p->n_global;
+  fin.lambda = p->lambda;
+  fin.c = p->c;
+  fin.w = w;
+  fin.Ut = p->Ut.get();
+  fin.uw = p->uw.get();
+  fin.D = p->D.get();
+  fin.d = p->d;
+  fin.k = p->k;
+  fin.mu = mu;
+  fin.obj = obj;
+  fullgrad_sums(c, p->dtype, p->xt->ptr, p->ld, p->n, p->y.get(), w, p->part_g, p->part_loss, p->sums, &fin);
 }
 
 // Exact sampling tables (svrg.cpp:90-106, :165-172), built once per problem.
@@ -392,7 +519,10 @@ void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64
   a.snapshot = snap;
   a.mu = mu;
   a.w_avg = w_avg;
-  DISPATCH_DTYPE(p->dtype, T, run_epoch_t<T>(p->ctx->c, p->ld, a));
+  Ctx& c = p->ctx->c;
+  if (c.prof_on) c.prof_mark("svrg_epoch");
+  DISPATCH_DTYPE(p->dtype, T, run_epoch_t<T>(c, p->ld, a));
+  if (c.prof_on) c.prof_mark("svrg_epoch");
 }
 
 // ---- elementwise helpers ----------------------------------------------------
@@ -615,6 +745,9 @@ static void ctx_init(Ctx& c, int device) {
   c.device = device;
   SKR_CUDA(cudaSetDevice(device));
   SKR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  SKR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+  SKR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+  SKR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
   SKR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   SKR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -664,12 +797,47 @@ int skr_ctx_destroy(skr_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
     if (ctx->c.solver) cusolverDnDestroy(ctx->c.solver);
+    cudaStreamSynchronize(ctx->c.aux);
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaEventDestroy(ctx->c.ev_fork);
+    cudaEventDestroy(ctx->c.ev_join);
+    cudaStreamDestroy(ctx->c.aux);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });
 }
 
 int skr_ctx_synchronize(skr_ctx* ctx) { return guard([&] { C_(ctx).sync(); }); }
+
+int skr_ctx_profile(skr_ctx* ctx, int enable) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    c.sync();
+    for (auto& kv : c.prof) kv.second.used = 0;
+    c.prof_on = enable != 0;
+  });
+}
+
+int skr_ctx_profile_read(skr_ctx* ctx, const char* key, double* total_ms, int64_t* launches) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    c.sync();
+    double tot = 0.0;
+    int64_t cnt = 0;
+    auto it = c.prof.find(key ? key : "");
+    if (it != c.prof.end()) {
+      const auto& sl = it->second;
+      for (size_t i = 0; i + 1 < sl.used; i += 2) {
+        float ms = 0.f;
+        SKR_CUDA(cudaEventElapsedTime(&ms, sl.ev[i], sl.ev[i + 1]));
+        tot += ms;
+        ++cnt;
+      }
+    }
+    *total_ms = tot;
+    *launches = cnt;
+  });
+}
 void* skr_ctx_stream(skr_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
 int64_t skr_ctx_kernel_launches(const skr_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,10 +91,32 @@ struct Ctx {
   int device = 0;
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;                    // side stream for overlapped small kernels
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cusolverDnHandle_t solver = nullptr;
   ncclComm_t comm = nullptr;
   int sm_count = 148;
   int64_t launches = 0;
+
+  // Optional CUDA-event timing of named hot kernels on the context stream
+  // (bench.py: the dominant kernel's average launch duration).
+  struct ProfSlot {
+    std::vector<cudaEvent_t> ev;  // start/stop pairs
+    size_t used = 0;
+  };
+  bool prof_on = false;
+  std::map<std::string, ProfSlot> prof;
+  cudaEvent_t prof_mark(const std::string& key) {
+    ProfSlot& s = prof[key];
+    if (s.used == s.ev.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      s.ev.push_back(e);
+    }
+    cudaEvent_t e = s.ev[s.used++];
+    cudaEventRecord(e, stream);
+    return e;
+  }
 
   // Row-sharded collectives (no-ops on one GPU).  Sum of doubles in place.
   void allreduce_sum(double* buf, size_t count) {

@@ -109,6 +109,16 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.load().skr_ctx_kernel_launches(self.h))
 
+    def profile(self, enable: bool = True):
+        """Enable (and reset) CUDA-event timing of the hot kernels."""
+        _check(_lib.load().skr_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self, key: str):
+        """(total device ms, launches) of a profiled kernel key."""
+        ms, cnt = f64(), i64()
+        _check(_lib.load().skr_ctx_profile_read(self.h, key.encode(), C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
     def close(self):
         if getattr(self, "h", None):
             _lib.load().skr_ctx_destroy(self.h)
