@@ -1,0 +1,408 @@
+// skridge_b200.hpp — header-only C++ host API over the C-ABI (skr.h).
+//
+// Mirrors the reference's public interface in proj/include/skridge/ for the
+// hot path — same names, argument meaning and exception types — so C++
+// callers switch by namespace (skridge:: -> skridge::b200::).  Everything runs
+// on the B200; this header only owns handles (RAII) and converts status codes
+// back into the reference's exceptions (errors.hpp:10-60, svrg.hpp:27-35).
+//
+//   reference                                  here
+//   DataMatrix (data_matrix.hpp:18-61)         b200::DataMatrix (device storage + scale)
+//   block_lanczos (sketch.hpp:55)              b200::block_lanczos
+//   build_sketched (precond.hpp:70)            b200::build_sketched -> b200::Preconditioner
+//   preconditioned_components (ridge.hpp:121)  b200::preconditioned_components
+//   PreconditionedRidge (ridge.hpp:78-119)     b200::PreconditionedRidge
+//   svrg_solve (svrg.hpp:136-137)              b200::svrg_solve (device index stream)
+//   sketched_preconditioned_svrg (ridge.hpp:150) b200::sketched_preconditioned_svrg
+//   reference_minimum (bench.hpp:24)           b200::reference_minimum
+#pragma once
+
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "skr.h"
+
+namespace skridge {
+namespace b200 {
+
+using Vector = std::vector<double>;
+
+// ---- errors (errors.hpp) ---------------------------------------------------
+struct DimensionError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct ParameterError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct InputError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct EmptyBasisError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct ScaleGuardError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+struct EpochRecord {
+  std::size_t epoch = 0;
+  double objective = 0.0;
+  std::optional<double> suboptimality;
+  double elapsed_ms = 0.0;
+};
+using ConvergenceTrace = std::vector<EpochRecord>;
+
+class DivergenceError : public std::runtime_error {
+ public:
+  DivergenceError(std::string what, ConvergenceTrace trace)
+      : std::runtime_error(std::move(what)), trace_(std::move(trace)) {}
+  const ConvergenceTrace& trace() const { return trace_; }
+
+ private:
+  ConvergenceTrace trace_;
+};
+
+inline void check(int rc) {
+  if (rc == SKR_OK) return;
+  const std::string m = skr_last_error();
+  switch (rc) {
+    case SKR_EDIM: throw DimensionError(m);
+    case SKR_EPARAM: throw ParameterError(m);
+    case SKR_EINPUT: throw InputError(m);
+    case SKR_EGUARD: throw ScaleGuardError(m);
+    case SKR_EEMPTY: throw EmptyBasisError(m);
+    default: throw DeviceError(m);
+  }
+}
+
+// ---- context ------------------------------------------------------------------
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    skr_ctx* c = nullptr;
+    check(skr_ctx_create(device, &c));
+    h_.reset(c, [](skr_ctx* p) { skr_ctx_destroy(p); });
+  }
+  Context(int device, int rank, int world, const char nccl_id[128]) {
+    skr_ctx* c = nullptr;
+    check(skr_ctx_create_dist(device, rank, world, nccl_id, &c));
+    h_.reset(c, [](skr_ctx* p) { skr_ctx_destroy(p); });
+  }
+  skr_ctx* get() const { return h_.get(); }
+  void synchronize() const { check(skr_ctx_synchronize(get())); }
+
+ private:
+  std::shared_ptr<skr_ctx> h_;
+};
+
+// ---- DataMatrix -----------------------------------------------------------------
+/// Device-resident DataMatrix.  `rows` is n x d row-major == the reference's
+/// d x n column-major DenseMatrix storage (pass DenseMatrix::data() directly).
+class DataMatrix {
+ public:
+  DataMatrix(const Context& ctx, const double* rows, std::size_t n, std::size_t d) : ctx_(ctx) {
+    skr_data* x = nullptr;
+    check(skr_data_create(ctx.get(), rows, (int64_t)n, (int64_t)d, SKR_F64, &x));
+    reset(x);
+  }
+  DataMatrix(const Context& ctx, const float* rows, std::size_t n, std::size_t d) : ctx_(ctx) {
+    skr_data* x = nullptr;
+    check(skr_data_create(ctx.get(), rows, (int64_t)n, (int64_t)d, SKR_F32, &x));
+    reset(x);
+  }
+  std::size_t rows() const { return (std::size_t)info().d; }   // dimension d
+  std::size_t cols() const { return (std::size_t)info().ng; }  // point count n
+  double scale() const { return info().scale; }
+  DataMatrix scaled(double factor) const {
+    skr_data* x = nullptr;
+    check(skr_data_scaled(h_.get(), factor, &x));
+    DataMatrix out(ctx_);
+    out.reset(x);
+    return out;
+  }
+  skr_data* get() const { return h_.get(); }
+  const Context& context() const { return ctx_; }
+
+ private:
+  explicit DataMatrix(const Context& ctx) : ctx_(ctx) {}
+  void reset(skr_data* x) { h_.reset(x, [](skr_data* p) { skr_data_destroy(p); }); }
+  struct Info { int64_t n, d, ng, r0; int dtype; double scale; };
+  Info info() const {
+    Info i{};
+    check(skr_data_info(h_.get(), &i.n, &i.d, &i.dtype, &i.scale, &i.ng, &i.r0));
+    return i;
+  }
+  Context ctx_;
+  std::shared_ptr<skr_data> h_;
+};
+
+// ---- sketch (sketch.hpp) -----------------------------------------------------------
+struct LanczosConfig {
+  std::size_t k = 0;
+  double eps_prime = 0.5;
+  std::uint64_t seed = 0;
+  std::optional<std::size_t> q_override;
+};
+
+/// Column-major factors exactly as the reference's DenseMatrix stores them.
+struct SketchedSvd {
+  Vector left;             // d x k, column j = basis vector j
+  Vector singular_values;  // k
+  Vector right;            // n x k (empty unless requested)
+  std::size_t d = 0, n = 0, k = 0, q = 0;
+  bool rank_reduced = false;
+};
+
+inline std::size_t lanczos_iterations(std::size_t n, double eps_prime) {
+  const double q = std::ceil(std::log((double)n) / std::sqrt(eps_prime));
+  return q < 2.0 ? 2 : (std::size_t)q;
+}
+
+inline SketchedSvd block_lanczos(const DataMatrix& a, const LanczosConfig& cfg, bool want_right = false) {
+  SketchedSvd out;
+  out.d = a.rows();
+  int64_t n_local = 0;
+  check(skr_data_info(a.get(), &n_local, nullptr, nullptr, nullptr, nullptr, nullptr));
+  out.n = (std::size_t)n_local;
+  out.left.assign(out.d * cfg.k, 0.0);
+  out.singular_values.assign(cfg.k, 0.0);
+  if (want_right) out.right.assign(out.n * cfg.k, 0.0);
+  int64_t k_used = 0, q_used = 0;
+  int rr = 0;
+  check(skr_lanczos(a.context().get(), a.get(), (int64_t)cfg.k, cfg.q_override ? (int64_t)*cfg.q_override : 0,
+                    cfg.eps_prime, cfg.seed, out.left.data(), out.singular_values.data(),
+                    want_right ? out.right.data() : nullptr, &k_used, &q_used, &rr));
+  out.k = (std::size_t)k_used;
+  out.q = (std::size_t)q_used;
+  out.rank_reduced = rr != 0;
+  out.left.resize(out.d * out.k);
+  out.singular_values.resize(out.k);
+  if (want_right) out.right.resize(out.n * out.k);
+  return out;
+}
+
+// ---- precond (precond.hpp) -------------------------------------------------------
+class Preconditioner {
+ public:
+  static Preconditioner identity(std::size_t dim, double lambda) {
+    if (!(lambda > 0.0) || !std::isfinite(lambda)) throw ParameterError("preconditioner: lambda must be positive");
+    Preconditioner p;
+    p.dim_ = dim;
+    p.lambda_ = lambda;
+    return p;
+  }
+  std::size_t dim() const { return dim_; }
+  std::size_t rank() const { return sigma_.size(); }
+  double lambda() const { return lambda_; }
+  double tail_coeff() const { return inv_sqrt_.empty() ? 1.0 : inv_sqrt_.back(); }
+  const Vector& inv_sqrt_diag() const { return inv_sqrt_; }
+  const Vector& basis() const { return basis_; }  // d x k column-major
+  const Vector& singular_values() const { return sigma_; }
+  double min_inv_eigenvalue() const {
+    const double lead = inv_sqrt_.empty() ? 1.0 : inv_sqrt_.front();
+    return lead * lead;
+  }
+  friend Preconditioner build_sketched(const SketchedSvd& sv, double lambda);
+
+ private:
+  std::size_t dim_ = 0;
+  double lambda_ = 0.0;
+  Vector basis_, sigma_, inv_sqrt_;
+};
+
+/// precond.cpp:120-136 (+ validate, :34-49)
+inline Preconditioner build_sketched(const SketchedSvd& sv, double lambda) {
+  if (!(lambda > 0.0) || !std::isfinite(lambda)) throw ParameterError("preconditioner: lambda must be positive");
+  if (sv.k < 1) throw ParameterError("build_sketched: factors must have rank >= 1");
+  Preconditioner p;
+  p.dim_ = sv.d;
+  p.lambda_ = lambda;
+  p.basis_ = sv.left;
+  p.sigma_ = sv.singular_values;
+  p.inv_sqrt_.resize(sv.k);
+  const double cap = 1.0 / std::sqrt(lambda) * (1.0 + 1e-12);
+  double prev = 0.0;
+  for (std::size_t j = 0; j < sv.k; ++j) {
+    const double s = sv.singular_values[j];
+    const double v = 1.0 / std::sqrt(s * s + lambda);
+    if (!(v > 0.0) || v > cap) throw InputError("preconditioner: coefficient out of range");
+    if (v < prev) throw InputError("preconditioner: coefficients must be non-decreasing");
+    p.inv_sqrt_[j] = prev = v;
+  }
+  return p;
+}
+
+// ---- svrg (svrg.hpp) -----------------------------------------------------------------
+struct SvrgConfig {
+  std::size_t epochs = 1;
+  std::size_t epoch_length = 1;
+  double step_size = 0.1;
+  std::uint64_t seed = 0;
+};
+
+struct SvrgResult {
+  Vector iterate;
+  ConvergenceTrace trace;
+};
+
+// ---- ridge (ridge.hpp) ----------------------------------------------------------------
+struct RidgeProblem {
+  DataMatrix data;
+  Vector labels;
+  double lambda;
+  RidgeProblem(DataMatrix d, Vector y, double lam) : data(std::move(d)), labels(std::move(y)), lambda(lam) {
+    if (!(lambda > 0.0)) throw ParameterError("ridge problem: lambda must be positive");
+  }
+  std::size_t dim() const { return data.rows(); }
+  std::size_t count() const { return data.cols(); }
+};
+
+inline DataMatrix scaled_design(const RidgeProblem& p) { return p.data.scaled(1.0 / std::sqrt((double)p.count())); }
+
+enum class ApplyMode { Dense, Lazy, Auto };
+
+/// The FiniteSumProblem of the reference (svrg.hpp:67-80) on the device:
+/// component_count, dimension, betas, strong_convexity, objective,
+/// full_gradient, component_gradient, plus the epoch kernel for external engines.
+class PreconditionedRidge {
+ public:
+  PreconditionedRidge(const RidgeProblem& p, const Preconditioner& pc) : ctx_(p.data.context()) {
+    if (pc.dim() != p.dim()) throw DimensionError("preconditioned components: dimension mismatch");
+    skr_problem* h = nullptr;
+    check(skr_problem_create(ctx_.get(), p.data.get(), p.labels.data(), p.lambda,
+                             pc.rank() ? pc.basis().data() : nullptr,
+                             pc.rank() ? pc.singular_values().data() : nullptr, (int64_t)pc.rank(), &h));
+    h_.reset(h, [](skr_problem* q) { skr_problem_destroy(q); });
+    int64_t n = 0, d = 0, k = 0;
+    check(skr_problem_info(h, &n, &d, &k, &alpha_, &beta_hat_, &max_row_sq_));
+    n_ = (std::size_t)n;
+    d_ = (std::size_t)d;
+    betas_.resize(n_ + d_);
+    check(skr_problem_betas(h, betas_.data()));
+  }
+  std::size_t component_count() const { return n_ + d_; }
+  std::size_t dimension() const { return d_; }
+  const Vector& betas() const { return betas_; }
+  double strong_convexity() const { return alpha_; }
+  double mean_beta() const { return beta_hat_; }
+  double max_row_sq() const { return max_row_sq_; }
+  ApplyMode mode() const { return ApplyMode::Dense; }
+  double objective(const Vector& w) const {
+    double out = 0.0;
+    check(skr_objective(h_.get(), w.data(), &out));
+    return out;
+  }
+  void full_gradient(const Vector& w, Vector& out) const {
+    out.resize(d_);
+    check(skr_full_gradient(h_.get(), w.data(), out.data(), nullptr));
+  }
+  void component_gradient(std::size_t i, const Vector& w, Vector& out) const {
+    out.resize(d_);
+    check(skr_component_gradient(h_.get(), (int64_t)i, w.data(), out.data()));
+  }
+  /// One EpochState epoch (svrg.hpp:53-62) over caller-supplied indices.
+  void epoch(const Vector& snapshot, const Vector& full_grad, const std::vector<int64_t>& idx, double eta,
+             Vector& w_avg) const {
+    w_avg.resize(d_);
+    check(skr_epoch(h_.get(), snapshot.data(), full_grad.data(), idx.data(), (int64_t)idx.size(), eta,
+                    w_avg.data()));
+  }
+  Vector apply_inv_sqrt(const Vector& v) const {
+    Vector out(d_);
+    check(skr_apply_inv_sqrt(h_.get(), v.data(), out.data()));
+    return out;
+  }
+  skr_problem* get() const { return h_.get(); }
+
+ private:
+  Context ctx_;
+  std::shared_ptr<skr_problem> h_;
+  std::size_t n_ = 0, d_ = 0;
+  double alpha_ = 0, beta_hat_ = 0, max_row_sq_ = 0;
+  Vector betas_;
+};
+
+inline std::shared_ptr<PreconditionedRidge> preconditioned_components(const RidgeProblem& p,
+                                                                      const Preconditioner& pc,
+                                                                      ApplyMode = ApplyMode::Auto) {
+  return std::make_shared<PreconditionedRidge>(p, pc);
+}
+
+inline double mean_beta(const PreconditionedRidge& p) { return p.mean_beta(); }
+
+/// svrg.cpp:152-211 on the device, drawing the reference's index stream.
+inline SvrgResult svrg_solve(const PreconditionedRidge& p, const SvrgConfig& cfg, const Vector& w0,
+                             std::optional<double> reference_value = std::nullopt) {
+  if (w0.size() != p.dimension()) throw DimensionError("svrg: start point length mismatch");
+  skr_svrg_config c{(int64_t)cfg.epochs, (int64_t)cfg.epoch_length, cfg.step_size, cfg.seed};
+  std::vector<skr_epoch_record> rec(cfg.epochs ? cfg.epochs : 1);
+  SvrgResult out;
+  out.iterate.resize(p.dimension());
+  int64_t done = 0;
+  const int rc = skr_svrg(p.get(), &c, w0.data(), reference_value ? *reference_value : NAN, out.iterate.data(),
+                          rec.data(), &done);
+  for (int64_t s = 0; s < done; ++s) {
+    EpochRecord r;
+    r.epoch = (std::size_t)rec[s].epoch;
+    r.objective = rec[s].objective;
+    if (!std::isnan(rec[s].suboptimality)) r.suboptimality = rec[s].suboptimality;
+    r.elapsed_ms = rec[s].elapsed_ms;
+    out.trace.push_back(r);
+  }
+  if (rc == SKR_EDIVERGED) throw DivergenceError(skr_last_error(), out.trace);
+  check(rc);
+  return out;
+}
+
+struct SketchedSolveResult {
+  Vector iterate;
+  ConvergenceTrace trace;
+  Vector singular_values;
+  std::size_t k_used = 0, q_used = 0;
+  double beta_hat = 0, sketch_ms = 0, precompute_ms = 0, solve_ms = 0;
+};
+
+/// ridge.cpp:413-454, with the BASELINE configs' explicit q.
+inline SketchedSolveResult sketched_preconditioned_svrg(const RidgeProblem& p, std::size_t k, const SvrgConfig& cfg,
+                                                        std::uint64_t sketch_seed,
+                                                        std::optional<double> reference_value = std::nullopt,
+                                                        std::optional<std::size_t> q_override = std::nullopt) {
+  if (k < 1 || k > std::min(p.dim(), p.count())) throw ParameterError("sketched svrg: k must satisfy 1 <= k <= min(d, n)");
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
+  SketchedSolveResult out;
+  auto t0 = clk::now();
+  LanczosConfig lc;
+  lc.k = k;
+  lc.seed = sketch_seed;
+  lc.q_override = q_override;
+  SketchedSvd sv = block_lanczos(scaled_design(p), lc);
+  out.sketch_ms = ms(t0);
+  out.singular_values = sv.singular_values;
+  out.k_used = sv.k;
+  out.q_used = sv.q;
+  t0 = clk::now();
+  auto comp = preconditioned_components(p, build_sketched(sv, p.lambda));
+  out.precompute_ms = ms(t0);
+  out.beta_hat = comp->mean_beta();
+  t0 = clk::now();
+  SvrgResult r = svrg_solve(*comp, cfg, Vector(p.dim(), 0.0), reference_value);
+  out.solve_ms = ms(t0);
+  out.iterate = comp->apply_inv_sqrt(r.iterate);
+  out.trace = std::move(r.trace);
+  return out;
+}
+
+struct ReferenceSolution {
+  Vector minimizer;
+  double minimum = 0.0;
+};
+
+/// bench.cpp:84-94 on the device.
+inline ReferenceSolution reference_minimum(const RidgeProblem& p) {
+  ReferenceSolution r;
+  r.minimizer.resize(p.dim());
+  check(skr_reference_minimum(p.data.context().get(), p.data.get(), p.labels.data(), p.lambda, r.minimizer.data(),
+                              &r.minimum));
+  return r;
+}
+
+}  // namespace b200
+}  // namespace skridge

@@ -769,7 +769,7 @@ int skr_ctx_create(int device, skr_ctx** out) {
 int skr_nccl_unique_id(char id_out[128]) {
   return guard([&] {
     ncclUniqueId id;
-    SKR_NCCL(ncclGetUniqueId(&id));
+    SKR_NCCL(nccl().GetUniqueId(&id));
     static_assert(sizeof(id) == 128, "ncclUniqueId size");
     std::memcpy(id_out, &id, 128);
   });
@@ -785,7 +785,7 @@ int skr_ctx_create_dist(int device, int rank, int world, const char id[128], skr
     if (world > 1) {
       ncclUniqueId uid;
       std::memcpy(&uid, id, 128);
-      SKR_NCCL(ncclCommInitRank(&x->c.comm, world, uid, rank));
+      SKR_NCCL(nccl().CommInitRank(&x->c.comm, world, uid, rank));
     }
     *out = x.release();
   });
@@ -795,7 +795,7 @@ int skr_ctx_destroy(skr_ctx* ctx) {
   return guard([&] {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
-    if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+    if (ctx->c.comm && nccl().CommDestroy) nccl().CommDestroy(ctx->c.comm);
     if (ctx->c.solver) cusolverDnDestroy(ctx->c.solver);
     cudaStreamSynchronize(ctx->c.aux);
     cudaStreamSynchronize(ctx->c.stream);

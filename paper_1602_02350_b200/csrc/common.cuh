@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -40,11 +41,44 @@ struct Error : std::runtime_error {
       ::skr::raise(SKR_ECUDA, std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
   } while (0)
 
+// NCCL is resolved at run time (dlopen) the first time a distributed context
+// is created: it reuses a libnccl.so.2 already in the process (torch's), so
+// loading this library never pins a different NCCL than the host framework's.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+inline NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h && getenv("SKR_NCCL_PATH")) h = dlopen(getenv("SKR_NCCL_PATH"), RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    }
+  }
+  return api;
+}
+
 #define SKR_NCCL(call)                                                                  \
   do {                                                                                  \
+    if (!::skr::nccl().AllReduce) ::skr::raise(SKR_ENCCL, "libnccl.so.2 not available"); \
     ncclResult_t r_ = (call);                                                           \
     if (r_ != ncclSuccess)                                                              \
-      ::skr::raise(SKR_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));      \
+      ::skr::raise(SKR_ENCCL, std::string(#call) + ": " + ::skr::nccl().GetErrorString(r_)); \
   } while (0)
 
 // Check the last launch and count it (gpu_launches evidence in bench.py).
@@ -120,13 +154,13 @@ struct Ctx {
 
   // Row-sharded collectives (no-ops on one GPU).  Sum of doubles in place.
   void allreduce_sum(double* buf, size_t count) {
-    if (world > 1 && count) SKR_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+    if (world > 1 && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
   }
   void allreduce_max(double* buf, size_t count) {
-    if (world > 1 && count) SKR_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, comm, stream));
+    if (world > 1 && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, comm, stream));
   }
   void allgather_bytes(const void* send, void* recv, size_t bytes_per_rank) {
-    if (world > 1) SKR_NCCL(ncclAllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
+    if (world > 1) SKR_NCCL(nccl().AllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
   }
   void sync() { SKR_CUDA(cudaStreamSynchronize(stream)); }
 };

@@ -272,3 +272,18 @@ def test_config_c1_end_to_end(O):
     assert abs(L - L_o) <= 1e-8 * abs(L_o)                      # BASELINE gate (fp64)
     # identical index sequence for the fp64 inner loop
     assert np.array_equal(pg.index_stream(cfg.seed, 50000), O.index_stream(po.betas(), cfg.seed, 50000))
+
+
+# ---- the drop-in boundary: the reference's own engine drives the GPU problem -------
+def test_reference_engine_drives_gpu_problem():
+    """tests/cpp/drop_in_svrg: the UNMODIFIED reference svrg_solve (oracle/_ref)
+    run on integration/skridge_gpu_problem.hpp's FiniteSumProblem vs on the
+    reference's own PreconditionedRidge; traces must agree to 1e-10."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "drop_in_svrg")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in binary is built only where the reference headers exist")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
