@@ -15,6 +15,7 @@
 #include "lanczos.cuh"
 #include "rng.cuh"
 #include "svrg.cuh"
+#include "sstep.cuh"
 
 using namespace skr;
 
@@ -96,6 +97,7 @@ struct skr_problem {
   int fg_grid = 0;
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
+  DBuf<double> s_state, s_M, s_p;  // s-step inner loop workspaces
 };
 
 // ---------------------------------------------------------------------------
@@ -500,9 +502,88 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
   }
 }
 
-void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m,
-               double eta, double* w_avg) {
+// K10 s-step: prep (all SMs) + chain (one cluster) per chunk of blocks.
+constexpr int64_t kSstepChunkBlocks = 1024;
+static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
+
+template <class T, int CPT, int L>
+void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
+                 double* w_avg) {
+  Ctx& c = p->ctx->c;
+  const int64_t ld = p->ld;
+  const int CS = (int)((ld + 128 * CPT - 1) / (128 * CPT));
+  if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
+  if (p->s_state.n < (size_t)2 * ld) p->s_state.alloc(2 * ld, c.stream);
+  const size_t mneed = (size_t)kSstepChunkBlocks * L * L, pneed = (size_t)kSstepChunkBlocks * L;
+  if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
+  if (p->s_p.n < pneed) p->s_p.alloc(pneed, c.stream);
+  auto prep = sstep_prep_kernel<T, L>;
+  auto chain = sstep_chain_kernel<T, CPT, L>;
+  constexpr size_t prep_smem = sstep_prep_smem<L>();
+  constexpr size_t chain_smem = sstep_chain_smem<CPT, L>();
+  static bool configured = false;
+  if (!configured) {
+    SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
+    SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem));
+    SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  SstepRows rows{p->xt_all, p->B.get(), ld, p->d, p->n_global};
+  sstep_init_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, ld, p->s_state.get());
+  SKR_LAUNCHED(&c);
+  const int64_t chunk_steps = kSstepChunkBlocks * L;
+  for (int64_t s0 = 0; s0 < m; s0 += chunk_steps) {
+    const int64_t steps = std::min(chunk_steps, m - s0);
+    const int64_t nblk = (steps + L - 1) / L;
+    prep<<<(unsigned)nblk, 256, prep_smem, c.stream>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
+                                                        p->reg_coef, mu, snap, eta, p->s_M.get(), p->s_p.get());
+    SKR_LAUNCHED(&c);
+    if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
+      SKR_CUDA(cudaMalloc(&dprof, 16 * sizeof(unsigned long long)));
+      SKR_CUDA(cudaMemset(dprof, 0, 16 * sizeof(unsigned long long)));
+    }
+    ChainArgs ca{rows, idx + s0, steps, p->s_M.get(), p->s_p.get(), mu, eta, p->s_state.get(), dprof};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(160);
+    cfg.dynamicSmemBytes = chain_smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SKR_CUDA(cudaLaunchKernelEx(&cfg, chain, ca));
+    SKR_LAUNCHED(&c);
+  }
+  sstep_finish_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->s_state.get(), ld, p->d, (double)m, w_avg);
+  SKR_LAUNCHED(&c);
+  if (dprof) {
+    unsigned long long h[16] = {};
+    SKR_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+    const double nb = (double)std::max<unsigned long long>(h[6], 1);
+    fprintf(stderr, "[skr] chain cycles/block: wait_full %.0f  step1 %.0f  exchange %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
+            h[0] / nb, h[1] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
+  }
+}
+
+void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
+               double* w_avg) {
   ensure_tables(p);
+  Ctx& c = p->ctx->c;
+  static const bool naive = getenv("SKR_K10") && std::string(getenv("SKR_K10")) == "naive";
+  if (c.prof_on) c.prof_mark("svrg_epoch");
+  if (!naive) {
+    if (p->ld <= 2048) {
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 64>(p, snap, mu, idx, m, eta, w_avg));
+    } else {
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 2, 32>(p, snap, mu, idx, m, eta, w_avg));
+    }
+    if (c.prof_on) c.prof_mark("svrg_epoch");
+    return;
+  }
   EpochArgs a;
   a.Xt = p->xt_all;
   a.B = p->B.get();
@@ -519,8 +600,6 @@ void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64
   a.snapshot = snap;
   a.mu = mu;
   a.w_avg = w_avg;
-  Ctx& c = p->ctx->c;
-  if (c.prof_on) c.prof_mark("svrg_epoch");
   DISPATCH_DTYPE(p->dtype, T, run_epoch_t<T>(c, p->ld, a));
   if (c.prof_on) c.prof_mark("svrg_epoch");
 }
