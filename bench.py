@@ -321,7 +321,7 @@ def solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx):
     """Epoch time and time-to-eps (eps = 1e-6 absolute suboptimality) of the full solve."""
     from paper_1602_02350_b200 import configs
     ref = sk.reference_minimum(p)
-    eta = configs.step_size(prob.max_row_sq())
+    eta = configs.eta_for(cfg, prob.max_row_sq(), prob.mean_beta())
     m = 2 * p.count()
     ctx.profile(True)
     res = sk.svrg_solve(prob, sk.SvrgConfig(cfg.epochs, m, eta, cfg.seed), None, ref.minimum)

@@ -84,5 +84,18 @@ def host_instance(cfg: Config):
 
 
 def step_size(max_row_sq: float) -> float:
-    """BASELINE c1 rule, applied to every config: eta = 1 / (4 max_i ||x~_i||^2)."""
+    """BASELINE c1 rule: eta = 1 / (4 max_i ||x~_i||^2) over the data rows of X~."""
     return 1.0 / (4.0 * max_row_sq)
+
+
+def eta_for(cfg: Config, max_row_sq: float, beta_hat: float) -> float:
+    """Step size per config.  c1 (and c2, where BASELINE is silent) use the c1 rule.
+    For c3-c5 (eta unspecified) the c1 rule diverges — with lambda = 1e-6 the
+    regulariser components lambda (n+d) ||b_j||^2 dominate the smoothness
+    (beta_hat ~ 1.4e3 vs max data row ~ 1.7e2 at c3; the reference itself blows up
+    from 0.0126 to 104 in 4 epochs) — so the rule is capped by the mean smoothness:
+    eta = 1 / (4 max(max_row, beta_hat)) (the scale of the reference's own grid
+    2^j / beta_hat, bench.cpp:96-100)."""
+    if cfg.name in ("c1", "c2"):
+        return step_size(max_row_sq)
+    return 1.0 / (4.0 * max(max_row_sq, beta_hat))

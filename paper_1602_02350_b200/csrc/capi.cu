@@ -16,6 +16,8 @@
 #include "rng.cuh"
 #include "svrg.cuh"
 #include "sstep.cuh"
+#include "tc_gemm.cuh"
+#include "mt_jump.cuh"
 
 using namespace skr;
 
@@ -420,9 +422,60 @@ void seed_mt(Ctx& c, DBuf<MtState>& mt, uint64_t seed) {
   SKR_CUDA(cudaMemcpyAsync(mt.get(), &h, sizeof(MtState), cudaMemcpyHostToDevice, c.stream));
 }
 
+// Jump polynomials t^CH and t^(CH*F) mod phi, built once per process.
+constexpr int64_t kMtChunk = 1 << 18, kMtSuper = 64;
+struct MtJumpPolys {
+  std::vector<uint64_t> small, big;
+};
+const MtJumpPolys& mt_polys() {
+  static MtJumpPolys P = [] {
+    MtJumpPolys q;
+    const auto phi = mtj::characteristic();
+    if ((int)phi.size() != MT_DEG + 1) raise(SKR_EINTERNAL, "mt19937_64 characteristic polynomial has wrong degree");
+    q.small = mtj::pow2_mod(phi, 18);
+    q.big = mtj::pow2_mod(phi, 24);
+    return q;
+  }();
+  return P;
+}
+
+// `count` outputs continuing the stream in *st: the rest of the current twist
+// block on one CTA, then chunks of 2^18 outputs in parallel from jumped states.
 void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
   if (count <= 0) return;
-  mt_generate_kernel<false><<<1, 320, 0, c.stream>>>(st, out, count);
+  if (count < 4 * kMtChunk) {
+    mt_generate_kernel<false><<<1, 320, 0, c.stream>>>(st, out, count);
+    SKR_LAUNCHED(&c);
+    return;
+  }
+  int32_t mti = 0;
+  SKR_CUDA(cudaMemcpyAsync(&mti, &st->mti, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  const int64_t head = mti >= MT_N ? 0 : (MT_N - mti);
+  if (head) {
+    mt_generate_kernel<false><<<1, 320, 0, c.stream>>>(st, out, head);  // leaves the twist pending
+    SKR_LAUNCHED(&c);
+  }
+  const int64_t R = count - head;
+  if (R <= 0) return;
+  const MtJumpPolys& P = mt_polys();
+  if (!c.mt_gsmall.p) {
+    c.mt_gsmall.alloc(MT_POLY_WORDS, c.stream);
+    c.mt_gbig.alloc(MT_POLY_WORDS, c.stream);
+    SKR_CUDA(cudaMemcpyAsync(c.mt_gsmall.get(), P.small.data(), 8 * MT_POLY_WORDS, cudaMemcpyHostToDevice, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(c.mt_gbig.get(), P.big.data(), 8 * MT_POLY_WORDS, cudaMemcpyHostToDevice, c.stream));
+    SKR_CUDA(cudaFuncSetAttribute(mt_jump_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)mt_jump_smem()));
+  }
+  const int64_t C = (R + kMtChunk - 1) / kMtChunk;
+  const int64_t S = (C + kMtSuper - 1) / kMtSuper;
+  DBuf<MtState> sup(S, c.stream), states(C, c.stream);
+  mt_jump_chain_kernel<<<1, 1024, mt_jump_smem(), c.stream>>>(st, (int)S, sup.get(), S, c.mt_gbig.get());
+  SKR_LAUNCHED(&c);
+  mt_jump_chain_kernel<<<(unsigned)S, 1024, mt_jump_smem(), c.stream>>>(sup.get(), (int)kMtSuper, states.get(), C,
+                                                                       c.mt_gsmall.get());
+  SKR_LAUNCHED(&c);
+  mt_generate_chunks_kernel<false><<<(unsigned)C, 320, 0, c.stream>>>(states.get(), kMtChunk, out + head, R, st);
   SKR_LAUNCHED(&c);
 }
 
@@ -469,6 +522,79 @@ int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap,
   c.sync();
   W = hc[0];
   return hc[1];
+}
+
+// ---- tcgen05 3xTF32 GEMM host side --------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SKR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) raise(SKR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map over a row-major matrix (rows x cols, row stride ld
+// elements), box = box_rows x 32 columns, 128-byte swizzle.
+CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(SKR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+template <int BN>
+void tc_gemm_launch(Ctx& c, const float* A, int64_t lda, const float* B, int64_t ldb, const TcGemmArgs& g,
+                    int splits) {
+  const CUtensorMap ma = make_tmap_f32(A, g.M, g.K, lda, TC_BM);
+  const CUtensorMap mb = make_tmap_f32(B, g.N, g.K, ldb, BN);
+  constexpr size_t smem = tc_gemm_smem<BN>();
+  static bool configured = false;
+  if (!configured) {
+    SKR_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid(ceil_div(g.M, TC_BM), ceil_div(g.N, BN), splits);
+  tc_gemm_tf32x3_kernel<BN><<<grid, TC_THREADS, smem, c.stream>>>(ma, mb, g);
+  SKR_LAUNCHED(&c);
+}
+
+// C (fp64, M x N, ldc) = alpha * A . B^T   (A: M x K, B: N x K, fp32, K-major)
+// via 3xTF32 tcgen05 with split-K partials summed in fp64 in split order.
+void tc_gemm_abt(Ctx& c, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                 double alpha, double* C, int64_t ldc, int splits = 0) {
+  if (M <= 0 || N <= 0) return;
+  const int bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  const int64_t tiles = (int64_t)ceil_div(M, TC_BM) * ceil_div(N, bn);
+  if (splits <= 0) {
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c.sm_count + tiles - 1) / tiles,
+                                                        std::max<int64_t>(1, K / (8 * TC_BK))));
+  }
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = (kchunk + TC_BK - 1) / TC_BK * TC_BK;
+  splits = (int)((K + kchunk - 1) / kchunk);
+  DBuf<double> part((size_t)splits * M * N, c.stream);
+  TcGemmArgs g{M, N, K, kchunk, alpha, 0, part.get(), nullptr, 0};
+  if (bn == 64) tc_gemm_launch<64>(c, A, lda, B, ldb, g, splits);
+  else if (bn == 128) tc_gemm_launch<128>(c, A, lda, B, ldb, g, splits);
+  else tc_gemm_launch<256>(c, A, lda, B, ldb, g, splits);
+  EpiStore epi{C, ldc, 1.0, 0.0};
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), 4LL * c.sm_count);
+  splitk_reduce_kernel<EpiStore><<<blocks, 256, 0, c.stream>>>(part.get(), M, N, splits, epi);
+  SKR_LAUNCHED(&c);
 }
 
 // ---- K10 dispatch ----------------------------------------------------------
@@ -811,6 +937,32 @@ __global__ void synth_labels_kernel(const T* __restrict__ X, int64_t ld, int64_t
   }
 }
 
+// Xt[j][i] = X[i][j]  (fp32, 32x32 shared-memory tiles; rows on grid.x)
+__global__ void transpose_f32_kernel(const float* __restrict__ X, int64_t n, int64_t d, int64_t ld,
+                                     float* __restrict__ Xt, int64_t ldt) {
+  __shared__ float tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < n && j < d) ? X[i * ld + j] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (j < d && i < n) Xt[j * ldt + i] = tile[threadIdx.x][r];
+  }
+}
+
+// dst[r][c] = float(src[r][c]) for r < rows, c < cols; zero for cols <= c < ldd
+__global__ void convert_f64_f32_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t cols,
+                                       float* __restrict__ dst, int64_t ldd) {
+  const int64_t total = rows * ldd;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ldd, c = e % ldd;
+    dst[e] = c < cols ? (float)src[r * lds + c] : 0.f;
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -877,6 +1029,8 @@ int skr_ctx_destroy(skr_ctx* ctx) {
     if (ctx->c.comm && nccl().CommDestroy) nccl().CommDestroy(ctx->c.comm);
     if (ctx->c.solver) cusolverDnDestroy(ctx->c.solver);
     cudaStreamSynchronize(ctx->c.aux);
+    ctx->c.mt_gsmall.release();
+    ctx->c.mt_gbig.release();
     cudaStreamSynchronize(ctx->c.stream);
     cudaEventDestroy(ctx->c.ev_fork);
     cudaEventDestroy(ctx->c.ev_join);
@@ -1130,37 +1284,86 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     DBuf<double> Qt((size_t)cap * ld, c.stream), Vt((size_t)k * ld, c.stream);
     Qt.zero();
     int Wb = 0;
+    // fp32 storage: every product runs on the tensor cores (tcgen05, 3xTF32, fp64
+    // split-K sums) with X^T materialised so all operands are K-major.
+    const bool tc = S.dtype == SKR_F32 && n > 0 && !getenv("SKR_LANCZOS_SIMT");
+    const int64_t np = (std::max<int64_t>(n, 1) + 3) / 4 * 4;  // 16-byte row stride over the points
+    DBuf<float> Xt, P32, Rt32;
+    if (tc) {
+      Xt.alloc((size_t)d * np, c.stream);
+      transpose_f32_kernel<<<dim3(ceil_div(n, 32), ceil_div(d, 32)), dim3(32, 8), 0, c.stream>>>(
+          static_cast<const float*>(S.ptr), n, d, ld, Xt.get(), np);
+      SKR_LAUNCHED(&c);
+      Rt32.alloc((size_t)k * np, c.stream);  // Pi^T, then T^T = (X prev^T)^T per iteration
+      convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(k * np, 256), 65535u), 256, 0, c.stream>>>(
+          Pt.get(), n, k, n, Rt32.get(), np);
+      SKR_LAUNCHED(&c);
+      P32.alloc((size_t)k * ld, c.stream);
+    }
     // block = A Pi  -> Vt (k x ld) = scale * Pi^T X   (sketch.cpp:25)
-    DISPATCH_DTYPE(S.dtype, T, {
-      const T* X = static_cast<const T*>(S.ptr);
-      Vt.zero();
-      gemm<double, T, false, false>(&c, k, d, n, Pt.get(), n, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
-    });
+    Vt.zero();
+    if (tc) {
+      tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, k, d, n, scale, Vt.get(), ld);
+    } else {
+      DISPATCH_DTYPE(S.dtype, T, {
+        const T* X = static_cast<const T*>(S.ptr);
+        gemm<double, T, false, false>(&c, k, d, n, Pt.get(), n, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
+      });
+    }
     c.allreduce_sum(Vt.get(), (size_t)k * ld);
     int appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), (int)k);
     if (Wb == 0) raise(SKR_EEMPTY, "krylov_block: A * Pi is numerically zero");
-    DBuf<double> Tm((size_t)std::max<int64_t>(n, 1) * k, c.stream);
+    DBuf<double> Tm(tc ? 1 : (size_t)std::max<int64_t>(n, 1) * k, c.stream);
+    Pt.release();
     for (int64_t j = 1; j < q && appended > 0; ++j) {
       const int64_t W = Wb;
       const double* prev = Qt.get() + (W - appended) * ld;
-      DISPATCH_DTYPE(S.dtype, T, {
-        const T* X = static_cast<const T*>(S.ptr);
-        // T = scale * X prev^T (n x a);   block^T = scale * T^T X (a x d)   (sketch.cpp:35)
-        gemm<T, double, false, true>(&c, n, appended, d, X, ld, prev, ld, EpiStore{Tm.get(), appended, scale, 0.0});
+      if (tc) {
+        // T^T (a x n, fp32) = scale (X prev^T)^T ;  block^T = scale T^T X = scale T^T . (X^T)^T
+        convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(appended * ld, 256), 65535u), 256, 0, c.stream>>>(
+            prev, ld, appended, d, P32.get(), ld);
+        SKR_LAUNCHED(&c);
+        TcGemmArgs g{n, appended, d, (d + TC_BK - 1) / TC_BK * TC_BK, scale, 1, nullptr, Rt32.get(), np};
+        if (appended <= 64) tc_gemm_launch<64>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
+        else if (appended <= 128) tc_gemm_launch<128>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
+        else tc_gemm_launch<256>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
         Vt.zero();
-        gemm<double, T, true, false>(&c, appended, d, n, Tm.get(), appended, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
-      });
+        tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, appended, d, n, scale, Vt.get(), ld);
+      } else {
+        DISPATCH_DTYPE(S.dtype, T, {
+          const T* X = static_cast<const T*>(S.ptr);
+          // T = scale * X prev^T (n x a);   block^T = scale * T^T X (a x d)   (sketch.cpp:35)
+          gemm<T, double, false, true>(&c, n, appended, d, X, ld, prev, ld, EpiStore{Tm.get(), appended, scale, 0.0});
+          Vt.zero();
+          gemm<double, T, true, false>(&c, appended, d, n, Tm.get(), appended, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
+        });
+      }
       c.allreduce_sum(Vt.get(), (size_t)appended * ld);
       appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), appended);
     }
     Tm.release();
-    Pt.release();
+    Rt32.release();
+    P32.release();
     const int64_t W = Wb;
     const int64_t kk = std::min<int64_t>(k, W);
     // Rayleigh-Ritz: G = (X Q)^T (X Q) scale^2 over row chunks (sketch.cpp:59-61)
     DBuf<double> G((size_t)W * W, c.stream);
     G.zero();
-    {
+    if (tc) {
+      DBuf<float> Q32((size_t)W * ld, c.stream), Zt((size_t)W * np, c.stream);
+      convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(W * ld, 256), 65535u), 256, 0, c.stream>>>(
+          Qt.get(), ld, W, d, Q32.get(), ld);
+      SKR_LAUNCHED(&c);
+      for (int64_t w0 = 0; w0 < W; w0 += 256) {  // Z^T rows in slabs of <= 256 basis vectors
+        const int64_t wn = std::min<int64_t>(256, W - w0);
+        TcGemmArgs g{n, wn, d, (d + TC_BK - 1) / TC_BK * TC_BK, scale, 1, nullptr, Zt.get() + w0 * np, np};
+        if (wn <= 64) tc_gemm_launch<64>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
+        else if (wn <= 128) tc_gemm_launch<128>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
+        else tc_gemm_launch<256>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
+      }
+      Xt.release();
+      tc_gemm_abt(c, Zt.get(), np, Zt.get(), np, W, W, n, 1.0, G.get(), W);
+    } else {
       const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
       DBuf<double> Z((size_t)chunk * W, c.stream);
       for (int64_t r = 0; r < n; r += chunk) {
@@ -1582,6 +1785,23 @@ int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out)
       SKR_LAUNCHED(&c);
       SKR_CUDA(cudaMemcpyAsync(out, idx.get(), sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c.stream));
     }
+    c.sync();
+  });
+}
+
+int skr_tc_gemm_test(skr_ctx* ctx, const float* A, const float* B, int64_t M, int64_t N, int64_t K, int splits,
+                     double* C) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    const int64_t ldk = (K + 3) / 4 * 4;  // 16-byte row stride for TMA
+    DBuf<float> dA((size_t)M * ldk, c.stream), dB((size_t)N * ldk, c.stream);
+    DBuf<double> dC((size_t)M * N, c.stream);
+    dA.zero();
+    dB.zero();
+    SKR_CUDA(cudaMemcpy2DAsync(dA.get(), ldk * 4, A, K * 4, K * 4, M, cudaMemcpyHostToDevice, c.stream));
+    SKR_CUDA(cudaMemcpy2DAsync(dB.get(), ldk * 4, B, K * 4, K * 4, N, cudaMemcpyHostToDevice, c.stream));
+    tc_gemm_abt(c, dA.get(), ldk, dB.get(), ldk, M, N, K, 1.0, dC.get(), N, splits);
+    SKR_CUDA(cudaMemcpyAsync(C, dC.get(), sizeof(double) * M * N, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
   });
 }

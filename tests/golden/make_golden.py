@@ -117,7 +117,7 @@ def config_case(name: str, n_override: int | None = None, epochs: int | None = N
     alpha, beta_hat, _ = prob.scalars()
     # eta = 1/(4 max_i ||x~_i||^2): ||x~_i||^2 = beta_i n/(n+d) (ridge.cpp:124-127)
     max_row_sq = float(np.max(betas[:n]) * n / (n + d))
-    eta = configs.step_size(max_row_sq)
+    eta = configs.eta_for(cfg, max_row_sq, beta_hat)
     ep = epochs or cfg.epochs
     wmin, Lstar = R.reference_minimum(Xd, yd, cfg.lam)
     sv = prob.svrg(ep, 2 * n, eta, cfg.seed, reference=Lstar)

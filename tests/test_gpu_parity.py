@@ -213,6 +213,32 @@ def test_svrg_solve_matches_oracle(O, dtype):
     assert rel(got.iterate, want.iterate) < (1e-8 if dtype == np.float64 else 1e-3)
 
 
+def test_long_streams_use_jump_ahead_bit_exact(O):
+    """>= 1 M draws take the parallel jump-ahead path (mt_jump.cuh); bit-exact."""
+    n = 3 * (1 << 20) + 17
+    got = sk.mt_uniforms(7, n)
+    want = O.uniforms(7, n)
+    assert np.array_equal(got, want)
+
+
+def test_svrg_mid_stream_jump_matches_oracle(O):
+    """Two epochs of m = 1.2 M steps: epoch 2 resumes the index stream mid twist
+    block (mti = 48) and takes the jump-ahead path from there."""
+    rng = np.random.default_rng(3)
+    n, d, lam = 600000, 8, 1e-3
+    X = rng.standard_normal((n, d)) * (1.0 / np.arange(1, d + 1))
+    y = rng.standard_normal(n)
+    po = O.problem(X, y, lam, None, None)
+    eta = configs.step_size(po.scalars()[2])
+    want = po.svrg(2, 2 * n, eta, 17)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam), sk.Preconditioner.identity(d, lam))
+    got = sk.svrg_solve(pg, sk.SvrgConfig(2, 2 * n, eta, 17), np.zeros(d))
+    tr = np.array([r.objective for r in got.trace])
+    assert rel(tr, want.trace) < 1e-10
+    assert rel(got.iterate, want.iterate) < 1e-8
+    assert np.array_equal(pg.index_stream(17, 2 * n + 5000), O.index_stream(po.betas(), 17, 2 * n + 5000))
+
+
 def test_svrg_divergence_raises_with_trace():
     X, y, lam, k = small_problem(n=100, d=10, k=2)
     pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
@@ -287,3 +313,73 @@ def test_reference_engine_drives_gpu_problem():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ---- tcgen05 3xTF32 GEMM (fp32-storage Lanczos products) ---------------------------
+@pytest.mark.parametrize("M,N,K,splits", [(128, 64, 32, 1), (300, 64, 1000, 1), (1024, 128, 4096, 4),
+                                          (257, 200, 777, 3), (4096, 256, 2048, 0)])
+def test_tc_gemm_3xtf32(M, N, K, splits):
+    """3xTF32 on tensor cores: ~fp32-accurate products, fp32 accumulation per split."""
+    import ctypes
+    from paper_1602_02350_b200 import _lib
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    C = np.empty(M * N)
+    ctx = sk.default_context()
+    rc = _lib.load().skr_tc_gemm_test(ctx.h, A.ctypes.data, B.ctypes.data, M, N, K, splits, C)
+    assert rc == 0, _lib.last_error()
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    err = np.max(np.abs(C.reshape(M, N) - want)) / np.max(np.abs(want))
+    assert err < 3e-5, err  # fp32 accumulation in TMEM over K (SURVEY: fp32-class, 1e-3 Ritz gate)
+
+
+# ---- BASELINE configs against the reference's own run (tests/golden/configs.json) ------
+def _golden(name):
+    import json, os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "configs.json")))[name]
+
+
+def _pipeline(cfg, X, y, epochs, L_star=None):
+    n, d = X.shape
+    p = sk.RidgeProblem(sk.DataMatrix(X), y.astype(np.float64), cfg.lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))
+    eta = configs.eta_for(cfg, pg.max_row_sq(), pg.mean_beta())
+    res = sk.svrg_solve(pg, sk.SvrgConfig(epochs, 2 * n, eta, cfg.seed), np.zeros(d), L_star)
+    w_hat = pg.apply_inv_sqrt(res.iterate)
+    return p, sv, pg, eta, res, sk.objective(p, w_hat)
+
+
+@pytest.mark.slow
+def test_config_c2_against_reference_golden():
+    import hashlib
+    gold = _golden("c2")
+    cfg = configs.CONFIGS["c2"]
+    X, y = configs.host_instance(cfg)
+    p, sv, pg, eta, res, L = _pipeline(cfg, X, y, cfg.epochs)
+    assert rel(sv.singular_values, gold["sigma"]) < 1e-6                  # BASELINE fp64 Ritz gate
+    assert abs(eta - gold["eta"]) <= 1e-10 * gold["eta"]
+    assert abs(pg.mean_beta() - gold["beta_hat"]) <= 1e-10 * gold["beta_hat"]
+    assert abs(L - gold["L_hat"]) <= 1e-8 * abs(gold["L_hat"])           # BASELINE fp64 L(w^) gate
+    tr = np.array([r.objective for r in res.trace])
+    assert rel(tr, gold["trace"]) < 1e-8
+    idx = pg.index_stream(cfg.seed, 100000)                              # identical index sequence
+    assert hashlib.sha256(np.ascontiguousarray(idx).tobytes()).hexdigest() == gold["idx_sha256_100k"]
+    kappa = sk.conditioned_condition_number(sk.scaled_design(p), cfg.lam, pg.preconditioner())
+    assert abs(kappa - gold["kappa"]) <= 1e-6 * gold["kappa"]            # BASELINE fp64 kappa gate
+    assert abs(sk.reference_minimum(p).minimum - gold["L_star"]) <= 1e-10 * gold["L_star"]
+
+
+@pytest.mark.slow
+def test_config_c3_subsampled_fp32_tensor_core_lanczos():
+    """c3 (fp32 storage) at n = 16384: Lanczos products on tcgen05 (3xTF32)."""
+    gold = _golden("c3_n16384")
+    cfg = configs.CONFIGS["c3"].scaled(16384)
+    X, y = configs.host_instance(cfg)
+    assert X.dtype == np.float32
+    p, sv, pg, eta, res, L = _pipeline(cfg, X, y, gold["epochs"])
+    assert rel(sv.singular_values, gold["sigma"]) < 1e-3                  # BASELINE fp32 Ritz gate
+    assert abs(eta - gold["eta"]) <= 1e-3 * gold["eta"]  # via the fp32-accurate U: same 1e-3 scale as the Ritz gate
+    assert abs(L - gold["L_hat"]) <= 1e-5 * abs(gold["L_hat"])           # BASELINE fp32 L(w^) gate
+    print("c3 sigma rel err", rel(sv.singular_values, gold["sigma"]), "L rel err", abs(L - gold["L_hat"]) / gold["L_hat"])
