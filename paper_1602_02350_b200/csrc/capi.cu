@@ -422,25 +422,22 @@ void seed_mt(Ctx& c, DBuf<MtState>& mt, uint64_t seed) {
   SKR_CUDA(cudaMemcpyAsync(mt.get(), &h, sizeof(MtState), cudaMemcpyHostToDevice, c.stream));
 }
 
-// Jump polynomials t^CH and t^(CH*F) mod phi, built once per process.
-constexpr int64_t kMtChunk = 1 << 18, kMtSuper = 64;
-struct MtJumpPolys {
-  std::vector<uint64_t> small, big;
-};
-const MtJumpPolys& mt_polys() {
-  static MtJumpPolys P = [] {
-    MtJumpPolys q;
+// Jump polynomials t^(CH F^l) mod phi (l < MTJ_MAX_LEVELS), built once per process.
+constexpr int64_t kMtChunk = 1 << 18;  // outputs per generating CTA
+constexpr int kMtFan = 4;              // states produced per CTA per tree level
+const std::vector<std::vector<uint64_t>>& mt_polys() {
+  static const std::vector<std::vector<uint64_t>> P = [] {
     const auto phi = mtj::characteristic();
     if ((int)phi.size() != MT_DEG + 1) raise(SKR_EINTERNAL, "mt19937_64 characteristic polynomial has wrong degree");
-    q.small = mtj::pow2_mod(phi, 18);
-    q.big = mtj::pow2_mod(phi, 24);
-    return q;
+    return mtj::pow2_mod_series(phi, 18, 2, MTJ_MAX_LEVELS);  // 2^18 * 4^l
   }();
   return P;
 }
 
-// `count` outputs continuing the stream in *st: the rest of the current twist
-// block on one CTA, then chunks of 2^18 outputs in parallel from jumped states.
+// `count` outputs continuing the stream in *st.  Long runs: the rest of the
+// current twist block on one CTA, then chunk start states by a jump tree
+// (each level: every CTA jumps its state 3 times by t^(CH 4^l)), then all chunks
+// generated in parallel; the last chunk's CTA writes the final state back.
 void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
   if (count <= 0) return;
   if (count < 4 * kMtChunk) {
@@ -458,24 +455,35 @@ void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
   }
   const int64_t R = count - head;
   if (R <= 0) return;
-  const MtJumpPolys& P = mt_polys();
-  if (!c.mt_gsmall.p) {
-    c.mt_gsmall.alloc(MT_POLY_WORDS, c.stream);
-    c.mt_gbig.alloc(MT_POLY_WORDS, c.stream);
-    SKR_CUDA(cudaMemcpyAsync(c.mt_gsmall.get(), P.small.data(), 8 * MT_POLY_WORDS, cudaMemcpyHostToDevice, c.stream));
-    SKR_CUDA(cudaMemcpyAsync(c.mt_gbig.get(), P.big.data(), 8 * MT_POLY_WORDS, cudaMemcpyHostToDevice, c.stream));
+  const int64_t C = (R + kMtChunk - 1) / kMtChunk;
+  int levels = 0;
+  for (int64_t span = 1; span < C; span *= kMtFan) ++levels;
+  if (levels > MTJ_MAX_LEVELS) raise(SKR_EPARAM, "random stream request too long");
+  const auto& P = mt_polys();
+  if (!c.mt_polys.p) {
+    c.mt_polys.alloc((int64_t)MTJ_MAX_LEVELS * (MT_POLY_WORDS + 1), c.stream);
+    for (int l = 0; l < MTJ_MAX_LEVELS; ++l)
+      SKR_CUDA(cudaMemcpyAsync(c.mt_polys.get() + (size_t)l * (MT_POLY_WORDS + 1), P[l].data(),
+                               8 * (MT_POLY_WORDS + 1), cudaMemcpyHostToDevice, c.stream));
     SKR_CUDA(cudaFuncSetAttribute(mt_jump_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)mt_jump_smem()));
+    c.sync();  // host vectors are static, but keep the upload ordered before first use
   }
-  const int64_t C = (R + kMtChunk - 1) / kMtChunk;
-  const int64_t S = (C + kMtSuper - 1) / kMtSuper;
-  DBuf<MtState> sup(S, c.stream), states(C, c.stream);
-  mt_jump_chain_kernel<<<1, 1024, mt_jump_smem(), c.stream>>>(st, (int)S, sup.get(), S, c.mt_gbig.get());
-  SKR_LAUNCHED(&c);
-  mt_jump_chain_kernel<<<(unsigned)S, 1024, mt_jump_smem(), c.stream>>>(sup.get(), (int)kMtSuper, states.get(), C,
-                                                                       c.mt_gsmall.get());
-  SKR_LAUNCHED(&c);
-  mt_generate_chunks_kernel<false><<<(unsigned)C, 320, 0, c.stream>>>(states.get(), kMtChunk, out + head, R, st);
+  // states at level l: stride CH * 4^l, count ceil(C / 4^l); level `levels` = *st
+  std::vector<int64_t> cnt(levels + 1);
+  int64_t span = 1;
+  for (int l = 0; l <= levels; ++l, span *= kMtFan) cnt[l] = (C + span - 1) / span;
+  DBuf<MtState> a(C, c.stream), b(C, c.stream);
+  const MtState* src = st;
+  MtState* dst = nullptr;
+  for (int l = levels - 1; l >= 0; --l) {
+    dst = (src == a.get()) ? b.get() : a.get();
+    mt_jump_chain_kernel<<<(unsigned)cnt[l + 1], 1024, mt_jump_smem(), c.stream>>>(
+        src, kMtFan, dst, cnt[l], c.mt_polys.get() + (size_t)l * (MT_POLY_WORDS + 1));
+    SKR_LAUNCHED(&c);
+    src = dst;
+  }
+  mt_generate_chunks_kernel<false><<<(unsigned)C, 320, 0, c.stream>>>(src, kMtChunk, out + head, R, st);
   SKR_LAUNCHED(&c);
 }
 
@@ -1029,8 +1037,7 @@ int skr_ctx_destroy(skr_ctx* ctx) {
     if (ctx->c.comm && nccl().CommDestroy) nccl().CommDestroy(ctx->c.comm);
     if (ctx->c.solver) cusolverDnDestroy(ctx->c.solver);
     cudaStreamSynchronize(ctx->c.aux);
-    ctx->c.mt_gsmall.release();
-    ctx->c.mt_gbig.release();
+    ctx->c.mt_polys.release();
     cudaStreamSynchronize(ctx->c.stream);
     cudaEventDestroy(ctx->c.ev_fork);
     cudaEventDestroy(ctx->c.ev_join);

@@ -131,7 +131,7 @@ struct Ctx {
   ncclComm_t comm = nullptr;
   int sm_count = 148;
   int64_t launches = 0;
-  DBuf<uint64_t> mt_gsmall, mt_gbig;  // mt19937_64 jump polynomials (device copies)
+  DBuf<uint64_t> mt_polys;  // mt19937_64 jump polynomials per tree level (device copy)
 
   // Optional CUDA-event timing of named hot kernels on the context stream
   // (bench.py: the dominant kernel's average launch duration).
