@@ -342,6 +342,83 @@ def solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx):
         "trace": [r.objective for r in res.trace][:10]}}
 
 
+def run_solve(args):
+    """End-to-end time-to-eps (eps = 1e-6 absolute suboptimality) per config on
+    this GPU: sketch (block_lanczos) + precompute (preconditioned_components) +
+    SVRG epochs until the first epoch with L(w_s) - L* <= eps (cap: cfg.epochs),
+    as SketchedSolveDiagnostics and bench.cpp:182-189 time it.  c5 adds the
+    BASELINE lambda sweep, preconditioned vs unpreconditioned, with one sketch
+    reused across lambdas (block_lanczos is lambda-independent)."""
+    from paper_1602_02350_b200 import configs, skridge as sk
+    ctx = sk.Context(0)
+    sk._default_ctx = ctx
+    eps = 1e-6
+    # one-time library initialisation (solver handles, kernel attributes, the
+    # mt19937_64 jump tables) on a small instance, outside every timed phase
+    wcfg = configs.CONFIGS["c1"]
+    wd = sk.DataMatrix.generate(sk.SynthSpec(1 << 19, 64, "f64", 9, 0, 0.0, False, 0.1), ctx)
+    wp = sk.RidgeProblem(wd, wd.labels(), 1e-3)
+    wsv = sk.block_lanczos(sk.scaled_design(wp), sk.LanczosConfig(8, 0.5, 1, 2))
+    wprob = sk.preconditioned_components(wp, sk.build_sketched(wsv, 1e-3))
+    sk.svrg_solve(wprob, sk.SvrgConfig(2, 1 << 20, configs.step_size(wprob.max_row_sq()), 1), None,
+                  sk.reference_minimum(wp).minimum)
+    del wprob, wp, wd, wcfg
+    for name in args.solve.split(","):
+        cfg = configs.CONFIGS[name]
+        spec = sk.SynthSpec(cfg.n, cfg.d, cfg.dtype, cfg.seed, cfg.spectrum, cfg.spectrum_param, cfg.t_scale, cfg.tau)
+        data = sk.DataMatrix.generate(spec, ctx)
+        y = data.labels()
+        # the sketch twice: the first call also grows the device memory pool to
+        # this size; the second (reported) is the steady-state cost
+        for _ in range(2):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            sv = sk.block_lanczos(sk.scaled_design(sk.RidgeProblem(data, y, cfg.lam)),
+                                  sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+            ctx.synchronize()
+            sketch_s = time.perf_counter() - t0
+        lams = [1e-4, 1e-6, 1e-8] if name == "c5" else [cfg.lam]
+        for lam in lams:
+            p = sk.RidgeProblem(data, y, lam)
+            t0 = time.perf_counter()
+            ref = sk.reference_minimum(p)
+            refmin_s = time.perf_counter() - t0
+            for method in (["sketched-svrg", "svrg"] if name == "c5" else ["sketched-svrg"]):
+                t0 = time.perf_counter()
+                pc = sk.build_sketched(sv, lam) if method == "sketched-svrg" else sk.Preconditioner.identity(cfg.d, lam)
+                prob = sk.preconditioned_components(p, pc)
+                ctx.synchronize()
+                pre_s = time.perf_counter() - t0
+                eta = configs.eta_for(cfg, prob.max_row_sq(), prob.mean_beta())
+                m = 2 * cfg.n
+                row = {"solve": name, "method": method, "lambda": lam, "n": cfg.n, "d": cfg.d, "dtype": cfg.dtype,
+                       "k": cfg.k if method == "sketched-svrg" else 0, "q": cfg.q, "m": m, "eta": eta,
+                       "beta_hat": prob.mean_beta(), "alpha": prob.strong_convexity(),
+                       "sketch_s": round(sketch_s, 4) if method == "sketched-svrg" else 0.0,
+                       "precompute_s": round(pre_s, 4), "reference_minimum_s": round(refmin_s, 4),
+                       "L_star": ref.minimum}
+                try:
+                    ctx.profile(True)
+                    res = sk.svrg_solve(prob, sk.SvrgConfig(cfg.epochs, m, eta, cfg.seed), None, ref.minimum,
+                                        stop_suboptimality=eps)
+                    k10_ms, k10_n = ctx.profile_read("svrg_epoch")
+                    ctx.profile(False)
+                    hit = next((r for r in res.trace if r.suboptimality is not None and r.suboptimality <= eps), None)
+                    setup = row["sketch_s"] + pre_s
+                    row.update({
+                        "epochs_run": len(res.trace), "epochs_to_eps": hit.epoch if hit else None,
+                        "time_to_eps_s": round(setup + hit.elapsed_ms / 1e3, 4) if hit else None,
+                        "epoch_ms": round(res.trace[-1].elapsed_ms / len(res.trace), 3),
+                        "inner_loop_ns_per_step": round(k10_ms / max(k10_n, 1) * 1e6 / m, 2),
+                        "suboptimality": [r.suboptimality for r in res.trace]})
+                except sk.DivergenceError as e:
+                    ctx.profile(False)
+                    row.update({"diverged": str(e), "suboptimality": [r.suboptimality for r in e.trace]})
+                print(json.dumps(row), flush=True)
+                del prob
+        del data
+
+
 def run_sweep(args):
     """K9 alone at every BASELINE shape (identity preconditioner: X~ = X, no copy)."""
     import torch
@@ -391,6 +468,7 @@ def run_sweep(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sweep", default="", help="comma list of configs: K9 alone at each shape")
+    ap.add_argument("--solve", default="", help="comma list of configs: end-to-end time-to-eps per config")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
@@ -403,6 +481,9 @@ def main():
     cfg = configs.CONFIGS[args.config]
     if args.sweep:
         run_sweep(args)
+        return
+    if args.solve:
+        run_solve(args)
         return
     if args.impl == "reference":
         rank, world, _ = dist_env()

@@ -165,6 +165,10 @@ int skr_epoch(skr_problem* p, const double* snapshot, const double* mu, const in
  * none.  On divergence returns SKR_EDIVERGED with the partial trace written. */
 int skr_svrg(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference,
              double* w_out, skr_epoch_record* trace, int64_t* epochs_done);
+/* skr_svrg that stops after the first epoch whose suboptimality (objective -
+ * reference) is <= target: the time-to-epsilon protocol of bench.cpp:182-189. */
+int skr_svrg_until(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double target,
+                   double* w_out, skr_epoch_record* trace, int64_t* epochs_done);
 /* the index stream skr_svrg would draw (test hook; `count` steps from seed) */
 int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out);
 /* NormalSampler(seed).uniform() x count from the device mt19937_64 (test hook) */

@@ -230,12 +230,22 @@ inline Preconditioner build_sketched(const SketchedSvd& sv, double lambda) {
 }
 
 // ---- svrg (svrg.hpp) -----------------------------------------------------------------
+enum class SvrgMode { Theoretical, Tuned };  // svrg.hpp:37 (a label; the solve is identical)
+
 struct SvrgConfig {
   std::size_t epochs = 1;
   std::size_t epoch_length = 1;
   double step_size = 0.1;
   std::uint64_t seed = 0;
+  SvrgMode mode = SvrgMode::Tuned;
 };
+
+/// bench.cpp:96-100: 2^j / beta_hat, j = -3..3.
+inline std::vector<double> eta_grid(double beta_hat) {
+  std::vector<double> g;
+  for (int j = -3; j <= 3; ++j) g.push_back(std::ldexp(1.0, j) / beta_hat);
+  return g;
+}
 
 struct SvrgResult {
   Vector iterate;
@@ -327,17 +337,35 @@ inline std::shared_ptr<PreconditionedRidge> preconditioned_components(const Ridg
 
 inline double mean_beta(const PreconditionedRidge& p) { return p.mean_beta(); }
 
+/// svrg.cpp:219-232.
+inline SvrgConfig theoretical_params(const PreconditionedRidge& p, double w0_gap, double epsilon) {
+  if (!(epsilon > 0.0) || !(w0_gap > 0.0)) throw ParameterError("theoretical_params: w0_gap and epsilon must be positive");
+  const double bh = p.mean_beta();
+  SvrgConfig cfg;
+  cfg.mode = SvrgMode::Theoretical;
+  cfg.epochs = (std::size_t)std::max(1.0, std::ceil(std::log(w0_gap / epsilon)));
+  cfg.epoch_length = (std::size_t)std::max(1.0, std::ceil(bh / p.strong_convexity()));
+  cfg.step_size = 0.1 / bh;
+  return cfg;
+}
+
 /// svrg.cpp:152-211 on the device, drawing the reference's index stream.
+/// `stop_suboptimality` (with a reference value) ends after the first epoch at
+/// or below it — the time-to-epsilon protocol; the reference runs every epoch.
 inline SvrgResult svrg_solve(const PreconditionedRidge& p, const SvrgConfig& cfg, const Vector& w0,
-                             std::optional<double> reference_value = std::nullopt) {
+                             std::optional<double> reference_value = std::nullopt,
+                             std::optional<double> stop_suboptimality = std::nullopt) {
   if (w0.size() != p.dimension()) throw DimensionError("svrg: start point length mismatch");
   skr_svrg_config c{(int64_t)cfg.epochs, (int64_t)cfg.epoch_length, cfg.step_size, cfg.seed};
   std::vector<skr_epoch_record> rec(cfg.epochs ? cfg.epochs : 1);
   SvrgResult out;
   out.iterate.resize(p.dimension());
   int64_t done = 0;
-  const int rc = skr_svrg(p.get(), &c, w0.data(), reference_value ? *reference_value : NAN, out.iterate.data(),
-                          rec.data(), &done);
+  const double ref = reference_value ? *reference_value : NAN;
+  const int rc = stop_suboptimality
+                     ? skr_svrg_until(p.get(), &c, w0.data(), ref, *stop_suboptimality, out.iterate.data(), rec.data(),
+                                      &done)
+                     : skr_svrg(p.get(), &c, w0.data(), ref, out.iterate.data(), rec.data(), &done);
   for (int64_t s = 0; s < done; ++s) {
     EpochRecord r;
     r.epoch = (std::size_t)rec[s].epoch;

@@ -423,20 +423,20 @@ void seed_mt(Ctx& c, DBuf<MtState>& mt, uint64_t seed) {
 }
 
 // Jump polynomials t^(CH F^l) mod phi (l < MTJ_MAX_LEVELS), built once per process.
-constexpr int64_t kMtChunk = 1 << 18;  // outputs per generating CTA
-constexpr int kMtFan = 4;              // states produced per CTA per tree level
+constexpr int64_t kMtChunk = 1 << 16;  // outputs per generating CTA
+constexpr int kMtFan = 2;              // states produced per CTA per tree level (one jump)
 const std::vector<std::vector<uint64_t>>& mt_polys() {
   static const std::vector<std::vector<uint64_t>> P = [] {
     const auto phi = mtj::characteristic();
     if ((int)phi.size() != MT_DEG + 1) raise(SKR_EINTERNAL, "mt19937_64 characteristic polynomial has wrong degree");
-    return mtj::pow2_mod_series(phi, 18, 2, MTJ_MAX_LEVELS);  // 2^18 * 4^l
+    return mtj::pow2_mod_series(phi, 16, 1, MTJ_MAX_LEVELS);  // t^(2^16 * 2^l)
   }();
   return P;
 }
 
 // `count` outputs continuing the stream in *st.  Long runs: the rest of the
-// current twist block on one CTA, then chunk start states by a jump tree
-// (each level: every CTA jumps its state 3 times by t^(CH 4^l)), then all chunks
+// current twist block on one CTA, then chunk start states by a binary jump tree
+// (level l: every CTA copies its state and jumps it once by t^(CH 2^l)), then all chunks
 // generated in parallel; the last chunk's CTA writes the final state back.
 void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
   if (count <= 0) return;
@@ -469,7 +469,7 @@ void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
                                   (int)mt_jump_smem()));
     c.sync();  // host vectors are static, but keep the upload ordered before first use
   }
-  // states at level l: stride CH * 4^l, count ceil(C / 4^l); level `levels` = *st
+  // states at level l: stride CH * 2^l, count ceil(C / 2^l); level `levels` = *st
   std::vector<int64_t> cnt(levels + 1);
   int64_t span = 1;
   for (int l = 0; l <= levels; ++l, span *= kMtFan) cnt[l] = (C + span - 1) / span;
@@ -503,7 +503,8 @@ void draw_indices(skr_problem* p, DBuf<double>& u, DBuf<int64_t>& idx, int64_t m
 // V (a rows x ld) is overwritten.  Returns the number of rows appended.
 int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap, double* V, int a) {
   DBuf<double> ref(1, c.stream), rdiag(a, c.stream), tau(a, c.stream);
-  row_norm_max_kernel<<<1, 1024, 0, c.stream>>>(V, ld, d, a, ref.get());
+  ref.zero();
+  row_norm_max_kernel<<<(unsigned)a, 256, 0, c.stream>>>(V, ld, d, a, ref.get());
   SKR_LAUNCHED(&c);
   if (W > 0) {
     DBuf<double> C((size_t)a * W, c.stream);
@@ -637,7 +638,7 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
 }
 
 // K10 s-step: prep (all SMs) + chain (one cluster) per chunk of blocks.
-constexpr int64_t kSstepChunkBlocks = 1024;
+constexpr int64_t kSstepChunkBlocks = 256;  // blocks per prep/chain launch pair (double-buffered)
 static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
 
 template <class T, int CPT, int L>
@@ -648,7 +649,7 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   const int CS = (int)((ld + 128 * CPT - 1) / (128 * CPT));
   if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
   if (p->s_state.n < (size_t)2 * ld) p->s_state.alloc(2 * ld, c.stream);
-  const size_t mneed = (size_t)kSstepChunkBlocks * L * L, pneed = (size_t)kSstepChunkBlocks * L;
+  const size_t mneed = (size_t)2 * kSstepChunkBlocks * L * L, pneed = (size_t)2 * kSstepChunkBlocks * L;
   if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
   if (p->s_p.n < pneed) p->s_p.alloc(pneed, c.stream);
   auto prep = sstep_prep_kernel<T, L>;
@@ -665,18 +666,29 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   SstepRows rows{p->xt_all, p->B.get(), ld, p->d, p->n_global};
   sstep_init_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, ld, p->s_state.get());
   SKR_LAUNCHED(&c);
+  // chunks of kSstepChunkBlocks blocks: prep(i+1) runs on the side stream (all
+  // free SMs) while chain(i) runs on the main stream; M/p are double-buffered.
   const int64_t chunk_steps = kSstepChunkBlocks * L;
-  for (int64_t s0 = 0; s0 < m; s0 += chunk_steps) {
+  SKR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+  int64_t chunk = 0;
+  for (int64_t s0 = 0; s0 < m; s0 += chunk_steps, ++chunk) {
+    const int b = (int)(chunk & 1);
+    double* Mb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * L * L;
+    double* pb = p->s_p.get() + (size_t)b * kSstepChunkBlocks * L;
     const int64_t steps = std::min(chunk_steps, m - s0);
     const int64_t nblk = (steps + L - 1) / L;
-    prep<<<(unsigned)nblk, 256, prep_smem, c.stream>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
-                                                        p->reg_coef, mu, snap, eta, p->s_M.get(), p->s_p.get());
+    if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
+    prep<<<(unsigned)nblk, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
+                                                     p->reg_coef, mu, snap, eta, Mb, pb);
     SKR_LAUNCHED(&c);
+    SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
+    SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
     if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
       SKR_CUDA(cudaMalloc(&dprof, 16 * sizeof(unsigned long long)));
       SKR_CUDA(cudaMemset(dprof, 0, 16 * sizeof(unsigned long long)));
     }
-    ChainArgs ca{rows, idx + s0, steps, p->s_M.get(), p->s_p.get(), mu, eta, p->s_state.get(), dprof};
+    ChainArgs ca{rows, idx + s0, steps, Mb, pb, mu, eta, p->s_state.get(), dprof};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(160);
@@ -691,6 +703,7 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     cfg.numAttrs = 1;
     SKR_CUDA(cudaLaunchKernelEx(&cfg, chain, ca));
     SKR_LAUNCHED(&c);
+    SKR_CUDA(cudaEventRecord(c.ev_chain[b], c.stream));
   }
   sstep_finish_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->s_state.get(), ld, p->d, (double)m, w_avg);
   SKR_LAUNCHED(&c);
@@ -983,10 +996,18 @@ int skr_abi_version(void) { return SKR_ABI_VERSION; }
 static void ctx_init(Ctx& c, int device) {
   c.device = device;
   SKR_CUDA(cudaSetDevice(device));
-  SKR_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-  SKR_CUDA(cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking));
+  // the main stream carries the latency-bound chain kernels: highest priority,
+  // so overlapped bulk work queued on the side stream never delays them
+  int prio_lo = 0, prio_hi = 0;
+  SKR_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  SKR_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, prio_hi));
+  SKR_CUDA(cudaStreamCreateWithPriority(&c.aux, cudaStreamNonBlocking, prio_lo));
   SKR_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
   SKR_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+  for (int b = 0; b < 2; ++b) {
+    SKR_CUDA(cudaEventCreateWithFlags(&c.ev_prep[b], cudaEventDisableTiming));
+    SKR_CUDA(cudaEventCreateWithFlags(&c.ev_chain[b], cudaEventDisableTiming));
+  }
   SKR_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   SKR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1041,6 +1062,10 @@ int skr_ctx_destroy(skr_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     cudaEventDestroy(ctx->c.ev_fork);
     cudaEventDestroy(ctx->c.ev_join);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(ctx->c.ev_prep[b]);
+      cudaEventDestroy(ctx->c.ev_chain[b]);
+    }
     cudaStreamDestroy(ctx->c.aux);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
@@ -1726,8 +1751,8 @@ int skr_epoch(skr_problem* p, const double* snapshot, const double* mu, const in
   });
 }
 
-int skr_svrg(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double* w_out,
-             skr_epoch_record* trace, int64_t* epochs_done) {
+static int svrg_impl(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double stop_at,
+                     double* w_out, skr_epoch_record* trace, int64_t* epochs_done) {
   return guard([&] {
     if (!p || !cfg) raise(SKR_EPARAM, "null argument");
     if (cfg->epochs < 1 || cfg->epoch_length < 1) raise(SKR_EPARAM, "svrg: epochs and epoch length must be >= 1");
@@ -1770,10 +1795,23 @@ int skr_svrg(skr_problem* p, const skr_svrg_config* cfg, const double* w0, doubl
         c.sync();
         raise(SKR_EDIVERGED, "svrg: objective diverged at epoch " + std::to_string(s));
       }
+      if (!std::isnan(stop_at) && !std::isnan(reference) && r.suboptimality <= stop_at) break;
     }
     SKR_CUDA(cudaMemcpyAsync(w_out, w.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
   });
+}
+
+int skr_svrg(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double* w_out,
+             skr_epoch_record* trace, int64_t* epochs_done) {
+  return svrg_impl(p, cfg, w0, reference, std::numeric_limits<double>::quiet_NaN(), w_out, trace, epochs_done);
+}
+
+int skr_svrg_until(skr_problem* p, const skr_svrg_config* cfg, const double* w0, double reference, double target,
+                   double* w_out, skr_epoch_record* trace, int64_t* epochs_done) {
+  if (!(target > 0.0) || std::isnan(reference))
+    return guard([] { raise(SKR_EPARAM, "svrg_until: needs a reference value and a positive target"); });
+  return svrg_impl(p, cfg, w0, reference, target, w_out, trace, epochs_done);
 }
 
 int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out) {

@@ -127,6 +127,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;                    // side stream for overlapped small kernels
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_prep[2] = {}, ev_chain[2] = {};  // s-step prep/chain double buffering
   cusolverDnHandle_t solver = nullptr;
   ncclComm_t comm = nullptr;
   int sm_count = 148;

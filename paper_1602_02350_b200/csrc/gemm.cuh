@@ -1,5 +1,5 @@
-// Tiled FP64-accumulate SIMT GEMM for the tall-skinny products around the hot
-// path (Krylov blocks, Rayleigh-Ritz Gram, preconditioner build).
+// FP64 tensor-core (DMMA) GEMM for the tall-skinny products around the hot path
+// (fp64 Krylov blocks, Rayleigh-Ritz Gram, preconditioner build).
 //
 //   C[M x N] (+)= alpha * op(A)[M x K] * op(B)[K x N]
 //
@@ -16,8 +16,7 @@
 
 namespace skr {
 
-constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 16, GEMM_THREADS = 256;
-constexpr int GEMM_PAD = 2;
+constexpr int GEMM_BK = 16, GEMM_THREADS = 256;
 
 template <class T>
 __device__ __forceinline__ double ld_as_double(const T* p) { return static_cast<double>(__ldg(p)); }
@@ -41,80 +40,100 @@ struct EpiPartial {  // split-K partial: ws[z][m][n]
   }
 };
 
-template <class TA, class TB, bool A_T, bool B_T, class Epi, bool PARTIAL>
-__global__ void __launch_bounds__(GEMM_THREADS)
+// FP64 tensor-core GEMM (DMMA, mma.sync m8n8k4 f64): CTA tile BM x BN x 16,
+// 8 warps of 32 x 32, register-staged double-buffered shared tiles (k-major, so
+// the m8n8k4 fragment loads are two conflict-free wavefronts).
+constexpr int GEMM_SP = 4;  // row pad (doubles): k-rows 0..3 start 8 banks apart
+constexpr size_t gemm_smem(int bm, int bn) { return sizeof(double) * 2 * GEMM_BK * (bm + bn + 2 * GEMM_SP); }
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <class TA, class TB, bool A_T, bool B_T, class Epi, bool PARTIAL, int BM, int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 2)
 gemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t lda,
             const TB* __restrict__ B, int64_t ldb, int64_t kchunk, Epi epi) {
-  __shared__ __align__(16) double As[2][GEMM_BK][GEMM_BM + GEMM_PAD];
-  __shared__ __align__(16) double Bs[2][GEMM_BK][GEMM_BN + GEMM_PAD];
-  const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
-  const int64_t m0 = (int64_t)blockIdx.x * GEMM_BM;
-  const int64_t n0 = (int64_t)blockIdx.y * GEMM_BN;
+  static_assert((BM / 32) * (BN / 32) == GEMM_THREADS / 32, "8 warps of 32x32");
+  constexpr int PA = (BM * GEMM_BK) / GEMM_THREADS, PB = (BN * GEMM_BK) / GEMM_THREADS;
+  constexpr int SP = GEMM_SP;
+  extern __shared__ __align__(16) double gemm_sm[];
+  auto As = reinterpret_cast<double(*)[GEMM_BK][BM + SP]>(gemm_sm);
+  auto Bs = reinterpret_cast<double(*)[GEMM_BK][BN + SP]>(gemm_sm + 2 * GEMM_BK * (BM + SP));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp % (BM / 32)) * 32, wn = (warp / (BM / 32)) * 32;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t kend = min(K, kbeg + kchunk);
 
-  double acc[4][4] = {};
-  double ra[4], rb[4];
+  double acc[4][4][2] = {};
+  double ra[PA], rb[PB];
 
-  auto load_a = [&](int64_t k0) {
+  // element p of this thread's share of the A tile: (mm, kk)
+  auto a_idx = [&](int p, int& mm, int& kk) {
+    const int e = tid + p * GEMM_THREADS;
+    if (!A_T) { kk = e % GEMM_BK; mm = e / GEMM_BK; }   // k fastest: row-contiguous A
+    else      { mm = e % BM; kk = e / BM; }             // m fastest: column-contiguous A
+  };
+  auto b_idx = [&](int p, int& nn, int& kk) {
+    const int e = tid + p * GEMM_THREADS;
+    if (!B_T) { nn = e % BN; kk = e / BN; }
+    else      { kk = e % GEMM_BK; nn = e / GEMM_BK; }
+  };
+  auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < PA; ++p) {
       int mm, kk;
-      if (!A_T) { kk = tid % 16; mm = tid / 16 + 16 * p; }
-      else      { mm = tid % 64; kk = tid / 64 + 4 * p; }
+      a_idx(p, mm, kk);
       const int64_t m = m0 + mm, k = k0 + kk;
       ra[p] = (m < M && k < kend) ? ld_as_double(A_T ? A + k * lda + m : A + m * lda + k) : 0.0;
     }
-  };
-  auto load_b = [&](int64_t k0) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < PB; ++p) {
       int nn, kk;
-      if (!B_T) { nn = tid % 64; kk = tid / 64 + 4 * p; }
-      else      { kk = tid % 16; nn = tid / 16 + 16 * p; }
+      b_idx(p, nn, kk);
       const int64_t n = n0 + nn, k = k0 + kk;
       rb[p] = (n < N && k < kend) ? ld_as_double(B_T ? B + n * ldb + k : B + k * ldb + n) : 0.0;
     }
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < PA; ++p) {
       int mm, kk;
-      if (!A_T) { kk = tid % 16; mm = tid / 16 + 16 * p; }
-      else      { mm = tid % 64; kk = tid / 64 + 4 * p; }
+      a_idx(p, mm, kk);
       As[buf][kk][mm] = ra[p];
-      int nn;
-      if (!B_T) { nn = tid % 64; kk = tid / 64 + 4 * p; }
-      else      { kk = tid % 16; nn = tid / 16 + 16 * p; }
+    }
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      int nn, kk;
+      b_idx(p, nn, kk);
       Bs[buf][kk][nn] = rb[p];
     }
   };
 
   if (kbeg < kend) {
-    load_a(kbeg);
-    load_b(kbeg);
+    load(kbeg);
     store(0);
     __syncthreads();
     int buf = 0;
+    const int fr = lane >> 2, fk = lane & 3;
     for (int64_t k0 = kbeg; k0 < kend; k0 += GEMM_BK) {
       const bool more = k0 + GEMM_BK < kend;
-      if (more) {
-        load_a(k0 + GEMM_BK);
-        load_b(k0 + GEMM_BK);
-      }
+      if (more) load(k0 + GEMM_BK);
 #pragma unroll
-      for (int kk = 0; kk < GEMM_BK; ++kk) {
-        const double2 a01 = *reinterpret_cast<const double2*>(&As[buf][kk][ty * 4]);
-        const double2 a23 = *reinterpret_cast<const double2*>(&As[buf][kk][ty * 4 + 2]);
-        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4 + 2]);
-        const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-        const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+      for (int k4 = 0; k4 < GEMM_BK; k4 += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[buf][k4 + fk][wm + 8 * i + fr];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k4 + fk][wn + 8 * j + fr];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       }
       if (more) {
         store(buf ^ 1);
@@ -123,16 +142,20 @@ gemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t l
       }
     }
   }
+  // C fragment: row lane/4, columns 2 (lane%4) + {0, 1}
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int64_t m = m0 + ty * 4 + i;
+    const int64_t m = m0 + wm + 8 * i + (lane >> 2);
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int64_t n = n0 + tx * 4 + j;
-      if (n >= N) continue;
-      if constexpr (PARTIAL) epi(m, n, acc[i][j], (int)blockIdx.z);
-      else epi(m, n, acc[i][j]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (n >= N) continue;
+        if constexpr (PARTIAL) epi(m, n, acc[i][j][h], (int)blockIdx.z);
+        else epi(m, n, acc[i][j][h]);
+      }
     }
   }
 }
@@ -151,11 +174,10 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int64_t M, i
 }
 
 // Host driver.  `splits` <= 0 picks a split count that fills ~2 waves.
-template <class TA, class TB, bool A_T, bool B_T, class Epi>
-void gemm(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, const TB* B,
-          int64_t ldb, Epi epi, int splits = 0) {
-  if (M <= 0 || N <= 0) return;
-  const int64_t tiles = (int64_t)ceil_div(M, GEMM_BM) * ceil_div(N, GEMM_BN);
+template <class TA, class TB, bool A_T, bool B_T, class Epi, int BM, int BN>
+void gemm_tiled(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, const TB* B,
+                int64_t ldb, Epi epi, int splits) {
+  const int64_t tiles = (int64_t)ceil_div(M, BM) * ceil_div(N, BN);
   if (splits <= 0) {
     const int64_t want = 2LL * ctx->sm_count;
     splits = tiles >= want ? 1 : (int)std::min<int64_t>((want + tiles - 1) / tiles,
@@ -166,21 +188,44 @@ void gemm(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, c
   kchunk = (kchunk + GEMM_BK - 1) / GEMM_BK * GEMM_BK;
   if (kchunk == 0) kchunk = GEMM_BK;
   splits = (int)std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
-  dim3 grid(ceil_div(M, GEMM_BM), ceil_div(N, GEMM_BN), splits);
+  dim3 grid(ceil_div(M, BM), ceil_div(N, BN), splits);
+  constexpr size_t smem = gemm_smem(BM, BN);
   if (splits == 1) {
-    gemm_kernel<TA, TB, A_T, B_T, Epi, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(
+    static bool attr = [] {
+      SKR_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, A_T, B_T, Epi, false, BM, BN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      return true;
+    }();
+    (void)attr;
+    gemm_kernel<TA, TB, A_T, B_T, Epi, false, BM, BN><<<grid, GEMM_THREADS, smem, ctx->stream>>>(
         M, N, K, A, lda, B, ldb, kchunk, epi);
     SKR_LAUNCHED(ctx);
     return;
   }
   DBuf<double> ws((size_t)splits * M * N, ctx->stream);
   EpiPartial part{ws.get(), M, N};
-  gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(
+  static bool attr_p = [] {
+    SKR_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true, BM, BN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return true;
+  }();
+  (void)attr_p;
+  gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true, BM, BN><<<grid, GEMM_THREADS, smem, ctx->stream>>>(
       M, N, K, A, lda, B, ldb, kchunk, part);
   SKR_LAUNCHED(ctx);
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), 4LL * ctx->sm_count);
   splitk_reduce_kernel<Epi><<<blocks, 256, 0, ctx->stream>>>(ws.get(), M, N, splits, epi);
   SKR_LAUNCHED(ctx);
+}
+
+template <class TA, class TB, bool A_T, bool B_T, class Epi>
+void gemm(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, const TB* B,
+          int64_t ldb, Epi epi, int splits = 0) {
+  if (M <= 0 || N <= 0) return;
+  if (M <= 64 && N > 64)
+    gemm_tiled<TA, TB, A_T, B_T, Epi, 64, 128>(ctx, M, N, K, A, lda, B, ldb, epi, splits);
+  else
+    gemm_tiled<TA, TB, A_T, B_T, Epi, 128, 64>(ctx, M, N, K, A, lda, B, ldb, epi, splits);
 }
 
 }  // namespace skr

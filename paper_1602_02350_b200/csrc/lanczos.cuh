@@ -44,16 +44,17 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
 // so each new basis vector matches the MGS one, not just its span.
 
 // out[0] = max_j ||V_j|| over `rows` rows of length d (row stride ld); one CTA.
+// *out = max_j ||V[j, :d]|| (one block per row; *out zeroed by the caller; norms
+// are non-negative so their bit patterns order like the values)
 __global__ void row_norm_max_kernel(const double* __restrict__ V, int64_t ld, int64_t d, int rows,
                                     double* __restrict__ out) {
   __shared__ double scratch[32];
-  double ref = 0.0;
-  for (int j = 0; j < rows; ++j) {
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s = fma(V[j * ld + i], V[j * ld + i], s);
-    ref = fmax(ref, sqrt(block_sum(s, scratch)));
-  }
-  if (threadIdx.x == 0) *out = ref;
+  const int j = blockIdx.x;
+  if (j >= rows) return;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s = fma(V[j * ld + i], V[j * ld + i], s);
+  const double nrm = sqrt(block_sum(s, scratch));
+  if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(nrm));
 }
 
 // rdiag[j] = R_jj from geqrf output (column-major, lda = ld): element (j,j) at j*ld + j.

@@ -396,6 +396,12 @@ kDenseModeMaxEntries = 200_000_000  # ridge.hpp:65 (the GPU has no lazy path; se
 
 
 # ---------------------------------------------------------------------------
+class SvrgMode(Enum):
+    """svrg.hpp:37 — provenance label of a config; the solve is identical."""
+    Theoretical = 0
+    Tuned = 1
+
+
 @dataclass
 class SvrgConfig:
     """svrg.hpp:39-45."""
@@ -403,6 +409,13 @@ class SvrgConfig:
     epoch_length: int = 1
     step_size: float = 0.1
     seed: int = 0
+    mode: "SvrgMode" = None  # label only (svrg.hpp:37,44); defaults to Tuned
+
+    def __post_init__(self):
+        if self.mode is None:
+            self.mode = SvrgMode.Tuned
+
+
 
 
 @dataclass
@@ -561,10 +574,27 @@ def mean_beta(p: PreconditionedRidge) -> float:
     return p.mean_beta()
 
 
+def theoretical_params(p: PreconditionedRidge, w0_gap: float, epsilon: float) -> SvrgConfig:
+    """svrg.cpp:219-232: S = max(1, ceil(ln(gap/eps))), m = max(1, ceil(beta_hat/alpha)),
+    eta = 0.1/beta_hat, mode Theoretical."""
+    if not (epsilon > 0.0) or not (w0_gap > 0.0):
+        raise ParameterError("theoretical_params: w0_gap and epsilon must be positive")
+    bh = mean_beta(p)
+    return SvrgConfig(int(max(1.0, math.ceil(math.log(w0_gap / epsilon)))),
+                      int(max(1.0, math.ceil(bh / p.strong_convexity()))), 0.1 / bh, 0, SvrgMode.Theoretical)
+
+
+def eta_grid(beta_hat: float) -> list:
+    """bench.cpp:96-100: 2^j / beta_hat, j = -3..3."""
+    return [math.ldexp(1.0, j) / beta_hat for j in range(-3, 4)]
+
+
 def svrg_solve(p: PreconditionedRidge, cfg: SvrgConfig, w0=None,
-               reference_value: Optional[float] = None) -> SvrgResult:
+               reference_value: Optional[float] = None, stop_suboptimality: Optional[float] = None) -> SvrgResult:
     """svrg.cpp:152-211 — GPU-native: the index stream is the reference's
-    NormalSampler(cfg.seed) stream, drawn on the device."""
+    NormalSampler(cfg.seed) stream, drawn on the device.  `stop_suboptimality`
+    (needs reference_value) ends the solve after the first epoch at or below it
+    (time-to-epsilon, bench.cpp:182-189); the reference always runs cfg.epochs."""
     w0 = np.zeros(p.d) if w0 is None else _f64(w0)
     if len(w0) != p.d:
         raise DimensionError("svrg: start point length mismatch")
@@ -573,7 +603,10 @@ def svrg_solve(p: PreconditionedRidge, cfg: SvrgConfig, w0=None,
     w = np.empty(p.d)
     done = i64()
     ref = float("nan") if reference_value is None else float(reference_value)
-    rc = _lib.load().skr_svrg(p.h, C.byref(c), w0, ref, w, tr, C.byref(done))
+    if stop_suboptimality is None:
+        rc = _lib.load().skr_svrg(p.h, C.byref(c), w0, ref, w, tr, C.byref(done))
+    else:
+        rc = _lib.load().skr_svrg_until(p.h, C.byref(c), w0, ref, float(stop_suboptimality), w, tr, C.byref(done))
     trace = [EpochRecord(int(r.epoch), float(r.objective),
                          None if math.isnan(r.suboptimality) else float(r.suboptimality),
                          float(r.elapsed_ms)) for r in tr[: done.value]]

@@ -239,6 +239,27 @@ def test_svrg_mid_stream_jump_matches_oracle(O):
     assert np.array_equal(pg.index_stream(17, 2 * n + 5000), O.index_stream(po.betas(), 17, 2 * n + 5000))
 
 
+def test_svrg_until_stops_at_target_with_same_prefix(O):
+    X, y, lam, k = small_problem(n=400, d=30, k=5)
+    n, d = X.shape
+    sv = O.block_lanczos(X, k, q=3, seed=2)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.build_sketched(sk.SketchedSvd(sv.U, sv.sigma, None, k, 3), lam))
+    Lstar = O.reference_minimum(X, y, lam)[1]
+    eta = configs.step_size(pg.max_row_sq())
+    full = sk.svrg_solve(pg, sk.SvrgConfig(12, 2 * n, eta, 5), None, Lstar)
+    target = full.trace[3].suboptimality * 1.0000001
+    part = sk.svrg_solve(pg, sk.SvrgConfig(12, 2 * n, eta, 5), None, Lstar, stop_suboptimality=target)
+    assert len(part.trace) == 4
+    assert [r.objective for r in part.trace] == [r.objective for r in full.trace[:4]]
+    with pytest.raises(sk.ParameterError):
+        sk.svrg_solve(pg, sk.SvrgConfig(2, 2 * n, eta, 5), None, None, stop_suboptimality=1e-6)
+    tp = sk.theoretical_params(pg, 1.0, 1e-6)
+    assert tp.mode == sk.SvrgMode.Theoretical and tp.epochs == 14
+    assert tp.epoch_length == math.ceil(pg.mean_beta() / pg.strong_convexity())
+    assert tp.step_size == 0.1 / pg.mean_beta()
+
+
 def test_svrg_divergence_raises_with_trace():
     X, y, lam, k = small_problem(n=100, d=10, k=2)
     pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
