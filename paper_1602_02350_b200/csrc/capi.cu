@@ -99,7 +99,7 @@ struct skr_problem {
   int fg_grid = 0;
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
-  DBuf<double> s_state, s_M, s_p;  // s-step inner loop workspaces
+  DBuf<double> s_state, s_M, s_p, s_X;  // s-step inner loop workspaces
 };
 
 // ---------------------------------------------------------------------------
@@ -291,8 +291,9 @@ void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const 
   SKR_LAUNCHED(&c);
 }
 
-// K9 dispatch: warp-per-row (v4) for d <= 1024 (<= 32 elements per lane), else the
-// bulk-copy staged tile kernel (v3).  SKR_K9_IMPL=2/3 forces the tile variants.
+// K9 dispatch: warp-per-row (v4) for fp64 rows with d <= 1024 (<= 32 elements per
+// lane) and short fp32 rows, else the bulk-copy staged tile kernel (v3).
+// SKR_K9_IMPL=4 forces warp-per-row, 2/3 the tile variants.
 template <class T>
 FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
                          double* part_g, double* part_loss, bool plan_only) {
@@ -305,7 +306,10 @@ FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double
     return e ? atoi(e) : 1;
   }();
   const int64_t row_bytes = ld * (int64_t)sizeof(T);
-  if ((env_impl == 0 || env_impl == 4) && ld <= 1024) {  // <= 32 elements per lane
+  // warp-per-row wins for fp64 rows (c2: 5.40 vs 3.36-3.62 TB/s for the tile kernel);
+  // for fp32 rows > 2 KB the bulk-copy tile kernel wins (c5: 5.46 vs 5.15 TB/s)
+  const bool rowwarp = env_impl == 4 || (env_impl == 0 && ld <= 1024 && (sizeof(T) == 8 || row_bytes <= 2048));
+  if (rowwarp && ld <= 1024) {  // <= 32 elements per lane
     FgPlan p;
     p.bytes = (int)row_bytes;
     const int ch = (int)((row_bytes + 511) / 512);  // 16-byte chunks per lane
@@ -407,7 +411,7 @@ void ensure_tables(skr_problem* p) {
   p->cum.alloc(N, c.stream);
   p->inv_nq.alloc(N, c.stream);
   p->total.alloc(1, c.stream);
-  cumulative_kernel<<<1, 1, 0, c.stream>>>(p->betas.get(), N, p->cum.get(), p->total.get());
+  cumulative_kernel<<<1, 512, 0, c.stream>>>(p->betas.get(), N, p->cum.get(), p->total.get());
   SKR_LAUNCHED(&c);
   inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.stream>>>(p->betas.get(), N, p->total.get(),
                                                                                   p->inv_nq.get());
@@ -638,7 +642,7 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
 }
 
 // K10 s-step: prep (all SMs) + chain (one cluster) per chunk of blocks.
-constexpr int64_t kSstepChunkBlocks = 256;  // blocks per prep/chain launch pair (double-buffered)
+constexpr int64_t kSstepChunkBlocks = 1024;  // blocks per prep/chain launch pair (double-buffered)
 static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
 
 template <class T, int CPT, int L>
@@ -651,11 +655,13 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   if (p->s_state.n < (size_t)2 * ld) p->s_state.alloc(2 * ld, c.stream);
   const size_t mneed = (size_t)2 * kSstepChunkBlocks * L * L, pneed = (size_t)2 * kSstepChunkBlocks * L;
   if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
+  if (p->s_X.n < mneed) p->s_X.alloc(mneed, c.stream);
   if (p->s_p.n < pneed) p->s_p.alloc(pneed, c.stream);
   auto prep = sstep_prep_kernel<T, L>;
-  auto chain = sstep_chain_kernel<T, CPT, L>;
+  constexpr int MXB = CPT == 1 ? 2 : 1;
+  auto chain = sstep_chain_kernel<T, CPT, L, MXB>;
   constexpr size_t prep_smem = sstep_prep_smem<L>();
-  constexpr size_t chain_smem = sstep_chain_smem<CPT, L>();
+  constexpr size_t chain_smem = sstep_chain_smem<CPT, L, MXB>();
   static bool configured = false;
   if (!configured) {
     SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
@@ -676,11 +682,12 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     const int b = (int)(chunk & 1);
     double* Mb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * L * L;
     double* pb = p->s_p.get() + (size_t)b * kSstepChunkBlocks * L;
+    double* Xb = p->s_X.get() + (size_t)b * kSstepChunkBlocks * L * L;
     const int64_t steps = std::min(chunk_steps, m - s0);
     const int64_t nblk = (steps + L - 1) / L;
     if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
     prep<<<(unsigned)nblk, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
-                                                     p->reg_coef, mu, snap, eta, Mb, pb);
+                                                     p->reg_coef, mu, snap, eta, Mb, pb, Xb);
     SKR_LAUNCHED(&c);
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
     SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
@@ -688,10 +695,10 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
       SKR_CUDA(cudaMalloc(&dprof, 16 * sizeof(unsigned long long)));
       SKR_CUDA(cudaMemset(dprof, 0, 16 * sizeof(unsigned long long)));
     }
-    ChainArgs ca{rows, idx + s0, steps, Mb, pb, mu, eta, p->s_state.get(), dprof};
+    ChainArgs ca{rows, idx + s0, steps, Mb, pb, Xb, mu, eta, p->s_state.get(), dprof};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(160);
+    cfg.blockDim = dim3(224);
     cfg.dynamicSmemBytes = chain_smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
@@ -711,8 +718,8 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     unsigned long long h[16] = {};
     SKR_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
     const double nb = (double)std::max<unsigned long long>(h[6], 1);
-    fprintf(stderr, "[skr] chain cycles/block: wait_full %.0f  step1 %.0f  exchange %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
-            h[0] / nb, h[1] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
+    fprintf(stderr, "[skr] chain cycles/block: total %.0f  dots(b+1) %.0f  xterm+bar %.0f  ready-wait %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
+            h[9] / nb, h[1] / nb, h[0] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
   }
 }
 
@@ -724,7 +731,7 @@ void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64
   if (c.prof_on) c.prof_mark("svrg_epoch");
   if (!naive) {
     if (p->ld <= 2048) {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 64>(p, snap, mu, idx, m, eta, w_avg));
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32>(p, snap, mu, idx, m, eta, w_avg));
     } else {
       DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 2, 32>(p, snap, mu, idx, m, eta, w_avg));
     }
@@ -1762,7 +1769,9 @@ static int svrg_impl(skr_problem* p, const skr_svrg_config* cfg, const double* w
     Ctx& c = p->ctx->c;
     using clk = std::chrono::steady_clock;
     const auto t0 = clk::now();
+    if (c.prof_on) c.prof_mark("tables");
     ensure_tables(p);
+    if (c.prof_on) c.prof_mark("tables");
     seed_mt(c, p->mt, cfg->seed);
     const int64_t m = cfg->epoch_length, ld = p->ld;
     DBuf<double> w(ld, c.stream), mu(ld, c.stream), obj(1, c.stream), u(m, c.stream);
@@ -1776,7 +1785,9 @@ static int svrg_impl(skr_problem* p, const skr_svrg_config* cfg, const double* w
     *epochs_done = 0;
     DBuf<double> wnext(ld, c.stream);
     for (int64_t s = 1; s <= cfg->epochs; ++s) {
+      if (c.prof_on) c.prof_mark("indices");
       draw_indices(p, u, idx, m);
+      if (c.prof_on) c.prof_mark("indices");
       run_epoch(p, w.get(), mu.get(), idx.get(), m, cfg->step_size, wnext.get());
       std::swap(w.p, wnext.p);
       // objective at w_s; its pass also yields mu for epoch s+1 (svrg.cpp:189,196)

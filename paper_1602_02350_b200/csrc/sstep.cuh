@@ -13,8 +13,15 @@
 // M and p depend only on the (pre-drawn) indices, mu and wbar, so the PREP
 // kernel computes them for every block on all SMs; the CHAIN kernel (one
 // thread-block cluster, each CTA owning a column slice) only does the
-// dependent part per block: a = R w0 (cluster-reduced through DSMEM, one
-// cluster barrier per block), delta = M (a - p), and the two rank-L updates.
+// dependent part per block.
+//
+// Look-ahead: with X_b = R_b R_{b-1}^T and e_b = R_b mu (also from PREP),
+//   a_b = R_b w_b = R_b w_{b-1} - eta X_b delta_{b-1} - eta L e_b,
+// so the partial dots a~_b = R_b w_{b-1} are computed (and their cluster
+// reduction through DSMEM started) while block b-1 is still being resolved; the
+// exchange latency leaves the dependent chain.  PREP folds eta L e_b into
+// p'_b = p_b + eta L e_b for every block but the first of a launch, whose a_0 is
+// computed directly.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -22,6 +29,7 @@
 #include "common.cuh"
 #include "svrg.cuh"
 #include "fullgrad.cuh"
+#include "gemm.cuh"
 
 namespace skr {
 namespace cg = cooperative_groups;
@@ -38,82 +46,100 @@ __device__ __forceinline__ double row_elem(const SstepRows& R, int64_t i, int64_
 }
 
 // ---------------------------------------------------------------------------
-// PREP: one CTA (256 threads) per block of L steps.
-//   Mout[b] (L x L, stored TRANSPOSED: Mout[b][j*L + i] = M[i][j]), pout[b] (L).  Padded steps (beyond `steps`)
-//   get c_l = 0, so delta_l = 0 there.
+// PREP: one CTA (256 threads, 8 warps) per block of L = 32 steps.  One FP64
+// tensor-core (DMMA m8n8k4) product of the block's rows against the staged rows
+// [R_b; R_{b-1}; mu; wbar] gives G = R_b R_b^T, X = R_b R_{b-1}^T (look-ahead),
+// e = R_b mu and b = R_b wbar in one pass over the rows (column chunks of 32,
+// register-prefetched one chunk ahead).  Then M = (I + eta C G_strict)^{-1} C by
+// forward substitution.  Outputs: Mout[b] (L x L, stored TRANSPOSED:
+// Mout[b][j*L + i] = M[i][j]), pout[b] (L), Xout[b] (transposed, blocks > 0 of
+// the launch).  Padded steps (beyond `steps`) get c_l = 0, so delta_l = 0 there.
 template <class T, int L>
 __global__ void __launch_bounds__(256)
 sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, const double* __restrict__ inv_nq,
                   double data_coef, double reg_coef, const double* __restrict__ mu,
                   const double* __restrict__ wbar, double eta, double* __restrict__ Mout,
-                  double* __restrict__ pout) {
-  constexpr int CW = 32;                    // column chunk staged in smem
-  constexpr int TPR = L / 4;                // 4x4 register tiles: TPR x TPR threads
-  __shared__ double chunk[CW][L + 2];       // chunk[k][l] = r_l[col0 + k]
-  __shared__ double muc[CW], wbc[CW];
+                  double* __restrict__ pout, double* __restrict__ Xout) {
+  static_assert(L == 32, "warp tiling assumes L = 32");
+  constexpr int KC = 32, SP = KC + 4;         // staged columns per chunk, padded row stride (conflict-free frags)
+  constexpr int NR = 2 * L + 8;               // staged rows: block b, block b-1, mu, wbar, zero pad
+  constexpr int NTN = NR / 8;                 // n-tiles (9)
+  constexpr int PER = NR * KC / 256;          // staged elements per thread per chunk (9)
+  constexpr int RS = NR + 1;                  // result row stride
   extern __shared__ double dyn[];
-  double (*Gs)[L + 1] = reinterpret_cast<double (*)[L + 1]>(dyn);          // L x (L+1)
-  double (*Xs)[L + 1] = reinterpret_cast<double (*)[L + 1]>(dyn + L * (L + 1));  // column j of T^{-1}
-  __shared__ double cvec[L], evec[L], bvec[L];
-  __shared__ int64_t ridx[L];
-  const int tid = threadIdx.x;
+  double* st = dyn;                           // [NR][SP] staging, then [L][RS] results
+  double (*Xs)[L + 1] = reinterpret_cast<double (*)[L + 1]>(dyn + NR * SP);  // column j of T^{-1}
+  __shared__ double cvec[L];
+  __shared__ int64_t ridx[2 * L];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * L;
+  const bool look = blockIdx.x > 0;  // the previous block of this launch exists (and is full)
   if (tid < L) {
     const int64_t t = t0 + tid;
     const int64_t i = t < steps ? idx[t] : -1;
     ridx[tid] = i;
+    ridx[L + tid] = look ? idx[t0 - L + tid] : -1;
     cvec[tid] = i < 0 ? 0.0 : (i < R.n ? data_coef : reg_coef) * inv_nq[i];
   }
   __syncthreads();
-  const int tr = tid / TPR, tc = tid % TPR;  // tile (tr, tc) when tid < TPR*TPR
-  const bool tiler = tid < TPR * TPR;
-  double g[4][4] = {};
-  double e_acc = 0.0, b_acc = 0.0;  // thread tid < L accumulates row tid
-  for (int64_t c0 = 0; c0 < R.d; c0 += CW) {
-    __syncthreads();
-    for (int e = tid; e < CW * L; e += blockDim.x) {
-      const int l = e / CW, k = e % CW;
-      const int64_t i = ridx[l], col = c0 + k;
-      chunk[k][l] = (i >= 0 && col < R.d) ? row_elem<T>(R, i, col) : 0.0;
-    }
-    if (tid < CW) {
-      const int64_t col = c0 + tid;
-      muc[tid] = col < R.d ? mu[col] : 0.0;
-      wbc[tid] = col < R.d ? wbar[col] : 0.0;
-    }
-    __syncthreads();
-    if (tiler) {
-#pragma unroll 4
-      for (int k = 0; k < CW; ++k) {
-        const double2 a01 = *reinterpret_cast<const double2*>(&chunk[k][4 * tr]);
-        const double2 a23 = *reinterpret_cast<const double2*>(&chunk[k][4 * tr + 2]);
-        const double2 b01 = *reinterpret_cast<const double2*>(&chunk[k][4 * tc]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&chunk[k][4 * tc + 2]);
-        const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
+  auto fetch = [&](int64_t c0, double (&v)[PER]) {
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * 256, r = e / KC;
+      const int64_t col = c0 + e % KC;
+      double x = 0.0;
+      if (col < R.d) {
+        if (r < 2 * L) {
+          const int64_t i = ridx[r];
+          if (i >= 0) x = row_elem<T>(R, i, col);
+        } else if (r == 2 * L) {
+          x = mu[col];
+        } else if (r == 2 * L + 1) {
+          x = wbar[col];
+        }
+      }
+      v[q] = x;
+    }
+  };
+  const int mt = warp & 3, nb = warp >> 2;  // m-tile; n-tiles nb, nb+2, ...
+  double acc[5][2] = {};
+  double v[PER];
+  fetch(0, v);
+  for (int64_t c0 = 0; c0 < R.d; c0 += KC) {
+    __syncthreads();
 #pragma unroll
-          for (int y = 0; y < 4; ++y) g[x][y] = fma(a[x], b[y], g[x][y]);
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * 256;
+      st[(e / KC) * SP + e % KC] = v[q];
+    }
+    __syncthreads();
+    if (c0 + KC < R.d) fetch(c0 + KC, v);  // next chunk in flight during the products
+#pragma unroll
+    for (int k4 = 0; k4 < KC; k4 += 4) {
+      const double a = st[(8 * mt + (lane >> 2)) * SP + k4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const int nt = nb + 2 * j;
+        if (nt < NTN) dmma_884(acc[j][0], acc[j][1], a, st[(8 * nt + (lane >> 2)) * SP + k4 + (lane & 3)]);
       }
     }
-    if (tid < L) {
-      for (int k = 0; k < CW; ++k) {
-        e_acc = fma(chunk[k][tid], muc[k], e_acc);
-        b_acc = fma(chunk[k][tid], wbc[k], b_acc);
-      }
-    }
-  }
-  if (tiler) {
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) Gs[4 * tr + x][4 * tc + y] = g[x][y];
-  }
-  if (tid < L) {
-    evec[tid] = e_acc;
-    bvec[tid] = b_acc;
   }
   __syncthreads();
+  double* res = st;  // res[i*RS + n]: n < L: G, L..2L-1: X, 2L: e, 2L+1: b
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const int nt = nb + 2 * j;
+    if (nt < NTN) {
+      const int i = 8 * mt + (lane >> 2), n = 8 * nt + 2 * (lane & 3);
+      res[i * RS + n] = acc[j][0];
+      res[i * RS + n + 1] = acc[j][1];
+    }
+  }
+  __syncthreads();
+  if (look) {  // X = R_b R_{b-1}^T stored transposed: Xt[j*L + i] = X[i][j]
+    double* Xb = Xout + (int64_t)blockIdx.x * L * L;
+    for (int e = tid; e < L * L; e += blockDim.x) Xb[e] = res[(e % L) * RS + L + e / L];
+  }
   // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward
   // substitution (thread j), then M = T^{-1} C  (M[i][j] = Tinv[i][j] c_j).
   double* Mb = Mout + (int64_t)blockIdx.x * L * L;
@@ -122,10 +148,11 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
     for (int i = 0; i < L; ++i) Xs[i][j] = i == j ? 1.0 : 0.0;
     for (int i = j + 1; i < L; ++i) {
       double s = 0.0;
-      for (int k2 = j; k2 < i; ++k2) s = fma(Gs[i][k2], Xs[k2][j], s);
+      for (int k2 = j; k2 < i; ++k2) s = fma(res[i * RS + k2], Xs[k2][j], s);
       Xs[i][j] = -eta * cvec[i] * s;
     }
-    pout[(int64_t)blockIdx.x * L + j] = eta * (double)j * evec[j] + bvec[j];
+    // p_j = eta (j-1) e_j + b_j (1-based), + eta L e_j when a_b is formed by look-ahead
+    pout[(int64_t)blockIdx.x * L + j] = eta * (double)(look ? j + L : j) * res[j * RS + 2 * L] + res[j * RS + 2 * L + 1];
   }
   __syncthreads();
   for (int e = tid; e < L * L; e += blockDim.x) {  // stored transposed: Mt[j][i] = M[i][j]
@@ -136,22 +163,30 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
 
 template <int L>
 constexpr size_t sstep_prep_smem() {
-  return sizeof(double) * 2 * L * (L + 1);
+  return sizeof(double) * ((2 * L + 8) * (32 + 4) + L * (L + 1));
 }
 
 // ---------------------------------------------------------------------------
-// CHAIN: one cluster of CS CTAs; each CTA = 4 consumer warps + 1 producer warp.
+// CHAIN: one cluster of CS CTAs; each CTA = 4 consumer warps + 2 producer warps
+// + 1 signaller warp.
 // CTA r owns columns [r*SW, r*SW + SW), SW = 128*CPT; consumer thread t owns
 // columns r*SW + t*CPT + [0, CPT) of w and of the running sum (registers).
-//  * producer warp: per block, loads the L indices and issues one bulk copy
+//  * row producer warp: per block, loads the L indices and issues one bulk copy
 //    (cp.async.bulk, 1-D TMA) per row slice into an NB-deep ring (full/empty
 //    mbarriers), running up to NB blocks ahead;
-//  * consumers: partial a = R w0 over the slice -> transposed warp reductions
-//    -> CTA partial published in shared memory; thread 0 then arrives
-//    (release, cluster scope) on every CTA's `ready` mbarrier; after waiting on
-//    its own `ready` (acquire) each CTA reads the CS partials through DSMEM,
-//    forms z = a - p, delta = M z (M prefetched into registers), and applies
-//    the two rank-L updates.  No cluster-wide barrier inside the loop.
+//  * M/X producer warp: bulk-copies M_b^T, X_b^T and p_b (from PREP) into an
+//    MXB-deep shared ring, so no consumer register or LSU slot holds them;
+//  * consumers, iteration b: (1) partial dots a~_{b+1} = R_{b+1} w_b over the
+//    slice -> transposed warp reductions -> pushed by remote DSMEM stores into
+//    apub[(b+1)%4][rank] of every CTA; (2) wait (acquire) on ready[b%4] —
+//    completed one iteration earlier, normally — sum the CS partials from local
+//    shared memory, z = a~_b - eta X_b delta_{b-1} - p'_b (threads L..2L-1 form
+//    the X term), delta_b = M_b z (M, X staged in shared memory by a producer
+//    warp); (3) the two rank-L updates with the rows of block b;
+//  * signaller warp: after each block's partials are pushed (local mbarrier),
+//    arrives (release, cluster scope) on every CTA's ready mbarrier, keeping
+//    the fence latency off the consumers.
+//    No cluster-wide barrier inside the loop.
 // w and the running sum persist in global state[0..ld) / [ld..2 ld) between
 // launches (one launch per chunk of blocks).
 struct ChainArgs {
@@ -159,7 +194,8 @@ struct ChainArgs {
   const int64_t* idx;   // chunk indices
   int64_t steps;        // steps in this chunk
   const double* M;      // nblk x L x L (transposed)
-  const double* p;      // nblk x L
+  const double* p;      // nblk x L  (p'_b: look-ahead correction folded in for b >= 1)
+  const double* X;      // nblk x L x L (transposed): R_b R_{b-1}^T, b >= 1
   const double* mu;     // ld
   double eta;
   double* state;        // [0, ld) w ; [ld, 2 ld) sum
@@ -191,22 +227,27 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-template <class T, int CPT, int L>
-__global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
+template <class T, int CPT, int L, int MXB>
+__global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
   constexpr int NT = 128, SW = NT * CPT, NB = kChainNB;
+  constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
   constexpr size_t ROWB = (size_t)SW * 8;  // bytes per row slot (fits an fp64 slice)
   extern __shared__ __align__(128) unsigned char sm[];
   unsigned char* rows = sm;                                                  // [NB][L][ROWB]
-  double* apub = reinterpret_cast<double*>(sm + (size_t)NB * L * ROWB);     // [2][L]
-  double* zbuf = apub + 2 * L;                                               // [L]
-  double* delta = zbuf + L;                                                  // [L]
-  double* delta2 = delta + L;                                                // [L]
-  double* wpart = delta2 + L;                                                // [4][L] (unused)
-  int64_t* ridx = reinterpret_cast<int64_t*>(wpart + 4 * L);                 // [NB][L]
+  double* mx = reinterpret_cast<double*>(sm + (size_t)NB * L * ROWB);       // [MXB][MXW] M_b^T, X_b^T, p_b
+  double* apub = mx + MXB * MXW;                                             // [4][16][L] partials pushed by each rank
+  double* zbuf = apub + 4 * 16 * L;                                          // [L]
+  double* xterm = zbuf + L;                                                  // [L] (X_b delta_{b-1})_i
+  double* dl = xterm + L;                                                    // [2][L] delta_b
+  double* delta2 = dl + 2 * L;                                               // [L]
+  int64_t* ridx = reinterpret_cast<int64_t*>(delta2 + L);                    // [NB][L]
   uint64_t* full = reinterpret_cast<uint64_t*>(ridx + NB * L);               // [NB]
   uint64_t* empty = full + NB;                                               // [NB]
-  uint64_t* ready = empty + NB;                                              // [2]
-  uint64_t* dmask = ready + 2;                                               // [NB] bit l: row l is a data row
+  uint64_t* ready = empty + NB;                                              // [4]
+  uint64_t* mx_full = ready + 4;                                             // [MXB]
+  uint64_t* mx_empty = mx_full + MXB;                                        // [MXB]
+  uint64_t* pub = mx_empty + MXB;                                            // [2] local: partials pushed
+  uint64_t* dmask = pub + 2;                                                 // [NB] bit l: row l is a data row
   double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [SW] current w slice
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -220,14 +261,42 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], 1);
     }
-    mbar_init(&ready[0], CS);
-    mbar_init(&ready[1], CS);
+    for (int q = 0; q < 4; ++q) mbar_init(&ready[q], CS);
+    for (int q = 0; q < MXB; ++q) {
+      mbar_init(&mx_full[q], 1);
+      mbar_init(&mx_empty[q], 1);
+    }
+    mbar_init(&pub[0], 4);
+    mbar_init(&pub[1], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // every CTA's barriers exist before any remote arrive
 
-  if (warp == 4) {
-    // ---------------- producer warp ----------------
+  if (warp == 6) {
+    // ---------------- signaller: once this CTA's partials of block j are pushed
+    // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
+    // release fence latency stays off the consumers' path.  pub is 2-deep: the
+    // consumers cannot complete phase j+2 before their ready[j] wait, which needs
+    // this warp's arrive for j.
+    for (int64_t j = 0; j < nblk; ++j) {
+      mbar_wait(&pub[j & 1], (uint32_t)((j >> 1) & 1));
+      if (lane < CS) mbar_arrive_remote(&ready[j & 3], (uint32_t)lane);
+    }
+  } else if (warp == 5) {
+    // ---------------- M/X producer: M_b^T, X_b^T, p_b by bulk copy ----------------
+    if (lane == 0) {
+      for (int64_t b = 0; b < nblk; ++b) {
+        const int slot = (int)(b % MXB);
+        if (b >= MXB) mbar_wait(&mx_empty[slot], (uint32_t)(((b / MXB) - 1) & 1));
+        double* dst = mx + slot * MXW;
+        mbar_expect_tx(&mx_full[slot], (uint32_t)(MXW * 8));
+        bulk_g2s(dst, a.M + b * L * L, (uint32_t)(L * L * 8), &mx_full[slot]);
+        bulk_g2s(dst + L * L, a.X + b * L * L, (uint32_t)(L * L * 8), &mx_full[slot]);  // b = 0: unused
+        bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- row producer warp ----------------
     const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);  // may be <= 0 past ld
     // indices are loaded one block ahead (their L2 latency overlaps the copies)
     int64_t nxt[L / 32];
@@ -295,6 +364,7 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
     }
   } else {
     // ---------------- consumer warps (128 threads) ----------------
+    static_assert(2 * L <= NT, "M and X rows are held by threads [0, 2L)");
     const int64_t col0 = slice0 + (int64_t)tid * CPT;
     bool act[CPT];
     double w[CPT], S[CPT], mu[CPT];
@@ -309,17 +379,117 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
     named_bar(1, NT);
     unsigned long long tp[8] = {};
     const bool prof = a.prof && cr == 0 && tid == 0;
+    // partial dots of block bb's rows (ring slot) with the current w slice, pushed
+    // (remote DSMEM stores) into apub[bb % 4][cr] of every CTA of the cluster
+    auto dots = [&](int64_t bb) {
+      const int slot = (int)(bb % NB);
+      const int Lbb = (int)min((int64_t)L, a.steps - bb * L);
+      mbar_wait(&full[slot], (uint32_t)((bb / NB) & 1));
+      const unsigned char* rb = rows + (size_t)slot * L * ROWB;
+      const uint64_t dm = dmask[slot];
+      constexpr int RPW = L / 4;        // rows per warp: warp q owns rows [q*L/4, (q+1)*L/4)
+      constexpr int CPL = SW / 32;      // columns per lane, interleaved (conflict-free)
+      double wl[CPL];
+      const int64_t valid = R.ld - slice0;  // columns past the copied slice hold stale smem
+      bool lok[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        lok[c] = (int64_t)(lane + 32 * c) < valid;
+        wl[c] = wsm[lane + 32 * c];
+      }
+      double v[RPW];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        const int l = warp * RPW + q;
+        const unsigned char* rowp = rb + (size_t)l * ROWB;
+        double s = 0.0;
+        if (sizeof(T) == 8 || ((dm >> l) & 1ull) == 0) {
+          const double* x = reinterpret_cast<const double*>(rowp) + lane;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? x[32 * c] : 0.0, wl[c], s);
+        } else {
+          const T* x = reinterpret_cast<const T*>(rowp) + lane;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? (double)x[32 * c] : 0.0, wl[c], s);
+        }
+        v[q] = l < Lbb ? s : 0.0;
+      }
+      warp_transpose_reduce<RPW>(v, lane);
+      if ((lane & ((32 / RPW) - 1)) == 0) {
+        const int off = ((bb & 3) * 16 + cr) * L + warp * RPW + row_of_lane<RPW>(lane);
+        for (int q = 0; q < CS; ++q) cluster.map_shared_rank(apub, q)[off] = v[0];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are pushed
+    };
+    // prologue: a_0 = R_0 w_0 directly
+    if (nblk > 0) {
+      dots(0);
+    }
     for (int64_t b = 0; b < nblk; ++b) {
-      const int slot = (int)(b % NB), par = (int)(b & 1);
+      const int slot = (int)(b % NB);
       const int Lb = (int)min((int64_t)L, a.steps - b * L);
       unsigned long long c0 = prof ? clock64() : 0;
-      mbar_wait(&full[slot], (uint32_t)((b / NB) & 1));
+      // 1. look-ahead partial dots of block b+1 with w_b, published to the cluster
+      if (b + 1 < nblk) dots(b + 1);
       unsigned long long c1 = prof ? clock64() : 0;
+      // M_b, X_b, p_b staged by the M/X producer
+      const int mslot = (int)(b % MXB);
+      const double* Ms = mx + mslot * MXW;
+      const double* Xs = Ms + L * L;
+      const double* ps = Ms + 2 * L * L;
+      mbar_wait(&mx_full[mslot], (uint32_t)((b / MXB) & 1));
+      // X term (threads L..2L-1): xterm_i = (X_b delta_{b-1})_i
+      if (tid >= L && tid < 2 * L && b > 0) {
+        const double* dp = dl + ((b - 1) & 1) * L;
+        const int i = tid - L;
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; k += 4) {
+          x0 = fma(Xs[k * L + i], dp[k], x0);
+          x1 = fma(Xs[(k + 1) * L + i], dp[k + 1], x1);
+          x2 = fma(Xs[(k + 2) * L + i], dp[k + 2], x2);
+          x3 = fma(Xs[(k + 3) * L + i], dp[k + 3], x3);
+        }
+        xterm[i] = (x0 + x1) + (x2 + x3);
+      }
+      named_bar(1, NT);  // xterm visible
+      unsigned long long c2 = prof ? clock64() : 0;
+      // 2. a_b: sum the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
+      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
+      unsigned long long c3 = prof ? clock64() : 0;
+      if (tid < L) {
+        double part[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) part[q] = q < CS ? apub[((b & 3) * 16 + q) * L + tid] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += part[q];
+        if (b > 0) s -= a.eta * xterm[tid];
+        zbuf[tid] = s - ps[tid];
+      }
+      named_bar(1, NT);
+      unsigned long long c4 = prof ? clock64() : 0;
+      // delta_b = M_b z (thread tid < L: row tid, four partial sums)
+      double* dcur = dl + (b & 1) * L;
+      if (tid < L) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; k += 4) {
+          d0 = fma(Ms[k * L + tid], zbuf[k], d0);
+          d1 = fma(Ms[(k + 1) * L + tid], zbuf[k + 1], d1);
+          d2 = fma(Ms[(k + 2) * L + tid], zbuf[k + 2], d2);
+          d3 = fma(Ms[(k + 3) * L + tid], zbuf[k + 3], d3);
+        }
+        const double dv = (d0 + d1) + (d2 + d3);
+        dcur[tid] = dv;
+        delta2[tid] = (double)(Lb - tid) * dv;  // (Lb - l + 1) weight, 1-based l
+      }
+      named_bar(1, NT);
+      if (tid == 0) mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
+      unsigned long long c5 = prof ? clock64() : 0;
+      // 3. w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
-      const int64_t* ri = ridx + slot * L;
-      // 1. a_l over this CTA's slice: warp q owns rows [q*L/4, (q+1)*L/4) entirely;
-      //    lane j takes columns j, j+32, ... of the slice (w from shared memory), one
-      //    transposed warp reduction per warp — no cross-warp stage.
       const uint64_t dm = dmask[slot];
       auto elem = [&](int l, int c) -> double {
         if constexpr (sizeof(T) == 8) {
@@ -329,80 +499,6 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
                                     : reinterpret_cast<const double*>(rb + (size_t)l * ROWB)[tid * CPT + c];
         }
       };
-      {
-        constexpr int RPW = L / 4;        // rows per warp
-        constexpr int CPL = SW / 32;      // columns per lane
-        double wl[CPL];
-        // columns past the copied slice (ld - slice0) hold stale shared memory: mask them
-        const int64_t valid = R.ld - slice0;
-        bool lok[CPL];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {  // interleaved: lane j takes columns j, j+32, ... (conflict-free)
-          lok[c] = (int64_t)(lane + 32 * c) < valid;
-          wl[c] = wsm[lane + 32 * c];
-        }
-        double v[RPW];
-#pragma unroll
-        for (int q = 0; q < RPW; ++q) {
-          const int l = warp * RPW + q;
-          const unsigned char* rowp = rb + (size_t)l * ROWB;
-          double s = 0.0;
-          if (sizeof(T) == 8 || ((dm >> l) & 1ull) == 0) {
-            const double* x = reinterpret_cast<const double*>(rowp) + lane;
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? x[32 * c] : 0.0, wl[c], s);
-          } else {
-            const T* x = reinterpret_cast<const T*>(rowp) + lane;
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? (double)x[32 * c] : 0.0, wl[c], s);
-          }
-          v[q] = l < Lb ? s : 0.0;
-        }
-        warp_transpose_reduce<RPW>(v, lane);
-        if ((lane & ((32 / RPW) - 1)) == 0) apub[par * L + warp * RPW + row_of_lane<RPW>(lane)] = v[0];
-      }
-      // M column `tid` and p_tid of this block: loads in flight across the exchange
-      double Mc[L];
-      double pl = 0.0;
-      if (tid < L) {
-        const double* Mg = a.M + b * L * L;
-#pragma unroll
-        for (int k = 0; k < L; ++k) Mc[k] = Mg[(int64_t)k * L + tid];
-        pl = a.p[b * L + tid];
-      }
-      named_bar(1, NT);  // this CTA's partials are complete before they are published
-      unsigned long long c2 = prof ? clock64() : 0;
-      // 2. publish to the cluster and gather the CS partials (DSMEM)
-      if (tid < CS) mbar_arrive_remote(&ready[par], (uint32_t)tid);
-      mbar_wait_cluster(&ready[par], (uint32_t)((b >> 1) & 1));
-      unsigned long long c3 = prof ? clock64() : 0;
-      if (tid < L) {
-        double part[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) part[q] = q < CS ? cluster.map_shared_rank(apub, q)[par * L + tid] : 0.0;
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) s += part[q];
-        zbuf[tid] = s - pl;
-      }
-      named_bar(1, NT);
-      unsigned long long c4 = prof ? clock64() : 0;
-      // delta = M z (thread tid < L: row tid, four partial sums)
-      if (tid < L) {
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int k = 0; k < L; k += 4) {
-          d0 = fma(Mc[k], zbuf[k], d0);
-          d1 = fma(Mc[k + 1], zbuf[k + 1], d1);
-          d2 = fma(Mc[k + 2], zbuf[k + 2], d2);
-          d3 = fma(Mc[k + 3], zbuf[k + 3], d3);
-        }
-        delta[tid] = (d0 + d1) + (d2 + d3);
-        delta2[tid] = (double)(Lb - tid) * delta[tid];  // (Lb - l + 1) weight, 1-based l
-      }
-      named_bar(1, NT);
-      unsigned long long c5 = prof ? clock64() : 0;
-      // 3. w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         if (!act[c]) continue;
@@ -410,14 +506,14 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
         int l = 0;
         for (; l + 3 < Lb; l += 4) {
           const double x0 = elem(l, c), x1 = elem(l + 1, c), x2 = elem(l + 2, c), x3 = elem(l + 3, c);
-          const double4 dd = *reinterpret_cast<const double4*>(delta + l);
+          const double4 dd = *reinterpret_cast<const double4*>(dcur + l);
           const double4 ee = *reinterpret_cast<const double4*>(delta2 + l);
           u0 = fma(dd.x, x0, u0); u1 = fma(dd.y, x1, u1); u2 = fma(dd.z, x2, u2); u3 = fma(dd.w, x3, u3);
           v0 = fma(ee.x, x0, v0); v1 = fma(ee.y, x1, v1); v2 = fma(ee.z, x2, v2); v3 = fma(ee.w, x3, v3);
         }
         for (; l < Lb; ++l) {
           const double x = elem(l, c);
-          u0 = fma(delta[l], x, u0);
+          u0 = fma(dcur[l], x, u0);
           v0 = fma(delta2[l], x, v0);
         }
         const double u = (u0 + u1) + (u2 + u3), v = (v0 + v1) + (v2 + v3);
@@ -426,16 +522,17 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
         w[c] = w0 - a.eta * u - a.eta * (double)Lb * mu[c];
         wsm[tid * CPT + c] = w[c];
       }
-      named_bar(1, NT);  // every consumer is done with rows[slot], zbuf, delta; new w visible
+      named_bar(1, NT);  // every consumer is done with rows[slot], zbuf, delta2; new w visible
       if (tid == 0) mbar_arrive_local(&empty[slot]);
       if (prof) {
         const unsigned long long c6 = clock64();
-        tp[0] += c1 - c0; tp[1] += c2 - c1; tp[2] += c3 - c2; tp[3] += c4 - c3; tp[4] += c5 - c4; tp[5] += c6 - c5;
+        tp[0] += c2 - c1; tp[7] += c6 - c0; tp[1] += c1 - c0; tp[2] += c3 - c2; tp[3] += c4 - c3; tp[4] += c5 - c4; tp[5] += c6 - c5;
         tp[6] += 1;
       }
     }
     if (prof)
       for (int q = 0; q < 7; ++q) atomicAdd(a.prof + q, tp[q]);
+    if (prof) atomicAdd(a.prof + 9, tp[7]);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       if (!act[c]) continue;
@@ -446,10 +543,11 @@ __global__ void __launch_bounds__(160, 1) sstep_chain_kernel(ChainArgs a) {
   cluster.sync();  // no CTA exits while others may still read its smem / arrive on its barriers
 }
 
-template <int CPT, int L>
+template <int CPT, int L, int MXB>
 constexpr size_t sstep_chain_smem() {
-  return (size_t)kChainNB * L * 128 * CPT * 8 + sizeof(double) * (2 * L + L + 2 * L + 4 * L) +
-         sizeof(int64_t) * kChainNB * L + sizeof(uint64_t) * (3 * kChainNB + 2) + sizeof(double) * 128 * CPT + 128;
+  return (size_t)kChainNB * L * 128 * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
+         sizeof(double) * (4 * 16 * L + L + L + 2 * L + L) + sizeof(int64_t) * kChainNB * L +
+         sizeof(uint64_t) * (3 * kChainNB + 4 + 2 * MXB + 2) + sizeof(double) * 128 * CPT + 128;
 }
 
 // w_avg = S / m ; zero padding.

@@ -16,18 +16,73 @@ namespace skr {
 // sum and running prefix in index order (one thread; a parallel scan would
 // reassociate and could flip indices at table boundaries).  Also writes
 // total to *total_out.
-__global__ void cumulative_kernel(const double* __restrict__ beta, int64_t N,
-                                  double* __restrict__ cum, double* __restrict__ total_out) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// One CTA.  Warp 0 lane 0 runs the two dependent fp64 chains (total, then the
+// running prefix) out of shared memory; warps 1.. stream beta in (and compute the
+// quotients beta_i / total, which are independent) one tile ahead and write the
+// finished prefix tile back, so the chain never waits on global memory.
+constexpr int CUM_T = 2048;
+__global__ void __launch_bounds__(512) cumulative_kernel(const double* __restrict__ beta, int64_t N,
+                                                         double* __restrict__ cum, double* __restrict__ total_out) {
+  __shared__ double buf[2][CUM_T];
+  __shared__ double s_total;
+  const int t = threadIdx.x, nl = blockDim.x - 32;  // loader threads: t >= 32
+  const int64_t ntile = (N + CUM_T - 1) / CUM_T;
+  auto load = [&](int64_t tile, bool div, double tot) {
+    double* b = buf[tile & 1];
+    for (int j = t - 32; j < CUM_T; j += nl) {
+      const int64_t i = tile * CUM_T + j;
+      const double v = i < N ? beta[i] : 0.0;
+      b[j] = div ? __ddiv_rn(v, tot) : v;
+    }
+  };
+  auto store = [&](int64_t tile) {
+    const double* b = buf[tile & 1];
+    for (int j = t - 32; j < CUM_T; j += nl) {
+      const int64_t i = tile * CUM_T + j;
+      if (i < N) cum[i] = b[j];
+    }
+  };
+  // total = sum_i beta_i in index order (svrg.cpp:92-94)
   double total = 0.0;
-  for (int64_t i = 0; i < N; ++i) total = __dadd_rn(total, beta[i]);
-  double run = 0.0;
-  for (int64_t i = 0; i < N; ++i) {
-    run = __dadd_rn(run, __ddiv_rn(beta[i], total));
-    cum[i] = run;
+  if (t >= 32) load(0, false, 0.0);
+  __syncthreads();
+  for (int64_t k = 0; k < ntile; ++k) {
+    if (t >= 32 && k + 1 < ntile) load(k + 1, false, 0.0);
+    if (t == 0) {
+      const int cnt = (int)min((int64_t)CUM_T, N - k * CUM_T);
+      const double* b = buf[k & 1];
+      for (int j = 0; j < cnt; ++j) total = __dadd_rn(total, b[j]);
+    }
+    __syncthreads();
   }
-  cum[N - 1] = 1.0;
-  *total_out = total;
+  if (t == 0) s_total = total;
+  __syncthreads();
+  const double tot = s_total;
+  // run += beta_i / total; cum_i = run  (svrg.cpp:95-104)
+  double run = 0.0;
+  if (t >= 32) load(0, true, tot);
+  __syncthreads();
+  for (int64_t k = 0; k < ntile; ++k) {
+    if (t >= 32) {
+      if (k >= 1) store(k - 1);
+      if (k + 1 < ntile) load(k + 1, true, tot);
+    }
+    if (t == 0) {
+      const int cnt = (int)min((int64_t)CUM_T, N - k * CUM_T);
+      double* b = buf[k & 1];
+      for (int j = 0; j < cnt; ++j) {
+        run = __dadd_rn(run, b[j]);
+        b[j] = run;
+      }
+    }
+    __syncthreads();
+  }
+  if (t >= 32 && ntile > 0) store(ntile - 1);
+  __syncthreads();
+  if (t == 0) {
+    cum[N - 1] = 1.0;
+    *total_out = tot;
+  }
 }
 
 // inv_nq_i = total / (N * beta_i)  (svrg.cpp:167-172)
