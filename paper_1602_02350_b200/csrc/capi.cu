@@ -718,8 +718,8 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     unsigned long long h[16] = {};
     SKR_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
     const double nb = (double)std::max<unsigned long long>(h[6], 1);
-    fprintf(stderr, "[skr] chain cycles/block: total %.0f  dots(b+1) %.0f  xterm+bar %.0f  ready-wait %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
-            h[9] / nb, h[1] / nb, h[0] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
+    fprintf(stderr, "[skr] chain cycles/block: total %.0f  (rows-wait %.0f)  dots(b+1) %.0f  xterm+bar %.0f  ready-wait %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
+            h[9] / nb, h[10] / nb, h[1] / nb, h[0] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
   }
 }
 

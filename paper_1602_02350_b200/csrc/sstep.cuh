@@ -235,13 +235,16 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   unsigned char* rows = sm;                                                  // [NB][L][ROWB]
   double* mx = reinterpret_cast<double*>(sm + (size_t)NB * L * ROWB);       // [MXB][MXW] M_b^T, X_b^T, p_b
-  double* apub = mx + MXB * MXW;                                             // [4][16][L] partials pushed by each rank
-  double* zbuf = apub + 4 * 16 * L;                                          // [L]
-  double* xterm = zbuf + L;                                                  // [L] (X_b delta_{b-1})_i
-  double* dl = xterm + L;                                                    // [2][L] delta_b
-  double* delta2 = dl + 2 * L;                                               // [L]
-  int64_t* ridx = reinterpret_cast<int64_t*>(delta2 + L);                    // [NB][L]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ridx + NB * L);               // [NB]
+  // PUSH (CPT = 1): every rank pushes its partials into apub[slot][rank] of all
+  // ranks and gathers locally; pull (CPT = 2, where shared memory is tight): each
+  // rank keeps its own apub[slot] and the gather reads the ranks remotely.
+  constexpr bool PUSH = CPT == 1;
+  double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
+  double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
+  double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
+  double* dl = zbuf + L;                                                     // [L] delta_b
+  double* delta2 = dl + L;                                                   // [L]
+  uint64_t* full = reinterpret_cast<uint64_t*>(delta2 + L);                  // [NB]
   uint64_t* empty = full + NB;                                               // [NB]
   uint64_t* ready = empty + NB;                                              // [4]
   uint64_t* mx_full = ready + 4;                                             // [MXB]
@@ -325,7 +328,6 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
 #pragma unroll
       for (int h = 0; h < L / 32; ++h) {
         const int64_t i = cur[h];
-        ridx[slot * L + lane + 32 * h] = i;
         if (i >= 0 && slice_elems > 0) bytes += (uint32_t)(slice_elems * (i < R.n ? (int64_t)sizeof(T) : 8));
         const unsigned bal = __ballot_sync(0xffffffffu, i >= 0 && i < R.n);
         mask |= (uint64_t)bal << (32 * h);
@@ -377,14 +379,16 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       wsm[tid * CPT + c] = w[c];
     }
     named_bar(1, NT);
-    unsigned long long tp[8] = {};
+    unsigned long long tp[9] = {};
     const bool prof = a.prof && cr == 0 && tid == 0;
     // partial dots of block bb's rows (ring slot) with the current w slice, pushed
     // (remote DSMEM stores) into apub[bb % 4][cr] of every CTA of the cluster
     auto dots = [&](int64_t bb) {
       const int slot = (int)(bb % NB);
       const int Lbb = (int)min((int64_t)L, a.steps - bb * L);
+      const unsigned long long w0c = prof ? clock64() : 0;
       mbar_wait(&full[slot], (uint32_t)((bb / NB) & 1));
+      if (prof) tp[8] += clock64() - w0c;
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
       const uint64_t dm = dmask[slot];
       constexpr int RPW = L / 4;        // rows per warp: warp q owns rows [q*L/4, (q+1)*L/4)
@@ -415,9 +419,20 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
         v[q] = l < Lbb ? s : 0.0;
       }
       warp_transpose_reduce<RPW>(v, lane);
-      if ((lane & ((32 / RPW) - 1)) == 0) {
-        const int off = ((bb & 3) * 16 + cr) * L + warp * RPW + row_of_lane<RPW>(lane);
-        for (int q = 0; q < CS; ++q) cluster.map_shared_rank(apub, q)[off] = v[0];
+      // lane (32/RPW) r holds row r: broadcast the warp's RPW sums, then lane q < CS
+      // writes them to rank q with 16-byte stores
+      double vals[RPW];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) vals[r] = __shfl_sync(0xffffffffu, v[0], (32 / RPW) * r);
+      if (PUSH) {
+        if (lane < CS) {
+          double* dst = cluster.map_shared_rank(apub, lane) + ((bb & 3) * 16 + cr) * L + warp * RPW;
+#pragma unroll
+          for (int r = 0; r < RPW; r += 2) *reinterpret_cast<double2*>(dst + r) = make_double2(vals[r], vals[r + 1]);
+        }
+      } else if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) apub[(bb & 3) * L + warp * RPW + r] = vals[r];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are pushed
@@ -441,7 +456,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       mbar_wait(&mx_full[mslot], (uint32_t)((b / MXB) & 1));
       // X term (threads L..2L-1): xterm_i = (X_b delta_{b-1})_i
       if (tid >= L && tid < 2 * L && b > 0) {
-        const double* dp = dl + ((b - 1) & 1) * L;
+        const double* dp = dl;  // delta_{b-1}: overwritten only after the next two barriers
         const int i = tid - L;
         double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
 #pragma unroll
@@ -461,7 +476,10 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       if (tid < L) {
         double part[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) part[q] = q < CS ? apub[((b & 3) * 16 + q) * L + tid] : 0.0;
+        for (int q = 0; q < 16; ++q)
+          part[q] = q >= CS ? 0.0
+                    : PUSH  ? apub[((b & 3) * 16 + q) * L + tid]
+                            : cluster.map_shared_rank(apub, q)[(b & 3) * L + tid];
         double s = 0.0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) s += part[q];
@@ -471,7 +489,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       named_bar(1, NT);
       unsigned long long c4 = prof ? clock64() : 0;
       // delta_b = M_b z (thread tid < L: row tid, four partial sums)
-      double* dcur = dl + (b & 1) * L;
+      double* dcur = dl;
       if (tid < L) {
         double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
@@ -532,7 +550,10 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
     }
     if (prof)
       for (int q = 0; q < 7; ++q) atomicAdd(a.prof + q, tp[q]);
-    if (prof) atomicAdd(a.prof + 9, tp[7]);
+    if (prof) {
+      atomicAdd(a.prof + 9, tp[7]);
+      atomicAdd(a.prof + 10, tp[8]);
+    }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       if (!act[c]) continue;
@@ -546,7 +567,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
 template <int CPT, int L, int MXB>
 constexpr size_t sstep_chain_smem() {
   return (size_t)kChainNB * L * 128 * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
-         sizeof(double) * (4 * 16 * L + L + L + 2 * L + L) + sizeof(int64_t) * kChainNB * L +
+         sizeof(double) * (4 * (CPT == 1 ? 16 : 1) * L + 3 * L) +
          sizeof(uint64_t) * (3 * kChainNB + 4 + 2 * MXB + 2) + sizeof(double) * 128 * CPT + 128;
 }
 
