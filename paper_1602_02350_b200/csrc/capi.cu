@@ -100,6 +100,11 @@ struct skr_problem {
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
   DBuf<double> s_state, s_M, s_p, s_X;  // s-step inner loop workspaces
+  // pinned host staging for the host-buffer entry points: [0, ld) w, [ld, 2 ld] mu and the objective
+  double* io_host = nullptr;
+  ~skr_problem() {
+    if (io_host) cudaFreeHost(io_host);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -1339,8 +1344,13 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       SKR_LAUNCHED(&c);
       P32.alloc((size_t)k * ld, c.stream);
     }
+    // "lanczos_gemm" marks bracket the Krylov / Rayleigh-Ritz products only (bench: GEMM TFLOP/s)
+    auto gmark = [&] {
+      if (c.prof_on) c.prof_mark("lanczos_gemm");
+    };
     // block = A Pi  -> Vt (k x ld) = scale * Pi^T X   (sketch.cpp:25)
     Vt.zero();
+    gmark();
     if (tc) {
       tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, k, d, n, scale, Vt.get(), ld);
     } else {
@@ -1349,6 +1359,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
         gemm<double, T, false, false>(&c, k, d, n, Pt.get(), n, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
       });
     }
+    gmark();
     c.allreduce_sum(Vt.get(), (size_t)k * ld);
     int appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), (int)k);
     if (Wb == 0) raise(SKR_EEMPTY, "krylov_block: A * Pi is numerically zero");
@@ -1357,6 +1368,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     for (int64_t j = 1; j < q && appended > 0; ++j) {
       const int64_t W = Wb;
       const double* prev = Qt.get() + (W - appended) * ld;
+      gmark();
       if (tc) {
         // T^T (a x n, fp32) = scale (X prev^T)^T ;  block^T = scale T^T X = scale T^T . (X^T)^T
         convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(appended * ld, 256), 65535u), 256, 0, c.stream>>>(
@@ -1377,6 +1389,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
           gemm<double, T, true, false>(&c, appended, d, n, Tm.get(), appended, X, ld, EpiStore{Vt.get(), ld, scale, 0.0});
         });
       }
+      gmark();
       c.allreduce_sum(Vt.get(), (size_t)appended * ld);
       appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), appended);
     }
@@ -1388,6 +1401,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     // Rayleigh-Ritz: G = (X Q)^T (X Q) scale^2 over row chunks (sketch.cpp:59-61)
     DBuf<double> G((size_t)W * W, c.stream);
     G.zero();
+    gmark();
     if (tc) {
       DBuf<float> Q32((size_t)W * ld, c.stream), Zt((size_t)W * np, c.stream);
       convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(W * ld, 256), 65535u), 256, 0, c.stream>>>(
@@ -1414,6 +1428,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
         gemm<double, double, true, false>(&c, W, W, rows, Z.get(), W, Z.get(), W, EpiStore{G.get(), W, 1.0, 1.0});
       }
     }
+    gmark();
     c.allreduce_sum(G.get(), (size_t)W * W);
     // eigendecomposition on the device (cuSOLVER syevd), reference ordering/sign rules
     DBuf<double> evals(W, c.stream), vals_desc(W, c.stream), Wt((size_t)kk * W, c.stream);
@@ -1622,7 +1637,8 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     p->half.alloc(ld, c.stream);
     p->pinv.alloc(ld, c.stream);
     p->wv.alloc(ld, c.stream);
-    p->muv.alloc(ld, c.stream);
+    p->muv.alloc(ld + 1, c.stream);  // mu, then the objective at [ld]: one device->host copy
+    SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));
     p->objv.alloc(1, c.stream);
     p->wv.zero();
     c.sync();
@@ -1690,11 +1706,16 @@ int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) 
     if (!p) raise(SKR_EPARAM, "null problem");
     check_vec(w, "w");
     Ctx& c = p->ctx->c;
-    upload_padded(c, p->wv.get(), w, p->d, p->ld);
-    problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->objv.get() : nullptr);
-    if (mu) SKR_CUDA(cudaMemcpyAsync(mu, p->muv.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
-    if (obj) SKR_CUDA(cudaMemcpyAsync(obj, p->objv.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    // pinned staging: both copies are asynchronous DMA, the padding of wv stays zero
+    const int64_t d = p->d, ld = p->ld;
+    std::memcpy(p->io_host, w, sizeof(double) * d);
+    SKR_CUDA(cudaMemcpyAsync(p->wv.get(), p->io_host, sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
+    problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->muv.get() + ld : nullptr);
+    SKR_CUDA(cudaMemcpyAsync(p->io_host + ld, p->muv.get(), sizeof(double) * (obj ? ld + 1 : d),
+                             cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    if (mu) std::memcpy(mu, p->io_host + ld, sizeof(double) * d);
+    if (obj) *obj = p->io_host[2 * ld];
   });
 }
 

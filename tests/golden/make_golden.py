@@ -6,13 +6,14 @@ oracle/Makefile) — never the restatement — and stores inputs and outputs:
   tests/golden/small.npz   small known-answer cases (streams, eigensolver,
                            block_lanczos incl. rank drop, preconditioned
                            components, SVRG trace + index stream, L*, kappa~)
-  tests/golden/configs.json  BASELINE configs c1, c2 (and c3 row-subsampled)
+  tests/golden/configs.json  BASELINE configs c1, c2 (c3, c4, c5 row-subsampled to n = 16384; c5 at
+                           lambda 1e-6 and 1e-8, and unpreconditioned at 1e-6)
                            composed as SURVEY §0 fact 6 prescribes: sigma~,
                            beta_hat, alpha, eta, per-epoch objectives, L(w^), L*,
                            kappa~ (d <= 2000), index-stream head; inputs come
                            from paper_1602_02350_b200.configs.host_instance.
 
-Usage:  python tests/golden/make_golden.py [small] [c1] [c2] [c3]
+Usage:  python tests/golden/make_golden.py [small] [c1] [c2] [c3] [c4] [c5]
 """
 from __future__ import annotations
 
@@ -99,11 +100,14 @@ def small():
     print("small.npz written", len(out), "arrays")
 
 
-def config_case(name: str, n_override: int | None = None, epochs: int | None = None, kappa: bool = True):
+def config_case(name: str, n_override: int | None = None, epochs: int | None = None, kappa: bool = True,
+                lam: float | None = None, sketched: bool = True):
     R = oracle.ref()
     cfg = configs.CONFIGS[name]
     if n_override:
         cfg = cfg.scaled(n_override)
+    if lam is not None:
+        cfg = configs.Config(**{**cfg.__dict__, "lam": lam})
     t0 = time.time()
     X, y = configs.host_instance(cfg)
     Xd = X.astype(np.float64)
@@ -112,7 +116,8 @@ def config_case(name: str, n_override: int | None = None, epochs: int | None = N
     digest = hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest()
     sk = R.block_lanczos(Xd, cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
     t_l = time.time() - t0
-    prob = R.problem(Xd, yd, cfg.lam, sk.U, sk.sigma, 0)
+    # unsketched baseline (Preconditioner::identity == RidgeFiniteSum, test_ridge.cpp:109-127)
+    prob = R.problem(Xd, yd, cfg.lam, sk.U, sk.sigma, 0) if sketched else R.problem(Xd, yd, cfg.lam, None, None, 0)
     betas = prob.betas()
     alpha, beta_hat, _ = prob.scalars()
     # eta = 1/(4 max_i ||x~_i||^2): ||x~_i||^2 = beta_i n/(n+d) (ridge.cpp:124-127)
@@ -121,11 +126,11 @@ def config_case(name: str, n_override: int | None = None, epochs: int | None = N
     ep = epochs or cfg.epochs
     wmin, Lstar = R.reference_minimum(Xd, yd, cfg.lam)
     sv = prob.svrg(ep, 2 * n, eta, cfg.seed, reference=Lstar)
-    w_hat = R.apply_inv_sqrt(sk.U, sk.sigma, cfg.lam, sv.iterate)
+    w_hat = R.apply_inv_sqrt(sk.U, sk.sigma, cfg.lam, sv.iterate) if sketched else sv.iterate
     L = R.objective(Xd, yd, cfg.lam, w_hat)
     idx = R.index_stream(betas, cfg.seed, 100000)
     rec = {
-        "config": name, "n": n, "d": d, "dtype": cfg.dtype, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam,
+        "config": name, "n": n, "d": d, "dtype": cfg.dtype, "k": cfg.k if sketched else 0, "q": cfg.q, "lambda": cfg.lam,
         "seed": cfg.seed, "epochs": ep, "m": 2 * n, "x_sha256": digest,
         "sigma": sk.sigma.tolist(), "k_used": sk.k, "alpha": alpha, "beta_hat": beta_hat,
         "max_row_sq": max_row_sq, "eta": eta, "trace": sv.trace.tolist(), "L_hat": L, "L_star": Lstar,
@@ -133,7 +138,7 @@ def config_case(name: str, n_override: int | None = None, epochs: int | None = N
         "seconds": {"lanczos": t_l, "total": time.time() - t0},
         "source": "oracle/_ref (unmodified reference library)",
     }
-    if kappa and d <= 2000:
+    if kappa and d <= 2000 and sketched:
         rec["kappa"] = R.conditioned_cond(Xd, cfg.lam, sk.U, sk.sigma)
     print(name, "done in", round(time.time() - t0, 1), "s", flush=True)
     return rec
@@ -151,6 +156,12 @@ def main():
         db["c2"] = config_case("c2")
     if "c3" in which:
         db["c3_n16384"] = config_case("c3", n_override=16384, epochs=4, kappa=False)
+    if "c4" in which:
+        db["c4_n16384"] = config_case("c4", n_override=16384, epochs=12, kappa=False)
+    if "c5" in which:
+        for lam, tag in ((1e-6, "l6"), (1e-8, "l8")):
+            db[f"c5_n16384_{tag}"] = config_case("c5", n_override=16384, epochs=6, lam=lam)
+        db["c5_n16384_l6_svrg"] = config_case("c5", n_override=16384, epochs=6, lam=1e-6, sketched=False)
     with open(path, "w") as f:
         json.dump(db, f, indent=1)
     print("configs.json:", list(db))

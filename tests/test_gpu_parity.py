@@ -404,3 +404,34 @@ def test_config_c3_subsampled_fp32_tensor_core_lanczos():
     assert abs(eta - gold["eta"]) <= 1e-3 * gold["eta"]  # via the fp32-accurate U: same 1e-3 scale as the Ritz gate
     assert abs(L - gold["L_hat"]) <= 1e-5 * abs(gold["L_hat"])           # BASELINE fp32 L(w^) gate
     print("c3 sigma rel err", rel(sv.singular_values, gold["sigma"]), "L rel err", abs(L - gold["L_hat"]) / gold["L_hat"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["c4_n16384", "c5_n16384_l6", "c5_n16384_l8", "c5_n16384_l6_svrg"])
+def test_config_c4_c5_subsampled_against_reference_golden(key):
+    """c4 (heavy-tailed rows, d = 4096, k = 256) and c5 (lambda sweep; preconditioned and
+    unpreconditioned SVRG) at n = 16384 against the unmodified reference at the BASELINE
+    fp32 gates.  Data are fp32-rounded; the reference computes in fp64 on the same values."""
+    gold = _golden(key)
+    base = configs.CONFIGS[key[:2]].scaled(gold["n"])
+    cfg = configs.Config(**{**base.__dict__, "lam": gold["lambda"]})
+    X, y = configs.host_instance(cfg)
+    assert X.dtype == np.float32
+    n, d = X.shape
+    p = sk.RidgeProblem(sk.DataMatrix(X), y.astype(np.float64), cfg.lam)
+    if gold["k"]:
+        sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+        assert rel(sv.singular_values, gold["sigma"]) < 1e-3                  # BASELINE fp32 Ritz gate
+        pc = sk.build_sketched(sv, cfg.lam)
+    else:
+        pc = sk.Preconditioner.identity(d, cfg.lam)
+    pg = sk.preconditioned_components(p, pc)
+    eta = configs.eta_for(cfg, pg.max_row_sq(), pg.mean_beta())
+    assert abs(eta - gold["eta"]) <= 1e-3 * gold["eta"]
+    res = sk.svrg_solve(pg, sk.SvrgConfig(gold["epochs"], 2 * n, eta, cfg.seed), np.zeros(d))
+    L = sk.objective(p, pg.apply_inv_sqrt(res.iterate))
+    assert abs(L - gold["L_hat"]) <= 1e-5 * abs(gold["L_hat"])           # BASELINE fp32 L(w^) gate
+    if "kappa" in gold:
+        kappa = sk.conditioned_condition_number(sk.scaled_design(p), cfg.lam, pc)
+        assert abs(kappa - gold["kappa"]) <= 1e-3 * gold["kappa"]        # BASELINE fp32 kappa gate
+    assert abs(sk.reference_minimum(p).minimum - gold["L_star"]) <= 1e-8 * gold["L_star"]
