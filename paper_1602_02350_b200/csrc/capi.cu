@@ -274,7 +274,7 @@ FgPlan run_fullgrad_tiles(Ctx& c, int64_t ld, int64_t n, const T* X, const doubl
 
 template <class T, int CH, int RPI>
 void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
-                    double* part_g, double* part_loss, bool plan_only) {
+                    double* part_g, double* part_loss, bool plan_only, const UwHead& head) {
   auto kern = fullgrad_rowwarp_kernel<T, CH, RPI>;
   const size_t smem = 2 * ld * sizeof(double);
   static int per_sm = 0;
@@ -289,19 +289,29 @@ void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const 
   const int64_t warps_needed = (n + RPI - 1) / RPI;
   p.nt = kRowwarpThreads;
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((warps_needed + NWR - 1) / NWR, (int64_t)per_sm * c.sm_count));
+  if (head.Ut) p.grid = (int)std::max<int64_t>(p.grid, (head.k + 1 + NWR - 1) / NWR);  // k+1 head warps
   if (plan_only) return;
   if (getenv("SKR_DEBUG"))
     fprintf(stderr, "[skr] K9 rowwarp: CH=%d RPI=%d smem=%zu per_sm=%d grid=%d\n", CH, RPI, smem, per_sm, p.grid);
-  kern<<<p.grid, kRowwarpThreads, smem, c.stream>>>(X, ld, n, y, w, part_g, part_loss);
+  kern<<<p.grid, kRowwarpThreads, smem, c.stream>>>(X, ld, n, y, w, part_g, part_loss, head);
   SKR_LAUNCHED(&c);
 }
 
 // K9 dispatch: warp-per-row (v4) for fp64 rows with d <= 1024 (<= 32 elements per
 // lane) and short fp32 rows, else the bulk-copy staged tile kernel (v3).
 // SKR_K9_IMPL=4 forces warp-per-row, 2/3 the tile variants.
+// Warp-per-row wins for fp64 rows (c2: 5.40 vs 3.36-3.62 TB/s for the tile kernel);
+// for fp32 rows > 2 KB the bulk-copy tile kernel wins (c5: 5.46 vs 5.15 TB/s).
+bool k9_uses_rowwarp(int64_t ld, int dtype) {
+  static const int env_impl = getenv("SKR_K9_IMPL") ? atoi(getenv("SKR_K9_IMPL")) : 0;
+  const int64_t row_bytes = ld * (dtype == SKR_F64 ? 8 : 4);
+  if (ld > 1024) return false;
+  return env_impl == 4 || (env_impl == 0 && (dtype == SKR_F64 || row_bytes <= 2048));
+}
 template <class T>
 FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
-                         double* part_g, double* part_loss, bool plan_only) {
+                         double* part_g, double* part_loss, bool plan_only,
+                         const UwHead& head = UwHead{nullptr, nullptr, 0, 0}) {
   static int env_impl = [] {
     const char* e = getenv("SKR_K9_IMPL");
     return e ? atoi(e) : 0;
@@ -310,18 +320,15 @@ FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double
     const char* e = getenv("SKR_K9_RPI");
     return e ? atoi(e) : 1;
   }();
-  const int64_t row_bytes = ld * (int64_t)sizeof(T);
-  // warp-per-row wins for fp64 rows (c2: 5.40 vs 3.36-3.62 TB/s for the tile kernel);
-  // for fp32 rows > 2 KB the bulk-copy tile kernel wins (c5: 5.46 vs 5.15 TB/s)
-  const bool rowwarp = env_impl == 4 || (env_impl == 0 && ld <= 1024 && (sizeof(T) == 8 || row_bytes <= 2048));
-  if (rowwarp && ld <= 1024) {  // <= 32 elements per lane
+  if (k9_uses_rowwarp(ld, sizeof(T) == 8 ? SKR_F64 : SKR_F32)) {  // <= 32 elements per lane
+    const int64_t row_bytes = ld * (int64_t)sizeof(T);
     FgPlan p;
     p.bytes = (int)row_bytes;
     const int ch = (int)((row_bytes + 511) / 512);  // 16-byte chunks per lane
 #define RW(CHV)                                                                                         \
   if (ch <= CHV) {                                                                                      \
-    if (env_rpi == 2) launch_rowwarp<T, CHV, 2>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);  \
-    else launch_rowwarp<T, CHV, 1>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);               \
+    if (env_rpi == 2) launch_rowwarp<T, CHV, 2>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head); \
+    else launch_rowwarp<T, CHV, 1>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head);              \
     return p;                                                                                           \
   }
     RW(2) RW(4) RW(8)
@@ -334,6 +341,7 @@ FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double
 struct FinalizeArgs {  // set when the pass should end in mu / obj directly
   double n = 1, lambda = 0, c = 1;
   const double *w = nullptr, *Ut = nullptr, *uw = nullptr, *D = nullptr;
+  UwHead head{nullptr, nullptr, 0, 0};  // warp-per-row pass computes uw itself
   int64_t d = 0, k = 0;
   double *mu = nullptr, *obj = nullptr;
 };
@@ -346,7 +354,8 @@ void fullgrad_sums(Ctx& c, int dtype, const void* X, int64_t ld, int64_t n, cons
                    DBuf<double>& sums, const FinalizeArgs* fin = nullptr) {
   FgPlan plan;
   DISPATCH_DTYPE(dtype, T, plan = run_fullgrad_main<T>(c, ld, std::max<int64_t>(n, 1), (const T*)X, y, w, nullptr,
-                                                        nullptr, true));
+                                                        nullptr, true,
+                                                        fin ? fin->head : UwHead{nullptr, nullptr, 0, 0}));
   const size_t need_g = (size_t)plan.grid * ld;
   if (part_g.n < need_g) part_g.alloc(need_g, c.stream);
   if (part_loss.n < (size_t)plan.grid) part_loss.alloc(plan.grid, c.stream);
@@ -355,9 +364,10 @@ void fullgrad_sums(Ctx& c, int dtype, const void* X, int64_t ld, int64_t n, cons
   if (n > 0) {
     if (c.prof_on) c.prof_mark("fullgrad");
     DISPATCH_DTYPE(dtype, T, run_fullgrad_main<T>(c, ld, n, static_cast<const T*>(X), y, w, part_g.get(),
-                                                  part_loss.get(), false));
+                                                  part_loss.get(), false,
+                                                  fin ? fin->head : UwHead{nullptr, nullptr, 0, 0}));
     if (c.prof_on) c.prof_mark("fullgrad");
-    fullgrad_colreduce_kernel<<<ceil_div(ld + 1, 32), 256, 0, c.stream>>>(
+    fullgrad_colreduce_kernel<<<ceil_div(ld + 1, 8), 256, 0, c.stream>>>(
         part_g.get(), part_loss.get(), ld, plan.grid, direct ? fin->d : 0, direct ? fin->n : 1.0,
         direct ? fin->lambda : 0.0, direct ? fin->w : nullptr, direct ? fin->Ut : nullptr, direct ? fin->uw : nullptr,
         direct ? fin->k : 0, direct ? fin->D : nullptr, direct ? fin->c : 1.0, direct ? fin->mu : nullptr,
@@ -390,10 +400,15 @@ void apply_inv_sqrt_dev(Ctx& c, const skr_problem* p, const double* v, double* p
 void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) {
   Ctx& c = p->ctx->c;
   // U^T w and w.w for lambda P^{-1} w and the regulariser norm (applied in the
-  // fused reduction); a few small CTAs ordered before the streaming pass
-  proj_kernel<<<ceil_div((p->k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), p->ld, p->d, p->k, w, p->uw.get());
-  SKR_LAUNCHED(&c);
+  // column reduction): computed by the first k+1 warps of the warp-per-row pass
+  // itself, or by a separate small launch ordered before the tile pass.
   FinalizeArgs fin;
+  if (k9_uses_rowwarp(p->ld, p->dtype) && p->n > 0) {
+    fin.head = UwHead{p->Ut.get(), p->uw.get(), p->d, p->k};
+  } else {
+    proj_kernel<<<ceil_div((p->k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), p->ld, p->d, p->k, w, p->uw.get());
+    SKR_LAUNCHED(&c);
+  }
   fin.n = (double)p->n_global;
   fin.lambda = p->lambda;
   fin.c = p->c;

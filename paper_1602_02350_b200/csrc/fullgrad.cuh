@@ -318,11 +318,30 @@ fullgrad_tma_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const double
 // once at the end through shared memory.
 constexpr int kRowwarpThreads = 384;  // 12 warps, one CTA per SM at <= 168 registers
 
+__device__ __noinline__ void head_projection(const double* __restrict__ Ut, double* __restrict__ uw, int64_t ld,
+                                             int64_t d, int64_t k, const double* __restrict__ w, int64_t j,
+                                             int lane) {
+  const double* row = j < k ? Ut + j * ld : w;
+  double s = 0.0;
+  for (int64_t i = lane; i < d; i += 32) s = fma(row[i], w[i], s);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) uw[j] = s;
+}
+
+// Optional head work: warps 0..k of the grid first compute uw[j] = U_j . w
+// (uw[k] = w . w) for the column reduction, saving a launch.
+struct UwHead {
+  const double* Ut;  // k x ld, or nullptr: no head work
+  double* uw;
+  int64_t d, k;
+};
+
 template <class T, int CH, int RPI>
 __global__ void __launch_bounds__(kRowwarpThreads, 1)
 fullgrad_rowwarp_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const double* __restrict__ y,
                         const double* __restrict__ w, double* __restrict__ part_g,
-                        double* __restrict__ part_loss) {
+                        double* __restrict__ part_loss, UwHead head) {
   constexpr int PER = 16 / sizeof(T);
   constexpr int E = CH * PER;  // elements per lane per row
   extern __shared__ double sw[];  // [0, ld): w; [ld, 2 ld): warp combine buffer
@@ -338,6 +357,7 @@ fullgrad_rowwarp_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const do
   for (int e = 0; e < E; ++e) acc[e] = 0.0;
   double loss = 0.0;
   const int64_t gw = (int64_t)blockIdx.x * nw + warp, GW = (int64_t)gridDim.x * nw;
+  if (head.Ut && gw <= head.k) head_projection(head.Ut, head.uw, ld, head.d, head.k, w, gw, lane);
   for (int64_t r0 = gw * RPI; r0 < n; r0 += GW * RPI) {
     T x[RPI][E];
     double yv[RPI];
@@ -396,10 +416,9 @@ fullgrad_rowwarp_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const do
   }
 }
 
-// Single-level deterministic reduction + finalisation: block b owns columns
-// [32b, 32b+32) (column ld = the loss); warp q sums partials q, q+8, ... with
-// lane = column (coalesced), the 8 warp sums are added in warp order, and the
-// block writes mu = sums/n + lambda (c^2 w + U (D^2 - c^2) U^T w) for its columns
+// Single-level deterministic reduction + finalisation: one warp per column
+// (column ld = the loss), lanes sum the per-CTA partials in a fixed order, and
+// the warp writes mu = sums/n + lambda (c^2 w + U (D^2 - c^2) U^T w) for its column
 // (P^{-1} = c^2 I + U (D^2 - c^2) U^T; ridge.cpp:232-235) — or the raw sums when
 // mu == nullptr (distributed path, allreduced afterwards).
 __global__ void __launch_bounds__(256)
@@ -409,42 +428,40 @@ fullgrad_colreduce_kernel(const double* __restrict__ part_g, const double* __res
                           const double* __restrict__ uw, int64_t k, const double* __restrict__ D,
                           double c, double* __restrict__ mu, double* __restrict__ obj,
                           double* __restrict__ sums) {
-  __shared__ double red[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  if (j <= ld) {
-    const double* src = j < ld ? part_g + j : part_loss;
-    const int64_t stride = j < ld ? ld : 1;
-    int b = warp;
-    for (; b + 24 < parts; b += 32) {
-      a0 += src[(int64_t)b * stride];
-      a1 += src[(int64_t)(b + 8) * stride];
-      a2 += src[(int64_t)(b + 16) * stride];
-      a3 += src[(int64_t)(b + 24) * stride];
-    }
-    for (; b < parts; b += 8) a0 += src[(int64_t)b * stride];
+  // one warp per column (j == ld: the loss); lanes take partials lane, lane+32, ...
+  // in a fixed order, then a butterfly: deterministic, ~parts/32 loads in flight per lane
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j > ld) return;
+  const double* src = j < ld ? part_g + j : part_loss;
+  const int64_t stride = j < ld ? ld : 1;
+  double a0 = 0.0, a1 = 0.0;
+  int b = lane;
+  for (; b + 32 < parts; b += 64) {
+    a0 += src[(int64_t)b * stride];
+    a1 += src[(int64_t)(b + 32) * stride];
   }
-  red[warp][lane] = (a0 + a1) + (a2 + a3);
-  __syncthreads();
-  if (warp != 0 || j > ld) return;
-  double acc = 0.0;
+  if (b < parts) a0 += src[(int64_t)b * stride];
+  double acc = a0 + a1;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc += red[q][lane];
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  const double cc = c * c;
   if (sums) {
-    sums[j] = acc;
+    if (lane == 0) sums[j] = acc;
   } else if (j < ld) {
-    if (j < d) {
-      double r = c * c * w[j];
-      for (int64_t l = 0; l < k; ++l) r = fma(Ut[l * ld + j], (D[l] * D[l] - c * c) * uw[l], r);
-      mu[j] = acc * (1.0 / n) + lambda * r;
-    } else {
-      mu[j] = 0.0;
-    }
+    // lambda P^{-1} w_j = lambda (c^2 w_j + sum_l U_lj (D_l^2 - c^2) (U^T w)_l), lanes split l
+    double r = 0.0;
+    if (j < d)
+      for (int64_t l = lane; l < k; l += 32) r = fma(Ut[l * ld + j], (D[l] * D[l] - cc) * uw[l], r);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+    if (lane == 0) mu[j] = j < d ? acc * (1.0 / n) + lambda * (cc * w[j] + r) : 0.0;
   } else if (obj) {
-    double reg = c * c * uw[k];
-    for (int64_t l = 0; l < k; ++l) reg += (D[l] * D[l] - c * c) * uw[l] * uw[l];
-    *obj = acc / (2.0 * n) + 0.5 * lambda * reg;
+    double reg = 0.0;
+    for (int64_t l = lane; l < k; l += 32) reg += (D[l] * D[l] - cc) * uw[l] * uw[l];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) reg += __shfl_xor_sync(0xffffffffu, reg, off);
+    if (lane == 0) *obj = acc / (2.0 * n) + 0.5 * lambda * (cc * uw[k] + reg);
   }
 }
 
