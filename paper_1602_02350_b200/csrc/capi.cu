@@ -525,6 +525,57 @@ void draw_indices(skr_problem* p, DBuf<double>& u, DBuf<int64_t>& idx, int64_t m
 // MgsBasis::append_block (factorize.cpp:53-71): BCGS2 against the accepted
 // basis Qt[0..W), Householder QR of the block, drop |R_jj| < 1e-12 * ref.
 // V (a rows x ld) is overwritten.  Returns the number of rows appended.
+// CholeskyQR2 of the projected block (rows of V): twice G = V V^T, G = L L^T
+// (potrf), V <- L^{-1} V (trtri + DMMA GEMM).  R_jj = L1_jj L2_jj > 0, the sign
+// convention of the Householder path.  Returns false (V untouched) when the
+// block is too ill-conditioned for it — Cholesky breakdown or some R_jj below
+// 1e-6 of the reference norm, where the 1e-12 drop rule could matter — and the
+// caller falls back to Householder QR, which applies the drop rule exactly.
+bool cholqr2_append(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap, double* V, int a,
+                    const double* ref) {
+  DBuf<double> G((size_t)a * a, c.stream), Vb((size_t)a * ld, c.stream), Vc((size_t)a * ld, c.stream),
+      diag(2 * (size_t)a, c.stream);
+  DBuf<int> info(3, c.stream);
+  info.zero();
+  int lw = 0;
+  SKR_SOLVER(cusolverDnDpotrf_bufferSize(c.solver, CUBLAS_FILL_MODE_LOWER, a, G.get(), a, &lw));
+  size_t tw_dev = 0, tw_host = 0;
+  SKR_SOLVER(cusolverDnXtrtri_bufferSize(c.solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, a, CUDA_R_64F,
+                                         G.get(), a, &tw_dev, &tw_host));
+  DBuf<double> work(std::max<size_t>((size_t)lw, tw_dev / 8 + 1), c.stream);
+  std::vector<unsigned char> hwork(tw_host + 1);
+  const double* cur = V;
+  double* nxt = Vb.get();
+  for (int pass = 0; pass < 2; ++pass) {
+    gemm<double, double, false, true>(&c, a, a, d, cur, ld, cur, ld, EpiStore{G.get(), a, 1.0, 0.0});
+    SKR_SOLVER(cusolverDnDpotrf(c.solver, CUBLAS_FILL_MODE_LOWER, a, G.get(), a, work.get(), lw, info.get() + pass));
+    chol_diag_kernel<<<ceil_div(a, 256), 256, 0, c.stream>>>(G.get(), a, diag.get() + (size_t)pass * a);
+    SKR_LAUNCHED(&c);
+    SKR_SOLVER(cusolverDnXtrtri(c.solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, a, CUDA_R_64F, G.get(), a,
+                                work.get(), tw_dev, hwork.data(), tw_host, info.get() + 2));
+    zero_upper_cm_kernel<<<ceil_div((int64_t)a * a, 256), 256, 0, c.stream>>>(G.get(), a);
+    SKR_LAUNCHED(&c);
+    // rows of the new block: L^{-1} (column-major lower) times the rows of cur
+    gemm<double, double, true, false>(&c, a, d, a, G.get(), a, cur, ld, EpiStore{nxt, ld, 1.0, 0.0});
+    if (pass == 0) {
+      cur = nxt;
+      nxt = Vc.get();  // V itself stays untouched for the Householder fallback
+    }
+  }
+  int hc[3] = {W, 0, 0};
+  DBuf<int> cnt(3, c.stream);
+  SKR_CUDA(cudaMemcpyAsync(cnt.get(), hc, sizeof(hc), cudaMemcpyHostToDevice, c.stream));
+  cholqr_select_kernel<<<1, 1024, 0, c.stream>>>(Qt, ld, d, cnt.get(), (int)cap, Vc.get(), diag.get(), a, ref,
+                                                  info.get(),
+                                                  kCholQrMinRatio);
+  SKR_LAUNCHED(&c);
+  SKR_CUDA(cudaMemcpyAsync(hc, cnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (hc[2]) return false;  // rejected: nothing was appended
+  W = hc[0];
+  return true;
+}
+
 int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap, double* V, int a) {
   DBuf<double> ref(1, c.stream), rdiag(a, c.stream), tau(a, c.stream);
   ref.zero();
@@ -536,6 +587,11 @@ int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap,
       gemm<double, double, false, true>(&c, a, W, d, V, ld, Qt, ld, EpiStore{C.get(), W, 1.0, 0.0});
       gemm<double, double, false, false>(&c, a, d, W, C.get(), W, Qt, ld, EpiStore{V, ld, -1.0, 1.0});
     }
+  }
+  static const bool householder_only = getenv("SKR_QR_HOUSEHOLDER") != nullptr;
+  if (!householder_only && a <= d && W + a <= cap) {
+    const int W0 = W;
+    if (cholqr2_append(c, Qt, ld, d, W, cap, V, a, ref.get())) return W - W0;
   }
   int lwork = 0, lwork2 = 0;
   SKR_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, (int)d, a, V, (int)ld, &lwork));
@@ -1020,6 +1076,34 @@ extern "C" {
 const char* skr_last_error(void) { return g_err.c_str(); }
 int skr_abi_version(void) { return SKR_ABI_VERSION; }
 
+// The dense solvers allocate internal device memory lazily on first use; do
+// that now, while the memory pool is still small (measured: a first trtri after
+// the pool had grown to ~150 GB cost ~1 s at c5).
+static void solver_warmup(Ctx& c) {
+  constexpr int a = 32;
+  std::vector<double> eye((size_t)a * a, 0.0);
+  for (int i = 0; i < a; ++i) eye[(size_t)i * a + i] = 1.0;
+  DBuf<double> A((size_t)a * a, c.stream), ev(a, c.stream);
+  DBuf<int> info(1, c.stream);
+  int lw = 0, lw2 = 0;
+  SKR_SOLVER(cusolverDnDpotrf_bufferSize(c.solver, CUBLAS_FILL_MODE_LOWER, a, A.get(), a, &lw));
+  SKR_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, A.get(), a,
+                                         ev.get(), &lw2));
+  size_t tw_dev = 0, tw_host = 0;
+  SKR_SOLVER(cusolverDnXtrtri_bufferSize(c.solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, a, CUDA_R_64F,
+                                         A.get(), a, &tw_dev, &tw_host));
+  DBuf<double> work(std::max<size_t>(std::max(lw, lw2), tw_dev / 8 + 1), c.stream);
+  std::vector<unsigned char> hwork(tw_host + 1);
+  SKR_CUDA(cudaMemcpyAsync(A.get(), eye.data(), sizeof(double) * a * a, cudaMemcpyHostToDevice, c.stream));
+  SKR_SOLVER(cusolverDnDpotrf(c.solver, CUBLAS_FILL_MODE_LOWER, a, A.get(), a, work.get(), lw, info.get()));
+  SKR_SOLVER(cusolverDnXtrtri(c.solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, a, CUDA_R_64F, A.get(), a,
+                              work.get(), tw_dev, hwork.data(), tw_host, info.get()));
+  SKR_CUDA(cudaMemcpyAsync(A.get(), eye.data(), sizeof(double) * a * a, cudaMemcpyHostToDevice, c.stream));
+  SKR_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, a, A.get(), a, ev.get(),
+                              work.get(), std::max(lw, lw2), info.get()));
+  c.sync();
+}
+
 static void ctx_init(Ctx& c, int device) {
   c.device = device;
   SKR_CUDA(cudaSetDevice(device));
@@ -1042,6 +1126,7 @@ static void ctx_init(Ctx& c, int device) {
   SKR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   SKR_SOLVER(cusolverDnCreate(&c.solver));
   SKR_SOLVER(cusolverDnSetStream(c.solver, c.stream));
+  solver_warmup(c);
 }
 
 int skr_ctx_create(int device, skr_ctx** out) {

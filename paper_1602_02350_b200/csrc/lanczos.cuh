@@ -87,6 +87,48 @@ __global__ void qr_select_kernel(double* __restrict__ Qt, int64_t ld, int64_t d,
   }
 }
 
+// CholeskyQR acceptance threshold: R_jj >= kCholQrMinRatio * max original norm
+constexpr double kCholQrMinRatio = 1e-6;
+
+// out[j] = L_jj of a column-major a x a factor
+__global__ void chol_diag_kernel(const double* __restrict__ L, int a, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < a) out[j] = L[(int64_t)j * a + j];
+}
+// zero the strictly upper triangle of a column-major a x a matrix (element (i,j) at j*a + i, i < j)
+__global__ void zero_upper_cm_kernel(double* __restrict__ A, int a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)a * a) return;
+  const int64_t j = e / a, i = e % a;
+  if (i < j) A[e] = 0.0;
+}
+// Accept the CholeskyQR2 block when both factorizations succeeded and every
+// R_jj = L1_jj L2_jj clears min_ratio * ref: then append all rows (up to cap).
+// count = {W (in/out), appended (out), rejected (out)}.
+__global__ void cholqr_select_kernel(double* __restrict__ Qt, int64_t ld, int64_t d, int* __restrict__ count, int cap,
+                                     const double* __restrict__ Q, const double* __restrict__ diag, int a,
+                                     const double* __restrict__ ref, const int* __restrict__ info, double min_ratio) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = (info[0] != 0 || info[1] != 0 || info[2] != 0 || !(*ref > 0.0)) ? 1 : 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < a; j += blockDim.x) {
+    const double r = diag[j] * diag[a + j];
+    if (!(r >= min_ratio * *ref)) bad = 1;
+  }
+  __syncthreads();
+  const int W = count[0];
+  const int take = bad ? 0 : min(a, cap - W);
+  for (int64_t e = threadIdx.x; e < (int64_t)take * ld; e += blockDim.x) {
+    const int64_t j = e / ld, i = e % ld;
+    Qt[(int64_t)(W + j) * ld + i] = i < d ? Q[j * ld + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    count[0] = W + take;
+    count[1] = take;
+    count[2] = bad;
+  }
+}
+
 // V[j] *= sign(R_jj)  (Haar fix-up of an orthogonal factor: Q diag(sign diag R))
 __global__ void qr_sign_rows_kernel(double* __restrict__ Q, int64_t ld, int64_t d, const double* __restrict__ rdiag,
                                     int rows) {
