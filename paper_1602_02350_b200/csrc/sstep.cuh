@@ -412,9 +412,19 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
 #pragma unroll
           for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? x[32 * c] : 0.0, wl[c], s);
         } else {
+          // fp32 data row: widen once and write the fp64 values back in place (the
+          // slot is sized for fp64), so the update of this block reads fp64 rows only
           const T* x = reinterpret_cast<const T*>(rowp) + lane;
+          double xv[CPL];
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? (double)x[32 * c] : 0.0, wl[c], s);
+          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? (double)x[32 * c] : 0.0;
+          __syncwarp();  // every lane has read its fp32 values before any fp64 store lands
+          double* xd = reinterpret_cast<double*>(const_cast<unsigned char*>(rowp)) + lane;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            xd[32 * c] = xv[c];
+            s = fma(xv[c], wl[c], s);
+          }
         }
         v[q] = l < Lbb ? s : 0.0;
       }
@@ -508,14 +518,9 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       unsigned long long c5 = prof ? clock64() : 0;
       // 3. w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
-      const uint64_t dm = dmask[slot];
+      // every row of the slot is fp64 by now (fp32 rows were widened in place by dots())
       auto elem = [&](int l, int c) -> double {
-        if constexpr (sizeof(T) == 8) {
-          return reinterpret_cast<const double*>(rb + (size_t)l * ROWB)[tid * CPT + c];
-        } else {
-          return ((dm >> l) & 1ull) ? (double)reinterpret_cast<const T*>(rb + (size_t)l * ROWB)[tid * CPT + c]
-                                    : reinterpret_cast<const double*>(rb + (size_t)l * ROWB)[tid * CPT + c];
-        }
+        return reinterpret_cast<const double*>(rb + (size_t)l * ROWB)[tid * CPT + c];
       };
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
