@@ -121,6 +121,10 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
  * y: n_local labels (double). */
 int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
                        const double* U, const double* sigma, int64_t k, skr_problem** out);
+/* Second handle on the same problem bound to another context (same device, one
+ * GPU): X~ shared, tables copied, private workspaces — for concurrent SVRG chains
+ * (the eta-grid x seed protocol of bench.cpp:140-193). */
+int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out);
 int skr_problem_destroy(skr_problem* p);
 /* alpha = strong_convexity (ridge.cpp:152-157), beta_hat = mean_beta
  * (svrg.cpp:213-217), max_row_sq = max_i ||x~_i||^2 over data rows */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "skr_apply_inv_sqrt": (cint, [vp, dptr, dptr]),
     "skr_epoch": (cint, [vp, dptr, dptr, lptr, i64, f64, dptr]),
     "skr_svrg": (cint, [vp, P(SvrgConfigC), dptr, f64, dptr, P(EpochRecordC), P(i64)]),
+    "skr_problem_clone": (cint, [vp, vp, P(vp)]),
     "skr_svrg_until": (cint, [vp, P(SvrgConfigC), dptr, f64, f64, dptr, P(EpochRecordC), P(i64)]),
     "skr_index_stream": (cint, [vp, u64, i64, lptr]),
     "skr_mt_uniforms": (cint, [vp, u64, i64, dptr]),

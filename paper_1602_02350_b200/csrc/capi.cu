@@ -1747,6 +1747,67 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
   });
 }
 
+// A second handle on the same preconditioned problem bound to another context
+// (its own streams): X~ is shared, the small tables are copied, workspaces are
+// private — so independent SVRG chains (the eta x seed protocol of
+// bench.cpp:140-193) run concurrently on one GPU.
+int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!src || !out) raise(SKR_EPARAM, "null argument");
+    if (src->ctx->c.world != 1 || c.world != 1) raise(SKR_EPARAM, "problem clone: single-GPU contexts only");
+    if (src->ctx->c.device != c.device) raise(SKR_EPARAM, "problem clone: contexts must share the device");
+    SKR_CUDA(cudaStreamSynchronize(src->ctx->c.stream));
+    auto p = std::make_unique<skr_problem>();
+    p->ctx = ctx;
+    p->dtype = src->dtype;
+    p->n = src->n;
+    p->n_global = src->n_global;
+    p->row0 = src->row0;
+    p->d = src->d;
+    p->ld = src->ld;
+    p->k = src->k;
+    p->lambda = src->lambda;
+    p->c = src->c;
+    p->data_coef = src->data_coef;
+    p->reg_coef = src->reg_coef;
+    p->alpha = src->alpha;
+    p->beta_hat = src->beta_hat;
+    p->max_row_sq = src->max_row_sq;
+    p->xt = src->xt;
+    p->xt_all = src->xt_all;
+    auto copy = [&](DBuf<double>& dst, const DBuf<double>& from) {
+      if (!from.n) return;
+      dst.alloc(from.n, c.stream);
+      SKR_CUDA(cudaMemcpyAsync(dst.get(), from.get(), sizeof(double) * from.n, cudaMemcpyDeviceToDevice, c.stream));
+    };
+    copy(p->B, src->B);
+    copy(p->y, src->y);
+    copy(p->Ut, src->Ut);
+    copy(p->D, src->D);
+    copy(p->betas, src->betas);
+    p->y_all = p->y.get();
+    if (src->tables) {
+      copy(p->cum, src->cum);
+      copy(p->inv_nq, src->inv_nq);
+      copy(p->total, src->total);
+      p->tables = true;
+    }
+    const int64_t k = p->k, ld = p->ld;
+    p->uw.alloc(std::max<int64_t>(k, 1) + 1, c.stream);
+    p->uh.alloc(std::max<int64_t>(k, 1) + 1, c.stream);
+    p->half.alloc(ld, c.stream);
+    p->pinv.alloc(ld, c.stream);
+    p->wv.alloc(ld, c.stream);
+    p->muv.alloc(ld + 1, c.stream);
+    SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));
+    p->objv.alloc(1, c.stream);
+    p->wv.zero();
+    c.sync();
+    *out = p.release();
+  });
+}
+
 int skr_problem_destroy(skr_problem* p) {
   return guard([&] {
     if (!p) return;

@@ -703,3 +703,97 @@ def gaussian_matrix(rows: int, cols: int, seed: int, ctx: Context | None = None)
     out = np.empty(rows * cols)
     _check(_lib.load().skr_gaussian_matrix(ctx.h, int(rows), int(cols), int(seed), out))
     return out.reshape(cols, rows).T
+
+
+# ---------------------------------------------------------------------------
+# Convergence experiment (bench.hpp:31-59, bench.cpp:96-193) with the eta-grid
+# runs of one (method, seed) executed CONCURRENTLY on one GPU: each grid point
+# is an independent SVRG chain on a clone of the problem (skr_problem_clone:
+# shared X~, private workspaces) bound to its own context (own streams).  A
+# chain occupies one thread-block cluster (<= 16 SMs), so the 7 grid points fill
+# the GPU instead of running back to back as in the reference.
+@dataclass
+class BenchConfig:
+    """bench.hpp:31-38."""
+    lam: float = 1e-6
+    k: int = 30
+    epochs: int = 20
+    eta: Optional[float] = None
+    seeds: list = field(default_factory=lambda: [0])
+    mode: ApplyMode = ApplyMode.Auto
+
+
+@dataclass
+class ConvergenceRow:
+    """bench.hpp:40-46."""
+    method: str
+    seed: int
+    epoch: int
+    suboptimality: float
+    elapsed_ms: float
+
+
+def _clone_problem(pre: PreconditionedRidge, ctx: Context) -> PreconditionedRidge:
+    h = vp()
+    _check(_lib.load().skr_problem_clone(pre.h, ctx.h, C.byref(h)))
+    c = object.__new__(PreconditionedRidge)
+    c.__dict__.update(pre.__dict__)
+    c.h = h
+    return c
+
+
+def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7) -> list:
+    """bench.cpp:140-193: both methods, one row per (method, seed, epoch) with the
+    suboptimality against one shared reference solve; epoch length 2(n+d); eta
+    tuned over eta_grid (bench.cpp:96-100) unless fixed — the grid point with the
+    lowest final suboptimality wins (first in grid order on ties), divergent
+    runs are discarded.  The sketched method runs block_lanczos with eps' = 0.5
+    and the seed, as sketched_preconditioned_svrg does (ridge.cpp:427-431)."""
+    from concurrent.futures import ThreadPoolExecutor
+    if not cfg.seeds:
+        raise ParameterError("bench: at least one seed required")
+    problem = RidgeProblem(p.data, p.labels, cfg.lam)
+    ref = reference_minimum(problem)
+    n, d = problem.count(), problem.dim()
+    m = 2 * (n + d)
+    start = max(objective(problem, np.zeros(d)) - ref.minimum, 0.0)
+    plain = preconditioned_components(problem, Preconditioner.identity(d, cfg.lam))
+    ctxs = [Context(p.data.ctx.device) for _ in range(max(1, int(lanes)))]
+    rows = []
+
+    def run_once(job):
+        lane, pre, eta, seed = job
+        clone = _clone_problem(pre, ctxs[lane])
+        try:
+            res = svrg_solve(clone, SvrgConfig(cfg.epochs, m, eta, seed, SvrgMode.Tuned), np.zeros(d), ref.minimum)
+            tr = res.trace
+            final = tr[-1].suboptimality if tr and tr[-1].suboptimality is not None else math.inf
+            return (final if math.isfinite(final) else math.inf), tr
+        except DivergenceError:
+            return math.inf, []
+        finally:
+            del clone
+
+    with ThreadPoolExecutor(max_workers=len(ctxs)) as pool:
+        for sketched in (False, True):
+            method = "sketched-svrg" if sketched else "svrg"
+            for seed in cfg.seeds:
+                if sketched:
+                    sv = block_lanczos(scaled_design(problem), LanczosConfig(cfg.k, 0.5, int(seed)))
+                    pre = preconditioned_components(problem, build_sketched(sv, cfg.lam), cfg.mode)
+                else:
+                    pre = plain
+                grid = [cfg.eta] if cfg.eta is not None else eta_grid(mean_beta(pre))
+                jobs = [(i % len(ctxs), pre, eta, int(seed)) for i, eta in enumerate(grid)]
+                results = list(pool.map(run_once, jobs))
+                best, best_tr = math.inf, []
+                for final, tr in results:  # strict '<' in grid order, as bench.cpp:180
+                    if final < best:
+                        best, best_tr = final, tr
+                if not best_tr:
+                    raise DivergenceError("bench: every step size diverged for method " + method, [])
+                rows.append(ConvergenceRow(method, int(seed), 0, start, 0.0))
+                for rec in best_tr:
+                    rows.append(ConvergenceRow(method, int(seed), rec.epoch,
+                                               max(rec.suboptimality or 0.0, 0.0), rec.elapsed_ms))
+    return rows

@@ -435,3 +435,34 @@ def test_config_c4_c5_subsampled_against_reference_golden(key):
         kappa = sk.conditioned_condition_number(sk.scaled_design(p), cfg.lam, pc)
         assert abs(kappa - gold["kappa"]) <= 1e-3 * gold["kappa"]        # BASELINE fp32 kappa gate
     assert abs(sk.reference_minimum(p).minimum - gold["L_star"]) <= 1e-8 * gold["L_star"]
+
+
+def test_run_convergence_concurrent_grid_matches_sequential_runs(O):
+    """bench.cpp:140-193 on the GPU: the eta grid of each (method, seed) runs as
+    concurrent chains on problem clones; the chosen runs must equal sequential
+    svrg_solve runs bit for bit, and the trace must match the oracle's SVRG."""
+    X, y, lam, k = small_problem(n=1500, d=40, k=5, lam=1e-3)
+    n, d = X.shape
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    cfg = sk.BenchConfig(lam=lam, k=k, epochs=3, seeds=[0, 1])
+    rows = sk.run_convergence(p, cfg)
+    assert len(rows) == 2 * 2 * (cfg.epochs + 1)
+    ref = sk.reference_minimum(p)
+    m = 2 * (n + d)
+    plain = sk.preconditioned_components(p, sk.Preconditioner.identity(d, lam))
+    best, best_tr = np.inf, None
+    for eta in sk.eta_grid(plain.mean_beta()):
+        try:
+            tr = sk.svrg_solve(plain, sk.SvrgConfig(cfg.epochs, m, eta, 1), np.zeros(d), ref.minimum).trace
+        except sk.DivergenceError:
+            continue
+        if tr[-1].suboptimality < best:
+            best, best_tr, best_eta = tr[-1].suboptimality, tr, eta
+    got = [r for r in rows if r.method == "svrg" and r.seed == 1 and r.epoch > 0]
+    assert [r.suboptimality for r in got] == [max(t.suboptimality, 0.0) for t in best_tr]
+    # the chosen run is the reference's own SVRG on the same step size and seed
+    po = O.problem(X, y, lam, None, None)
+    want = po.svrg(cfg.epochs, m, best_eta, 1, reference=ref.minimum)
+    assert rel(np.array([t.objective for t in best_tr]), want.trace) < 1e-10
+    sk_rows = [r for r in rows if r.method == "sketched-svrg"]
+    assert len(sk_rows) == 2 * (cfg.epochs + 1) and all(r.suboptimality >= 0.0 for r in sk_rows)
