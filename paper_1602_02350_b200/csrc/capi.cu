@@ -272,6 +272,30 @@ FgPlan run_fullgrad_tiles(Ctx& c, int64_t ld, int64_t n, const T* X, const doubl
   return p;
 }
 
+template <class T, int CH, int NB, int NTH>
+void launch_rowring(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
+                    double* part_g, double* part_loss, bool plan_only, const UwHead& head) {
+  auto kern = fullgrad_rowring_kernel<T, CH, NB, NTH>;
+  const size_t smem = rowring_smem<NB, NTH>(ld, sizeof(T));
+  static int per_sm = 0;
+  static size_t configured = 0;
+  if (configured != smem) {
+    SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, smem));
+    per_sm = std::max(per_sm, 1);
+    configured = smem;
+  }
+  constexpr int NWR = NTH / 32;
+  p.nt = NTH;
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + NWR - 1) / NWR, (int64_t)per_sm * c.sm_count));
+  if (head.Ut) p.grid = (int)std::max<int64_t>(p.grid, (head.k + 1 + NWR - 1) / NWR);  // k+1 head warps
+  if (plan_only) return;
+  if (getenv("SKR_DEBUG"))
+    fprintf(stderr, "[skr] K9 rowring: CH=%d NB=%d smem=%zu per_sm=%d grid=%d\n", CH, NB, smem, per_sm, p.grid);
+  kern<<<p.grid, NTH, smem, c.stream>>>(X, ld, n, y, w, part_g, part_loss, head);
+  SKR_LAUNCHED(&c);
+}
+
 template <class T, int CH, int RPI>
 void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
                     double* part_g, double* part_loss, bool plan_only, const UwHead& head) {
@@ -302,12 +326,27 @@ void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const 
 // SKR_K9_IMPL=4 forces warp-per-row, 2/3 the tile variants.
 // Warp-per-row wins for fp64 rows (c2: 5.40 vs 3.36-3.62 TB/s for the tile kernel);
 // for fp32 rows > 2 KB the bulk-copy tile kernel wins (c5: 5.46 vs 5.15 TB/s).
-bool k9_uses_rowwarp(int64_t ld, int dtype) {
+enum class K9Path { Ring, RowWarp, Tile };
+// Measured per shape (profiles/k9_tune*.sh, round 1):
+//   fp64 rows > 4 KB (c2): bulk-copy ring NB 4 x 192 threads 6.14 TB/s, register
+//     warp-per-row 5.40, tile kernel 3.4-3.6;
+//   fp32 rows of 2-4 KB (c5): see k9_ring_fp32 below; tile kernel 5.16-5.46;
+//   rows <= 2 KB (c1, L2-resident): register warp-per-row.
+K9Path k9_path(int64_t ld, int dtype) {
   static const int env_impl = getenv("SKR_K9_IMPL") ? atoi(getenv("SKR_K9_IMPL")) : 0;
+  static const bool ring_fp32 = getenv("SKR_K9_RING_FP32") != nullptr;
   const int64_t row_bytes = ld * (dtype == SKR_F64 ? 8 : 4);
-  if (ld > 1024) return false;
-  return env_impl == 4 || (env_impl == 0 && (dtype == SKR_F64 || row_bytes <= 2048));
+  if (ld > 1024) return K9Path::Tile;
+  if (env_impl == 4) return K9Path::RowWarp;
+  if (env_impl == 5) return K9Path::Ring;
+  if (env_impl == 2 || env_impl == 3) return K9Path::Tile;
+  if (row_bytes <= 2048) return K9Path::RowWarp;
+  if (dtype == SKR_F64) return row_bytes > 4096 ? K9Path::Ring : K9Path::RowWarp;
+  return ring_fp32 ? K9Path::Ring : K9Path::Tile;
 }
+// Both warp-per-row paths compute U^T w in their first warps (UwHead).
+bool k9_uses_rowwarp(int64_t ld, int dtype) { return k9_path(ld, dtype) != K9Path::Tile; }
+
 template <class T>
 FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double* y, const double* w,
                          double* part_g, double* part_loss, bool plan_only,
@@ -320,12 +359,23 @@ FgPlan run_fullgrad_main(Ctx& c, int64_t ld, int64_t n, const T* X, const double
     const char* e = getenv("SKR_K9_RPI");
     return e ? atoi(e) : 1;
   }();
-  if (k9_uses_rowwarp(ld, sizeof(T) == 8 ? SKR_F64 : SKR_F32)) {  // <= 32 elements per lane
+  const K9Path path = k9_path(ld, sizeof(T) == 8 ? SKR_F64 : SKR_F32);
+  if (path != K9Path::Tile) {  // <= 32 elements per lane
     const int64_t row_bytes = ld * (int64_t)sizeof(T);
     FgPlan p;
     p.bytes = (int)row_bytes;
     const int ch = (int)((row_bytes + 511) / 512);  // 16-byte chunks per lane
+    // ring depth x threads: 192 KB of rows in flight per SM (6 warps x 4 x 8 KB for fp64 c2 rows)
+    static const int ring_cfg = getenv("SKR_K9_RING") ? atoi(getenv("SKR_K9_RING")) : 0;
 #define RW(CHV)                                                                                         \
+  if (ch <= CHV && path == K9Path::Ring) {                                                             \
+    if (row_bytes <= 4096 && ring_cfg == 0)                                                             \
+      launch_rowring<T, CHV, 8, 192>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head);       \
+    else if (ring_cfg == 1) launch_rowring<T, CHV, 3, 256>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head); \
+    else if (ring_cfg == 3) launch_rowring<T, CHV, 2, 384>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head); \
+    else launch_rowring<T, CHV, 4, 192>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head);      \
+    return p;                                                                                           \
+  }                                                                                                     \
   if (ch <= CHV) {                                                                                      \
     if (env_rpi == 2) launch_rowwarp<T, CHV, 2>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head); \
     else launch_rowwarp<T, CHV, 1>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only, head);              \

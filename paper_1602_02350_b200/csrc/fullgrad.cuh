@@ -416,6 +416,130 @@ fullgrad_rowwarp_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const do
   }
 }
 
+// K9 v5 for narrow rows: warp per row (as v4), but each warp streams its rows
+// through a private NB-deep shared-memory ring filled by the bulk-copy engine
+// (cp.async.bulk, one 1-D copy per row, mbarrier complete_tx).  NB rows per warp
+// stay in flight without holding registers, and no block barrier is needed
+// inside the loop: the warp re-arms a slot right after consuming it.
+template <class T, int CH, int NB, int NTH>
+__global__ void __launch_bounds__(NTH, 1)
+fullgrad_rowring_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const double* __restrict__ y,
+                        const double* __restrict__ w, double* __restrict__ part_g,
+                        double* __restrict__ part_loss, UwHead head) {
+  constexpr int PER = 16 / sizeof(T);
+  constexpr int E = CH * PER;  // elements per lane per row
+  extern __shared__ __align__(128) unsigned char rr_sm[];
+  double* sw = reinterpret_cast<double*>(rr_sm);  // [0, ld): w; [ld, 2 ld): warp combine buffer
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t row_bytes = (uint32_t)(ld * sizeof(T));
+  unsigned char* ring = rr_sm + ((2 * ld * sizeof(double) + 127) / 128) * 128;
+  unsigned char* mine = ring + (size_t)warp * NB * row_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)nw * NB * row_bytes) + warp * NB;
+  for (int64_t i = threadIdx.x; i < ld; i += blockDim.x) sw[i] = w[i];
+  const int64_t gw = (int64_t)blockIdx.x * nw + warp, GW = (int64_t)gridDim.x * nw;
+  if (lane == 0) {
+    for (int s = 0; s < NB; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (lane == 0) {
+    for (int s = 0; s < NB; ++s) {
+      const int64_t row = gw + (int64_t)s * GW;
+      if (row < n) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(mine + (size_t)s * row_bytes, X + row * ld, row_bytes, &bars[s]);
+      }
+    }
+  }
+  if (head.Ut && gw <= head.k) head_projection(head.Ut, head.uw, ld, head.d, head.k, w, gw, lane);
+  const int64_t chunks_per_row = ld / PER;  // ld is a multiple of 16 elements
+  bool act[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) act[c] = (int64_t)lane + 32 * c < chunks_per_row;
+  double acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.0;
+  double loss = 0.0;
+  int64_t j = 0;
+  for (int64_t row = gw; row < n; row += GW, ++j) {
+    const int s = (int)(j % NB);
+    const double yv = y[row];
+    mbar_wait(&bars[s], (uint32_t)((j / NB) & 1));
+    const unsigned char* slot = mine + (size_t)s * row_bytes;
+    T x[E];
+    if constexpr (sizeof(T) == 8) {
+      const double2* src = reinterpret_cast<const double2*>(slot);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const double2 v = act[c] ? src[lane + 32 * c] : make_double2(0.0, 0.0);
+        x[2 * c] = v.x;
+        x[2 * c + 1] = v.y;
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(slot);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const float4 v = act[c] ? src[lane + 32 * c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * c] = v.x;
+        x[4 * c + 1] = v.y;
+        x[4 * c + 2] = v.z;
+        x[4 * c + 3] = v.w;
+      }
+    }
+    double sdot = 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (!act[c]) continue;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) sdot = fma((double)x[c * PER + e], sw[(lane + 32 * c) * PER + e], sdot);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+    const double r = sdot - yv;
+    loss = fma(r, r, loss);  // identical on every lane; lane 0 reports it
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = fma(r, (double)x[e], acc[e]);
+    __syncwarp();  // every lane is done with slot s
+    if (lane == 0) {
+      const int64_t nxt = row + (int64_t)NB * GW;
+      if (nxt < n) {
+        mbar_expect_tx(&bars[s], row_bytes);
+        bulk_g2s(mine + (size_t)s * row_bytes, X + nxt * ld, row_bytes, &bars[s]);
+      }
+    }
+  }
+  // combine the warps of this CTA in warp order (deterministic)
+  double* buf = sw + ld;
+  __shared__ double sloss[32];
+  for (int q = 0; q < nw; ++q) {
+    if (warp == q) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (!act[c]) continue;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int64_t col = ((int64_t)lane + 32 * c) * PER + e;
+          buf[col] = (q == 0 ? 0.0 : buf[col]) + acc[c * PER + e];
+        }
+      }
+      if (lane == 0) sloss[q] = loss;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = threadIdx.x; i < ld; i += blockDim.x) part_g[(int64_t)blockIdx.x * ld + i] = buf[i];
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int q = 0; q < nw; ++q) l += sloss[q];
+    part_loss[blockIdx.x] = l;
+  }
+}
+
+template <int NB, int NTH>
+inline size_t rowring_smem(int64_t ld, size_t elem) {
+  return ((2 * ld * sizeof(double) + 127) / 128) * 128 + (size_t)(NTH / 32) * NB * ld * elem +
+         (size_t)(NTH / 32) * NB * sizeof(uint64_t);
+}
+
 // Single-level deterministic reduction + finalisation: one warp per column
 // (column ld = the loss), lanes sum the per-CTA partials in a fixed order, and
 // the warp writes mu = sums/n + lambda (c^2 w + U (D^2 - c^2) U^T w) for its column
