@@ -292,7 +292,7 @@ def run_ours(args, cfg):
         "passes_per_s": round(1e3 / ms_step, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": "fullgrad_kernel (K9)", "kernel_ms": round(k9_avg, 5), "peak_source": src,
+                     "kernel": k9_kernel_name(cfg), "kernel_ms": round(k9_avg, 5), "peak_source": src,
                      "bytes_per_launch": bytes_per_gpu},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": d * 8,
                 "d2h_bytes_per_step": d * 8 + 8, "ms_per_step": round(e2e_s * 1e3, 4)},
@@ -324,6 +324,17 @@ def run_ours(args, cfg):
         print(json.dumps(out))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def k9_kernel_name(cfg) -> str:
+    """The K9 variant the library dispatches for this shape (capi.cu k9_path)."""
+    ld = (cfg.d + 15) // 16 * 16
+    row_bytes = ld * (8 if cfg.dtype == "f64" else 4)
+    if ld > 1024 or (cfg.dtype == "f32" and row_bytes > 2048):
+        return "fullgrad_tma_kernel (K9 v3: bulk-copy tile ring)"
+    if cfg.dtype == "f64" and row_bytes > 4096:
+        return "fullgrad_rowring_kernel (K9 v5: warp per row, bulk-copy row ring)"
+    return "fullgrad_rowwarp_kernel (K9 v4: warp per row)"
 
 
 FP64_DMMA_TFLOPS = 35.5  # cuBLAS DGEMM 8192^3 measured on this pool's B200 (profiles/fp64_peak.py)
