@@ -771,12 +771,12 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
 constexpr int64_t kSstepChunkBlocks = 1024;  // blocks per prep/chain launch pair (double-buffered)
 static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
 
-template <class T, int CPT, int L>
+template <class T, int CPT, int L, int NT>
 void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
                  double* w_avg) {
   Ctx& c = p->ctx->c;
   const int64_t ld = p->ld;
-  const int CS = (int)((ld + 128 * CPT - 1) / (128 * CPT));
+  const int CS = (int)((ld + NT * CPT - 1) / (NT * CPT));
   if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
   if (p->s_state.n < (size_t)2 * ld) p->s_state.alloc(2 * ld, c.stream);
   const size_t mneed = (size_t)2 * kSstepChunkBlocks * L * L, pneed = (size_t)2 * kSstepChunkBlocks * L;
@@ -784,10 +784,10 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   if (p->s_X.n < mneed) p->s_X.alloc(mneed, c.stream);
   if (p->s_p.n < pneed) p->s_p.alloc(pneed, c.stream);
   auto prep = sstep_prep_kernel<T, L>;
-  constexpr int MXB = CPT == 1 ? 2 : 1;
-  auto chain = sstep_chain_kernel<T, CPT, L, MXB>;
+  constexpr int MXB = (CPT == 1 && NT == 128) ? 2 : 1;
+  auto chain = sstep_chain_kernel<T, CPT, L, MXB, NT>;
   constexpr size_t prep_smem = sstep_prep_smem<L>();
-  constexpr size_t chain_smem = sstep_chain_smem<CPT, L, MXB>();
+  constexpr size_t chain_smem = sstep_chain_smem<CPT, L, MXB, NT>();
   static bool configured = false;
   if (!configured) {
     SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
@@ -824,7 +824,7 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     ChainArgs ca{rows, idx + s0, steps, Mb, pb, Xb, mu, eta, p->s_state.get(), dprof};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(224);
+    cfg.blockDim = dim3(NT + 96);
     cfg.dynamicSmemBytes = chain_smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
@@ -856,10 +856,16 @@ void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64
   static const bool naive = getenv("SKR_K10") && std::string(getenv("SKR_K10")) == "naive";
   if (c.prof_on) c.prof_mark("svrg_epoch");
   if (!naive) {
-    if (p->ld <= 2048) {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32>(p, snap, mu, idx, m, eta, w_avg));
-    } else {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 2, 32>(p, snap, mu, idx, m, eta, w_avg));
+    static const bool wide_cpt2 = getenv("SKR_K10_CPT2") != nullptr;
+    static const int env_nt = getenv("SKR_K10_NT") ? atoi(getenv("SKR_K10_NT")) : 0;
+    if (p->ld <= 2048 && env_nt == 256) {
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 256>(p, snap, mu, idx, m, eta, w_avg));
+    } else if (p->ld <= 2048) {
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 128>(p, snap, mu, idx, m, eta, w_avg));
+    } else if (wide_cpt2) {
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 2, 32, 128>(p, snap, mu, idx, m, eta, w_avg));
+    } else {  // d > 2048: 8 consumer warps per CTA, one column each
+      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 256>(p, snap, mu, idx, m, eta, w_avg));
     }
     if (c.prof_on) c.prof_mark("svrg_epoch");
     return;

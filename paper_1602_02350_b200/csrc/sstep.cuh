@@ -227,9 +227,10 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-template <class T, int CPT, int L, int MXB>
-__global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
-  constexpr int NT = 128, SW = NT * CPT, NB = kChainNB;
+template <class T, int CPT, int L, int MXB, int NT>
+__global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
+  constexpr int NCW = NT / 32;  // consumer warps; then row producer, M/X producer, signaller
+  constexpr int SW = NT * CPT, NB = kChainNB;
   constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
   constexpr size_t ROWB = (size_t)SW * 8;  // bytes per row slot (fits an fp64 slice)
   extern __shared__ __align__(128) unsigned char sm[];
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
   // PUSH (CPT = 1): every rank pushes its partials into apub[slot][rank] of all
   // ranks and gathers locally; pull (CPT = 2, where shared memory is tight): each
   // rank keeps its own apub[slot] and the gather reads the ranks remotely.
-  constexpr bool PUSH = CPT == 1;
+  constexpr bool PUSH = CPT == 1 && NT == 128;
   double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
   double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
   double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
@@ -269,13 +270,13 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       mbar_init(&mx_full[q], 1);
       mbar_init(&mx_empty[q], 1);
     }
-    mbar_init(&pub[0], 4);
-    mbar_init(&pub[1], 4);
+    mbar_init(&pub[0], NCW);
+    mbar_init(&pub[1], NCW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // every CTA's barriers exist before any remote arrive
 
-  if (warp == 6) {
+  if (warp == NCW + 2) {
     // ---------------- signaller: once this CTA's partials of block j are pushed
     // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
     // release fence latency stays off the consumers' path.  pub is 2-deep: the
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       mbar_wait(&pub[j & 1], (uint32_t)((j >> 1) & 1));
       if (lane < CS) mbar_arrive_remote(&ready[j & 3], (uint32_t)lane);
     }
-  } else if (warp == 5) {
+  } else if (warp == NCW + 1) {
     // ---------------- M/X producer: M_b^T, X_b^T, p_b by bulk copy ----------------
     if (lane == 0) {
       for (int64_t b = 0; b < nblk; ++b) {
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
         bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == NCW) {
     // ---------------- row producer warp ----------------
     const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);  // may be <= 0 past ld
     // indices are loaded one block ahead (their L2 latency overlaps the copies)
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
       if (prof) tp[8] += clock64() - w0c;
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
       const uint64_t dm = dmask[slot];
-      constexpr int RPW = L / 4;        // rows per warp: warp q owns rows [q*L/4, (q+1)*L/4)
+      constexpr int RPW = L / NCW;      // rows per warp: warp q owns rows [q*RPW, (q+1)*RPW)
       constexpr int CPL = SW / 32;      // columns per lane, interleaved (conflict-free)
       double wl[CPL];
       const int64_t valid = R.ld - slice0;  // columns past the copied slice hold stale smem
@@ -569,11 +570,11 @@ __global__ void __launch_bounds__(224, 1) sstep_chain_kernel(ChainArgs a) {
   cluster.sync();  // no CTA exits while others may still read its smem / arrive on its barriers
 }
 
-template <int CPT, int L, int MXB>
+template <int CPT, int L, int MXB, int NT>
 constexpr size_t sstep_chain_smem() {
-  return (size_t)kChainNB * L * 128 * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
-         sizeof(double) * (4 * (CPT == 1 ? 16 : 1) * L + 3 * L) +
-         sizeof(uint64_t) * (3 * kChainNB + 4 + 2 * MXB + 2) + sizeof(double) * 128 * CPT + 128;
+  return (size_t)kChainNB * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
+         sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 3 * L) +
+         sizeof(uint64_t) * (3 * kChainNB + 4 + 2 * MXB + 2) + sizeof(double) * NT * CPT + 128;
 }
 
 // w_avg = S / m ; zero padding.
