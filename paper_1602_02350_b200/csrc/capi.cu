@@ -1794,7 +1794,6 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     p->pinv.alloc(ld, c.stream);
     p->wv.alloc(ld, c.stream);
     p->muv.alloc(ld + 1, c.stream);  // mu, then the objective at [ld]: one device->host copy
-    SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));
     p->objv.alloc(1, c.stream);
     p->wv.zero();
     c.sync();
@@ -1856,7 +1855,6 @@ int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out) {
     p->pinv.alloc(ld, c.stream);
     p->wv.alloc(ld, c.stream);
     p->muv.alloc(ld + 1, c.stream);
-    SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));
     p->objv.alloc(1, c.stream);
     p->wv.zero();
     c.sync();
@@ -1925,6 +1923,7 @@ int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) 
     Ctx& c = p->ctx->c;
     // pinned staging: both copies are asynchronous DMA, the padding of wv stays zero
     const int64_t d = p->d, ld = p->ld;
+    if (!p->io_host) SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));  // first call only
     std::memcpy(p->io_host, w, sizeof(double) * d);
     SKR_CUDA(cudaMemcpyAsync(p->wv.get(), p->io_host, sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
     problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->muv.get() + ld : nullptr);
