@@ -184,6 +184,11 @@ int skr_tc_gemm_test(skr_ctx* ctx, const float* A, const float* B, int64_t M, in
 int skr_gaussian_matrix(skr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);
 
 /* ---- diagnostics ------------------------------------------------------- */
+/* dataset_spectrum (bench.cpp:205-212) on the UNSCALED data handle: eigenvalues of
+ * X^T X / n, descending, zero past rank min(d, n); eigs has d entries.  The ratio
+ * diagnostics over it (theoretical_ratio, avg_condition_number, run_ratio_curve)
+ * are O(d) host arithmetic in skridge_b200.hpp. */
+int skr_dataset_spectrum(skr_ctx* ctx, const skr_data* X, double* eigs);
 /* objective(p, w) of the ORIGINAL ridge problem (ridge.cpp:33-43) */
 int skr_ridge_objective(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
                         const double* w, double* out);

@@ -24,6 +24,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <limits>
 #include <vector>
 
 #include "skr.h"
@@ -37,6 +38,7 @@ using Vector = std::vector<double>;
 struct DimensionError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ParameterError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct InputError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct DegenerateSpectrumError : InputError { using InputError::InputError; };
 struct EmptyBasisError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ScaleGuardError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -430,6 +432,66 @@ inline ReferenceSolution reference_minimum(const RidgeProblem& p) {
   check(skr_reference_minimum(p.data.context().get(), p.data.get(), p.labels.data(), p.lambda, r.minimizer.data(),
                               &r.minimum));
   return r;
+}
+
+// ---- ratio / spectrum diagnostics (precond.hpp:13-20,81-91; bench.cpp:195-212) --------
+struct SpectrumSummary {
+  Vector eigenvalues;  // descending, >= 0
+  double lambda = 0.0;
+  SpectrumSummary() = default;
+  SpectrumSummary(Vector eigs, double lam) : eigenvalues(std::move(eigs)), lambda(lam) {  // precond.cpp:23-32
+    double prev = std::numeric_limits<double>::infinity();
+    const double floor = eigenvalues.empty() ? 0.0 : -1e-10 * std::max(1.0, eigenvalues.front());
+    for (double& v : eigenvalues) {
+      if (v < floor) throw InputError("spectrum: negative eigenvalue");
+      if (v < 0.0) v = 0.0;
+      if (v > prev) throw InputError("spectrum: eigenvalues must be descending");
+      prev = v;
+    }
+  }
+  std::size_t dim() const { return eigenvalues.size(); }
+};
+
+struct RatioRow {
+  std::size_t k = 0;
+  double ratio = 0.0;
+};
+
+/// bench.cpp:205-212: one device SYRK + eigensolve of X^T X / n.
+inline SpectrumSummary dataset_spectrum(const RidgeProblem& p) {
+  Vector e(p.dim());
+  check(skr_dataset_spectrum(p.data.context().get(), p.data.get(), e.data()));
+  return SpectrumSummary(std::move(e), p.lambda);
+}
+
+/// precond.cpp:165-172.
+inline double avg_condition_number(const SpectrumSummary& spec) {
+  if (spec.eigenvalues.empty()) throw InputError("avg_condition_number: empty spectrum");
+  const double denom = spec.eigenvalues.back() + spec.lambda;
+  if (!(denom > 0.0)) throw InputError("avg_condition_number: lam_min + lambda must be positive");
+  double tr = 0.0;
+  for (double v : spec.eigenvalues) tr += v + spec.lambda;
+  return tr / denom;
+}
+
+/// precond.cpp:208-219.
+inline double theoretical_ratio(const SpectrumSummary& spec, std::size_t k) {
+  const std::size_t d = spec.dim();
+  if (k < 1 || k > d) throw ParameterError("theoretical_ratio: k must satisfy 1 <= k <= d");
+  double head = 0.0, tail = 0.0;
+  for (std::size_t i = 0; i < k; ++i) head += spec.eigenvalues[i];
+  for (std::size_t i = k; i < d; ++i) tail += spec.eigenvalues[i];
+  const double denom = static_cast<double>(k) * spec.eigenvalues[k - 1] + tail;
+  if (denom == 0.0) throw DegenerateSpectrumError("theoretical_ratio: zero denominator");
+  return (head + tail) / denom;
+}
+
+/// bench.cpp:195-203.
+inline std::vector<RatioRow> run_ratio_curve(const SpectrumSummary& spec, std::size_t k_max) {
+  if (k_max < 1 || k_max > spec.dim()) throw ParameterError("ratio curve: k_max must satisfy 1 <= k_max <= d");
+  std::vector<RatioRow> rows;
+  for (std::size_t k = 1; k <= k_max; ++k) rows.push_back({k, theoretical_ratio(spec, k)});
+  return rows;
 }
 
 }  // namespace b200

@@ -174,6 +174,34 @@ class _Backend:
                 x, n, d, lam, Uf, s, k, int(unguarded), C.byref(out)))
         return out.value
 
+    # ratio diagnostics: the unmodified reference only (no C restatement)
+    def dataset_spectrum(self, x, lam) -> np.ndarray:
+        if self.prefix == "skro_":
+            raise NotImplementedError("dataset_spectrum: reference backend only")
+        x = _c64(x)
+        n, d = x.shape
+        out = np.empty(d)
+        self._check(self._fn("dataset_spectrum", cint, [_dp, i64, i64, f64, _dp])(x, n, d, lam, out))
+        return out
+
+    def theoretical_ratio(self, eigs, lam, k) -> float:
+        if self.prefix == "skro_":
+            raise NotImplementedError("theoretical_ratio: reference backend only")
+        e = _c64(eigs)
+        out = f64()
+        self._check(self._fn("theoretical_ratio", cint, [_dp, i64, f64, i64, P(f64)])(e, len(e), lam, k,
+                                                                                    C.byref(out)))
+        return out.value
+
+    def avg_condition_number(self, eigs, lam) -> float:
+        if self.prefix == "skro_":
+            raise NotImplementedError("avg_condition_number: reference backend only")
+        e = _c64(eigs)
+        out = f64()
+        self._check(self._fn("avg_condition_number", cint, [_dp, i64, f64, P(f64)])(e, len(e), lam,
+                                                                                  C.byref(out)))
+        return out.value
+
     def build_sketched(self, sigma, lam):
         sigma = _c64(sigma)
         return build_sketched(sigma, lam)

@@ -185,6 +185,30 @@ int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double
   });
 }
 
+// dataset_spectrum (bench.cpp:205-212), theoretical_ratio (precond.cpp:208-219),
+// avg_condition_number (precond.cpp:165-172).
+int ref_dataset_spectrum(const double* x, std::int64_t n, std::int64_t d, double lambda, double* eigs) {
+  return guard([&] {
+    RidgeProblem p(DataMatrix(colmajor(x, d, n)), Vector(static_cast<std::size_t>(n), 0.0), lambda);
+    SpectrumSummary s = dataset_spectrum(p);
+    std::memcpy(eigs, s.eigenvalues.data(), sizeof(double) * d);
+  });
+}
+
+int ref_theoretical_ratio(const double* eigs, std::int64_t d, double lambda, std::int64_t k, double* out) {
+  return guard([&] {
+    SpectrumSummary s(Vector(eigs, eigs + d), lambda);
+    *out = theoretical_ratio(s, static_cast<std::size_t>(k));
+  });
+}
+
+int ref_avg_condition_number(const double* eigs, std::int64_t d, double lambda, double* out) {
+  return guard([&] {
+    SpectrumSummary s(Vector(eigs, eigs + d), lambda);
+    *out = avg_condition_number(s);
+  });
+}
+
 // Preconditioner::apply_inv_sqrt (precond.cpp:67-80).
 int ref_apply_inv_sqrt(std::int64_t d, const double* U, const double* sigma, std::int64_t k,
                        double lambda, const double* v, double* out) {

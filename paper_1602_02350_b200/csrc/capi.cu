@@ -2171,6 +2171,38 @@ static void scaled_gram_dev(Ctx& c, const skr_data* X, double factor, DBuf<doubl
   c.allreduce_sum(G.get(), (size_t)d * ld);
 }
 
+// dataset_spectrum (bench.cpp:205-212): eigenvalues of the scaled design's
+// Gram X^T X / n, descending; zero past rank min(d, n) like the reference's
+// truncated SVD.  Host-side SpectrumSummary validation clamps round-off.
+int skr_dataset_spectrum(skr_ctx* ctx, const skr_data* X, double* eigs) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X || !eigs) raise(SKR_EPARAM, "null argument");
+    const int64_t d = X->st->d, ld = X->st->ld;
+    DBuf<double> G;
+    scaled_gram_dev(c, X, 1.0 / std::sqrt((double)X->n_global), G);
+    DBuf<double> Gd((size_t)d * d, c.stream), ev(d, c.stream);
+    compact_kernel<<<ceil_div(d * d, 256), 256, 0, c.stream>>>(G.get(), d, ld, Gd.get());
+    SKR_LAUNCHED(&c);
+    G.release();
+    int lwork = 0;
+    SKR_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)d,
+                                           Gd.get(), (int)d, ev.get(), &lwork));
+    DBuf<double> work(std::max(lwork, 1), c.stream);
+    DBuf<int> info(1, c.stream);
+    SKR_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, Gd.get(),
+                                (int)d, ev.get(), work.get(), lwork, info.get()));
+    std::vector<double> asc(d);
+    int hinfo = 0;
+    SKR_CUDA(cudaMemcpyAsync(asc.data(), ev.get(), sizeof(double) * d, cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hinfo != 0) raise(SKR_EINTERNAL, "dataset_spectrum: eigensolver did not converge");
+    const int64_t r = std::min<int64_t>(d, X->n_global);
+    for (int64_t i = 0; i < d; ++i) eigs[i] = i < r ? asc[d - 1 - i] : 0.0;
+  });
+}
+
 int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, double* w_out,
                           double* min_out) {
   return guard([&] {

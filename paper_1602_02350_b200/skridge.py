@@ -797,3 +797,86 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7) -> list:
                     rows.append(ConvergenceRow(method, int(seed), rec.epoch,
                                                max(rec.suboptimality or 0.0, 0.0), rec.elapsed_ms))
     return rows
+
+
+# ---------------------------------------------------------------------------
+# Ratio / spectrum diagnostics (precond.hpp:13-20,81-91; precond.cpp:23-32,165-172,
+# 208-219; bench.cpp:195-212).  The spectrum is one device SYRK + eigensolve;
+# the rest is O(d) host arithmetic.
+class DegenerateSpectrumError(InputError):
+    """errors.hpp DegenerateSpectrumError."""
+
+
+@dataclass
+class SpectrumSummary:
+    """precond.hpp:13-20: eigenvalues descending and >= 0 (round-off clamped)."""
+    eigenvalues: np.ndarray
+    lam: float = 0.0
+
+    def __post_init__(self):
+        e = _f64(self.eigenvalues).copy()
+        floor = -1e-10 * max(1.0, float(e[0])) if len(e) else 0.0
+        prev = math.inf
+        for i, v in enumerate(e):
+            if v < floor:
+                raise InputError("spectrum: negative eigenvalue")
+            if v < 0.0:
+                e[i] = v = 0.0
+            if v > prev:
+                raise InputError("spectrum: eigenvalues must be descending")
+            prev = v
+        self.eigenvalues = e
+
+    def dim(self) -> int:
+        return len(self.eigenvalues)
+
+
+@dataclass
+class RatioRow:
+    """bench.hpp:50-53."""
+    k: int
+    ratio: float
+
+
+def dataset_spectrum(p: RidgeProblem) -> SpectrumSummary:
+    """bench.cpp:205-212 on the device: all d eigenvalues of X^T X / n, zero past rank."""
+    out = np.empty(p.dim())
+    _check(_lib.load().skr_dataset_spectrum(p.data.ctx.h, p.data.h, out))
+    return SpectrumSummary(out, p.lam)
+
+
+def avg_condition_number(spec: SpectrumSummary) -> float:
+    """precond.cpp:165-172: sum_i (lam_i + lambda) / (lam_min + lambda)."""
+    if spec.dim() == 0:
+        raise InputError("avg_condition_number: empty spectrum")
+    denom = spec.eigenvalues[-1] + spec.lam
+    if not (denom > 0.0):
+        raise InputError("avg_condition_number: lam_min + lambda must be positive")
+    tr = 0.0
+    for v in spec.eigenvalues:
+        tr += v + spec.lam
+    return tr / denom
+
+
+def theoretical_ratio(spec: SpectrumSummary, k: int) -> float:
+    """precond.cpp:208-219: (head + tail) / (k lam_k + tail), sums in index order."""
+    d = spec.dim()
+    if k < 1 or k > d:
+        raise ParameterError("theoretical_ratio: k must satisfy 1 <= k <= d")
+    head = 0.0
+    for i in range(k):
+        head += spec.eigenvalues[i]
+    tail = 0.0
+    for i in range(k, d):
+        tail += spec.eigenvalues[i]
+    denom = float(k) * spec.eigenvalues[k - 1] + tail
+    if denom == 0.0:
+        raise DegenerateSpectrumError("theoretical_ratio: zero denominator")
+    return (head + tail) / denom
+
+
+def run_ratio_curve(spec: SpectrumSummary, k_max: int) -> list:
+    """bench.cpp:195-203."""
+    if k_max < 1 or k_max > spec.dim():
+        raise ParameterError("ratio curve: k_max must satisfy 1 <= k_max <= d")
+    return [RatioRow(k, theoretical_ratio(spec, k)) for k in range(1, k_max + 1)]

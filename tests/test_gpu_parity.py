@@ -466,3 +466,32 @@ def test_run_convergence_concurrent_grid_matches_sequential_runs(O):
     assert rel(np.array([t.objective for t in best_tr]), want.trace) < 1e-10
     sk_rows = [r for r in rows if r.method == "sketched-svrg"]
     assert len(sk_rows) == 2 * (cfg.epochs + 1) and all(r.suboptimality >= 0.0 for r in sk_rows)
+
+
+def test_ratio_diagnostics_match_reference():
+    """dataset_spectrum / theoretical_ratio / avg_condition_number / run_ratio_curve
+    (bench.cpp:195-212, precond.cpp:165-219) against the unmodified reference."""
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    O = oracle.ref()
+    X, y, lam, _ = small_problem(n=300, d=40)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    spec = sk.dataset_spectrum(p)
+    want = O.dataset_spectrum(X, lam)
+    assert np.max(np.abs(spec.eigenvalues - want)) <= 1e-12 * want[0]
+    for k in (1, 5, 40):
+        assert abs(sk.theoretical_ratio(spec, k) - O.theoretical_ratio(want, lam, k)) <= 1e-10 * O.theoretical_ratio(
+            want, lam, k)
+    assert sk.theoretical_ratio(spec, 1) == 1.0
+    assert abs(sk.avg_condition_number(spec) - O.avg_condition_number(want, lam)) <= 1e-10 * O.avg_condition_number(
+        want, lam)
+    rows = sk.run_ratio_curve(spec, 10)
+    assert [r.k for r in rows] == list(range(1, 11)) and all(r.ratio >= 1.0 - 1e-15 for r in rows)
+    with pytest.raises(sk.ParameterError):
+        sk.run_ratio_curve(spec, 41)
+    # rank-deficient data (n < d): zeros past rank, like the reference's truncated SVD
+    Xs, ys, _, _ = small_problem(n=20, d=40)
+    ps = sk.RidgeProblem(sk.DataMatrix(Xs), ys, lam)
+    e = sk.dataset_spectrum(ps).eigenvalues
+    assert np.all(e[20:] == 0.0) and e[19] > 0.0
+    np.testing.assert_allclose(e[:20], O.dataset_spectrum(Xs, lam)[:20], rtol=1e-9, atol=1e-14 * e[0])

@@ -81,3 +81,40 @@ def test_shard_rows_partition(n, world):
     counts = [c for _, c in rows]
     for r in range(world):
         assert sharding.layout_from_counts(counts, r) == (n, rows[r][0])
+
+
+def test_ratio_host_functions_match_reference():
+    """theoretical_ratio / avg_condition_number / run_ratio_curve / SpectrumSummary
+    validation (precond.cpp:23-32,165-172,208-219; bench.cpp:195-203) are host
+    arithmetic: checked here against the unmodified reference on given spectra."""
+    import numpy as np
+    import pytest
+    import oracle
+    from paper_1602_02350_b200 import skridge as sk
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    R = oracle.ref()
+    rng = np.random.default_rng(3)
+    e = np.sort(rng.exponential(size=50))[::-1] * 3.0
+    e[-5:] = 0.0
+    lam = 1e-4
+    spec = sk.SpectrumSummary(e, lam)
+    for k in (1, 2, 17, 45):
+        assert sk.theoretical_ratio(spec, k) == R.theoretical_ratio(e, lam, k)
+    assert sk.avg_condition_number(spec) == R.avg_condition_number(e, lam)
+    assert [r.ratio for r in sk.run_ratio_curve(spec, 45)] == [R.theoretical_ratio(e, lam, k) for k in range(1, 46)]
+    bad = e.copy()
+    bad[3] = bad[2] * 2
+    with pytest.raises(sk.InputError):
+        sk.SpectrumSummary(bad, lam)
+    neg = e.copy()
+    neg[-1] = -1e-3
+    with pytest.raises(sk.InputError):
+        sk.SpectrumSummary(neg, lam)
+    tiny = e.copy()
+    tiny[-1] = -1e-14
+    assert sk.SpectrumSummary(tiny, lam).eigenvalues[-1] == 0.0
+    with pytest.raises(sk.ParameterError):
+        sk.theoretical_ratio(spec, 0)
+    with pytest.raises(sk.DegenerateSpectrumError):
+        sk.theoretical_ratio(sk.SpectrumSummary(np.zeros(4), lam), 2)
