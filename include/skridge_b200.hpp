@@ -201,9 +201,36 @@ class Preconditioner {
     const double lead = inv_sqrt_.empty() ? 1.0 : inv_sqrt_.front();
     return lead * lead;
   }
+  // precond.cpp:67-118: O(dk) host maps of the value type (off the hot path; the
+  // device applies P^{-1/2} inside skr_problem_* and skr_apply_inv_sqrt)
+  Vector apply_inv_sqrt(const Vector& v) const { return apply(v, false); }
+  Vector apply_sqrt(const Vector& v) const { return apply(v, true); }
+  double inv_sqrt_sq_norm(double v_sq_norm, const Vector& proj) const {
+    if (proj.size() != rank()) throw DimensionError("inv_sqrt_sq_norm: projection length mismatch");
+    const double c = tail_coeff();
+    double s = c * c * v_sq_norm;
+    for (std::size_t j = 0; j < proj.size(); ++j) s += (inv_sqrt_[j] * inv_sqrt_[j] - c * c) * proj[j] * proj[j];
+    return s;
+  }
   friend Preconditioner build_sketched(const SketchedSvd& sv, double lambda);
 
  private:
+  Vector apply(const Vector& v, bool sqrt_map) const {
+    if (v.size() != dim_) throw DimensionError(sqrt_map ? "apply_sqrt: vector length mismatch"
+                                                        : "apply_inv_sqrt: vector length mismatch");
+    const double c = sqrt_map ? 1.0 / tail_coeff() : tail_coeff();
+    Vector out(dim_);
+    for (std::size_t i = 0; i < dim_; ++i) out[i] = c * v[i];
+    const std::size_t k = rank();
+    for (std::size_t j = 0; j < k; ++j) {
+      const double* u = basis_.data() + j * dim_;
+      double pj = 0.0;
+      for (std::size_t i = 0; i < dim_; ++i) pj += u[i] * v[i];
+      pj *= (sqrt_map ? 1.0 / inv_sqrt_[j] : inv_sqrt_[j]) - c;
+      for (std::size_t i = 0; i < dim_; ++i) out[i] += u[i] * pj;
+    }
+    return out;
+  }
   std::size_t dim_ = 0;
   double lambda_ = 0.0;
   Vector basis_, sigma_, inv_sqrt_;

@@ -1624,8 +1624,11 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       });
       sq.zero();
       if (n > 0) {
-        col_sq_norms_kernel<<<std::min<unsigned>((unsigned)n, 1024u), (unsigned)((kk + 31) / 32 * 32), 0, c.stream>>>(
-            Vm.get(), n, (int)kk, sq.get());
+        const unsigned nb = std::min<unsigned>((unsigned)n, 1024u);
+        DBuf<double> part((size_t)nb * kk, c.stream);
+        col_sq_norms_kernel<<<nb, (unsigned)((kk + 31) / 32 * 32), 0, c.stream>>>(Vm.get(), n, (int)kk, part.get());
+        SKR_LAUNCHED(&c);
+        col_sq_reduce_kernel<<<ceil_div(kk, 256), 256, 0, c.stream>>>(part.get(), (int)nb, (int)kk, sq.get());
         SKR_LAUNCHED(&c);
       }
       c.allreduce_sum(sq.get(), kk);

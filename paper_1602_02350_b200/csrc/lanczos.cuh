@@ -211,13 +211,22 @@ __global__ void svd_sign_kernel(double* __restrict__ Ut, int64_t ld, int64_t d,
 }
 
 // Column norms of a rows x k row-major block (k <= 1024): out[j] += sum_i V[i,j]^2.
+// per-block partial column sums of squares (part[b][j]); summed in block order by
+// col_sq_reduce_kernel, so the result is run-to-run deterministic
 __global__ void col_sq_norms_kernel(const double* __restrict__ V, int64_t rows, int k,
-                                    double* __restrict__ out) {
+                                    double* __restrict__ part) {
   const int j = threadIdx.x;
   if (j >= k) return;
   double s = 0.0;
   for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) s = fma(V[i * k + j], V[i * k + j], s);
-  atomicAdd(out + j, s);
+  part[(int64_t)blockIdx.x * k + j] = s;
+}
+__global__ void col_sq_reduce_kernel(const double* __restrict__ part, int blocks, int k, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double s = 0.0;
+  for (int b = 0; b < blocks; ++b) s += part[(int64_t)b * k + j];
+  out[j] = s;
 }
 
 // V[i,j] *= flip[j] / sqrt(sq[j])  (zero norm -> left unscaled, sketch.cpp:82-83)

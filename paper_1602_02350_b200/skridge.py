@@ -362,6 +362,36 @@ class Preconditioner:
         """sigma~ recovered from the coefficients (what the C-ABI takes)."""
         return self._sigma
 
+    # precond.cpp:67-118: O(dk) host maps of the value type (off the hot path; the
+    # device applies P^{-1/2} inside the problem and PreconditionedRidge.apply_inv_sqrt)
+    def _apply(self, v, sqrt_map: bool) -> np.ndarray:
+        v = _f64(v)
+        if len(v) != self._dim:
+            raise DimensionError(("apply_sqrt" if sqrt_map else "apply_inv_sqrt") + ": vector length mismatch")
+        c = 1.0 / self._tail if sqrt_map else self._tail
+        out = c * v
+        if self.rank():
+            proj = self._basis.T @ v
+            coef = (1.0 / self._inv_sqrt if sqrt_map else self._inv_sqrt) - c
+            out = out + self._basis @ (proj * coef)
+        return out
+
+    def apply_inv_sqrt(self, v) -> np.ndarray:
+        return self._apply(v, False)
+
+    def apply_sqrt(self, v) -> np.ndarray:
+        return self._apply(v, True)
+
+    def inv_sqrt_sq_norm(self, v_sq_norm: float, proj) -> float:
+        proj = _f64(proj)
+        if len(proj) != self.rank():
+            raise DimensionError("inv_sqrt_sq_norm: projection length mismatch")
+        c2 = self._tail * self._tail
+        s = c2 * v_sq_norm
+        for j in range(len(proj)):
+            s += (self._inv_sqrt[j] * self._inv_sqrt[j] - c2) * proj[j] * proj[j]
+        return s
+
 
 def _check_lambda(lam):
     if not (lam > 0.0) or not math.isfinite(lam):
