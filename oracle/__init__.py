@@ -174,6 +174,16 @@ class _Backend:
                 x, n, d, lam, Uf, s, k, int(unguarded), C.byref(out)))
         return out.value
 
+    def generate_synthetic(self, n, d, decay, noise_std, seed):
+        """dataset.cpp:16-79 (reference backend only): (X n x d, y)."""
+        if self.prefix == "skro_":
+            raise NotImplementedError("generate_synthetic: reference backend only")
+        X = np.empty((n, d))
+        y = np.empty(n)
+        self._check(self._fn("generate_synthetic", cint, [i64, i64, cint, f64, u64, _dp, _dp])(
+            n, d, decay, noise_std, seed, X, y))
+        return X, y
+
     # ratio diagnostics: the unmodified reference only (no C restatement)
     def dataset_spectrum(self, x, lam) -> np.ndarray:
         if self.prefix == "skro_":

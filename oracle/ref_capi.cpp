@@ -18,6 +18,7 @@
 #include <string>
 
 #include "skridge/bench.hpp"
+#include "skridge/dataset.hpp"
 #include "skridge/data_matrix.hpp"
 #include "skridge/errors.hpp"
 #include "skridge/factorize.hpp"
@@ -182,6 +183,25 @@ int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double
       for (std::size_t i = 0; i < m.rows(); ++i) tr += m(i, i);
       *out = tr / eig.values.back();
     }
+  });
+}
+
+// generate_synthetic (dataset.cpp:16-79): the reference's own synthetic instance
+// (decay 0: 1/q, 1: 1/q^2), written as n x d row-major (= its d x n column-major).
+int ref_generate_synthetic(std::int64_t n, std::int64_t d, int decay, double noise_std, std::uint64_t seed,
+                           double* x_out, double* y_out) {
+  return guard([&] {
+    SyntheticSpec spec;
+    spec.n = static_cast<std::size_t>(n);
+    spec.d = static_cast<std::size_t>(d);
+    spec.decay = decay ? SpectrumDecay::Quadratic : SpectrumDecay::Linear;
+    spec.noise_std = noise_std;
+    spec.seed = seed;
+    LabeledDataset ds = generate_synthetic(spec);
+    DenseMatrix m = ds.data.densified();
+    for (std::int64_t i = 0; i < n; ++i)
+      for (std::int64_t j = 0; j < d; ++j) x_out[i * d + j] = m(static_cast<std::size_t>(j), static_cast<std::size_t>(i));
+    std::memcpy(y_out, ds.labels.data(), sizeof(double) * n);
   });
 }
 
