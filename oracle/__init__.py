@@ -174,14 +174,14 @@ class _Backend:
                 x, n, d, lam, Uf, s, k, int(unguarded), C.byref(out)))
         return out.value
 
-    def generate_synthetic(self, n, d, decay, noise_std, seed):
+    def generate_synthetic(self, n, d, decay, noise_std, seed, normalize_columns=True):
         """dataset.cpp:16-79 (reference backend only): (X n x d, y)."""
         if self.prefix == "skro_":
             raise NotImplementedError("generate_synthetic: reference backend only")
         X = np.empty((n, d))
         y = np.empty(n)
-        self._check(self._fn("generate_synthetic", cint, [i64, i64, cint, f64, u64, _dp, _dp])(
-            n, d, decay, noise_std, seed, X, y))
+        self._check(self._fn("generate_synthetic", cint, [i64, i64, cint, f64, u64, cint, _dp, _dp])(
+            n, d, decay, noise_std, seed, int(normalize_columns), X, y))
         return X, y
 
     # ratio diagnostics: the unmodified reference only (no C restatement)

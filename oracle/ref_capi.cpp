@@ -189,7 +189,7 @@ int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double
 // generate_synthetic (dataset.cpp:16-79): the reference's own synthetic instance
 // (decay 0: 1/q, 1: 1/q^2), written as n x d row-major (= its d x n column-major).
 int ref_generate_synthetic(std::int64_t n, std::int64_t d, int decay, double noise_std, std::uint64_t seed,
-                           double* x_out, double* y_out) {
+                           int normalize_columns, double* x_out, double* y_out) {
   return guard([&] {
     SyntheticSpec spec;
     spec.n = static_cast<std::size_t>(n);
@@ -197,6 +197,7 @@ int ref_generate_synthetic(std::int64_t n, std::int64_t d, int decay, double noi
     spec.decay = decay ? SpectrumDecay::Quadratic : SpectrumDecay::Linear;
     spec.noise_std = noise_std;
     spec.seed = seed;
+    spec.normalize_columns = normalize_columns != 0;
     LabeledDataset ds = generate_synthetic(spec);
     DenseMatrix m = ds.data.densified();
     for (std::int64_t i = 0; i < n; ++i)

@@ -517,3 +517,33 @@ def test_acceptance_speedup_criterion_on_gpu():
             wins += 1
     print("acceptance criterion 9:", wins, "/ 10")
     assert wins >= 8
+
+
+@pytest.mark.slow
+def test_acceptance_ritz_criteria_on_gpu():
+    """The reference's acceptance criteria 1 and 2 (acceptance_main.cpp:114-160)
+    through this block_lanczos: on its synthetic 200 x 400 instance (1/q spectrum,
+    seed 20240, raw columns), k = 10, eps' = 0.5, seeds 0..19:
+      1. |sigma~_i^2 - sigma_i^2| <= 0.5 sigma_11^2 for every i <= 10 in >= 17/20 seeds,
+         each run under 1 s;
+      2. ||X - V~ Sigma~ U~^T||_2 <= 1.5 sigma_11 in >= 17/20 seeds.
+    The exact SVD (numpy) is the test's oracle, as exact_truncated_svd is the reference's."""
+    import time
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    X, _ = oracle.ref().generate_synthetic(400, 200, 0, 0.1, 20240, normalize_columns=False)
+    s_exact = np.linalg.svd(X, compute_uv=False)
+    tail2 = s_exact[10] ** 2
+    a = sk.DataMatrix(X)
+    per_vector = spectral = 0
+    worst = 0.0
+    for seed in range(20):
+        t0 = time.perf_counter()
+        sv = sk.block_lanczos(a, sk.LanczosConfig(10, 0.5, seed))
+        worst = max(worst, time.perf_counter() - t0)
+        per_vector += bool(np.all(np.abs(sv.singular_values ** 2 - s_exact[:10] ** 2) <= 0.5 * tail2))
+        R = X - (sv.right * sv.singular_values) @ sv.left.T
+        spectral += bool(np.linalg.norm(R, 2) <= 1.5 * s_exact[10])
+    print("criterion 1:", per_vector, "/ 20, slowest", round(worst, 4), "s; criterion 2:", spectral, "/ 20")
+    assert per_vector >= 17 and worst < 1.0
+    assert spectral >= 17
