@@ -189,6 +189,11 @@ int skr_gaussian_matrix(skr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed,
  * diagnostics over it (theoretical_ratio, avg_condition_number, run_ratio_curve)
  * are O(d) host arithmetic in skridge_b200.hpp. */
 int skr_dataset_spectrum(skr_ctx* ctx, const skr_data* X, double* eigs);
+/* sym_eigs(data.gram()) of the (scaled) data handle on the device, reference
+ * conventions (factorize.cpp:87-165): evals descending (d), evecs d x d
+ * column-major with eigenvector j in column j — the input of build_optimal
+ * (precond.cpp:144-162). */
+int skr_gram_eigs(skr_ctx* ctx, const skr_data* X, double* evals, double* evecs);
 /* objective(p, w) of the ORIGINAL ridge problem (ridge.cpp:33-43) */
 int skr_ridge_objective(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
                         const double* w, double* out);

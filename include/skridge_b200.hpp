@@ -258,6 +258,25 @@ inline Preconditioner build_sketched(const SketchedSvd& sv, double lambda) {
   return p;
 }
 
+/// precond.cpp:138-142.
+inline Preconditioner build_exact(const SketchedSvd& sv, double lambda) { return build_sketched(sv, lambda); }
+
+/// precond.cpp:144-162: full-rank preconditioner from sym_eigs(data.gram()) on the
+/// device; guarded at d <= 2000 like the reference.
+inline Preconditioner build_optimal(const DataMatrix& data, double lambda) {
+  const std::size_t d = data.rows();
+  if (d > 2000) throw ScaleGuardError("build_optimal: dimension exceeds the dense diagnostic guard");
+  Vector vals(d), vecs(d * d);
+  check(skr_gram_eigs(data.context().get(), data.get(), vals.data(), vecs.data()));
+  SketchedSvd sv;
+  sv.d = d;
+  sv.k = d;
+  sv.left = std::move(vecs);  // column j = eigenvector j
+  sv.singular_values.resize(d);
+  for (std::size_t j = 0; j < d; ++j) sv.singular_values[j] = std::sqrt(std::max(vals[j], 0.0));
+  return build_sketched(sv, lambda);
+}
+
 // ---- svrg (svrg.hpp) -----------------------------------------------------------------
 enum class SvrgMode { Theoretical, Tuned };  // svrg.hpp:37 (a label; the solve is identical)
 

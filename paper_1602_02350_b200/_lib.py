@@ -69,6 +69,7 @@ SIGNATURES = {
     "skr_svrg": (cint, [vp, P(SvrgConfigC), dptr, f64, dptr, P(EpochRecordC), P(i64)]),
     "skr_problem_clone": (cint, [vp, vp, P(vp)]),
     "skr_dataset_spectrum": (cint, [vp, vp, dptr]),
+    "skr_gram_eigs": (cint, [vp, vp, dptr, dptr]),
     "skr_svrg_until": (cint, [vp, P(SvrgConfigC), dptr, f64, f64, dptr, P(EpochRecordC), P(i64)]),
     "skr_index_stream": (cint, [vp, u64, i64, lptr]),
     "skr_mt_uniforms": (cint, [vp, u64, i64, dptr]),

@@ -2206,6 +2206,38 @@ int skr_dataset_spectrum(skr_ctx* ctx, const skr_data* X, double* eigs) {
   });
 }
 
+// sym_eigs(data.gram()) on the device (factorize.cpp:87-165 conventions: values
+// descending, each eigenvector's largest-|entry| positive) — build_optimal's input
+// (precond.cpp:144-162).  evecs: d x d column-major, eigenvector j in column j.
+int skr_gram_eigs(skr_ctx* ctx, const skr_data* X, double* evals, double* evecs) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X || !evals || !evecs) raise(SKR_EPARAM, "null argument");
+    const int64_t d = X->st->d, ld = X->st->ld;
+    DBuf<double> G;
+    scaled_gram_dev(c, X, 1.0, G);  // data.gram() of the logical (scaled) matrix
+    DBuf<double> Gd((size_t)d * d, c.stream), ev(d, c.stream), vd(d, c.stream), Wt((size_t)d * d, c.stream);
+    compact_kernel<<<ceil_div(d * d, 256), 256, 0, c.stream>>>(G.get(), d, ld, Gd.get());
+    SKR_LAUNCHED(&c);
+    G.release();
+    int lwork = 0;
+    SKR_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d,
+                                           Gd.get(), (int)d, ev.get(), &lwork));
+    DBuf<double> work(std::max(lwork, 1), c.stream);
+    DBuf<int> info(1, c.stream);
+    SKR_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)d, Gd.get(), (int)d,
+                                ev.get(), work.get(), lwork, info.get()));
+    eig_post_kernel<<<(unsigned)d, 256, 0, c.stream>>>(Gd.get(), ev.get(), (int)d, (int)d, Wt.get(), vd.get());
+    SKR_LAUNCHED(&c);
+    int hinfo = 0;
+    SKR_CUDA(cudaMemcpyAsync(evals, vd.get(), sizeof(double) * d, cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(evecs, Wt.get(), sizeof(double) * d * d, cudaMemcpyDeviceToHost, c.stream));  // row j = column j
+    SKR_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hinfo != 0) raise(SKR_EINTERNAL, "sym_eigs: eigensolver did not converge");
+  });
+}
+
 int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, double* w_out,
                           double* min_out) {
   return guard([&] {

@@ -319,6 +319,7 @@ class PreconditionerKind(Enum):
     Sketched = 0
     Exact = 1
     Identity = 2
+    Optimal = 3
 
 
 class Preconditioner:
@@ -592,6 +593,33 @@ class PreconditionedRidge:
                 pass
             self.h = None
 
+
+
+def build_exact(sv: SketchedSvd, lam: float) -> Preconditioner:
+    """precond.cpp:138-142: build_sketched on exact factors, kind Exact."""
+    p = build_sketched(sv, lam)
+    p._kind = PreconditionerKind.Exact
+    return p
+
+
+CONDITION_GUARD_DIM = 2000  # kConditionGuardDim (precond.cpp:14)
+
+
+def build_optimal(data: DataMatrix, lam: float) -> Preconditioner:
+    """precond.cpp:144-162: the full-rank preconditioner from sym_eigs(data.gram())
+    (device SYRK + eigensolve, reference sign/order conventions); guarded at d <= 2000."""
+    _check_lambda(lam)
+    d = data.d
+    if d > CONDITION_GUARD_DIM:
+        raise ScaleGuardError("build_optimal: dimension exceeds the dense diagnostic guard")
+    vals = np.empty(d)
+    vecs = np.empty(d * d)
+    _check(_lib.load().skr_gram_eigs(data.ctx.h, data.h, vals, vecs))
+    U = vecs.reshape(d, d).T.copy()  # column j = eigenvector j
+    inv = 1.0 / np.sqrt(np.maximum(vals, 0.0) + lam)
+    p = Preconditioner(PreconditionerKind.Optimal, d, U, inv, float(inv[-1]), lam)
+    p._sigma = np.sqrt(np.maximum(vals, 0.0))
+    return p
 
 def preconditioned_components(p: RidgeProblem, precond: Preconditioner,
                               mode: ApplyMode = ApplyMode.Auto) -> PreconditionedRidge:

@@ -547,3 +547,37 @@ def test_acceptance_ritz_criteria_on_gpu():
     print("criterion 1:", per_vector, "/ 20, slowest", round(worst, 4), "s; criterion 2:", spectral, "/ 20")
     assert per_vector >= 17 and worst < 1.0
     assert spectral >= 17
+
+
+@pytest.mark.slow
+def test_acceptance_exact_and_optimal_preconditioner_criteria_on_gpu():
+    """The reference's acceptance criteria 3 and 5 (acceptance_main.cpp:162-187,
+    229-245) through this implementation, on its own decayed instances
+    (dataset.cpp, 1/q^2 spectrum, raw columns, n = 2d):
+      3. build_exact on the exact top-k factors: kappa~ <= (k lam_k + sum_{i>k} lam_i)/lambda + d;
+      5. build_optimal (device sym_eigs of the Gram): kappa~ = d within 1e-6."""
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    R = oracle.ref()
+    for inst in range(8):
+        d = 40 + (inst % 4) * 20
+        k = 4 + inst % 5
+        lam = 1e-2 if inst % 2 == 0 else 1e-4
+        X, _ = R.generate_synthetic(2 * d, d, 1, 0.1, 3000 + inst, normalize_columns=False)
+        a = sk.DataMatrix(X)
+        Ux, s, Vt = np.linalg.svd(X.T, full_matrices=False)  # reference orientation d x n
+        sv = sk.SketchedSvd(Ux[:, :k].copy(), s[:k].copy(), Vt[:k].T.copy(), k, 0)
+        p = sk.build_exact(sv, lam)
+        assert p.kind() == sk.PreconditionerKind.Exact
+        ev = np.sort(np.linalg.eigvalsh(X.T @ X))[::-1]
+        bound = (k * ev[k - 1] + ev[k:].sum()) / lam + d
+        assert sk.conditioned_condition_number(a, lam, p) <= bound + 1e-6
+    for inst in range(6):
+        d = 30 + (inst % 3) * 15
+        X, _ = R.generate_synthetic(2 * d, d, 1, 0.1, 6000 + inst, normalize_columns=False)
+        a = sk.DataMatrix(X)
+        p = sk.build_optimal(a, 1e-3)
+        assert p.kind() == sk.PreconditionerKind.Optimal and p.rank() == d
+        assert abs(sk.conditioned_condition_number(a, 1e-3, p) - d) <= 1e-6
+    with pytest.raises(sk.ScaleGuardError):
+        sk.build_optimal(sk.DataMatrix(np.zeros((4, 2001))), 1e-3)
