@@ -80,6 +80,15 @@ int skr_ctx_profile_read(skr_ctx* ctx, const char* key, double* total_ms, int64_
 int skr_data_create(skr_ctx* ctx, const void* rows, int64_t n, int64_t d, int dtype,
                     skr_data** out);
 /* same, but the rows already live in device memory (ld = row stride in elements) */
+/* DataMatrix(SparseMatrix) (data_matrix.hpp:24; sparse_matrix.hpp:12-14): this
+ * rank's points as CSR — byte-identical to the reference's CSC over points —
+ * row_ptr (n+1), strictly increasing col_idx (< d) per row, finite nonzero values.
+ * Sparse handles go through block_lanczos, the preconditioned problem (Lazy mode:
+ * X~ is never materialised), SVRG, the objective, reference_minimum and the
+ * Gram-based diagnostics; skr_data_download is dense-only. */
+int skr_data_create_csr(skr_ctx* ctx, int64_t n, int64_t d, const int64_t* row_ptr, const int32_t* col_idx,
+                        const double* vals, skr_data** out);
+int skr_data_is_sparse(const skr_data* x, int* sparse, int64_t* nnz);
 int skr_data_create_device(skr_ctx* ctx, const void* dev_rows, int64_t ld, int64_t n,
                            int64_t d, int dtype, skr_data** out);
 /* DataMatrix::scaled (data_matrix.cpp:56-61): shares storage, scale *= factor */

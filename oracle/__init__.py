@@ -138,6 +138,56 @@ class _Backend:
         Vm = V[: n * kk].reshape(kk, n).T if V is not None else None
         return Sketch(Um, sig[:kk].copy(), Vm, kk, qu.value, bool(rr.value))
 
+    # -- sparse inputs (reference backend only): (row_ptr, col_idx, vals, d) CSR over
+    #    points == the reference's CSC over points (sparse_matrix.hpp:8-14) ---------
+    @staticmethod
+    def _csr(csr):
+        rp, ci, va, d = csr
+        return (np.ascontiguousarray(rp, dtype=np.int64), np.ascontiguousarray(ci, dtype=np.int32), _c64(va),
+                len(rp) - 1, int(d))
+
+    def block_lanczos_csr(self, csr, k, q=0, seed=0, scale=None, eps_prime=0.5, want_right=True):
+        if self.prefix == "skro_":
+            raise NotImplementedError("sparse inputs: reference backend only")
+        rp, ci, va, n, d = self._csr(csr)
+        scale = 1.0 / math.sqrt(n) if scale is None else scale
+        U, sig = np.zeros(d * k), np.zeros(k)
+        V = np.zeros(n * k) if want_right else None
+        ku, qu, rr = i64(), i64(), cint()
+        ip64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+        f = self._fn("block_lanczos_csr", cint, [ip64, ip32, _dp, i64, i64, f64, i64, i64, f64, u64, _dp, _dp,
+                                                 vp, P(i64), P(i64), P(cint)])
+        self._check(f(rp, ci, va, n, d, scale, k, q, eps_prime, seed, U, sig,
+                      V.ctypes.data if V is not None else None, C.byref(ku), C.byref(qu), C.byref(rr)))
+        kk = ku.value
+        return Sketch(U[: d * kk].reshape(kk, d).T, sig[:kk].copy(),
+                      V[: n * kk].reshape(kk, n).T if V is not None else None, kk, qu.value, bool(rr.value))
+
+    def objective_csr(self, csr, y, lam, w) -> float:
+        rp, ci, va, n, d = self._csr(csr)
+        ip64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+        out = f64()
+        self._check(self._fn("objective_csr", cint, [ip64, ip32, _dp, i64, i64, _dp, f64, _dp, P(f64)])(
+            rp, ci, va, n, d, _c64(y), lam, _c64(w), C.byref(out)))
+        return out.value
+
+    def reference_minimum_csr(self, csr, y, lam):
+        rp, ci, va, n, d = self._csr(csr)
+        ip64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+        w, mn = np.empty(d), f64()
+        self._check(self._fn("reference_minimum_csr", cint, [ip64, ip32, _dp, i64, i64, _dp, f64, _dp, P(f64)])(
+            rp, ci, va, n, d, _c64(y), lam, w, C.byref(mn)))
+        return w, mn.value
+
+    def problem_csr(self, csr, y, lam, U=None, sigma=None, mode=2) -> "Problem":
+        """PreconditionedRidge over sparse data; mode 0 Dense, 1 Lazy, 2 Auto (ridge.hpp:121-123)."""
+        if self.prefix == "skro_":
+            raise NotImplementedError("sparse inputs: reference backend only")
+        return Problem(self, None, y, lam, U, sigma, mode, csr=csr)
+
     # -- ridge.cpp / bench.cpp / precond.cpp -----------------------------------
     def objective(self, x, y, lam, w) -> float:
         x = _c64(x)
@@ -258,15 +308,26 @@ def build_sketched(sigma, lam):
 class Problem:
     """PreconditionedRidge (Dense mode for the port; any mode for the reference)."""
 
-    def __init__(self, be: _Backend, x, y, lam, U, sigma, mode):
+    def __init__(self, be: _Backend, x, y, lam, U, sigma, mode, csr=None):
         self.be = be
-        x = _c64(x)
-        self.n, self.d = x.shape
+        if csr is not None:
+            rp, ci, va, self.n, self.d = _Backend._csr(csr)
+        else:
+            x = _c64(x)
+            self.n, self.d = x.shape
         self.k = 0 if U is None else U.shape[1]
         self.lam = lam
         Uf = _c64(np.asarray(U).ravel(order="F")) if self.k else np.zeros(1)
         h = vp()
-        if be.prefix == "skro_":
+        if csr is not None:
+            s = _c64(sigma) if self.k else np.zeros(1)
+            ip64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+            ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+            be._check(be._fn("problem_create_csr", cint, [ip64, ip32, _dp, i64, i64, _dp, f64, _dp, _dp, i64, cint,
+                                                          P(vp)])(
+                rp, ci, va, self.n, self.d, _c64(y), lam, Uf, s, self.k, mode, C.byref(h)))
+            self._destroy = be._fn("problem_destroy", cint, [vp])
+        elif be.prefix == "skro_":
             D, c = build_sketched(sigma, lam) if self.k else (np.zeros(1), 1.0)
             be._check(be._fn("problem_create", cint, [_dp, i64, i64, _dp, f64, _dp, _dp, i64, f64,
                                                       P(vp)])(

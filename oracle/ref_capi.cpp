@@ -19,6 +19,7 @@
 
 #include "skridge/bench.hpp"
 #include "skridge/dataset.hpp"
+#include "skridge/sparse_matrix.hpp"
 #include "skridge/data_matrix.hpp"
 #include "skridge/errors.hpp"
 #include "skridge/factorize.hpp"
@@ -183,6 +184,69 @@ int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double
       for (std::size_t i = 0; i < m.rows(); ++i) tr += m(i, i);
       *out = tr / eig.values.back();
     }
+  });
+}
+
+// ---- sparse inputs: CSR over points (row_ptr n+1, col_idx, vals) is the
+// reference's CSC over points (sparse_matrix.hpp:8-14) byte for byte ----
+DataMatrix csr_data(const std::int64_t* row_ptr, const std::int32_t* col_idx, const double* vals, std::int64_t n,
+                    std::int64_t d, double scale = 1.0) {
+  const std::int64_t nnz = row_ptr[n];
+  std::vector<std::size_t> cp(row_ptr, row_ptr + n + 1), ri(col_idx, col_idx + nnz);
+  return DataMatrix(SparseMatrix(static_cast<std::size_t>(d), static_cast<std::size_t>(n), std::move(cp),
+                                 std::move(ri), Vector(vals, vals + nnz)),
+                    scale);
+}
+
+int ref_block_lanczos_csr(const std::int64_t* row_ptr, const std::int32_t* col_idx, const double* vals,
+                          std::int64_t n, std::int64_t d, double scale, std::int64_t k, std::int64_t q,
+                          double eps_prime, std::uint64_t seed, double* U, double* sigma, double* V,
+                          std::int64_t* k_used, std::int64_t* q_used, int* rank_reduced) {
+  return guard([&] {
+    DataMatrix a = csr_data(row_ptr, col_idx, vals, n, d, scale);
+    LanczosConfig cfg;
+    cfg.k = static_cast<std::size_t>(k);
+    cfg.eps_prime = eps_prime;
+    cfg.seed = seed;
+    if (q > 0) cfg.q_override = static_cast<std::size_t>(q);
+    SketchedSvd sv = block_lanczos(a, cfg);
+    std::memcpy(U, sv.left.data(), sizeof(double) * sv.left.size());
+    std::memcpy(sigma, sv.singular_values.data(), sizeof(double) * sv.k);
+    if (V) std::memcpy(V, sv.right.data(), sizeof(double) * sv.right.size());
+    *k_used = static_cast<std::int64_t>(sv.k);
+    *q_used = static_cast<std::int64_t>(sv.q);
+    *rank_reduced = sv.rank_reduced ? 1 : 0;
+  });
+}
+
+int ref_objective_csr(const std::int64_t* row_ptr, const std::int32_t* col_idx, const double* vals, std::int64_t n,
+                      std::int64_t d, const double* y, double lambda, const double* w, double* out) {
+  return guard([&] {
+    RidgeProblem p(csr_data(row_ptr, col_idx, vals, n, d), Vector(y, y + n), lambda);
+    *out = objective(p, Vector(w, w + d));
+  });
+}
+
+int ref_reference_minimum_csr(const std::int64_t* row_ptr, const std::int32_t* col_idx, const double* vals,
+                              std::int64_t n, std::int64_t d, const double* y, double lambda, double* w_out,
+                              double* min_out) {
+  return guard([&] {
+    RidgeProblem p(csr_data(row_ptr, col_idx, vals, n, d), Vector(y, y + n), lambda);
+    ReferenceSolution r = reference_minimum(p);
+    std::memcpy(w_out, r.minimizer.data(), sizeof(double) * d);
+    *min_out = r.minimum;
+  });
+}
+
+int ref_problem_create_csr(const std::int64_t* row_ptr, const std::int32_t* col_idx, const double* vals,
+                           std::int64_t n, std::int64_t d, const double* y, double lambda, const double* U,
+                           const double* sigma, std::int64_t k, int mode, void** out) {
+  return guard([&] {
+    RidgeProblem p(csr_data(row_ptr, col_idx, vals, n, d), Vector(y, y + n), lambda);
+    Preconditioner pc = make_precond(d, U, sigma, k, lambda);
+    ApplyMode m = mode == 0 ? ApplyMode::Dense : mode == 1 ? ApplyMode::Lazy : ApplyMode::Auto;
+    auto pre = preconditioned_components(p, pc, m);
+    *out = new RefProblem{std::move(p), std::move(pc), std::move(pre)};
   });
 }
 

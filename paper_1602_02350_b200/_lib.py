@@ -17,6 +17,8 @@ i64, u64, f64, cint = C.c_int64, C.c_uint64, C.c_double, C.c_int
 vp, cp = C.c_void_p, C.c_char_p
 P = C.POINTER
 dptr = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+i64ptr = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+i32ptr = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 lptr = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 
 
@@ -68,6 +70,8 @@ SIGNATURES = {
     "skr_epoch": (cint, [vp, dptr, dptr, lptr, i64, f64, dptr]),
     "skr_svrg": (cint, [vp, P(SvrgConfigC), dptr, f64, dptr, P(EpochRecordC), P(i64)]),
     "skr_problem_clone": (cint, [vp, vp, P(vp)]),
+    "skr_data_create_csr": (cint, [vp, i64, i64, i64ptr, i32ptr, dptr, P(vp)]),
+    "skr_data_is_sparse": (cint, [vp, P(cint), P(i64)]),
     "skr_dataset_spectrum": (cint, [vp, vp, dptr]),
     "skr_gram_eigs": (cint, [vp, vp, dptr, dptr]),
     "skr_svrg_until": (cint, [vp, P(SvrgConfigC), dptr, f64, f64, dptr, P(EpochRecordC), P(i64)]),

@@ -18,6 +18,7 @@
 #include "sstep.cuh"
 #include "tc_gemm.cuh"
 #include "mt_jump.cuh"
+#include "sparse.cuh"
 
 using namespace skr;
 
@@ -67,10 +68,17 @@ struct skr_ctx {
 struct Storage {
   int dtype = SKR_F64;
   int64_t n = 0, d = 0, ld = 0;
-  void* ptr = nullptr;  // device rows, n x ld
+  void* ptr = nullptr;  // device rows, n x ld (dense storage)
   bool owns = true;
   cudaStream_t stream = nullptr;
   DBuf<double> labels;  // synthetic generator output (local rows)
+  // sparse storage (ptr == nullptr): CSR over points (= the reference's CSC) and
+  // CSR over features (its transpose), fp64 values
+  bool sparse = false;
+  int64_t nnz = 0;
+  DBuf<int64_t> rptr, fptr;
+  DBuf<int32_t> ridx, fidx;  // ridx: feature of each point-row entry; fidx: point of each feature-row entry
+  DBuf<double> rval, fval;
   ~Storage() {
     if (owns && ptr) cudaFreeAsync(ptr, stream);
   }
@@ -969,6 +977,15 @@ __global__ void floor_kernel(double* __restrict__ b, int64_t n, const double* __
     b[i] = fmax(b[i], fl);
 }
 
+// r_i <- (r_i - y_i)^2
+__global__ void sq_residual_kernel(double* __restrict__ r, const double* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double e = r[i] - y[i];
+    r[i] = e * e;
+  }
+}
+
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
   // deterministic single-CTA sum (fixed thread/stride order)
   __shared__ double scratch[32];
@@ -1294,6 +1311,79 @@ int skr_data_create(skr_ctx* ctx, const void* rows, int64_t n, int64_t d, int dt
   });
 }
 
+// Sparse data (the reference's DataMatrix(SparseMatrix), data_matrix.hpp:24 and the
+// SparseMatrix invariants of sparse_matrix.hpp:12-14): this rank's points as CSR
+// (row_ptr n+1, strictly increasing col_idx < d per row, finite nonzero values).
+int skr_data_create_csr(skr_ctx* ctx, int64_t n, int64_t d, const int64_t* row_ptr, const int32_t* col_idx,
+                        const double* vals, skr_data** out) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (n < 0 || d < 1 || d > INT32_MAX) raise(SKR_EDIM, "sparse data matrix: bad shape");
+    if (!row_ptr || !out) raise(SKR_EPARAM, "null argument");
+    if (row_ptr[0] != 0) raise(SKR_EINPUT, "sparse matrix: row_ptr[0] must be 0");
+    const int64_t nnz = row_ptr[n];
+    if (nnz > 0 && (!col_idx || !vals)) raise(SKR_EPARAM, "null argument");
+    std::vector<int64_t> fcount(d + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (row_ptr[i + 1] < row_ptr[i]) raise(SKR_EINPUT, "sparse matrix: row_ptr must be non-decreasing");
+      for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+        const int64_t f = col_idx[t];
+        if (f < 0 || f >= d) raise(SKR_EINPUT, "sparse matrix: index out of range");
+        if (t > row_ptr[i] && f <= col_idx[t - 1]) raise(SKR_EINPUT, "sparse matrix: indices must be strictly increasing");
+        if (!std::isfinite(vals[t]) || vals[t] == 0.0) raise(SKR_EINPUT, "sparse matrix: values must be finite and nonzero");
+        ++fcount[f + 1];
+      }
+    }
+    // transpose on the host (ingest, not the hot path): CSR over features, points increasing
+    for (int64_t f = 0; f < d; ++f) fcount[f + 1] += fcount[f];
+    std::vector<int64_t> fptr(fcount), fill(fcount.begin(), fcount.end() - 1);
+    std::vector<int32_t> fidx((size_t)std::max<int64_t>(nnz, 1));
+    std::vector<double> fval((size_t)std::max<int64_t>(nnz, 1));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+        const int64_t pos = fill[col_idx[t]]++;
+        fidx[pos] = (int32_t)i;
+        fval[pos] = vals[t];
+      }
+    auto st = std::make_shared<Storage>();
+    st->dtype = SKR_F64;
+    st->n = n;
+    st->d = d;
+    st->ld = (d + 15) / 16 * 16;
+    st->stream = c.stream;
+    st->sparse = true;
+    st->nnz = nnz;
+    st->rptr.alloc(n + 1, c.stream);
+    st->fptr.alloc(d + 1, c.stream);
+    st->ridx.alloc(std::max<int64_t>(nnz, 1), c.stream);
+    st->fidx.alloc(std::max<int64_t>(nnz, 1), c.stream);
+    st->rval.alloc(std::max<int64_t>(nnz, 1), c.stream);
+    st->fval.alloc(std::max<int64_t>(nnz, 1), c.stream);
+    SKR_CUDA(cudaMemcpyAsync(st->rptr.get(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(st->fptr.get(), fptr.data(), sizeof(int64_t) * (d + 1), cudaMemcpyHostToDevice, c.stream));
+    if (nnz > 0) {
+      SKR_CUDA(cudaMemcpyAsync(st->ridx.get(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+      SKR_CUDA(cudaMemcpyAsync(st->rval.get(), vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.stream));
+      SKR_CUDA(cudaMemcpyAsync(st->fidx.get(), fidx.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+      SKR_CUDA(cudaMemcpyAsync(st->fval.get(), fval.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, c.stream));
+    }
+    auto x = std::make_unique<skr_data>();
+    x->ctx = ctx;
+    x->st = st;
+    shard_layout(c, n, &x->n_global, &x->row0);
+    c.sync();
+    *out = x.release();
+  });
+}
+
+int skr_data_is_sparse(const skr_data* x, int* sparse, int64_t* nnz) {
+  return guard([&] {
+    if (!x) raise(SKR_EPARAM, "null handle");
+    if (sparse) *sparse = x->st->sparse ? 1 : 0;
+    if (nnz) *nnz = x->st->nnz;
+  });
+}
+
 int skr_data_create_device(skr_ctx* ctx, const void* dev_rows, int64_t ld, int64_t n, int64_t d, int dtype,
                            skr_data** out) {
   return guard([&] {
@@ -1338,6 +1428,7 @@ int skr_data_info(const skr_data* x, int64_t* n, int64_t* d, int* dtype, double*
 
 int skr_data_download(const skr_data* x, void* rows_out) {
   return guard([&] {
+    if (x && x->st->sparse) raise(SKR_EPARAM, "data download: dense data only");
     if (!x) raise(SKR_EPARAM, "null handle");
     Ctx& c = x->ctx->c;
     const size_t s = dtype_size(x->st->dtype);
@@ -1486,7 +1577,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     int Wb = 0;
     // fp32 storage: every product runs on the tensor cores (tcgen05, 3xTF32, fp64
     // split-K sums) with X^T materialised so all operands are K-major.
-    const bool tc = S.dtype == SKR_F32 && n > 0 && !getenv("SKR_LANCZOS_SIMT");
+    const bool tc = !S.sparse && S.dtype == SKR_F32 && n > 0 && !getenv("SKR_LANCZOS_SIMT");
     const int64_t np = (std::max<int64_t>(n, 1) + 3) / 4 * 4;  // 16-byte row stride over the points
     DBuf<float> Xt, P32, Rt32;
     if (tc) {
@@ -1507,7 +1598,13 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     // block = A Pi  -> Vt (k x ld) = scale * Pi^T X   (sketch.cpp:25)
     Vt.zero();
     gmark();
-    if (tc) {
+    if (S.sparse) {
+      // Vt^T (d x k) = scale X^T Pi over the feature-major CSR, Pi as n x k rows
+      DBuf<double> Pn((size_t)std::max<int64_t>(n, 1) * k, c.stream), tmp((size_t)d * k, c.stream);
+      transpose_f64(c, Pt.get(), k, n, n, Pn.get(), k);
+      csr_spmm(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, Pn.get(), k, k, scale, tmp.get(), k);
+      transpose_f64(c, tmp.get(), d, k, k, Vt.get(), ld);
+    } else if (tc) {
       tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, k, d, n, scale, Vt.get(), ld);
     } else {
       DISPATCH_DTYPE(S.dtype, T, {
@@ -1520,12 +1617,22 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     int appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), (int)k);
     if (Wb == 0) raise(SKR_EEMPTY, "krylov_block: A * Pi is numerically zero");
     DBuf<double> Tm(tc ? 1 : (size_t)std::max<int64_t>(n, 1) * k, c.stream);
+    DBuf<double> prevT(S.sparse ? (size_t)d * k : 0, c.stream), tmpK(S.sparse ? (size_t)d * k : 0, c.stream);
     Pt.release();
     for (int64_t j = 1; j < q && appended > 0; ++j) {
       const int64_t W = Wb;
       const double* prev = Qt.get() + (W - appended) * ld;
       gmark();
-      if (tc) {
+      if (S.sparse) {
+        // T (n x a) = scale X prev^T (point-major CSR, prev^T as d x a rows); block^T = scale T^T X
+        transpose_f64(c, prev, appended, d, ld, prevT.get(), appended);
+        csr_spmm(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, prevT.get(), appended, appended, scale, Tm.get(),
+                 appended);
+        csr_spmm(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, Tm.get(), appended, appended, scale, tmpK.get(),
+                 appended);
+        Vt.zero();
+        transpose_f64(c, tmpK.get(), d, appended, appended, Vt.get(), ld);
+      } else if (tc) {
         // T^T (a x n, fp32) = scale (X prev^T)^T ;  block^T = scale T^T X = scale T^T . (X^T)^T
         convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(appended * ld, 256), 65535u), 256, 0, c.stream>>>(
             prev, ld, appended, d, P32.get(), ld);
@@ -1558,7 +1665,18 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     DBuf<double> G((size_t)W * W, c.stream);
     G.zero();
     gmark();
-    if (tc) {
+    if (S.sparse) {
+      // Z (n x W) = scale X Q^T in row chunks, G += Z^T Z
+      DBuf<double> QT((size_t)d * W, c.stream);
+      transpose_f64(c, Qt.get(), W, d, ld, QT.get(), W);
+      const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
+      DBuf<double> Z((size_t)chunk * W, c.stream);
+      for (int64_t r = 0; r < n; r += chunk) {
+        const int64_t rows = std::min(chunk, n - r);
+        csr_spmm(c, S.rptr.get() + r, S.ridx.get(), S.rval.get(), rows, QT.get(), W, W, scale, Z.get(), W);
+        gemm<double, double, true, false>(&c, W, W, rows, Z.get(), W, Z.get(), W, EpiStore{G.get(), W, 1.0, 1.0});
+      }
+    } else if (tc) {
       DBuf<float> Q32((size_t)W * ld, c.stream), Zt((size_t)W * np, c.stream);
       convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(W * ld, 256), 65535u), 256, 0, c.stream>>>(
           Qt.get(), ld, W, d, Q32.get(), ld);
@@ -1618,10 +1736,16 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       // V_j = (Q^T A)^T w_j / ||.|| = scale X u_j / ||.||  (sketch.cpp:78-86); u_j after the sign flip,
       // so V carries the same flip as normalize_svd_signs applies (factorize.cpp:167-178)
       DBuf<double> Vm((size_t)std::max<int64_t>(n, 1) * kk, c.stream), sq(kk, c.stream), ones(kk, c.stream);
-      DISPATCH_DTYPE(S.dtype, T, {
-        const T* X = static_cast<const T*>(S.ptr);
-        gemm<T, double, false, true>(&c, n, kk, d, X, ld, Ut.get(), ld, EpiStore{Vm.get(), kk, scale, 0.0});
-      });
+      if (S.sparse) {
+        DBuf<double> UT((size_t)d * kk, c.stream);
+        transpose_f64(c, Ut.get(), kk, d, ld, UT.get(), kk);
+        csr_spmm(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, UT.get(), kk, kk, scale, Vm.get(), kk);
+      } else {
+        DISPATCH_DTYPE(S.dtype, T, {
+          const T* X = static_cast<const T*>(S.ptr);
+          gemm<T, double, false, true>(&c, n, kk, d, X, ld, Ut.get(), ld, EpiStore{Vm.get(), kk, scale, 0.0});
+        });
+      }
       sq.zero();
       if (n > 0) {
         const unsigned nb = std::min<unsigned>((unsigned)n, 1024u);
@@ -2136,7 +2260,21 @@ int skr_gaussian_matrix(skr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed,
 static double ridge_objective_dev(Ctx& c, const skr_data* X, const double* y_dev, double lambda, const double* w_dev,
                                   DBuf<double>& pg, DBuf<double>& pl, DBuf<double>& sums) {
   const Storage& S = *X->st;
-  fullgrad_sums(c, S.dtype, S.ptr, S.ld, S.n, y_dev, w_dev, pg, pl, sums);
+  if (S.sparse) {  // r = X w - y by SpMV, loss = sum r^2 (single-CTA sum: deterministic)
+    if (sums.n < (size_t)S.ld + 1) sums.alloc(S.ld + 1, c.stream);
+    sums.zero();
+    if (S.n > 0) {
+      DBuf<double> r(S.n, c.stream);
+      csr_spmv(c, S.rptr.get(), S.ridx.get(), S.rval.get(), S.n, w_dev, X->scale, r.get());
+      sq_residual_kernel<<<ceil_div(S.n, 256), 256, 0, c.stream>>>(r.get(), y_dev, S.n);
+      SKR_LAUNCHED(&c);
+      sum_kernel<<<1, 1024, 0, c.stream>>>(r.get(), S.n, sums.get() + S.ld);
+      SKR_LAUNCHED(&c);
+    }
+    c.allreduce_sum(sums.get() + S.ld, 1);
+  } else {
+    fullgrad_sums(c, S.dtype, S.ptr, S.ld, S.n, y_dev, w_dev, pg, pl, sums);
+  }
   std::vector<double> hs(S.ld + 1), hw(S.ld);
   SKR_CUDA(cudaMemcpyAsync(hs.data(), sums.get(), sizeof(double) * (S.ld + 1), cudaMemcpyDeviceToHost, c.stream));
   SKR_CUDA(cudaMemcpyAsync(hw.data(), w_dev, sizeof(double) * S.ld, cudaMemcpyDeviceToHost, c.stream));
@@ -2167,6 +2305,17 @@ static void scaled_gram_dev(Ctx& c, const skr_data* X, double factor, DBuf<doubl
   const double s = X->scale * factor;
   G.alloc((size_t)d * ld, c.stream);
   G.zero();
+  if (S.sparse) {  // densified row chunks through the same DMMA product
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(S.n, 1), (int64_t)(1 << 27) / ld));
+    DBuf<double> Xc((size_t)chunk * ld, c.stream);
+    for (int64_t r = 0; r < S.n; r += chunk) {
+      const int64_t rows = std::min(chunk, S.n - r);
+      csr_densify(c, S.rptr.get() + r, S.ridx.get(), S.rval.get(), rows, Xc.get(), ld);
+      gemm<double, double, true, false>(&c, d, d, rows, Xc.get(), ld, Xc.get(), ld, EpiStore{G.get(), ld, s * s, 1.0});
+    }
+    c.allreduce_sum(G.get(), (size_t)d * ld);
+    return;
+  }
   DISPATCH_DTYPE(S.dtype, T, {
     const T* Xp = static_cast<const T*>(S.ptr);
     gemm<T, T, true, false>(&c, d, d, S.n, Xp, ld, Xp, ld, EpiStore{G.get(), ld, s * s, 0.0});
@@ -2254,10 +2403,14 @@ int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, doub
     DBuf<double> yd(std::max<int64_t>(n, 1), c.stream), rhs(ld, c.stream);
     if (n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
     rhs.zero();
-    DISPATCH_DTYPE(S.dtype, T, {
-      gemm<T, double, true, false>(&c, d, 1, n, static_cast<const T*>(S.ptr), ld, yd.get(), 1,
-                                   EpiStore{rhs.get(), 1, 1.0 / (double)X->n_global, 0.0});
-    });
+    if (S.sparse) {
+      csr_spmv(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, yd.get(), 1.0 / (double)X->n_global, rhs.get());
+    } else {
+      DISPATCH_DTYPE(S.dtype, T, {
+        gemm<T, double, true, false>(&c, d, 1, n, static_cast<const T*>(S.ptr), ld, yd.get(), 1,
+                                     EpiStore{rhs.get(), 1, 1.0 / (double)X->n_global, 0.0});
+      });
+    }
     c.allreduce_sum(rhs.get(), d);
     // Cholesky on the device (bench.cpp:22-48)
     DBuf<double> Gd((size_t)d * d, c.stream);

@@ -181,6 +181,34 @@ class DataMatrix:
         self._scale, self.n_global, self.row0 = sc.value, ng.value, r0.value
 
     @classmethod
+    def from_csr(cls, row_ptr, col_idx, values, d: int, ctx: Context | None = None) -> "DataMatrix":
+        """DataMatrix(SparseMatrix) (data_matrix.hpp:24): this rank's points as CSR
+        (= the reference's CSC over points; strictly increasing indices, finite
+        nonzero values, sparse_matrix.hpp:12-14).  Accepts scipy.sparse too."""
+        ctx = ctx or default_context()
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        va = _f64(values)
+        h = vp()
+        _check(_lib.load().skr_data_create_csr(ctx.h, len(rp) - 1, int(d), rp, ci, va, C.byref(h)))
+        return cls(ctx=ctx, _handle=h)
+
+    @classmethod
+    def from_scipy(cls, m, ctx: Context | None = None) -> "DataMatrix":
+        """Points as the rows of a scipy.sparse matrix (converted to canonical CSR)."""
+        m = m.tocsr()
+        m.sum_duplicates()
+        m.sort_indices()
+        m.eliminate_zeros()
+        return cls.from_csr(m.indptr, m.indices, m.data, m.shape[1], ctx)
+
+    @property
+    def sparse(self) -> bool:
+        sp, nnz = cint(), i64()
+        _check(_lib.load().skr_data_is_sparse(self.h, C.byref(sp), C.byref(nnz)))
+        return bool(sp.value)
+
+    @classmethod
     def generate(cls, spec: "SynthSpec", ctx: Context | None = None) -> "DataMatrix":
         ctx = ctx or default_context()
         c = SynthSpecC(spec.n, spec.d, 1 if spec.dtype == "f32" else 0, spec.seed, spec.spectrum,
