@@ -108,6 +108,9 @@ struct skr_problem {
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
   DBuf<double> s_state, s_M, s_p, s_X;  // s-step inner loop workspaces
+  // Lazy mode (sparse data): X~ is never materialised; Pm = X U^T (n x k) and workspaces
+  bool lazy = false;
+  DBuf<double> Pm, lz_r, lz_r2, lz_s, lz_g1, lz_g2, lz_v, lz_loss, lz_UT;
   // pinned host staging for the host-buffer entry points: [0, ld) w, [ld, 2 ld] mu and the objective
   double* io_host = nullptr;
   ~skr_problem() {
@@ -454,9 +457,65 @@ void apply_inv_sqrt_dev(Ctx& c, const skr_problem* p, const double* v, double* p
   SKR_LAUNCHED(&c);
 }
 
+__global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
+template <class T>
+struct EpiXtilde;
+__global__ void scale_cols_kernel(double* __restrict__ P, int64_t rows, int64_t k, const double* __restrict__ D,
+                                  double c);
+
+// Lazy-mode full gradient + objective over sparse rows (ridge.cpp:200-236 with
+// X~ = c X + (P o (D - c)) U^T): s = c X w + P v, r = s - y, mu = (c X^T r +
+// U ((D - c) o P^T r)) / n + lambda P^{-1} w.  Every sum is in a fixed order.
+void lazy_fullgrad(skr_problem* p, const double* w, double* mu, double* obj, double* snap_s = nullptr) {
+  Ctx& c = p->ctx->c;
+  const Storage& S = *p->xt;
+  const int64_t n = p->n, d = p->d, ld = p->ld, k = p->k;
+  if (!p->lz_r.p) {
+    p->lz_r.alloc(std::max<int64_t>(n, 1), c.stream);
+    p->lz_r2.alloc(std::max<int64_t>(n, 1), c.stream);
+    p->lz_g1.alloc(ld, c.stream);
+    p->lz_g2.alloc(std::max<int64_t>(k, 1), c.stream);
+    p->lz_v.alloc(std::max<int64_t>(k, 1), c.stream);
+    p->lz_loss.alloc(1, c.stream);
+  }
+  if (c.prof_on) c.prof_mark("fullgrad");
+  proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, w, p->uw.get());
+  SKR_LAUNCHED(&c);
+  if (k > 0) {
+    lazy_scale_kernel<<<ceil_div(k, 256), 256, 0, c.stream>>>(p->uw.get(), p->D.get(), p->c, k, p->lz_v.get());
+    SKR_LAUNCHED(&c);
+  }
+  p->lz_loss.zero();
+  p->lz_g1.zero();
+  p->lz_g2.zero();
+  if (n > 0) {
+    lazy_residual_kernel<<<ceil_div(n * 32, 256), 256, 0, c.stream>>>(S.rptr.get(), S.ridx.get(), S.rval.get(), n, w,
+                                                                      p->Pm.get(), k, p->lz_v.get(), p->c,
+                                                                      p->y.get(), snap_s, p->lz_r.get(),
+                                                                      p->lz_r2.get());
+    SKR_LAUNCHED(&c);
+    sum_kernel<<<1, 1024, 0, c.stream>>>(p->lz_r2.get(), n, p->lz_loss.get());
+    SKR_LAUNCHED(&c);
+    csr_spmv(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, p->lz_r.get(), 1.0, p->lz_g1.get());
+    if (k > 0)
+      gemm<double, double, true, false>(&c, k, 1, n, p->Pm.get(), k, p->lz_r.get(), 1,
+                                        EpiStore{p->lz_g2.get(), 1, 1.0, 0.0});
+  }
+  lazy_finalize_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->lz_g1.get(), p->lz_g2.get(), p->Ut.get(), ld, d, k,
+                                                                 p->D.get(), p->c, w, p->uw.get(),
+                                                                 1.0 / (double)p->n_global, p->lambda,
+                                                                 p->lz_loss.get(), mu, obj);
+  SKR_LAUNCHED(&c);
+  if (c.prof_on) c.prof_mark("fullgrad");
+}
+
 // K9 on the problem: mu (ld, device) and optional obj (device scalar) at w (device, ld).
 void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) {
   Ctx& c = p->ctx->c;
+  if (p->lazy) {
+    lazy_fullgrad(p, w, mu, obj);
+    return;
+  }
   // U^T w and w.w for lambda P^{-1} w and the regulariser norm (applied in the
   // column reduction): computed by the first k+1 warps of the warp-per-row pass
   // itself, or by a separate small launch ordered before the tile pass.
@@ -857,10 +916,62 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   }
 }
 
+// Lazy epoch (sparse rows): per-epoch snapshot quantities on all SMs, then the
+// sequential chain in one CTA (lazy_epoch_kernel).
+void lazy_run_epoch(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
+                    double* w_avg) {
+  Ctx& c = p->ctx->c;
+  const Storage& S = *p->xt;
+  const int64_t n = p->n, d = p->d, ld = p->ld, k = p->k;
+  const int64_t kk = std::max<int64_t>(k, 1);
+  if (!p->lz_UT.p) {
+    p->lz_UT.alloc((size_t)d * kk, c.stream);
+    p->lz_UT.zero();
+    transpose_f64(c, p->Ut.get(), k, d, ld, p->lz_UT.get(), k);
+  }
+  DBuf<double> sbar(std::max<int64_t>(n, 1), c.stream), r(std::max<int64_t>(n, 1), c.stream),
+      r2(std::max<int64_t>(n, 1), c.stream), half(ld, c.stream), xmu(std::max<int64_t>(n, 1), c.stream),
+      bg(kk + 1, c.stream), z0(kk + 1, c.stream), v(kk, c.stream), base(ld, c.stream), Sb(ld, c.stream),
+      scratch(kk + 1, c.stream);
+  // z0 = U^T wbar (+ wbar.wbar), v = (D - c) o z0, sbar_i = x~_i . wbar
+  proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, snap, z0.get());
+  SKR_LAUNCHED(&c);
+  proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, mu, bg.get());
+  SKR_LAUNCHED(&c);
+  if (k > 0) {
+    lazy_scale_kernel<<<ceil_div(k, 256), 256, 0, c.stream>>>(z0.get(), p->D.get(), p->c, k, v.get());
+    SKR_LAUNCHED(&c);
+  }
+  if (n > 0) {
+    lazy_residual_kernel<<<ceil_div(n * 32, 256), 256, 0, c.stream>>>(S.rptr.get(), S.ridx.get(), S.rval.get(), n,
+                                                                      snap, p->Pm.get(), k, v.get(), p->c, p->y.get(),
+                                                                      sbar.get(), r.get(), r2.get());
+    SKR_LAUNCHED(&c);
+    csr_spmv(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, mu, 1.0, xmu.get());
+  }
+  apply_inv_sqrt_dev(c, p, snap, scratch.get(), half.get());  // (P^{-1/2} wbar)_j
+  SKR_CUDA(cudaMemcpyAsync(base.get(), snap, sizeof(double) * ld, cudaMemcpyDeviceToDevice, c.stream));
+  Sb.zero();
+  LazyEpochArgs a{S.rptr.get(), S.ridx.get(), S.rval.get(), n, d, ld, k, p->Pm.get(), p->lz_UT.get(), p->D.get(),
+                  p->c, p->data_coef, p->reg_coef, idx, p->inv_nq.get(), m, eta, sbar.get(), half.get(), xmu.get(),
+                  mu, bg.get(), z0.get(), snap, base.get(), Sb.get(), w_avg};
+  const size_t smem = lazy_epoch_smem(k);
+  if (smem > 48 * 1024)
+    SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lazy_epoch_kernel<<<1, kLazyThreads, smem, c.stream>>>(a);
+  SKR_LAUNCHED(&c);
+}
+
 void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
                double* w_avg) {
   ensure_tables(p);
   Ctx& c = p->ctx->c;
+  if (p->lazy) {
+    if (c.prof_on) c.prof_mark("svrg_epoch");
+    lazy_run_epoch(p, snap, mu, idx, m, eta, w_avg);
+    if (c.prof_on) c.prof_mark("svrg_epoch");
+    return;
+  }
   static const bool naive = getenv("SKR_K10") && std::string(getenv("SKR_K10")) == "naive";
   if (c.prof_on) c.prof_mark("svrg_epoch");
   if (!naive) {
@@ -1831,7 +1942,26 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     rowmax.zero();
     // P = X U (n x k) with ||x_i||^2 -> data betas; X~ = c X + (P o (D - c)) U^T
     DBuf<double> P((size_t)std::max<int64_t>(n, 1) * std::max<int64_t>(k, 1), c.stream);
-    DISPATCH_DTYPE(S.dtype, T, {
+    if (S.sparse) {
+      // Lazy mode (ridge.cpp:104-113 picks it for large n d; here for every sparse
+      // input): P = X U^T by SpMM, betas from ||x_i||^2 and P, no X~
+      if (c.world != 1) raise(SKR_EPARAM, "sparse data: preconditioned problems run on one GPU");
+      if (k > 0 && n > 0) {
+        DBuf<double> UT((size_t)d * k, c.stream);
+        transpose_f64(c, p->Ut.get(), k, d, ld, UT.get(), k);
+        csr_spmm(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, UT.get(), k, k, 1.0, P.get(), k);
+      }
+      if (n > 0) {
+        lazy_betas_kernel<<<ceil_div(n * 32, 256), 256, 0, c.stream>>>(S.rptr.get(), S.rval.get(), n, P.get(), k,
+                                                                       p->D.get(), p->c, p->data_coef,
+                                                                       p->betas.get() + p->row0, rowmax.get());
+        SKR_LAUNCHED(&c);
+      }
+      p->lazy = true;
+      p->xt = X->st;
+      p->Pm = std::move(P);
+    }
+    if (!S.sparse) DISPATCH_DTYPE(S.dtype, T, {
       const T* Xp = static_cast<const T*>(S.ptr);
       if (k > 0) gemm<T, double, false, true>(&c, n, k, d, Xp, ld, p->Ut.get(), ld, EpiStore{P.get(), k, 1.0, 0.0});
       if (n > 0) {
@@ -1887,7 +2017,7 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     SKR_CUDA(cudaMemcpyAsync(&p->max_row_sq, rowmax.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     // all rows of X~ and y on every rank for the (sequential, replicated) inner loop
     if (c.world == 1) {
-      p->xt_all = p->xt->ptr;
+      p->xt_all = p->xt->ptr;  // nullptr in Lazy mode
       p->y_all = p->y.get();
     } else {
       std::vector<int64_t> counts;
@@ -1968,6 +2098,9 @@ int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out) {
     copy(p->Ut, src->Ut);
     copy(p->D, src->D);
     copy(p->betas, src->betas);
+    copy(p->Pm, src->Pm);
+    copy(p->lz_UT, src->lz_UT);
+    p->lazy = src->lazy;
     p->y_all = p->y.get();
     if (src->tables) {
       copy(p->cum, src->cum);
@@ -2025,6 +2158,29 @@ int skr_problem_transformed(const skr_problem* p, void* rows_out) {
     if (!p) raise(SKR_EPARAM, "null problem");
     Ctx& c = p->ctx->c;
     const size_t s = dtype_size(p->dtype);
+    if (p->lazy) {  // materialise X~ = c X + (P o (D - c)) U^T on demand (diagnostics / tests)
+      const Storage& S = *p->xt;
+      DBuf<double> Xd((size_t)std::max<int64_t>(p->n, 1) * p->ld, c.stream), Xt_((size_t)std::max<int64_t>(p->n, 1) * p->ld,
+                                                                                c.stream);
+      csr_densify(c, S.rptr.get(), S.ridx.get(), S.rval.get(), p->n, Xd.get(), p->ld);
+      DBuf<double> Ps((size_t)std::max<int64_t>(p->n, 1) * std::max<int64_t>(p->k, 1), c.stream);
+      if (p->k > 0 && p->n > 0) {
+        SKR_CUDA(cudaMemcpyAsync(Ps.get(), p->Pm.get(), sizeof(double) * p->n * p->k, cudaMemcpyDeviceToDevice, c.stream));
+        scale_cols_kernel<<<std::min<unsigned>(ceil_div(p->n * p->k, 256), 65535u), 256, 0, c.stream>>>(
+            Ps.get(), p->n, p->k, p->D.get(), p->c);
+        SKR_LAUNCHED(&c);
+        Xt_.zero();
+        gemm<double, double, false, false>(&c, p->n, p->d, p->k, Ps.get(), p->k, p->Ut.get(), p->ld,
+                                           EpiXtilde<double>{Xd.get(), Xt_.get(), p->ld, p->c}, 1);
+      } else {
+        SKR_CUDA(cudaMemcpyAsync(Xt_.get(), Xd.get(), sizeof(double) * p->n * p->ld, cudaMemcpyDeviceToDevice, c.stream));
+      }
+      if (p->n > 0)
+        SKR_CUDA(cudaMemcpy2DAsync(rows_out, p->d * 8, Xt_.get(), p->ld * 8, p->d * 8, p->n, cudaMemcpyDeviceToHost,
+                                   c.stream));
+      c.sync();
+      return;
+    }
     if (p->n > 0)
       SKR_CUDA(cudaMemcpy2DAsync(rows_out, p->d * s, p->xt->ptr, p->ld * s, p->d * s, p->n, cudaMemcpyDeviceToHost,
                                  c.stream));
@@ -2080,12 +2236,33 @@ int skr_component_gradient(skr_problem* p, int64_t i, const double* w, double* o
     if (i < 0 || i >= p->n_global + p->d) raise(SKR_EINPUT, "component_gradient: index out of range");
     Ctx& c = p->ctx->c;
     upload_padded(c, p->wv.get(), w, p->d, p->ld);
-    DISPATCH_DTYPE(p->dtype, T, {
-      component_gradient_kernel<T><<<1, 256, 0, c.stream>>>(static_cast<const T*>(p->xt_all), p->B.get(), p->ld, p->d,
-                                                            p->n_global, p->y_all, p->data_coef, p->reg_coef, i,
-                                                            p->wv.get(), p->muv.get());
+    if (p->lazy && i < p->n) {
+      // x~_i as a dense row (ridge.cpp:238-262 Lazy branch), then the dense component formula
+      DBuf<double> row(p->ld, c.stream);
+      const Storage& S = *p->xt;
+      lazy_row_kernel<<<ceil_div(p->ld, 256), 256, 0, c.stream>>>(S.rptr.get(), S.ridx.get(), S.rval.get(), i,
+                                                                  p->Pm.get(), p->k, p->Ut.get(), p->ld, p->d,
+                                                                  p->D.get(), p->c, row.get());
       SKR_LAUNCHED(&c);
-    });
+      lazy_row_scatter_kernel<<<1, 256, 0, c.stream>>>(S.rptr.get(), S.ridx.get(), S.rval.get(), i, p->c, row.get());
+      SKR_LAUNCHED(&c);
+      component_gradient_kernel<double><<<1, 256, 0, c.stream>>>(row.get(), p->B.get(), p->ld, p->d, 1, p->y.get() + i,
+                                                                 p->data_coef, p->reg_coef, 0, p->wv.get(),
+                                                                 p->muv.get());
+      SKR_LAUNCHED(&c);
+    } else if (p->lazy) {
+      component_gradient_kernel<double><<<1, 256, 0, c.stream>>>(nullptr, p->B.get(), p->ld, p->d, p->n_global, p->y_all,
+                                                                 p->data_coef, p->reg_coef, i, p->wv.get(),
+                                                                 p->muv.get());
+      SKR_LAUNCHED(&c);
+    } else {
+      DISPATCH_DTYPE(p->dtype, T, {
+        component_gradient_kernel<T><<<1, 256, 0, c.stream>>>(static_cast<const T*>(p->xt_all), p->B.get(), p->ld,
+                                                              p->d, p->n_global, p->y_all, p->data_coef, p->reg_coef,
+                                                              i, p->wv.get(), p->muv.get());
+        SKR_LAUNCHED(&c);
+      });
+    }
     SKR_CUDA(cudaMemcpyAsync(out, p->muv.get(), sizeof(double) * p->d, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
   });

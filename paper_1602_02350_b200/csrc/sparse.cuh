@@ -118,3 +118,260 @@ inline void csr_spmv(Ctx& c, const int64_t* ptr, const int32_t* idx, const doubl
 }
 
 }  // namespace skr
+
+namespace skr {
+
+// ---- Lazy preconditioned problem over sparse rows (ridge.cpp:93-150,174-236 with
+// mode Lazy): X~ = c X + (P o (D - c)) U^T is never formed; P = X U^T (n x k). ----
+
+// beta_i = coef (c^2 ||x_i||^2 + sum_l (D_l^2 - c^2) P_il^2)   (ridge.cpp:124-127); rowmax = max ||x~_i||^2
+__global__ void __launch_bounds__(256) lazy_betas_kernel(const int64_t* __restrict__ ptr,
+                                                         const double* __restrict__ val, int64_t n,
+                                                         const double* __restrict__ P, int64_t k,
+                                                         const double* __restrict__ D, double c, double coef,
+                                                         double* __restrict__ beta, double* __restrict__ rowmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t t = ptr[i] + lane; t < ptr[i + 1]; t += 32) s = fma(val[t], val[t], s);
+  double q = 0.0;
+  for (int64_t l = lane; l < k; l += 32) {
+    const double pl = P[i * k + l];
+    q = fma((D[l] * D[l] - c * c) * pl, pl, q);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, off);
+    q += __shfl_xor_sync(0xffffffffu, q, off);
+  }
+  const double nrm = c * c * s + q;
+  if (lane == 0) {
+    beta[i] = coef * nrm;
+    atomicMax(reinterpret_cast<unsigned long long*>(rowmax), (unsigned long long)__double_as_longlong(fmax(nrm, 0.0)));
+  }
+}
+
+// s_i = x~_i . w = c x_i . w + P_i . v  (v = (D - c) o U^T w);  r2_i = (s_i - y_i)^2, r_i = s_i - y_i
+__global__ void __launch_bounds__(256) lazy_residual_kernel(const int64_t* __restrict__ ptr,
+                                                            const int32_t* __restrict__ idx,
+                                                            const double* __restrict__ val, int64_t n,
+                                                            const double* __restrict__ w,
+                                                            const double* __restrict__ P, int64_t k,
+                                                            const double* __restrict__ v, double c,
+                                                            const double* __restrict__ y, double* __restrict__ s_out,
+                                                            double* __restrict__ r_out, double* __restrict__ r2_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t t = ptr[i] + lane; t < ptr[i + 1]; t += 32) a = fma(val[t], w[idx[t]], a);
+  for (int64_t l = lane; l < k; l += 32) b = fma(P[i * k + l], v[l], b);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  if (lane == 0) {
+    const double s = c * a + b;
+    const double r = s - y[i];
+    if (s_out) s_out[i] = s;
+    r_out[i] = r;
+    r2_out[i] = r * r;
+  }
+}
+
+// v_l = (D_l - c) u_l
+__global__ void lazy_scale_kernel(const double* __restrict__ u, const double* __restrict__ D, double c, int64_t k,
+                                  double* __restrict__ v) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < k) v[l] = (D[l] - c) * u[l];
+}
+
+// mu_f = (c g1_f + sum_l U_lf (D_l - c) g2_l) / n + lambda (c^2 w_f + sum_l U_lf (D_l^2 - c^2) u_l);
+// thread 0 of block 0 also finishes the objective from the loss sum.
+__global__ void lazy_finalize_kernel(const double* __restrict__ g1, const double* __restrict__ g2,
+                                     const double* __restrict__ Ut, int64_t ld, int64_t d, int64_t k,
+                                     const double* __restrict__ D, double c, const double* __restrict__ w,
+                                     const double* __restrict__ uw, double inv_n, double lambda,
+                                     const double* __restrict__ loss, double* __restrict__ mu,
+                                     double* __restrict__ obj) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < ld) {
+    if (f < d) {
+      double a = c * g1[f], r = c * c * w[f];
+      for (int64_t l = 0; l < k; ++l) {
+        const double uf = Ut[l * ld + f];
+        a = fma(uf, (D[l] - c) * g2[l], a);
+        r = fma(uf, (D[l] * D[l] - c * c) * uw[l], r);
+      }
+      mu[f] = a * inv_n + lambda * r;
+    } else {
+      mu[f] = 0.0;
+    }
+  }
+  if (obj && f == 0) {
+    double reg = c * c * uw[k];
+    for (int64_t l = 0; l < k; ++l) reg += (D[l] * D[l] - c * c) * uw[l] * uw[l];
+    *obj = *loss * (0.5 * inv_n) + 0.5 * lambda * reg;
+  }
+}
+
+// row i of X~ as a dense ld-vector: c x_i + U ((D - c) o P_i)   (zero padded)
+__global__ void lazy_row_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                const double* __restrict__ val, int64_t i, const double* __restrict__ P, int64_t k,
+                                const double* __restrict__ Ut, int64_t ld, int64_t d, const double* __restrict__ D,
+                                double c, double* __restrict__ out) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= ld) return;
+  double s = 0.0;
+  if (f < d)
+    for (int64_t l = 0; l < k; ++l) s = fma(Ut[l * ld + f], (D[l] - c) * P[i * k + l], s);
+  out[f] = s;
+}
+__global__ void lazy_row_scatter_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                        const double* __restrict__ val, int64_t i, double c,
+                                        double* __restrict__ out) {
+  for (int64_t t = ptr[i] + threadIdx.x; t < ptr[i + 1]; t += blockDim.x) out[idx[t]] += c * val[t];
+}
+
+}  // namespace skr
+
+namespace skr {
+
+// ---- Lazy SVRG epoch over sparse rows (LazyEpochState, ridge.cpp:283-400) ------------
+// w_t = base_t + U h_t - tau_t mu with tau_t = eta t, z = U^T w tracked like the
+// reference (z -= eta (delta D o P_i + U^T mu)), so a data step costs O(nnz_i + k)
+// and a regulariser step O(k) — the reference's per-step O(d) axpy of mu into base
+// is folded into tau.  The epoch average uses
+//   sum_{t=1..m} w_t = m base_0 + sum_s (m-s+1) dbase_s + U sum_s (m-s+1) dh_s - eta m(m+1)/2 mu.
+// One CTA runs the sequential chain; all sums are in a fixed order.
+struct LazyEpochArgs {
+  const int64_t* rptr;
+  const int32_t* ridx;
+  const double* rval;
+  int64_t n, d, ld, k;
+  const double* P;      // n x k
+  const double* UT;     // d x k (row f = U_f)
+  const double* D;      // k
+  double c, data_coef, reg_coef;
+  const int64_t* idx;   // m
+  const double* inv_nq; // N
+  int64_t m;
+  double eta;
+  const double* s_bar;  // n: x~_i . wbar
+  const double* half;   // d: (P^{-1/2} wbar)_j
+  const double* xmu;    // n: x_i . mu
+  const double* mu;     // ld
+  const double* bg;     // k: U^T mu
+  const double* z0;     // k: U^T wbar
+  const double* snap;   // ld: wbar
+  double* base;         // ld scratch (starts as wbar)
+  double* Sb;           // ld scratch (zero)
+  double* w_avg;        // ld out
+};
+
+constexpr int kLazyThreads = 256;
+
+__device__ __forceinline__ double lazy_block_sum(double v, double* red, int tid) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < kLazyThreads / 32; ++q) s += red[q];
+  return s;
+}
+
+__global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochArgs a) {
+  extern __shared__ double lz_sm[];
+  const int64_t k = a.k;
+  double* h = lz_sm;          // k
+  double* z = h + k;          // k
+  double* Sh = z + k;         // k
+  double* Dm = Sh + k;        // k: D - c
+  double* Dd = Dm + k;        // k: D
+  double* red = Dd + k;       // 3 x 8
+  const int tid = threadIdx.x;
+  for (int64_t l = tid; l < k; l += kLazyThreads) {
+    h[l] = 0.0;
+    z[l] = a.z0[l];
+    Sh[l] = 0.0;
+    Dm[l] = a.D[l] - a.c;
+    Dd[l] = a.D[l];
+  }
+  __syncthreads();
+  for (int64_t t = 1; t <= a.m; ++t) {
+    const int64_t i = a.idx[t - 1];
+    const double q = a.inv_nq[i];
+    const double tau = a.eta * (double)(t - 1);
+    const double wgt = (double)(a.m - t + 1);
+    const bool data = i < a.n;
+    const double* row = data ? a.P + i * k : a.UT + (i - a.n) * k;
+    double A = 0.0, B = 0.0, Cz = 0.0;
+    int64_t b0 = 0, b1 = 0;
+    if (data) {
+      b0 = a.rptr[i];
+      b1 = a.rptr[i + 1];
+      for (int64_t e = b0 + tid; e < b1; e += kLazyThreads) A = fma(a.rval[e], a.base[a.ridx[e]], A);
+    } else if (tid == 0) {
+      A = a.base[i - a.n];
+    }
+    for (int64_t l = tid; l < k; l += kLazyThreads) {
+      const double r = row[l];
+      B = fma(r, h[l], B);
+      Cz = fma(Dm[l] * r, z[l], Cz);
+    }
+    A = lazy_block_sum(A, red, tid);
+    B = lazy_block_sum(B, red + 8, tid);
+    Cz = lazy_block_sum(Cz, red + 16, tid);
+    double delta;
+    if (data) {
+      const double inner = a.c * (A + B - tau * a.xmu[i]) + Cz;
+      delta = a.data_coef * (inner - a.s_bar[i]) * q;
+    } else {
+      const int64_t j = i - a.n;
+      const double inner = a.c * (A + B - tau * a.mu[j]) + Cz;
+      delta = a.reg_coef * (inner - a.half[j]) * q;
+    }
+    __syncthreads();  // every thread has read red/h/z/base before the updates
+    const double ed = a.eta * delta;
+    if (data) {
+      for (int64_t e = b0 + tid; e < b1; e += kLazyThreads) {
+        const int64_t f = a.ridx[e];
+        const double dv = -ed * a.c * a.rval[e];
+        a.base[f] += dv;
+        a.Sb[f] = fma(wgt, dv, a.Sb[f]);
+      }
+    } else if (tid == 0) {
+      const int64_t j = i - a.n;
+      const double dv = -ed * a.c;
+      a.base[j] += dv;
+      a.Sb[j] = fma(wgt, dv, a.Sb[j]);
+    }
+    for (int64_t l = tid; l < k; l += kLazyThreads) {
+      const double r = row[l];
+      const double dh = -ed * Dm[l] * r;
+      h[l] += dh;
+      Sh[l] = fma(wgt, dh, Sh[l]);
+      z[l] -= a.eta * fma(delta, Dd[l] * r, a.bg[l]);
+    }
+    __syncthreads();
+  }
+  // w_avg = (m wbar + Sb) / m + U Sh / m - eta (m + 1) / 2 mu
+  const double inv_m = 1.0 / (double)a.m, half_tau = 0.5 * a.eta * (double)(a.m + 1);
+  for (int64_t f = tid; f < a.ld; f += kLazyThreads) {
+    if (f < a.d) {
+      double lift = 0.0;
+      for (int64_t l = 0; l < k; ++l) lift = fma(a.UT[f * k + l], Sh[l], lift);
+      a.w_avg[f] = a.snap[f] + a.Sb[f] * inv_m + lift * inv_m - half_tau * a.mu[f];
+    } else {
+      a.w_avg[f] = 0.0;
+    }
+  }
+}
+
+inline size_t lazy_epoch_smem(int64_t k) { return sizeof(double) * (5 * std::max<int64_t>(k, 1) + 24); }
+
+}  // namespace skr

@@ -582,7 +582,8 @@ class PreconditionedRidge:
 
     # PreconditionedRidge extras
     def mode(self) -> ApplyMode:
-        return ApplyMode.Dense
+        """Dense for dense data (X~ materialised); Lazy for sparse data (ridge.cpp:283-400)."""
+        return ApplyMode.Lazy if self.problem_.data.sparse else ApplyMode.Dense
 
     def preconditioner(self) -> Preconditioner:
         return self.precond_
