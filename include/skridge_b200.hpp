@@ -24,6 +24,8 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <fstream>
+#include <sstream>
 #include <limits>
 #include <vector>
 
@@ -38,7 +40,17 @@ using Vector = std::vector<double>;
 struct DimensionError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ParameterError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct InputError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
-struct DegenerateSpectrumError : InputError { using InputError::InputError; };
+struct DegenerateSpectrumError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DegenerateDataError : std::runtime_error { using std::runtime_error::runtime_error; };
+class ParseError : public std::runtime_error {  // errors.hpp:52-61
+ public:
+  ParseError(std::size_t line, const std::string& what)
+      : std::runtime_error("line " + std::to_string(line) + ": " + what), line_(line) {}
+  std::size_t line() const { return line_; }
+
+ private:
+  std::size_t line_;
+};
 struct EmptyBasisError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ScaleGuardError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -108,6 +120,20 @@ class DataMatrix {
     skr_data* x = nullptr;
     check(skr_data_create(ctx.get(), rows, (int64_t)n, (int64_t)d, SKR_F32, &x));
     reset(x);
+  }
+  /// DataMatrix(SparseMatrix) (data_matrix.hpp:24): points as CSR (= the reference's CSC)
+  static DataMatrix from_csr(const Context& ctx, std::size_t n, std::size_t d, const std::vector<int64_t>& row_ptr,
+                             const std::vector<int32_t>& col_idx, const std::vector<double>& vals) {
+    skr_data* x = nullptr;
+    check(skr_data_create_csr(ctx.get(), (int64_t)n, (int64_t)d, row_ptr.data(), col_idx.data(), vals.data(), &x));
+    DataMatrix out(ctx);
+    out.reset(x);
+    return out;
+  }
+  bool is_sparse() const {
+    int sp = 0;
+    check(skr_data_is_sparse(h_.get(), &sp, nullptr));
+    return sp != 0;
   }
   std::size_t rows() const { return (std::size_t)info().d; }   // dimension d
   std::size_t cols() const { return (std::size_t)info().ng; }  // point count n
@@ -478,6 +504,74 @@ inline ReferenceSolution reference_minimum(const RidgeProblem& p) {
   check(skr_reference_minimum(p.data.context().get(), p.data.get(), p.labels.data(), p.lambda, r.minimizer.data(),
                               &r.minimum));
   return r;
+}
+
+// ---- sparse corpus I/O (dataset.hpp:37-49, dataset.cpp:80-198) ------------------------------
+struct LabeledDataset {
+  DataMatrix data;
+  Vector labels;
+  std::string provenance;
+};
+
+/// dataset.cpp:87-162: "label idx:value ..." lines, 1-based strictly increasing
+/// indices, '#' comments; d = the largest index seen; zero values are dropped.
+inline LabeledDataset read_sparse_corpus(const Context& ctx, const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw InputError("corpus: cannot open " + path);
+  std::vector<int64_t> row_ptr{0};
+  std::vector<int32_t> col_idx;
+  std::vector<double> vals;
+  Vector labels;
+  std::size_t max_index = 0, lineno = 0;
+  std::string raw;
+  auto parse_double = [](const std::string& t, double& v) {
+    std::size_t used = 0;
+    v = std::stod(t, &used);
+    if (used != t.size()) throw std::invalid_argument(t);
+  };
+  while (std::getline(in, raw)) {
+    ++lineno;
+    const auto hash = raw.find('#');
+    std::istringstream line(hash == std::string::npos ? raw : raw.substr(0, hash));
+    std::string tok;
+    if (!(line >> tok)) continue;
+    double label;
+    try {
+      parse_double(tok, label);
+    } catch (const std::exception&) {
+      throw ParseError(lineno, "bad label '" + tok + "'");
+    }
+    labels.push_back(label);
+    std::size_t prev = 0;
+    while (line >> tok) {
+      const auto colon = tok.find(':');
+      if (colon == std::string::npos || colon == 0 || colon + 1 >= tok.size())
+        throw ParseError(lineno, "bad feature '" + tok + "'");
+      std::size_t index;
+      double value;
+      try {
+        std::size_t used = 0;
+        const long long ri = std::stoll(tok.substr(0, colon), &used);
+        if (used != colon || ri < 1) throw std::invalid_argument(tok);
+        index = (std::size_t)ri;
+        parse_double(tok.substr(colon + 1), value);
+      } catch (const std::exception&) {
+        throw ParseError(lineno, "bad feature '" + tok + "'");
+      }
+      if (index <= prev) throw ParseError(lineno, "feature indices must be strictly increasing");
+      if (!std::isfinite(value)) throw ParseError(lineno, "non-finite value");
+      prev = index;
+      max_index = std::max(max_index, index);
+      if (value != 0.0) {
+        col_idx.push_back((int32_t)(index - 1));
+        vals.push_back(value);
+      }
+    }
+    row_ptr.push_back((int64_t)vals.size());
+  }
+  if (labels.empty()) throw InputError("corpus: no data lines in " + path);
+  if (max_index == 0) throw DegenerateDataError("corpus: no features seen");
+  return LabeledDataset{DataMatrix::from_csr(ctx, labels.size(), max_index, row_ptr, col_idx, vals), labels, path};
 }
 
 // ---- ratio / spectrum diagnostics (precond.hpp:13-20,81-91; bench.cpp:195-212) --------

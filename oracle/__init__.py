@@ -234,6 +234,23 @@ class _Backend:
             n, d, decay, noise_std, seed, int(normalize_columns), X, y))
         return X, y
 
+    def read_sparse_corpus(self, path):
+        """dataset.cpp:87-162 (reference backend only): (row_ptr, col_idx, vals, d), labels."""
+        if self.prefix == "skro_":
+            raise NotImplementedError("read_sparse_corpus: reference backend only")
+        n, d, nnz = i64(), i64(), i64()
+        p = path.encode()
+        self._check(self._fn("read_corpus_sizes", cint, [C.c_char_p, P(i64), P(i64), P(i64)])(
+            p, C.byref(n), C.byref(d), C.byref(nnz)))
+        rp = np.empty(n.value + 1, dtype=np.int64)
+        ci = np.empty(max(nnz.value, 1), dtype=np.int32)
+        va = np.empty(max(nnz.value, 1))
+        y = np.empty(n.value)
+        ip64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+        self._check(self._fn("read_corpus", cint, [C.c_char_p, ip64, ip32, _dp, _dp])(p, rp, ci, va, y))
+        return (rp, ci[: nnz.value], va[: nnz.value], d.value), y
+
     # ratio diagnostics: the unmodified reference only (no C restatement)
     def dataset_spectrum(self, x, lam) -> np.ndarray:
         if self.prefix == "skro_":

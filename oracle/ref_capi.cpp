@@ -250,6 +250,31 @@ int ref_problem_create_csr(const std::int64_t* row_ptr, const std::int32_t* col_
   });
 }
 
+// read_sparse_corpus (dataset.cpp:87-162): sizes, then the CSR-over-points arrays.
+// Parse errors return the status of their exception type; ParseError -> 3 (input).
+int ref_read_corpus_sizes(const char* path, std::int64_t* n, std::int64_t* d, std::int64_t* nnz) {
+  return guard([&] {
+    LabeledDataset ds = read_sparse_corpus(path);
+    const SparseMatrix* sp = ds.data.sparse();
+    *n = static_cast<std::int64_t>(sp->cols());
+    *d = static_cast<std::int64_t>(sp->rows());
+    *nnz = static_cast<std::int64_t>(sp->nnz());
+  });
+}
+
+int ref_read_corpus(const char* path, std::int64_t* row_ptr, std::int32_t* col_idx, double* vals, double* labels) {
+  return guard([&] {
+    LabeledDataset ds = read_sparse_corpus(path);
+    const SparseMatrix* sp = ds.data.sparse();
+    for (std::size_t j = 0; j <= sp->cols(); ++j) row_ptr[j] = static_cast<std::int64_t>(sp->col_ptr()[j]);
+    for (std::size_t t = 0; t < sp->nnz(); ++t) {
+      col_idx[t] = static_cast<std::int32_t>(sp->row_idx()[t]);
+      vals[t] = sp->values()[t];
+    }
+    std::memcpy(labels, ds.labels.data(), sizeof(double) * ds.labels.size());
+  });
+}
+
 // generate_synthetic (dataset.cpp:16-79): the reference's own synthetic instance
 // (decay 0: 1/q, 1: 1/q^2), written as n x d row-major (= its d x n column-major).
 int ref_generate_synthetic(std::int64_t n, std::int64_t d, int decay, double noise_std, std::uint64_t seed,

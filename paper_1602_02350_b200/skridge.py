@@ -890,8 +890,20 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7) -> list:
 # Ratio / spectrum diagnostics (precond.hpp:13-20,81-91; precond.cpp:23-32,165-172,
 # 208-219; bench.cpp:195-212).  The spectrum is one device SYRK + eigensolve;
 # the rest is O(d) host arithmetic.
-class DegenerateSpectrumError(InputError):
-    """errors.hpp DegenerateSpectrumError."""
+class DegenerateSpectrumError(SkridgeError, RuntimeError):
+    """errors.hpp:45-49."""
+
+
+class DegenerateDataError(SkridgeError, RuntimeError):
+    """errors.hpp:39-43."""
+
+
+class ParseError(SkridgeError, RuntimeError):
+    """errors.hpp:51-61: carries the 1-based line number."""
+
+    def __init__(self, line: int, what: str):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
 
 
 @dataclass
@@ -967,3 +979,100 @@ def run_ratio_curve(spec: SpectrumSummary, k_max: int) -> list:
     if k_max < 1 or k_max > spec.dim():
         raise ParameterError("ratio curve: k_max must satisfy 1 <= k_max <= d")
     return [RatioRow(k, theoretical_ratio(spec, k)) for k in range(1, k_max + 1)]
+
+
+# ---------------------------------------------------------------------------
+# Sparse corpus I/O (dataset.hpp:37-49, dataset.cpp:80-198): host text parsing
+# into a device CSR DataMatrix.
+@dataclass
+class LabeledDataset:
+    data: DataMatrix
+    labels: np.ndarray
+    provenance: str = ""
+
+
+def _strict_float(tok: str) -> float:
+    if "_" in tok or tok != tok.strip():
+        raise ValueError(tok)
+    return float(tok)
+
+
+def read_sparse_corpus(path: str, ctx: Context | None = None) -> LabeledDataset:
+    """dataset.cpp:87-162: lines "label idx:value ...", 1-based strictly increasing
+    indices, '#' comments, blank lines skipped, zero values dropped, d = the
+    largest index seen."""
+    try:
+        f = open(path)
+    except OSError:
+        raise InputError("corpus: cannot open " + path)
+    rp, ci, va, labels = [0], [], [], []
+    max_index = 0
+    with f:
+        for lineno, raw in enumerate(f, start=1):
+            toks = raw.split("#", 1)[0].split()
+            if not toks:
+                continue
+            try:
+                labels.append(_strict_float(toks[0]))
+            except ValueError:
+                raise ParseError(lineno, f"bad label '{toks[0]}'")
+            prev = 0
+            for tok in toks[1:]:
+                colon = tok.find(":")
+                if colon <= 0 or colon + 1 >= len(tok):
+                    raise ParseError(lineno, f"bad feature '{tok}'")
+                try:
+                    head = tok[:colon]
+                    if "_" in head or not head.lstrip("+-").isdigit():
+                        raise ValueError(tok)
+                    index = int(head)
+                    if index < 1:
+                        raise ValueError(tok)
+                    value = _strict_float(tok[colon + 1:])
+                except ValueError:
+                    raise ParseError(lineno, f"bad feature '{tok}'")
+                if index <= prev:
+                    raise ParseError(lineno, "feature indices must be strictly increasing")
+                if not math.isfinite(value):
+                    raise ParseError(lineno, "non-finite value")
+                prev = index
+                max_index = max(max_index, index)
+                if value != 0.0:
+                    ci.append(index - 1)
+                    va.append(value)
+            rp.append(len(va))
+    if not labels:
+        raise InputError("corpus: no data lines in " + path)
+    if max_index == 0:
+        raise DegenerateDataError("corpus: no features seen")
+    data = DataMatrix.from_csr(np.asarray(rp, dtype=np.int64), np.asarray(ci, dtype=np.int32),
+                               np.asarray(va, dtype=np.float64), max_index, ctx)
+    return LabeledDataset(data, np.asarray(labels, dtype=np.float64), path)
+
+
+def write_sparse_corpus(row_ptr, col_idx, values, labels, path: str, scale: float = 1.0):
+    """dataset.cpp:164-186 for CSR rows: "%.17g" labels and values, 1-based indices."""
+    rp = np.asarray(row_ptr)
+    with open(path, "w") as out:
+        for i in range(len(labels)):
+            parts = ["%.17g" % labels[i]]
+            for t in range(rp[i], rp[i + 1]):
+                parts.append("%d:%s" % (int(col_idx[t]) + 1, "%.17g" % (scale * values[t])))
+            out.write(" ".join(parts) + "\n")
+
+
+def average_norm_normalize(ds: LabeledDataset, row_ptr=None, values=None) -> LabeledDataset:
+    """dataset.cpp:188-198: scale the data by 1 / (mean point norm), summed in point
+    order.  Needs the host CSR arrays the DataMatrix was built from."""
+    rp, va = np.asarray(row_ptr), np.asarray(values, dtype=np.float64)
+    n = len(rp) - 1
+    if n == 0:
+        raise DegenerateDataError("normalize: empty dataset")
+    total = 0.0
+    for i in range(n):
+        seg = va[rp[i]:rp[i + 1]]
+        total += math.sqrt(float(np.dot(seg, seg)))
+    mean = total / n
+    if mean == 0.0:
+        raise DegenerateDataError("normalize: all columns are zero")
+    return LabeledDataset(ds.data.scaled(1.0 / mean), ds.labels.copy(), ds.provenance)

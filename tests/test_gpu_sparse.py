@@ -169,3 +169,28 @@ def test_lazy_sketched_pipeline_and_unpreconditioned(R):
     got0 = sk.svrg_solve(plain, sk.SvrgConfig(3, 2 * n, eta0, 1), np.zeros(d))
     want0 = R.problem_csr(csr, y, lam, None, None, mode=1).svrg(3, 2 * n, eta0, 1)
     assert rel([r.objective for r in got0.trace], want0.trace) < 1e-10
+
+
+def test_corpus_file_end_to_end(R, tmp_path):
+    """read_sparse_corpus -> average_norm_normalize -> sketched Lazy SVRG on the
+    device, against the reference reading the same file."""
+    from paper_1602_02350_b200 import configs
+    csr, y = sparse_instance(n=500, d=60, seed=9)
+    path = str(tmp_path / "corpus.txt")
+    sk.write_sparse_corpus(csr[0], csr[1], csr[2], y, path)
+    ds = sk.read_sparse_corpus(path)
+    (rp, ci, va, d), yr = R.read_sparse_corpus(path)
+    assert ds.data.sparse and ds.data.d == d and np.array_equal(ds.labels, yr)
+    norm = sk.average_norm_normalize(ds, rp, va)
+    mean = np.mean([np.linalg.norm(va[rp[i]:rp[i + 1]]) for i in range(len(rp) - 1)])
+    assert abs(norm.data.scale() - 1.0 / mean) <= 1e-15 / mean
+    lam = 1e-3
+    p = sk.RidgeProblem(ds.data, ds.labels, lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(6, 0.5, 2, 3))
+    want_sv = R.block_lanczos_csr((rp, ci, va, d), 6, q=3, seed=2)
+    assert rel(sv.singular_values, want_sv.sigma) < 1e-10
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, lam))
+    eta = configs.step_size(pg.max_row_sq())
+    got = sk.svrg_solve(pg, sk.SvrgConfig(4, 2 * len(yr), eta, 2), np.zeros(d))
+    want = R.problem_csr((rp, ci, va, d), yr, lam, want_sv.U, want_sv.sigma, mode=1).svrg(4, 2 * len(yr), eta, 2)
+    assert rel([r.objective for r in got.trace], want.trace) < 1e-9
