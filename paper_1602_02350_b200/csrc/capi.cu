@@ -79,6 +79,7 @@ struct Storage {
   DBuf<int64_t> rptr, fptr;
   DBuf<int32_t> ridx, fidx;  // ridx: feature of each point-row entry; fidx: point of each feature-row entry
   DBuf<double> rval, fval;
+  SplitCSR fsplit;  // feature rows cut for load balance (power-law feature popularity)
   ~Storage() {
     if (owns && ptr) cudaFreeAsync(ptr, stream);
   }
@@ -496,7 +497,7 @@ void lazy_fullgrad(skr_problem* p, const double* w, double* mu, double* obj, dou
     SKR_LAUNCHED(&c);
     sum_kernel<<<1, 1024, 0, c.stream>>>(p->lz_r2.get(), n, p->lz_loss.get());
     SKR_LAUNCHED(&c);
-    csr_spmv(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, p->lz_r.get(), 1.0, p->lz_g1.get());
+    split_spmv(c, S.fsplit, S.fidx.get(), S.fval.get(), d, p->lz_r.get(), 1.0, p->lz_g1.get());
     if (k > 0)
       gemm<double, double, true, false>(&c, k, 1, n, p->Pm.get(), k, p->lz_r.get(), 1,
                                         EpiStore{p->lz_g2.get(), 1, 1.0, 0.0});
@@ -955,10 +956,16 @@ void lazy_run_epoch(skr_problem* p, const double* snap, const double* mu, const 
   LazyEpochArgs a{S.rptr.get(), S.ridx.get(), S.rval.get(), n, d, ld, k, p->Pm.get(), p->lz_UT.get(), p->D.get(),
                   p->c, p->data_coef, p->reg_coef, idx, p->inv_nq.get(), m, eta, sbar.get(), half.get(), xmu.get(),
                   mu, bg.get(), z0.get(), snap, base.get(), Sb.get(), w_avg};
-  const size_t smem = lazy_epoch_smem(k);
-  if (smem > 48 * 1024)
-    SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  lazy_epoch_kernel<<<1, kLazyThreads, smem, c.stream>>>(a);
+  const size_t smem_in = lazy_epoch_smem(k, ld);
+  if (smem_in <= 200 * 1024) {  // the iterate's base vector lives in shared memory
+    SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_in));
+    lazy_epoch_kernel<true><<<1, kLazyThreads, smem_in, c.stream>>>(a);
+  } else {
+    const size_t smem = lazy_epoch_smem(k, 0);
+    if (smem > 48 * 1024)
+      SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lazy_epoch_kernel<false><<<1, kLazyThreads, smem, c.stream>>>(a);
+  }
   SKR_LAUNCHED(&c);
 }
 
@@ -1472,6 +1479,7 @@ int skr_data_create_csr(skr_ctx* ctx, int64_t n, int64_t d, const int64_t* row_p
     st->fval.alloc(std::max<int64_t>(nnz, 1), c.stream);
     SKR_CUDA(cudaMemcpyAsync(st->rptr.get(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
     SKR_CUDA(cudaMemcpyAsync(st->fptr.get(), fptr.data(), sizeof(int64_t) * (d + 1), cudaMemcpyHostToDevice, c.stream));
+    build_split(c, fptr.data(), d, st->fsplit);
     if (nnz > 0) {
       SKR_CUDA(cudaMemcpyAsync(st->ridx.get(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
       SKR_CUDA(cudaMemcpyAsync(st->rval.get(), vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.stream));
@@ -1713,7 +1721,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       // Vt^T (d x k) = scale X^T Pi over the feature-major CSR, Pi as n x k rows
       DBuf<double> Pn((size_t)std::max<int64_t>(n, 1) * k, c.stream), tmp((size_t)d * k, c.stream);
       transpose_f64(c, Pt.get(), k, n, n, Pn.get(), k);
-      csr_spmm(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, Pn.get(), k, k, scale, tmp.get(), k);
+      split_spmm(c, S.fsplit, S.fidx.get(), S.fval.get(), d, Pn.get(), k, k, scale, tmp.get(), k);
       transpose_f64(c, tmp.get(), d, k, k, Vt.get(), ld);
     } else if (tc) {
       tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, k, d, n, scale, Vt.get(), ld);
@@ -1739,7 +1747,7 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
         transpose_f64(c, prev, appended, d, ld, prevT.get(), appended);
         csr_spmm(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, prevT.get(), appended, appended, scale, Tm.get(),
                  appended);
-        csr_spmm(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, Tm.get(), appended, appended, scale, tmpK.get(),
+        split_spmm(c, S.fsplit, S.fidx.get(), S.fval.get(), d, Tm.get(), appended, appended, scale, tmpK.get(),
                  appended);
         Vt.zero();
         transpose_f64(c, tmpK.get(), d, appended, appended, Vt.get(), ld);
@@ -2581,7 +2589,7 @@ int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, doub
     if (n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
     rhs.zero();
     if (S.sparse) {
-      csr_spmv(c, S.fptr.get(), S.fidx.get(), S.fval.get(), d, yd.get(), 1.0 / (double)X->n_global, rhs.get());
+      split_spmv(c, S.fsplit, S.fidx.get(), S.fval.get(), d, yd.get(), 1.0 / (double)X->n_global, rhs.get());
     } else {
       DISPATCH_DTYPE(S.dtype, T, {
         gemm<T, double, true, false>(&c, d, 1, n, static_cast<const T*>(S.ptr), ld, yd.get(), 1,

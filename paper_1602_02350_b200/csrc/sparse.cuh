@@ -284,6 +284,7 @@ __device__ __forceinline__ double lazy_block_sum(double v, double* red, int tid)
   return s;
 }
 
+template <bool SMEM_BASE>
 __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochArgs a) {
   extern __shared__ double lz_sm[];
   const int64_t k = a.k;
@@ -293,7 +294,10 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochAr
   double* Dm = Sh + k;        // k: D - c
   double* Dd = Dm + k;        // k: D
   double* red = Dd + k;       // 3 x 8
+  double* base = SMEM_BASE ? red + 24 : a.base;  // the gathered state, in shared memory when d fits
   const int tid = threadIdx.x;
+  if (SMEM_BASE)
+    for (int64_t f = tid; f < a.ld; f += kLazyThreads) base[f] = a.base[f];
   for (int64_t l = tid; l < k; l += kLazyThreads) {
     h[l] = 0.0;
     z[l] = a.z0[l];
@@ -314,9 +318,9 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochAr
     if (data) {
       b0 = a.rptr[i];
       b1 = a.rptr[i + 1];
-      for (int64_t e = b0 + tid; e < b1; e += kLazyThreads) A = fma(a.rval[e], a.base[a.ridx[e]], A);
+      for (int64_t e = b0 + tid; e < b1; e += kLazyThreads) A = fma(a.rval[e], base[a.ridx[e]], A);
     } else if (tid == 0) {
-      A = a.base[i - a.n];
+      A = base[i - a.n];
     }
     for (int64_t l = tid; l < k; l += kLazyThreads) {
       const double r = row[l];
@@ -341,13 +345,13 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochAr
       for (int64_t e = b0 + tid; e < b1; e += kLazyThreads) {
         const int64_t f = a.ridx[e];
         const double dv = -ed * a.c * a.rval[e];
-        a.base[f] += dv;
+        base[f] += dv;
         a.Sb[f] = fma(wgt, dv, a.Sb[f]);
       }
     } else if (tid == 0) {
       const int64_t j = i - a.n;
       const double dv = -ed * a.c;
-      a.base[j] += dv;
+      base[j] += dv;
       a.Sb[j] = fma(wgt, dv, a.Sb[j]);
     }
     for (int64_t l = tid; l < k; l += kLazyThreads) {
@@ -372,6 +376,121 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch_kernel(LazyEpochAr
   }
 }
 
-inline size_t lazy_epoch_smem(int64_t k) { return sizeof(double) * (5 * std::max<int64_t>(k, 1) + 24); }
+inline size_t lazy_epoch_smem(int64_t k, int64_t ld_base) {
+  return sizeof(double) * (5 * std::max<int64_t>(k, 1) + 24 + ld_base);
+}
+
+}  // namespace skr
+
+namespace skr {
+
+// ---- load balance for skewed rows (power-law feature popularity): rows longer
+// than kSplitNnz are cut into consecutive sub-rows; a warp per sub-row writes a
+// partial, and a second pass sums each row's partials in sub-row order, so the
+// result stays deterministic. ----
+constexpr int64_t kSplitNnz = 2048;
+
+struct SplitCSR {
+  DBuf<int64_t> ptr;    // S + 1: entry offsets of the sub-rows
+  DBuf<int64_t> first;  // rows + 1: first sub-row of each row
+  DBuf<int32_t> row;    // S: row of each sub-row
+  int64_t S = 0;
+};
+
+// host: the split of a CSR with row pointer rp (rows + 1)
+inline void build_split(Ctx& c, const int64_t* rp, int64_t rows, SplitCSR& out) {
+  std::vector<int64_t> sp{0}, first{0};
+  std::vector<int32_t> srow;
+  for (int64_t r = 0; r < rows; ++r) {
+    const int64_t b = rp[r], e = rp[r + 1];
+    int64_t t = b;
+    do {
+      const int64_t u = std::min(e, t + kSplitNnz);
+      sp.push_back(u);
+      srow.push_back((int32_t)r);
+      t = u;
+    } while (t < e);
+    first.push_back((int64_t)srow.size());
+  }
+  out.S = (int64_t)srow.size();
+  out.ptr.alloc(out.S + 1, c.stream);
+  out.first.alloc(rows + 1, c.stream);
+  out.row.alloc(std::max<int64_t>(out.S, 1), c.stream);
+  SKR_CUDA(cudaMemcpyAsync(out.ptr.get(), sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice, c.stream));
+  SKR_CUDA(cudaMemcpyAsync(out.first.get(), first.data(), sizeof(int64_t) * first.size(), cudaMemcpyHostToDevice,
+                           c.stream));
+  if (out.S)
+    SKR_CUDA(cudaMemcpyAsync(out.row.get(), srow.data(), sizeof(int32_t) * srow.size(), cudaMemcpyHostToDevice,
+                             c.stream));
+  c.sync();  // the host vectors go out of scope
+}
+
+// part[u] = sum over sub-row u of val * x[idx]   (warp per sub-row)
+__global__ void __launch_bounds__(256) split_spmv_kernel(const int64_t* __restrict__ sptr,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val, int64_t S,
+                                                         const double* __restrict__ x, double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= S) return;
+  double acc = 0.0;
+  for (int64_t t = sptr[u] + lane; t < sptr[u + 1]; t += 32) acc = fma(val[t], x[idx[t]], acc);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) part[u] = acc;
+}
+
+// out[r] = alpha * sum_{u in row r's sub-rows} part[u] (ncols-wide rows, part row stride ncols)
+__global__ void split_reduce_kernel(const int64_t* __restrict__ first, int64_t rows, const double* __restrict__ part,
+                                    int64_t ncols, double alpha, double* __restrict__ out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * ncols) return;
+  const int64_t r = e / ncols, j = e % ncols;
+  double s = 0.0;
+  for (int64_t u = first[r]; u < first[r + 1]; ++u) s += part[u * ncols + j];
+  out[r * ldo + j] = alpha * s;
+}
+
+// part[u][j] = sum over sub-row u of val * B[idx][j]   (warp per sub-row, lanes over j)
+__global__ void __launch_bounds__(256) split_spmm_kernel(const int64_t* __restrict__ sptr,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val, int64_t S,
+                                                         const double* __restrict__ B, int64_t ldb, int64_t ncols,
+                                                         double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= S) return;
+  const int64_t b = sptr[u], e = sptr[u + 1];
+  for (int64_t j0 = 0; j0 < ncols; j0 += 32) {
+    const int64_t j = j0 + lane;
+    double acc = 0.0;
+    if (j < ncols)
+      for (int64_t t = b; t < e; ++t) acc = fma(val[t], B[(int64_t)idx[t] * ldb + j], acc);
+    if (j < ncols) part[u * ncols + j] = acc;
+  }
+}
+
+// balanced SpMV / SpMM over a split CSR (rows = number of CSR rows)
+inline void split_spmv(Ctx& c, const SplitCSR& sp, const int32_t* idx, const double* val, int64_t rows,
+                       const double* x, double alpha, double* out) {
+  if (rows <= 0) return;
+  DBuf<double> part(std::max<int64_t>(sp.S, 1), c.stream);
+  split_spmv_kernel<<<ceil_div(sp.S * 32, 256), 256, 0, c.stream>>>(sp.ptr.get(), idx, val, sp.S, x, part.get());
+  SKR_LAUNCHED(&c);
+  split_reduce_kernel<<<ceil_div(rows, 256), 256, 0, c.stream>>>(sp.first.get(), rows, part.get(), 1, alpha, out, 1);
+  SKR_LAUNCHED(&c);
+}
+
+inline void split_spmm(Ctx& c, const SplitCSR& sp, const int32_t* idx, const double* val, int64_t rows,
+                       const double* B, int64_t ldb, int64_t ncols, double alpha, double* out, int64_t ldo) {
+  if (rows <= 0 || ncols <= 0) return;
+  DBuf<double> part((size_t)std::max<int64_t>(sp.S, 1) * ncols, c.stream);
+  split_spmm_kernel<<<ceil_div(sp.S * 32, 256), 256, 0, c.stream>>>(sp.ptr.get(), idx, val, sp.S, B, ldb, ncols,
+                                                                    part.get());
+  SKR_LAUNCHED(&c);
+  split_reduce_kernel<<<ceil_div(rows * ncols, 256), 256, 0, c.stream>>>(sp.first.get(), rows, part.get(), ncols, alpha,
+                                                                         out, ldo);
+  SKR_LAUNCHED(&c);
+}
 
 }  // namespace skr
