@@ -202,7 +202,9 @@ struct ChainArgs {
   unsigned long long* prof;  // optional: per-phase cycle totals of CTA 0 / thread 0 (debug)
 };
 
-constexpr int kChainNB = 3;  // row-ring depth
+// row-ring depth: 4 for 1 KB row slices (blocks b, b+1 in use, two in flight), 3 when
+// the slices are 2 KB (shared memory)
+constexpr int chain_nb(int slice_doubles) { return slice_doubles <= 128 ? 4 : 3; }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -228,9 +230,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 
 template <class T, int CPT, int L, int MXB, int NT>
-__global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
-  constexpr int NCW = NT / 32;  // consumer warps; then row producer, M/X producer, signaller
-  constexpr int SW = NT * CPT, NB = kChainNB;
+__global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
+  // warps: NCW consumers | 2 delta warps | row producer | M/X producer | signaller
+  constexpr int NCW = NT / 32;
+  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4;
+  static_assert(2 * L <= 64, "the two delta warps hold the M and X rows");
+  constexpr int SW = NT * CPT, NB = chain_nb(NT * CPT);
   constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
   constexpr size_t ROWB = (size_t)SW * 8;  // bytes per row slot (fits an fp64 slice)
   extern __shared__ __align__(128) unsigned char sm[];
@@ -243,15 +248,16 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
   double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
   double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
   double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
-  double* dl = zbuf + L;                                                     // [L] delta_b
-  double* delta2 = dl + L;                                                   // [L]
-  uint64_t* full = reinterpret_cast<uint64_t*>(delta2 + L);                  // [NB]
+  double* dl = zbuf + L;                                                     // [2][L] delta_b (by parity)
+  double* delta2 = dl + 2 * L;                                               // [2][L]
+  uint64_t* full = reinterpret_cast<uint64_t*>(delta2 + 2 * L);              // [NB]
   uint64_t* empty = full + NB;                                               // [NB]
   uint64_t* ready = empty + NB;                                              // [4]
   uint64_t* mx_full = ready + 4;                                             // [MXB]
   uint64_t* mx_empty = mx_full + MXB;                                        // [MXB]
   uint64_t* pub = mx_empty + MXB;                                            // [2] local: partials pushed
-  uint64_t* dmask = pub + 2;                                                 // [NB] bit l: row l is a data row
+  uint64_t* dready = pub + 2;                                                // [2] local: delta_b published
+  uint64_t* dmask = dready + 2;                                              // [NB] bit l: row l is a data row
   double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [SW] current w slice
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -272,11 +278,13 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
     }
     mbar_init(&pub[0], NCW);
     mbar_init(&pub[1], NCW);
+    mbar_init(&dready[0], 1);
+    mbar_init(&dready[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // every CTA's barriers exist before any remote arrive
 
-  if (warp == NCW + 2) {
+  if (warp == WSIG) {
     // ---------------- signaller: once this CTA's partials of block j are pushed
     // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
     // release fence latency stays off the consumers' path.  pub is 2-deep: the
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
       mbar_wait(&pub[j & 1], (uint32_t)((j >> 1) & 1));
       if (lane < CS) mbar_arrive_remote(&ready[j & 3], (uint32_t)lane);
     }
-  } else if (warp == NCW + 1) {
+  } else if (warp == WMX) {
     // ---------------- M/X producer: M_b^T, X_b^T, p_b by bulk copy ----------------
     if (lane == 0) {
       for (int64_t b = 0; b < nblk; ++b) {
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
         bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
       }
     }
-  } else if (warp == NCW) {
+  } else if (warp == WROW) {
     // ---------------- row producer warp ----------------
     const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);  // may be <= 0 past ld
     // indices are loaded one block ahead (their L2 latency overlaps the copies)
@@ -365,9 +373,72 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
       atomicAdd(a.prof + 7, pw);
       atomicAdd(a.prof + 8, pi);
     }
+  } else if (warp == DW || warp == DW + 1) {
+    // ---------------- delta warps (64 threads): resolve block b while the consumers
+    // compute the look-ahead dots of block b+1 ----------------
+    const int j = tid - NT;  // 0..63
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int Lb = (int)min((int64_t)L, a.steps - b * L);
+      const int mslot = (int)(b % MXB);
+      const double* Ms = mx + mslot * MXW;
+      const double* Xs = Ms + L * L;
+      const double* ps = Ms + 2 * L * L;
+      mbar_wait(&mx_full[mslot], (uint32_t)((b / MXB) & 1));
+      // X term (threads L..2L-1): xterm_i = (X_b delta_{b-1})_i
+      if (j >= L && j < 2 * L && b > 0) {
+        const double* dp = dl + ((b - 1) & 1) * L;
+        const int i = j - L;
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; k += 4) {
+          x0 = fma(Xs[k * L + i], dp[k], x0);
+          x1 = fma(Xs[(k + 1) * L + i], dp[k + 1], x1);
+          x2 = fma(Xs[(k + 2) * L + i], dp[k + 2], x2);
+          x3 = fma(Xs[(k + 3) * L + i], dp[k + 3], x3);
+        }
+        xterm[i] = (x0 + x1) + (x2 + x3);
+      }
+      named_bar(2, 64);  // xterm visible
+      // a_b: the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
+      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
+      if (j < L) {
+        double part[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          part[q] = q >= CS ? 0.0
+                    : PUSH  ? apub[((b & 3) * 16 + q) * L + j]
+                            : cluster.map_shared_rank(apub, q)[(b & 3) * L + j];
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sum += part[q];
+        if (b > 0) sum -= a.eta * xterm[j];
+        zbuf[j] = sum - ps[j];
+      }
+      named_bar(2, 64);
+      // delta_b = M_b z (thread j < L: row j, four partial sums)
+      double* dcur = dl + (b & 1) * L;
+      double* d2 = delta2 + (b & 1) * L;
+      if (j < L) {
+        double d0 = 0.0, d1 = 0.0, d2v = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < L; k += 4) {
+          d0 = fma(Ms[k * L + j], zbuf[k], d0);
+          d1 = fma(Ms[(k + 1) * L + j], zbuf[k + 1], d1);
+          d2v = fma(Ms[(k + 2) * L + j], zbuf[k + 2], d2v);
+          d3 = fma(Ms[(k + 3) * L + j], zbuf[k + 3], d3);
+        }
+        const double dv = (d0 + d1) + (d2v + d3);
+        dcur[j] = dv;
+        d2[j] = (double)(Lb - j) * dv;  // (Lb - l + 1) weight, 1-based l
+      }
+      named_bar(2, 64);  // delta_b complete, zbuf / M / X reads done
+      if (j == 0) {
+        mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
+        mbar_arrive_local(&dready[b & 1]);   // delta_b visible to the consumers (release.cta)
+      }
+    }
   } else {
     // ---------------- consumer warps (128 threads) ----------------
-    static_assert(2 * L <= NT, "M and X rows are held by threads [0, 2L)");
     const int64_t col0 = slice0 + (int64_t)tid * CPT;
     bool act[CPT];
     double w[CPT], S[CPT], mu[CPT];
@@ -459,63 +530,12 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
       // 1. look-ahead partial dots of block b+1 with w_b, published to the cluster
       if (b + 1 < nblk) dots(b + 1);
       unsigned long long c1 = prof ? clock64() : 0;
-      // M_b, X_b, p_b staged by the M/X producer
-      const int mslot = (int)(b % MXB);
-      const double* Ms = mx + mslot * MXW;
-      const double* Xs = Ms + L * L;
-      const double* ps = Ms + 2 * L * L;
-      mbar_wait(&mx_full[mslot], (uint32_t)((b / MXB) & 1));
-      // X term (threads L..2L-1): xterm_i = (X_b delta_{b-1})_i
-      if (tid >= L && tid < 2 * L && b > 0) {
-        const double* dp = dl;  // delta_{b-1}: overwritten only after the next two barriers
-        const int i = tid - L;
-        double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-#pragma unroll
-        for (int k = 0; k < L; k += 4) {
-          x0 = fma(Xs[k * L + i], dp[k], x0);
-          x1 = fma(Xs[(k + 1) * L + i], dp[k + 1], x1);
-          x2 = fma(Xs[(k + 2) * L + i], dp[k + 2], x2);
-          x3 = fma(Xs[(k + 3) * L + i], dp[k + 3], x3);
-        }
-        xterm[i] = (x0 + x1) + (x2 + x3);
-      }
-      named_bar(1, NT);  // xterm visible
+      // delta_b from the delta warps (computed while this iteration's dots ran)
       unsigned long long c2 = prof ? clock64() : 0;
-      // 2. a_b: sum the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
-      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
-      unsigned long long c3 = prof ? clock64() : 0;
-      if (tid < L) {
-        double part[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          part[q] = q >= CS ? 0.0
-                    : PUSH  ? apub[((b & 3) * 16 + q) * L + tid]
-                            : cluster.map_shared_rank(apub, q)[(b & 3) * L + tid];
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) s += part[q];
-        if (b > 0) s -= a.eta * xterm[tid];
-        zbuf[tid] = s - ps[tid];
-      }
-      named_bar(1, NT);
-      unsigned long long c4 = prof ? clock64() : 0;
-      // delta_b = M_b z (thread tid < L: row tid, four partial sums)
-      double* dcur = dl;
-      if (tid < L) {
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int k = 0; k < L; k += 4) {
-          d0 = fma(Ms[k * L + tid], zbuf[k], d0);
-          d1 = fma(Ms[(k + 1) * L + tid], zbuf[k + 1], d1);
-          d2 = fma(Ms[(k + 2) * L + tid], zbuf[k + 2], d2);
-          d3 = fma(Ms[(k + 3) * L + tid], zbuf[k + 3], d3);
-        }
-        const double dv = (d0 + d1) + (d2 + d3);
-        dcur[tid] = dv;
-        delta2[tid] = (double)(Lb - tid) * dv;  // (Lb - l + 1) weight, 1-based l
-      }
-      named_bar(1, NT);
-      if (tid == 0) mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
+      mbar_wait(&dready[b & 1], (uint32_t)((b >> 1) & 1));
+      unsigned long long c3 = c2, c4 = c2;
+      const double* dcur = dl + (b & 1) * L;
+      const double* dd2 = delta2 + (b & 1) * L;
       unsigned long long c5 = prof ? clock64() : 0;
       // 3. w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
@@ -531,14 +551,14 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
         for (; l + 3 < Lb; l += 4) {
           const double x0 = elem(l, c), x1 = elem(l + 1, c), x2 = elem(l + 2, c), x3 = elem(l + 3, c);
           const double4 dd = *reinterpret_cast<const double4*>(dcur + l);
-          const double4 ee = *reinterpret_cast<const double4*>(delta2 + l);
+          const double4 ee = *reinterpret_cast<const double4*>(dd2 + l);
           u0 = fma(dd.x, x0, u0); u1 = fma(dd.y, x1, u1); u2 = fma(dd.z, x2, u2); u3 = fma(dd.w, x3, u3);
           v0 = fma(ee.x, x0, v0); v1 = fma(ee.y, x1, v1); v2 = fma(ee.z, x2, v2); v3 = fma(ee.w, x3, v3);
         }
         for (; l < Lb; ++l) {
           const double x = elem(l, c);
           u0 = fma(dcur[l], x, u0);
-          v0 = fma(delta2[l], x, v0);
+          v0 = fma(dd2[l], x, v0);
         }
         const double u = (u0 + u1) + (u2 + u3), v = (v0 + v1) + (v2 + v3);
         const double w0 = w[c];
@@ -546,7 +566,7 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
         w[c] = w0 - a.eta * u - a.eta * (double)Lb * mu[c];
         wsm[tid * CPT + c] = w[c];
       }
-      named_bar(1, NT);  // every consumer is done with rows[slot], zbuf, delta2; new w visible
+      named_bar(1, NT);  // every consumer is done with rows[slot]; new w visible
       if (tid == 0) mbar_arrive_local(&empty[slot]);
       if (prof) {
         const unsigned long long c6 = clock64();
@@ -572,9 +592,9 @@ __global__ void __launch_bounds__(NT + 96, 1) sstep_chain_kernel(ChainArgs a) {
 
 template <int CPT, int L, int MXB, int NT>
 constexpr size_t sstep_chain_smem() {
-  return (size_t)kChainNB * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
-         sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 3 * L) +
-         sizeof(uint64_t) * (3 * kChainNB + 4 + 2 * MXB + 2) + sizeof(double) * NT * CPT + 128;
+  return (size_t)chain_nb(NT * CPT) * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
+         sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 5 * L) +
+         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * NT * CPT + 128;
 }
 
 // w_avg = S / m ; zero padding.
