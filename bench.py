@@ -160,7 +160,8 @@ def run_ours(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # SKR_BENCH_DIST=1 runs the sharded (NCCL) path even at world 1 (a launch check)
+    if world > 1 or os.environ.get("SKR_BENCH_DIST") == "1":
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         nid = [sk.Context.nccl_unique_id() if rank == 0 else None]

@@ -151,7 +151,7 @@ void download_rows(Ctx& c, double* dst, const double* src, int64_t rows, int64_t
 void shard_layout(Ctx& c, int64_t n_local, int64_t* n_global, int64_t* row0,
                   std::vector<int64_t>* counts = nullptr) {
   std::vector<int64_t> all(c.world, n_local);
-  if (c.world > 1) {
+  if (c.dist) {
     DBuf<int64_t> send(1, c.stream), recv(c.world, c.stream);
     SKR_CUDA(cudaMemcpyAsync(send.get(), &n_local, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
     c.allgather_bytes(send.get(), recv.get(), sizeof(int64_t));
@@ -422,7 +422,7 @@ void fullgrad_sums(Ctx& c, int dtype, const void* X, int64_t ld, int64_t n, cons
   if (part_g.n < need_g) part_g.alloc(need_g, c.stream);
   if (part_loss.n < (size_t)plan.grid) part_loss.alloc(plan.grid, c.stream);
   if (sums.n < (size_t)ld + 1) sums.alloc(ld + 1, c.stream);
-  const bool direct = fin && c.world == 1;
+  const bool direct = fin && !c.dist;
   if (n > 0) {
     if (c.prof_on) c.prof_mark("fullgrad");
     DISPATCH_DTYPE(dtype, T, run_fullgrad_main<T>(c, ld, n, static_cast<const T*>(X), y, w, part_g.get(),
@@ -1345,11 +1345,12 @@ int skr_ctx_create_dist(int device, int rank, int world, const char id[128], skr
     ctx_init(x->c, device);
     x->c.rank = rank;
     x->c.world = world;
-    if (world > 1) {
-      ncclUniqueId uid;
-      std::memcpy(&uid, id, 128);
-      SKR_NCCL(nccl().CommInitRank(&x->c.comm, world, uid, rank));
-    }
+    // the distributed API always builds a communicator (world == 1 included: the
+    // whole sharded code path then runs on one GPU, collectives as NCCL copies)
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    SKR_NCCL(nccl().CommInitRank(&x->c.comm, world, uid, rank));
+    x->c.dist = true;
     *out = x.release();
   });
 }
@@ -2024,7 +2025,7 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     SKR_CUDA(cudaMemcpyAsync(&hsum, bsum.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     SKR_CUDA(cudaMemcpyAsync(&p->max_row_sq, rowmax.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     // all rows of X~ and y on every rank for the (sequential, replicated) inner loop
-    if (c.world == 1) {
+    if (!c.dist) {
       p->xt_all = p->xt->ptr;  // nullptr in Lazy mode
       p->y_all = p->y.get();
     } else {

@@ -124,6 +124,7 @@ struct DBuf {
 struct Ctx {
   int device = 0;
   int rank = 0, world = 1;
+  bool dist = false;  // created through the distributed API: collectives go through NCCL (even with world == 1)
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;                    // side stream for overlapped small kernels
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -156,13 +157,13 @@ struct Ctx {
 
   // Row-sharded collectives (no-ops on one GPU).  Sum of doubles in place.
   void allreduce_sum(double* buf, size_t count) {
-    if (world > 1 && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
+    if (dist && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, comm, stream));
   }
   void allreduce_max(double* buf, size_t count) {
-    if (world > 1 && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, comm, stream));
+    if (dist && count) SKR_NCCL(nccl().AllReduce(buf, buf, count, ncclDouble, ncclMax, comm, stream));
   }
   void allgather_bytes(const void* send, void* recv, size_t bytes_per_rank) {
-    if (world > 1) SKR_NCCL(nccl().AllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
+    if (dist) SKR_NCCL(nccl().AllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
   }
   void sync() { SKR_CUDA(cudaStreamSynchronize(stream)); }
 };

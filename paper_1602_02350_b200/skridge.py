@@ -83,7 +83,7 @@ class Context:
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         lib = _lib.load()
         h = vp()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # world == 1 with an id: the sharded path on one GPU
             if nccl_id is None or len(nccl_id) != 128:
                 raise ParameterError("distributed context needs the 128-byte NCCL id")
             _check(lib.skr_ctx_create_dist(device, rank, world, nccl_id, C.byref(h)))

@@ -581,3 +581,28 @@ def test_acceptance_exact_and_optimal_preconditioner_criteria_on_gpu():
         assert abs(sk.conditioned_condition_number(a, 1e-3, p) - d) <= 1e-6
     with pytest.raises(sk.ScaleGuardError):
         sk.build_optimal(sk.DataMatrix(np.zeros((4, 2001))), 1e-3)
+
+
+def test_distributed_code_path_on_one_gpu_matches(O):
+    """The sharded code path (NCCL communicator, allreduce of the Krylov partials,
+    Gram and gradient sums, allgather of X~ for the replicated inner loop,
+    distributed finalisation of the full gradient) run as a 1-rank NCCL job must
+    reproduce the single-GPU results — this exercises every NCCL call through
+    the dlopen'd library on the hardware available to this run."""
+    X, y, lam, k = small_problem(n=700, d=48, k=6)
+    n, d = X.shape
+    ctx1 = sk.Context(0, 0, 1, sk.Context.nccl_unique_id())
+    res = {}
+    for name, ctx in (("single", sk.default_context()), ("dist", ctx1)):
+        p = sk.RidgeProblem(sk.DataMatrix(X, ctx=ctx), y, lam)
+        sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(k, 0.5, 3, 3))
+        pg = sk.preconditioned_components(p, sk.build_sketched(sv, lam))
+        w = np.random.default_rng(1).standard_normal(d)
+        eta = configs.step_size(pg.max_row_sq())
+        tr = sk.svrg_solve(pg, sk.SvrgConfig(4, 2 * n, eta, 9), np.zeros(d)).trace
+        res[name] = (sv.singular_values, pg.betas(), pg.full_gradient(w), pg.objective(w),
+                     [r.objective for r in tr], sk.reference_minimum(p).minimum)
+    a, b = res["single"], res["dist"]
+    assert rel(a[0], b[0]) < 1e-14 and rel(a[1], b[1]) < 1e-14
+    assert rel(a[2], b[2]) < 1e-13 and abs(a[3] - b[3]) <= 1e-13 * abs(a[3])
+    assert rel(a[4], b[4]) < 1e-12 and abs(a[5] - b[5]) <= 1e-13 * abs(a[5])
