@@ -20,6 +20,8 @@
 #include "mt_jump.cuh"
 #include "sparse.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 using namespace skr;
 
 namespace {
@@ -459,6 +461,11 @@ void apply_inv_sqrt_dev(Ctx& c, const skr_problem* p, const double* v, double* p
 }
 
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
+__global__ void iota_kernel(int64_t* __restrict__ v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
 template <class T>
 struct EpiXtilde;
 __global__ void scale_cols_kernel(double* __restrict__ P, int64_t rows, int64_t k, const double* __restrict__ D,
@@ -932,9 +939,8 @@ void lazy_run_epoch(skr_problem* p, const double* snap, const double* mu, const 
   }
   DBuf<double> sbar(std::max<int64_t>(n, 1), c.stream), r(std::max<int64_t>(n, 1), c.stream),
       r2(std::max<int64_t>(n, 1), c.stream), half(ld, c.stream), xmu(std::max<int64_t>(n, 1), c.stream),
-      bg(kk + 1, c.stream), z0(kk + 1, c.stream), v(kk, c.stream), base(ld, c.stream), Sb(ld, c.stream),
-      scratch(kk + 1, c.stream);
-  // z0 = U^T wbar (+ wbar.wbar), v = (D - c) o z0, sbar_i = x~_i . wbar
+      bg(kk + 1, c.stream), z0(kk + 1, c.stream), v(kk, c.stream), base(ld, c.stream), scratch(kk + 1, c.stream);
+  // z0 = U^T wbar (+ wbar.wbar), bg = U^T mu, v = (D - c) o z0, sbar_i = x~_i . wbar, xmu = X mu
   proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, snap, z0.get());
   SKR_LAUNCHED(&c);
   proj_kernel<<<ceil_div((k + 1) * 32, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, mu, bg.get());
@@ -951,21 +957,58 @@ void lazy_run_epoch(skr_problem* p, const double* snap, const double* mu, const 
     csr_spmv(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, mu, 1.0, xmu.get());
   }
   apply_inv_sqrt_dev(c, p, snap, scratch.get(), half.get());  // (P^{-1/2} wbar)_j
+  // per-step metadata on all SMs
+  const int64_t N = p->n_global + d;
+  DBuf<LazyMeta> meta(std::max<int64_t>(m, 1), c.stream);
+  DBuf<double> dlog(std::max<int64_t>(m, 1), c.stream);
+  lazy_meta_kernel<<<ceil_div(m, 256), 256, 0, c.stream>>>(idx, m, n, S.rptr.get(), p->inv_nq.get(), sbar.get(),
+                                                            half.get(), xmu.get(), mu, meta.get());
+  SKR_LAUNCHED(&c);
+  // the chain
   SKR_CUDA(cudaMemcpyAsync(base.get(), snap, sizeof(double) * ld, cudaMemcpyDeviceToDevice, c.stream));
-  Sb.zero();
-  LazyEpochArgs a{S.rptr.get(), S.ridx.get(), S.rval.get(), n, d, ld, k, p->Pm.get(), p->lz_UT.get(), p->D.get(),
-                  p->c, p->data_coef, p->reg_coef, idx, p->inv_nq.get(), m, eta, sbar.get(), half.get(), xmu.get(),
-                  mu, bg.get(), z0.get(), snap, base.get(), Sb.get(), w_avg};
-  const size_t smem_in = lazy_epoch_smem(k, ld);
-  if (smem_in <= 200 * 1024) {  // the iterate's base vector lives in shared memory
-    SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_in));
-    lazy_epoch_kernel<true><<<1, kLazyThreads, smem_in, c.stream>>>(a);
+  LazyEpoch2Args a{S.ridx.get(), S.rval.get(), n, ld, k, p->Pm.get(), p->lz_UT.get(), p->D.get(), bg.get(), z0.get(),
+                   p->c, p->data_coef, p->reg_coef, eta, meta.get(), m, base.get(), dlog.get()};
+  const size_t smem_in = lazy_epoch2_smem(k, ld);
+  if (smem_in <= 200 * 1024) {
+    SKR_CUDA(cudaFuncSetAttribute(lazy_epoch2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_in));
+    lazy_epoch2_kernel<true><<<1, kLazyThreads, smem_in, c.stream>>>(a);
   } else {
-    const size_t smem = lazy_epoch_smem(k, 0);
+    const size_t smem = lazy_epoch2_smem(k, 0);
     if (smem > 48 * 1024)
-      SKR_CUDA(cudaFuncSetAttribute(lazy_epoch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    lazy_epoch_kernel<false><<<1, kLazyThreads, smem, c.stream>>>(a);
+      SKR_CUDA(cudaFuncSetAttribute(lazy_epoch2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lazy_epoch2_kernel<false><<<1, kLazyThreads, smem, c.stream>>>(a);
   }
+  SKR_LAUNCHED(&c);
+  // epoch average from the delta log: rows sorted stably by (row, step) -> Gamma
+  DBuf<int64_t> steps_in(std::max<int64_t>(m, 1), c.stream), rows_out(std::max<int64_t>(m, 1), c.stream),
+      steps_out(std::max<int64_t>(m, 1), c.stream);
+  iota_kernel<<<ceil_div(m, 256), 256, 0, c.stream>>>(steps_in.get(), m);
+  SKR_LAUNCHED(&c);
+  int end_bit = 1;
+  while (end_bit < 63 && (int64_t(1) << end_bit) <= N) ++end_bit;
+  size_t tmp_bytes = 0;
+  SKR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, idx, rows_out.get(), steps_in.get(), steps_out.get(),
+                                           (int)m, 0, end_bit, c.stream));
+  DBuf<unsigned char> tmp(std::max<size_t>(tmp_bytes, 1), c.stream);
+  SKR_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, idx, rows_out.get(), steps_in.get(), steps_out.get(),
+                                           (int)m, 0, end_bit, c.stream));
+  DBuf<double> gamma(N + ld, c.stream), g1(ld, c.stream), gP(kk, c.stream), gU(kk, c.stream);
+  gamma.zero();
+  g1.zero();
+  gP.zero();
+  gU.zero();
+  lazy_gamma_kernel<<<ceil_div(m, 256), 256, 0, c.stream>>>(rows_out.get(), steps_out.get(), m, dlog.get(), gamma.get());
+  SKR_LAUNCHED(&c);
+  split_spmv(c, S.fsplit, S.fidx.get(), S.fval.get(), d, gamma.get(), 1.0, g1.get());
+  if (k > 0) {
+    if (n > 0)
+      gemm<double, double, true, false>(&c, k, 1, n, p->Pm.get(), k, gamma.get(), 1, EpiStore{gP.get(), 1, 1.0, 0.0});
+    gemm<double, double, true, false>(&c, k, 1, d, p->lz_UT.get(), k, gamma.get() + p->n_global, 1,
+                                      EpiStore{gU.get(), 1, 1.0, 0.0});
+  }
+  lazy_average_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, g1.get(), gamma.get() + p->n_global, gP.get(),
+                                                               gU.get(), p->lz_UT.get(), p->D.get(), p->c, eta, d, ld,
+                                                               k, m, mu, w_avg);
   SKR_LAUNCHED(&c);
 }
 

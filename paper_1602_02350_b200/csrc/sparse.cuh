@@ -494,3 +494,201 @@ inline void split_spmm(Ctx& c, const SplitCSR& sp, const int32_t* idx, const dou
 }
 
 }  // namespace skr
+
+namespace skr {
+
+// ---- Lazy epoch v2: the chain only does what depends on the previous step.
+// Per-step metadata (row, 1/(N q), row extent, snapshot terms) is gathered on all
+// SMs first; the chain prefetches step t+1's metadata, row entries and projection
+// row into registers while step t runs; the running sums of the epoch average are
+// not accumulated in the chain at all — the chain logs delta_t, and afterwards
+// Gamma_i = sum_{t: i_t = i} (m - t) delta_t (rows sorted stably by (i, t)) gives
+//   sum_t base_t = m wbar - eta c (X^T Gamma_data + Gamma_reg),
+//   sum_t h_t    = -eta (D - c) o (P^T Gamma_data + U_rows^T Gamma_reg).
+struct LazyMeta {
+  int64_t i, b, e;   // component, row extent (data rows)
+  double q, sbar, xm;  // inv_nq, snapshot inner (or (P^{-1/2} wbar)_j), x_i . mu (or mu_j)
+};
+
+__global__ void lazy_meta_kernel(const int64_t* __restrict__ idx, int64_t m, int64_t n,
+                                 const int64_t* __restrict__ rptr, const double* __restrict__ inv_nq,
+                                 const double* __restrict__ s_bar, const double* __restrict__ half,
+                                 const double* __restrict__ xmu, const double* __restrict__ mu,
+                                 LazyMeta* __restrict__ meta) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const int64_t i = idx[t];
+  LazyMeta mt;
+  mt.i = i;
+  mt.q = inv_nq[i];
+  if (i < n) {
+    mt.b = rptr[i];
+    mt.e = rptr[i + 1];
+    mt.sbar = s_bar[i];
+    mt.xm = xmu[i];
+  } else {
+    mt.b = mt.e = 0;
+    mt.sbar = half[i - n];
+    mt.xm = mu[i - n];
+  }
+  meta[t] = mt;
+}
+
+struct LazyEpoch2Args {
+  const int32_t* ridx;
+  const double* rval;
+  int64_t n, ld, k;
+  const double* P;       // n x k
+  const double* UT;      // d x k
+  const double* D;       // k
+  const double* bg;      // k: U^T mu
+  const double* z0;      // k: U^T wbar
+  double c, data_coef, reg_coef, eta;
+  const LazyMeta* meta;  // m
+  int64_t m;
+  double* base;          // ld: wbar in, final base out (global when not in shared memory)
+  double* dlog;          // m: delta_t
+};
+
+template <bool SMEM_BASE>
+__global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch2_kernel(LazyEpoch2Args a) {
+  extern __shared__ double lz2_sm[];
+  const int64_t k = a.k;
+  double* h = lz2_sm;      // k
+  double* z = h + k;       // k
+  double* Dm = z + k;      // k
+  double* Dd = Dm + k;     // k
+  double* bg = Dd + k;     // k
+  double* red = bg + k;    // 3 x 8
+  double* base = SMEM_BASE ? red + 24 : a.base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (SMEM_BASE)
+    for (int64_t f = tid; f < a.ld; f += kLazyThreads) base[f] = a.base[f];
+  for (int64_t l = tid; l < k; l += kLazyThreads) {
+    h[l] = 0.0;
+    z[l] = a.z0[l];
+    Dm[l] = a.D[l] - a.c;
+    Dd[l] = a.D[l];
+    bg[l] = a.bg[l];
+  }
+  __syncthreads();
+  // registers for the current step (cur) and the prefetched next one (nx)
+  auto load_step = [&](int64_t t, LazyMeta& mt, int32_t& f, double& v, double& r) {
+    mt = a.meta[t];
+    f = 0;
+    v = 0.0;
+    if (mt.i < a.n && mt.b + tid < mt.e) {
+      f = a.ridx[mt.b + tid];
+      v = a.rval[mt.b + tid];
+    }
+    const double* row = mt.i < a.n ? a.P + mt.i * k : a.UT + (mt.i - a.n) * k;
+    r = tid < k ? row[tid] : 0.0;
+  };
+  LazyMeta cm, nm;
+  int32_t cf = 0, nf = 0;
+  double cv = 0.0, cr = 0.0, nv = 0.0, nr = 0.0;
+  if (a.m > 0) load_step(0, cm, cf, cv, cr);
+  for (int64_t t = 0; t < a.m; ++t) {
+    if (t + 1 < a.m) load_step(t + 1, nm, nf, nv, nr);  // in flight during step t
+    const bool data = cm.i < a.n;
+    const double* row = data ? a.P + cm.i * k : a.UT + (cm.i - a.n) * k;
+    double A = 0.0, B = 0.0, Cz = 0.0;
+    if (data) {
+      if (cm.b + tid < cm.e) A = cv * base[cf];
+      for (int64_t e = cm.b + tid + kLazyThreads; e < cm.e; e += kLazyThreads) A = fma(a.rval[e], base[a.ridx[e]], A);
+    } else if (tid == 0) {
+      A = base[cm.i - a.n];
+    }
+    if (tid < k) {
+      B = cr * h[tid];
+      Cz = Dm[tid] * cr * z[tid];
+    }
+    for (int64_t l = tid + kLazyThreads; l < k; l += kLazyThreads) {
+      const double rl = row[l];
+      B = fma(rl, h[l], B);
+      Cz = fma(Dm[l] * rl, z[l], Cz);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      A += __shfl_xor_sync(0xffffffffu, A, off);
+      B += __shfl_xor_sync(0xffffffffu, B, off);
+      Cz += __shfl_xor_sync(0xffffffffu, Cz, off);
+    }
+    if (lane == 0) {
+      red[warp] = A;
+      red[8 + warp] = B;
+      red[16 + warp] = Cz;
+    }
+    __syncthreads();
+    A = B = Cz = 0.0;
+#pragma unroll
+    for (int q = 0; q < kLazyThreads / 32; ++q) {
+      A += red[q];
+      B += red[8 + q];
+      Cz += red[16 + q];
+    }
+    const double tau = a.eta * (double)t;
+    const double inner = a.c * (A + B - tau * cm.xm) + Cz;
+    const double delta = (data ? a.data_coef : a.reg_coef) * (inner - cm.sbar) * cm.q;
+    const double ed = a.eta * delta;
+    if (data) {
+      if (cm.b + tid < cm.e) base[cf] -= ed * a.c * cv;
+      for (int64_t e = cm.b + tid + kLazyThreads; e < cm.e; e += kLazyThreads) base[a.ridx[e]] -= ed * a.c * a.rval[e];
+    } else if (tid == 0) {
+      base[cm.i - a.n] -= ed * a.c;
+    }
+    if (tid < k) {
+      h[tid] -= ed * Dm[tid] * cr;
+      z[tid] -= a.eta * fma(delta, Dd[tid] * cr, bg[tid]);
+    }
+    for (int64_t l = tid + kLazyThreads; l < k; l += kLazyThreads) {
+      const double rl = row[l];
+      h[l] -= ed * Dm[l] * rl;
+      z[l] -= a.eta * fma(delta, Dd[l] * rl, bg[l]);
+    }
+    if (tid == 0) a.dlog[t] = delta;
+    __syncthreads();
+    cm = nm;
+    cf = nf;
+    cv = nv;
+    cr = nr;
+  }
+  if (SMEM_BASE)
+    for (int64_t f = tid; f < a.ld; f += kLazyThreads) a.base[f] = base[f];
+}
+
+inline size_t lazy_epoch2_smem(int64_t k, int64_t ld_base) {
+  return sizeof(double) * (5 * std::max<int64_t>(k, 1) + 24 + ld_base);
+}
+
+// gamma over rows sorted by (row, step): Gamma[row] = sum (m - t) delta_t in step order
+__global__ void lazy_gamma_kernel(const int64_t* __restrict__ rows, const int64_t* __restrict__ steps, int64_t m,
+                                  const double* __restrict__ dlog, double* __restrict__ gamma) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= m || (p > 0 && rows[p] == rows[p - 1])) return;
+  double s = 0.0;
+  for (int64_t u = p; u < m && rows[u] == rows[p]; ++u) s = fma((double)(m - steps[u]), dlog[steps[u]], s);
+  gamma[rows[p]] = s;
+}
+
+// w_avg_f = wbar_f + (-eta c (g1_f + Gamma_reg_f)) / m + sum_l U_lf Sh_l / m - eta (m+1)/2 mu_f,
+// Sh_l = -eta (D_l - c) (gP_l + gU_l)
+__global__ void lazy_average_kernel(const double* __restrict__ snap, const double* __restrict__ g1,
+                                    const double* __restrict__ gamma_reg, const double* __restrict__ gP,
+                                    const double* __restrict__ gU, const double* __restrict__ UT,
+                                    const double* __restrict__ D, double c, double eta, int64_t d, int64_t ld,
+                                    int64_t k, int64_t m, const double* __restrict__ mu, double* __restrict__ w_avg) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= ld) return;
+  if (f >= d) {
+    w_avg[f] = 0.0;
+    return;
+  }
+  const double inv_m = 1.0 / (double)m;
+  double lift = 0.0;
+  for (int64_t l = 0; l < k; ++l) lift = fma(UT[f * k + l], -eta * (D[l] - c) * (gP[l] + gU[l]), lift);
+  const double sb = -eta * c * (g1[f] + gamma_reg[f]);
+  w_avg[f] = snap[f] + sb * inv_m + lift * inv_m - 0.5 * eta * (double)(m + 1) * mu[f];
+}
+
+}  // namespace skr
