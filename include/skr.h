@@ -189,6 +189,9 @@ int skr_mt_uniforms(skr_ctx* ctx, uint64_t seed, int64_t count, double* out);
 /* tcgen05 3xTF32 GEMM check: C (M x N fp64) = A (M x K fp32) . B (N x K fp32)^T (test hook) */
 int skr_tc_gemm_test(skr_ctx* ctx, const float* A, const float* B, int64_t M, int64_t N, int64_t K, int splits,
                      double* C);
+/* same with A given as its K x M row-major transpose (MN-major operand, the X^T products) (test hook) */
+int skr_tc_gemm_mn_test(skr_ctx* ctx, const float* At, const float* B, int64_t M, int64_t N, int64_t K, int splits,
+                        double* C);
 /* gaussian_matrix(rows, cols, seed) on the device, column-major (random.cpp:28-41) */
 int skr_gaussian_matrix(skr_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out);
 

@@ -78,6 +78,7 @@ SIGNATURES = {
     "skr_index_stream": (cint, [vp, u64, i64, lptr]),
     "skr_mt_uniforms": (cint, [vp, u64, i64, dptr]),
     "skr_tc_gemm_test": (cint, [vp, vp, vp, i64, i64, i64, cint, dptr]),
+    "skr_tc_gemm_mn_test": (cint, [vp, vp, vp, i64, i64, i64, cint, dptr]),
     "skr_gaussian_matrix": (cint, [vp, i64, i64, u64, dptr]),
     "skr_ridge_objective": (cint, [vp, vp, dptr, f64, dptr, P(f64)]),
     "skr_reference_minimum": (cint, [vp, vp, dptr, f64, dptr, P(f64)]),

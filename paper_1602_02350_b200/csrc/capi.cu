@@ -757,57 +757,85 @@ EncodeTiledFn encode_tiled() {
 
 // 2-D fp32 tensor map over a row-major matrix (rows x cols, row stride ld
 // elements), box = box_rows x 32 columns, 128-byte swizzle.
-CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
-                                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise(SKR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return m;
 }
 
-template <int BN>
-void tc_gemm_launch(Ctx& c, const float* A, int64_t lda, const float* B, int64_t ldb, const TcGemmArgs& g,
-                    int splits) {
-  const CUtensorMap ma = make_tmap_f32(A, g.M, g.K, lda, TC_BM);
-  const CUtensorMap mb = make_tmap_f32(B, g.N, g.K, ldb, BN);
+template <bool A_MN, int BN>
+void tc_launch(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,
+               int splits) {
+  const CUtensorMap mbh = make_tmap_f32(Bh, g.N, g.K, ldb, BN);
+  const CUtensorMap mbl = make_tmap_f32(Bl, g.N, g.K, ldb, BN);
   constexpr size_t smem = tc_gemm_smem<BN>();
   static bool configured = false;
   if (!configured) {
-    SKR_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SKR_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel<A_MN, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     configured = true;
   }
   dim3 grid(ceil_div(g.M, TC_BM), ceil_div(g.N, BN), splits);
-  tc_gemm_tf32x3_kernel<BN><<<grid, TC_THREADS, smem, c.stream>>>(ma, mb, g);
+  tc_gemm_tf32x3_kernel<A_MN, BN><<<grid, TC_THREADS, smem, c.stream>>>(ma, mbh, mbl, g);
   SKR_LAUNCHED(&c);
 }
 
-// C (fp64, M x N, ldc) = alpha * A . B^T   (A: M x K, B: N x K, fp32, K-major)
-// via 3xTF32 tcgen05 with split-K partials summed in fp64 in split order.
-void tc_gemm_abt(Ctx& c, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                 double alpha, double* C, int64_t ldc, int splits = 0) {
+inline int tc_bn(int64_t N) { return N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+
+// A: M x K K-major (lda), or (a_mn) the K x M row-major matrix read as its transpose;
+// B: N x K K-major as hi (Bh) + tf32 residual (Bl) arrays (ldb)
+template <bool A_MN>
+void tc_run(Ctx& c, const float* A, int64_t lda, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,
+            int splits) {
+  const CUtensorMap ma = A_MN ? make_tmap_f32(A, g.K, g.M, lda, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+                              : make_tmap_f32(A, g.M, g.K, lda, TC_BM);
+  const int bn = tc_bn(g.N);
+  if (bn == 64) tc_launch<A_MN, 64>(c, ma, Bh, Bl, ldb, g, splits);
+  else if (bn == 128) tc_launch<A_MN, 128>(c, ma, Bh, Bl, ldb, g, splits);
+  else tc_launch<A_MN, 256>(c, ma, Bh, Bl, ldb, g, splits);
+}
+
+// out[n * ldo + m] = alpha * sum_k A[m, k] B[n, k]  (i.e. C^T, fp64) via 3xTF32 tcgen05 with
+// split-K fp64 partials summed in split order (deterministic)
+void tc_gemm_t(Ctx& c, bool a_mn, const float* A, int64_t lda, const float* Bh, const float* Bl, int64_t ldb,
+               int64_t M, int64_t N, int64_t K, double alpha, double* out, int64_t ldo, int splits = 0) {
   if (M <= 0 || N <= 0) return;
-  const int bn = N <= 64 ? 64 : N <= 128 ? 128 : 256;
-  const int64_t tiles = (int64_t)ceil_div(M, TC_BM) * ceil_div(N, bn);
-  if (splits <= 0) {
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c.sm_count + tiles - 1) / tiles,
-                                                        std::max<int64_t>(1, K / (8 * TC_BK))));
-  }
+  const int64_t tiles = (int64_t)ceil_div(M, TC_BM) * ceil_div(N, tc_bn(N));
+  if (splits <= 0)
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>(c.sm_count / tiles, std::max<int64_t>(1, K / (8 * TC_BK))));
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + TC_BK - 1) / TC_BK * TC_BK;
-  splits = (int)((K + kchunk - 1) / kchunk);
+  splits = (int)std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
   DBuf<double> part((size_t)splits * M * N, c.stream);
-  TcGemmArgs g{M, N, K, kchunk, alpha, 0, part.get(), nullptr, 0};
-  if (bn == 64) tc_gemm_launch<64>(c, A, lda, B, ldb, g, splits);
-  else if (bn == 128) tc_gemm_launch<128>(c, A, lda, B, ldb, g, splits);
-  else tc_gemm_launch<256>(c, A, lda, B, ldb, g, splits);
-  EpiStore epi{C, ldc, 1.0, 0.0};
+  TcGemmArgs g{M, N, K, kchunk, alpha, 0, part.get(), nullptr, nullptr, 0};
+  if (a_mn) tc_run<true>(c, A, lda, Bh, Bl, ldb, g, splits);
+  else tc_run<false>(c, A, lda, Bh, Bl, ldb, g, splits);
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), 4LL * c.sm_count);
-  splitk_reduce_kernel<EpiStore><<<blocks, 256, 0, c.stream>>>(part.get(), M, N, splits, epi);
+  tc_splitk_reduce_kernel<<<blocks, 256, 0, c.stream>>>(part.get(), M, N, splits, out, ldo);
+  SKR_LAUNCHED(&c);
+}
+
+// out32[n * ldt + m] (+ tf32 residual into out32lo) = alpha * sum_k A[m, k] B[n, k], A = M x K K-major
+void tc_gemm_rows(Ctx& c, const float* A, int64_t lda, const float* Bh, const float* Bl, int64_t ldb, int64_t M,
+                  int64_t N, int64_t K, double alpha, float* out32, float* out32lo, int64_t ldt) {
+  if (M <= 0 || N <= 0) return;
+  TcGemmArgs g{M, N, K, (K + TC_BK - 1) / TC_BK * TC_BK, alpha, 1, nullptr, out32, out32lo, ldt};
+  tc_run<false>(c, A, lda, Bh, Bl, ldb, g, 1);
+}
+
+void f64_to_tf32x2(Ctx& c, const double* src, int64_t lds, int64_t rows, int64_t cols, float* hi, float* lo,
+                   int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return;
+  f64_to_tf32x2_kernel<<<std::min<unsigned>(ceil_div(rows * cols, 256), 8u * 148u * 4u), 256, 0, c.stream>>>(
+      src, lds, rows, cols, hi, lo, ldd);
   SKR_LAUNCHED(&c);
 }
 
@@ -1276,31 +1304,7 @@ __global__ void synth_labels_kernel(const T* __restrict__ X, int64_t ld, int64_t
 }
 
 // Xt[j][i] = X[i][j]  (fp32, 32x32 shared-memory tiles; rows on grid.x)
-__global__ void transpose_f32_kernel(const float* __restrict__ X, int64_t n, int64_t d, int64_t ld,
-                                     float* __restrict__ Xt, int64_t ldt) {
-  __shared__ float tile[32][33];
-  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int64_t i = i0 + r, j = j0 + threadIdx.x;
-    tile[r][threadIdx.x] = (i < n && j < d) ? X[i * ld + j] : 0.f;
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int64_t j = j0 + r, i = i0 + threadIdx.x;
-    if (j < d && i < n) Xt[j * ldt + i] = tile[threadIdx.x][r];
-  }
-}
-
 // dst[r][c] = float(src[r][c]) for r < rows, c < cols; zero for cols <= c < ldd
-__global__ void convert_f64_f32_kernel(const double* __restrict__ src, int64_t lds, int64_t rows, int64_t cols,
-                                       float* __restrict__ dst, int64_t ldd) {
-  const int64_t total = rows * ldd;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / ldd, c = e % ldd;
-    dst[e] = c < cols ? (float)src[r * lds + c] : 0.f;
-  }
-}
-
 }  // namespace
 
 // ===========================================================================
@@ -1739,20 +1743,23 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     Qt.zero();
     int Wb = 0;
     // fp32 storage: every product runs on the tensor cores (tcgen05, 3xTF32, fp64
-    // split-K sums) with X^T materialised so all operands are K-major.
+    // split-K sums). X is read in place in both orientations (MN-major A for the
+    // X^T products); Z^T = (scale X Q^T)^T is kept per appended block as fp32 hi +
+    // tf32 residual, so it feeds the next X^T product and is reused by the
+    // Rayleigh-Ritz Gram instead of being recomputed.
     const bool tc = !S.sparse && S.dtype == SKR_F32 && n > 0 && !getenv("SKR_LANCZOS_SIMT");
     const int64_t np = (std::max<int64_t>(n, 1) + 3) / 4 * 4;  // 16-byte row stride over the points
-    DBuf<float> Xt, P32, Rt32;
+    const float* X32 = static_cast<const float*>(S.ptr);
+    DBuf<float> Zh, Zl, Ph, Pl, Qh, Ql;
+    int64_t zdone = 0;  // basis rows whose Z^T rows exist
     if (tc) {
-      Xt.alloc((size_t)d * np, c.stream);
-      transpose_f32_kernel<<<dim3(ceil_div(n, 32), ceil_div(d, 32)), dim3(32, 8), 0, c.stream>>>(
-          static_cast<const float*>(S.ptr), n, d, ld, Xt.get(), np);
-      SKR_LAUNCHED(&c);
-      Rt32.alloc((size_t)k * np, c.stream);  // Pi^T, then T^T = (X prev^T)^T per iteration
-      convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(k * np, 256), 65535u), 256, 0, c.stream>>>(
-          Pt.get(), n, k, n, Rt32.get(), np);
-      SKR_LAUNCHED(&c);
-      P32.alloc((size_t)k * ld, c.stream);
+      Zh.alloc((size_t)cap * np, c.stream);
+      Zl.alloc((size_t)cap * np, c.stream);
+      Ph.alloc((size_t)k * np, c.stream);
+      Pl.alloc((size_t)k * np, c.stream);
+      f64_to_tf32x2(c, Pt.get(), n, k, n, Ph.get(), Pl.get(), np);
+      Qh.alloc((size_t)k * ld, c.stream);
+      Ql.alloc((size_t)k * ld, c.stream);
     }
     // "lanczos_gemm" marks bracket the Krylov / Rayleigh-Ritz products only (bench: GEMM TFLOP/s)
     auto gmark = [&] {
@@ -1768,7 +1775,10 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       split_spmm(c, S.fsplit, S.fidx.get(), S.fval.get(), d, Pn.get(), k, k, scale, tmp.get(), k);
       transpose_f64(c, tmp.get(), d, k, k, Vt.get(), ld);
     } else if (tc) {
-      tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, k, d, n, scale, Vt.get(), ld);
+      // Vt (k x ld) = scale (X^T Pi)^T
+      tc_gemm_t(c, true, X32, ld, Ph.get(), Pl.get(), np, d, k, n, scale, Vt.get(), ld);
+      Ph.release();
+      Pl.release();
     } else {
       DISPATCH_DTYPE(S.dtype, T, {
         const T* X = static_cast<const T*>(S.ptr);
@@ -1796,16 +1806,15 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
         Vt.zero();
         transpose_f64(c, tmpK.get(), d, appended, appended, Vt.get(), ld);
       } else if (tc) {
-        // T^T (a x n, fp32) = scale (X prev^T)^T ;  block^T = scale T^T X = scale T^T . (X^T)^T
-        convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(appended * ld, 256), 65535u), 256, 0, c.stream>>>(
-            prev, ld, appended, d, P32.get(), ld);
-        SKR_LAUNCHED(&c);
-        TcGemmArgs g{n, appended, d, (d + TC_BK - 1) / TC_BK * TC_BK, scale, 1, nullptr, Rt32.get(), np};
-        if (appended <= 64) tc_gemm_launch<64>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
-        else if (appended <= 128) tc_gemm_launch<128>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
-        else tc_gemm_launch<256>(c, static_cast<const float*>(S.ptr), ld, P32.get(), ld, g, 1);
+        // Z^T rows of this block (a x n, fp32 hi + residual) = scale (X prev^T)^T;
+        // block^T = scale (X^T Z)^T with X read MN-major
+        f64_to_tf32x2(c, prev, ld, appended, d, Qh.get(), Ql.get(), ld);
+        float* zh = Zh.get() + (W - appended) * np;
+        float* zl = Zl.get() + (W - appended) * np;
+        tc_gemm_rows(c, X32, ld, Qh.get(), Ql.get(), ld, n, appended, d, scale, zh, zl, np);
+        zdone = W;
         Vt.zero();
-        tc_gemm_abt(c, Rt32.get(), np, Xt.get(), np, appended, d, n, scale, Vt.get(), ld);
+        tc_gemm_t(c, true, X32, ld, zh, zl, np, d, appended, n, scale, Vt.get(), ld);
       } else {
         DISPATCH_DTYPE(S.dtype, T, {
           const T* X = static_cast<const T*>(S.ptr);
@@ -1820,8 +1829,6 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), appended);
     }
     Tm.release();
-    Rt32.release();
-    P32.release();
     const int64_t W = Wb;
     const int64_t kk = std::min<int64_t>(k, W);
     // Rayleigh-Ritz: G = (X Q)^T (X Q) scale^2 over row chunks (sketch.cpp:59-61)
@@ -1840,19 +1847,17 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
         gemm<double, double, true, false>(&c, W, W, rows, Z.get(), W, Z.get(), W, EpiStore{G.get(), W, 1.0, 1.0});
       }
     } else if (tc) {
-      DBuf<float> Q32((size_t)W * ld, c.stream), Zt((size_t)W * np, c.stream);
-      convert_f64_f32_kernel<<<std::min<unsigned>(ceil_div(W * ld, 256), 65535u), 256, 0, c.stream>>>(
-          Qt.get(), ld, W, d, Q32.get(), ld);
-      SKR_LAUNCHED(&c);
-      for (int64_t w0 = 0; w0 < W; w0 += 256) {  // Z^T rows in slabs of <= 256 basis vectors
-        const int64_t wn = std::min<int64_t>(256, W - w0);
-        TcGemmArgs g{n, wn, d, (d + TC_BK - 1) / TC_BK * TC_BK, scale, 1, nullptr, Zt.get() + w0 * np, np};
-        if (wn <= 64) tc_gemm_launch<64>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
-        else if (wn <= 128) tc_gemm_launch<128>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
-        else tc_gemm_launch<256>(c, static_cast<const float*>(S.ptr), ld, Q32.get() + w0 * ld, ld, g, 1);
+      // only the last block's Z rows are new (the earlier ones fed the Krylov products)
+      for (int64_t w0 = zdone; w0 < W; w0 += k) {
+        const int64_t wn = std::min<int64_t>(k, W - w0);
+        f64_to_tf32x2(c, Qt.get() + w0 * ld, ld, wn, d, Qh.get(), Ql.get(), ld);
+        tc_gemm_rows(c, X32, ld, Qh.get(), Ql.get(), ld, n, wn, d, scale, Zh.get() + w0 * np, Zl.get() + w0 * np, np);
       }
-      Xt.release();
-      tc_gemm_abt(c, Zt.get(), np, Zt.get(), np, W, W, n, 1.0, G.get(), W);
+      Qh.release();
+      Ql.release();
+      tc_gemm_t(c, false, Zh.get(), np, Zh.get(), Zl.get(), np, W, W, n, 1.0, G.get(), W);
+      Zh.release();
+      Zl.release();
     } else {
       const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
       DBuf<double> Z((size_t)chunk * W, c.stream);
@@ -2438,21 +2443,38 @@ int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out)
   });
 }
 
+// C (M x N, fp64 row-major) = A . B^T on the tensor-core path; a_mn: A is given as
+// its K x M row-major transpose (the data-matrix orientation of the X^T products)
+static void tc_gemm_test_impl(skr_ctx* ctx, const float* A, const float* B, int64_t M, int64_t N, int64_t K,
+                              int splits, int a_mn, double* C) {
+  Ctx& c = C_(ctx);
+  const int64_t ldk = (K + 3) / 4 * 4, ldm = (M + 3) / 4 * 4;  // 16-byte row strides for TMA
+  DBuf<float> dA((size_t)(a_mn ? K * ldm : M * ldk), c.stream), dB((size_t)N * ldk, c.stream),
+      dBl((size_t)N * ldk, c.stream);
+  DBuf<double> dCt((size_t)M * N, c.stream);
+  dA.zero();
+  dB.zero();
+  if (a_mn) SKR_CUDA(cudaMemcpy2DAsync(dA.get(), ldm * 4, A, M * 4, M * 4, K, cudaMemcpyHostToDevice, c.stream));
+  else SKR_CUDA(cudaMemcpy2DAsync(dA.get(), ldk * 4, A, K * 4, K * 4, M, cudaMemcpyHostToDevice, c.stream));
+  SKR_CUDA(cudaMemcpy2DAsync(dB.get(), ldk * 4, B, K * 4, K * 4, N, cudaMemcpyHostToDevice, c.stream));
+  tf32_lo_kernel<<<256, 256, 0, c.stream>>>(dB.get(), ldk, N, ldk, dBl.get(), ldk);
+  SKR_LAUNCHED(&c);
+  tc_gemm_t(c, a_mn != 0, dA.get(), a_mn ? ldm : ldk, dB.get(), dBl.get(), ldk, M, N, K, 1.0, dCt.get(), M, splits);
+  std::vector<double> h((size_t)M * N);
+  SKR_CUDA(cudaMemcpyAsync(h.data(), dCt.get(), sizeof(double) * M * N, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  for (int64_t m = 0; m < M; ++m)
+    for (int64_t j = 0; j < N; ++j) C[m * N + j] = h[j * M + m];
+}
+
 int skr_tc_gemm_test(skr_ctx* ctx, const float* A, const float* B, int64_t M, int64_t N, int64_t K, int splits,
                      double* C) {
-  return guard([&] {
-    Ctx& c = C_(ctx);
-    const int64_t ldk = (K + 3) / 4 * 4;  // 16-byte row stride for TMA
-    DBuf<float> dA((size_t)M * ldk, c.stream), dB((size_t)N * ldk, c.stream);
-    DBuf<double> dC((size_t)M * N, c.stream);
-    dA.zero();
-    dB.zero();
-    SKR_CUDA(cudaMemcpy2DAsync(dA.get(), ldk * 4, A, K * 4, K * 4, M, cudaMemcpyHostToDevice, c.stream));
-    SKR_CUDA(cudaMemcpy2DAsync(dB.get(), ldk * 4, B, K * 4, K * 4, N, cudaMemcpyHostToDevice, c.stream));
-    tc_gemm_abt(c, dA.get(), ldk, dB.get(), ldk, M, N, K, 1.0, dC.get(), N, splits);
-    SKR_CUDA(cudaMemcpyAsync(C, dC.get(), sizeof(double) * M * N, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-  });
+  return guard([&] { tc_gemm_test_impl(ctx, A, B, M, N, K, splits, 0, C); });
+}
+
+int skr_tc_gemm_mn_test(skr_ctx* ctx, const float* At, const float* B, int64_t M, int64_t N, int64_t K, int splits,
+                        double* C) {
+  return guard([&] { tc_gemm_test_impl(ctx, At, B, M, N, K, splits, 1, C); });
 }
 
 int skr_mt_uniforms(skr_ctx* ctx, uint64_t seed, int64_t count, double* out) {

@@ -572,9 +572,10 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch2_kernel(LazyEpoch2
     bg[l] = a.bg[l];
   }
   __syncthreads();
-  // registers for the current step (cur) and the prefetched next one (nx)
-  auto load_step = [&](int64_t t, LazyMeta& mt, int32_t& f, double& v, double& r) {
-    mt = a.meta[t];
+  // registers: the current step (c*), the next one (n*, its row entries in flight
+  // during step t) and the metadata two steps ahead (mm, in flight during step t) —
+  // every global load has a whole step to land before anything waits on it
+  auto load_row = [&](const LazyMeta& mt, int32_t& f, double& v, double& r) {
     f = 0;
     v = 0.0;
     if (mt.i < a.n && mt.b + tid < mt.e) {
@@ -584,12 +585,17 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch2_kernel(LazyEpoch2
     const double* row = mt.i < a.n ? a.P + mt.i * k : a.UT + (mt.i - a.n) * k;
     r = tid < k ? row[tid] : 0.0;
   };
-  LazyMeta cm, nm;
+  LazyMeta cm, nm, mm;
   int32_t cf = 0, nf = 0;
   double cv = 0.0, cr = 0.0, nv = 0.0, nr = 0.0;
-  if (a.m > 0) load_step(0, cm, cf, cv, cr);
+  if (a.m > 0) {
+    cm = a.meta[0];
+    load_row(cm, cf, cv, cr);
+  }
+  if (a.m > 1) nm = a.meta[1];
   for (int64_t t = 0; t < a.m; ++t) {
-    if (t + 1 < a.m) load_step(t + 1, nm, nf, nv, nr);  // in flight during step t
+    if (t + 2 < a.m) mm = a.meta[t + 2];
+    if (t + 1 < a.m) load_row(nm, nf, nv, nr);
     const bool data = cm.i < a.n;
     const double* row = data ? a.P + cm.i * k : a.UT + (cm.i - a.n) * k;
     double A = 0.0, B = 0.0, Cz = 0.0;
@@ -652,6 +658,7 @@ __global__ void __launch_bounds__(kLazyThreads, 1) lazy_epoch2_kernel(LazyEpoch2
     cf = nf;
     cv = nv;
     cr = nr;
+    nm = mm;
   }
   if (SMEM_BASE)
     for (int64_t f = tid; f < a.ld; f += kLazyThreads) a.base[f] = base[f];

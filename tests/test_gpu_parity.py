@@ -355,6 +355,23 @@ def test_tc_gemm_3xtf32(M, N, K, splits):
     assert err < 3e-5, err  # fp32 accumulation in TMEM over K (SURVEY: fp32-class, 1e-3 Ritz gate)
 
 
+@pytest.mark.parametrize("M,N,K,splits", [(128, 64, 32, 1), (256, 64, 1000, 1), (1024, 128, 4096, 4),
+                                          (384, 200, 777, 3), (2048, 256, 8192, 0), (1024, 64, 100000, 0)])
+def test_tc_gemm_3xtf32_mn_major(M, N, K, splits):
+    """The X^T products: A read MN-major straight from the K x M data layout."""
+    from paper_1602_02350_b200 import _lib
+    rng = np.random.default_rng(M * 7 + N + K)
+    At = rng.standard_normal((K, M)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    C = np.empty(M * N)
+    ctx = sk.default_context()
+    rc = _lib.load().skr_tc_gemm_mn_test(ctx.h, At.ctypes.data, B.ctypes.data, M, N, K, splits, C)
+    assert rc == 0, _lib.last_error()
+    want = At.astype(np.float64).T @ B.astype(np.float64).T
+    err = np.max(np.abs(C.reshape(M, N) - want)) / np.max(np.abs(want))
+    assert err < 3e-5, err
+
+
 # ---- BASELINE configs against the reference's own run (tests/golden/configs.json) ------
 def _golden(name):
     import json, os
