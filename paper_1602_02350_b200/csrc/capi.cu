@@ -783,12 +783,12 @@ void tc_launch(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* Bl, 
                                   (int)smem));
     configured = true;
   }
-  dim3 grid(ceil_div(g.M, TC_BM), ceil_div(g.N, BN), splits);
+  dim3 grid((unsigned)(ceil_div(g.M, TC_BM) * ceil_div(g.N, BN)), 1, splits);
   tc_gemm_tf32x3_kernel<A_MN, BN><<<grid, TC_THREADS, smem, c.stream>>>(ma, mbh, mbl, g);
   SKR_LAUNCHED(&c);
 }
 
-inline int tc_bn(int64_t N) { return N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+inline int tc_bn(int64_t N) { return N <= 64 ? 64 : 128; }
 
 // A: M x K K-major (lda), or (a_mn) the K x M row-major matrix read as its transpose;
 // B: N x K K-major as hi (Bh) + tf32 residual (Bl) arrays (ldb)
@@ -799,8 +799,7 @@ void tc_run(Ctx& c, const float* A, int64_t lda, const float* Bh, const float* B
                               : make_tmap_f32(A, g.M, g.K, lda, TC_BM);
   const int bn = tc_bn(g.N);
   if (bn == 64) tc_launch<A_MN, 64>(c, ma, Bh, Bl, ldb, g, splits);
-  else if (bn == 128) tc_launch<A_MN, 128>(c, ma, Bh, Bl, ldb, g, splits);
-  else tc_launch<A_MN, 256>(c, ma, Bh, Bl, ldb, g, splits);
+  else tc_launch<A_MN, 128>(c, ma, Bh, Bl, ldb, g, splits);
 }
 
 // out[n * ldo + m] = alpha * sum_k A[m, k] B[n, k]  (i.e. C^T, fp64) via 3xTF32 tcgen05 with
@@ -809,8 +808,21 @@ void tc_gemm_t(Ctx& c, bool a_mn, const float* A, int64_t lda, const float* Bh, 
                int64_t M, int64_t N, int64_t K, double alpha, double* out, int64_t ldo, int splits = 0) {
   if (M <= 0 || N <= 0) return;
   const int64_t tiles = (int64_t)ceil_div(M, TC_BM) * ceil_div(N, tc_bn(N));
-  if (splits <= 0)
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(c.sm_count / tiles, std::max<int64_t>(1, K / (8 * TC_BK))));
+  if (splits <= 0) {
+    // one CTA per SM: pick the split count whose last wave is fullest (fewest splits on ties)
+    const int64_t kmax = std::max<int64_t>(1, std::min<int64_t>(64, K / (8 * TC_BK)));
+    double best = -1.0;
+    splits = 1;
+    for (int64_t s = 1; s <= kmax; ++s) {
+      const int64_t ctas = tiles * s, waves = (ctas + c.sm_count - 1) / c.sm_count;
+      if (waves > 8 && s > 1) break;
+      const double eff = (double)ctas / (double)(waves * c.sm_count);
+      if (eff > best + 0.02) {
+        best = eff;
+        splits = (int)s;
+      }
+    }
+  }
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + TC_BK - 1) / TC_BK * TC_BK;
   splits = (int)std::max<int64_t>(1, (K + kchunk - 1) / kchunk);

@@ -21,7 +21,8 @@
 // MN-major A (the X^T products) lets X serve both orientations from one copy:
 // no transposed duplicate of the data matrix is ever built.
 //
-// One CTA = one 128 x BN output tile over a K-range (split-K over gridDim.z):
+// One CTA = one 128 x BN output tile over a K-range (split-K over gridDim.z);
+// N > 128 runs as several 128-wide tiles (stacked hi/lo needs 2N <= 256):
 //   warp 0    TMA producer: A tile (128 x 32: one 2-D box K-major with the
 //             128-byte swizzle, or four 32 x 32 boxes MN-major with the 128-byte/
 //             32-byte-atom swizzle), B_hi and B_lo tiles (BN x 32), NST-stage ring;
@@ -153,12 +154,16 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
   constexpr uint32_t ACC = tc_acc_cols<BN>();
   constexpr uint32_t TMEM_COLS = 512;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by offsetting the shared array itself so the compiler keeps the shared address space (LDS, not LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t bar_tma[NST], bar_conv[NST], bar_empty[NST], bar_done;
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * TC_BM, n0 = (int64_t)blockIdx.y * BN;
+  // tiles linearised N-fastest: the CTAs sharing an A tile run side by side, so A
+  // comes from HBM once and from L2 for the other N tiles
+  const int64_t ntn = (g.N + BN - 1) / BN;
+  const int64_t m0 = (int64_t)(blockIdx.x / ntn) * TC_BM, n0 = (int64_t)(blockIdx.x % ntn) * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
   const int64_t kend = min(g.K, kbeg + g.kchunk);
   const int nk = kend > kbeg ? (int)((kend - kbeg + TC_BK - 1) / TC_BK) : 0;
