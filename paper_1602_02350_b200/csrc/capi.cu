@@ -82,8 +82,9 @@ struct Storage {
   DBuf<int32_t> ridx, fidx;  // ridx: feature of each point-row entry; fidx: point of each feature-row entry
   DBuf<double> rval, fval;
   SplitCSR fsplit;  // feature rows cut for load balance (power-law feature popularity)
+  size_t bytes = 0;
   ~Storage() {
-    if (owns && ptr) cudaFreeAsync(ptr, stream);
+    if (owns && ptr) dev_free(ptr, bytes, stream);
   }
 };
 
@@ -178,7 +179,8 @@ std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d) {
   st->ld = padded_ld(d);
   st->stream = c.stream;
   const size_t bytes = (size_t)std::max<int64_t>(n, 1) * st->ld * dtype_size(dtype);
-  SKR_CUDA(cudaMallocAsync(&st->ptr, bytes, c.stream));
+  st->bytes = bytes;
+  SKR_CUDA(dev_malloc(&st->ptr, bytes, c.stream));
   SKR_CUDA(cudaMemsetAsync(st->ptr, 0, bytes, c.stream));
   return st;
 }
