@@ -941,7 +941,7 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     ChainArgs ca{rows, idx + s0, steps, Mb, pb, Xb, mu, eta, p->s_state.get(), dprof};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(NT + 160);
+    cfg.blockDim = dim3(chain_threads<T, CPT, NT>());
     cfg.dynamicSmemBytes = chain_smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];

@@ -202,6 +202,8 @@ struct ChainArgs {
   unsigned long long* prof;  // optional: per-phase cycle totals of CTA 0 / thread 0 (debug)
 };
 
+constexpr int kChainIdxAhead = 4;  // blocks of step indices the row producer keeps in flight
+
 // row-ring depth: 4 for 1 KB row slices (blocks b, b+1 in use, two in flight), 3 when
 // the slices are 2 KB (shared memory)
 constexpr int chain_nb(int slice_doubles) { return slice_doubles <= 128 ? 4 : 3; }
@@ -217,6 +219,17 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// 16-byte DSMEM store into CTA `rank` that completes `bytes` of the transaction
+// count of the mbarrier at the same offset there (no release fence, no signal:
+// the receiver's ordinary mbarrier wait makes the data visible)
+__device__ __forceinline__ void st_async_v2(double* local_dst, uint64_t* local_bar, uint32_t rank, double x, double y) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(local_dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(rdst),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -229,15 +242,22 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
+// consumers + 2 delta warps + row producer + M/X producer + signaller (or second
+// row producer) [+ two wideners for fp32 rows in push mode]
+template <class T, int CPT, int NT>
+constexpr int chain_threads() { return NT + 160 + ((CPT == 1 && NT == 128 && sizeof(T) == 4) ? 64 : 0); }
+
 template <class T, int CPT, int L, int MXB, int NT>
-__global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_kernel(ChainArgs a) {
   // warps: NCW consumers | 2 delta warps | row producer | M/X producer | signaller
   constexpr int NCW = NT / 32;
-  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4;
+  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4, WWID = NCW + 5;
   static_assert(2 * L <= 64, "the two delta warps hold the M and X rows");
   constexpr int SW = NT * CPT, NB = chain_nb(NT * CPT);
   constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
   constexpr size_t ROWB = (size_t)SW * 8;  // bytes per row slot (fits an fp64 slice)
+  constexpr int IA = kChainIdxAhead;       // index ring depth (blocks of indices in flight)
+  static_assert(L == 32, "one row per producer lane");
   extern __shared__ __align__(128) unsigned char sm[];
   unsigned char* rows = sm;                                                  // [NB][L][ROWB]
   double* mx = reinterpret_cast<double*>(sm + (size_t)NB * L * ROWB);       // [MXB][MXW] M_b^T, X_b^T, p_b
@@ -245,6 +265,12 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
   // ranks and gathers locally; pull (CPT = 2, where shared memory is tight): each
   // rank keeps its own apub[slot] and the gather reads the ranks remotely.
   constexpr bool PUSH = CPT == 1 && NT == 128;
+  constexpr int NP = PUSH ? 2 : 1;  // row producer warps
+  constexpr int RPP = L / NP;       // rows per producer warp
+  // fp32 data rows are widened to fp64 in their ring slot by two widener warps as
+  // soon as they land (push mode), so the consumers' dots and update read fp64
+  // only; in pull mode the consumers widen them in the dots.
+  constexpr bool PWIDEN = PUSH && sizeof(T) == 4;
   double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
   double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
   double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
@@ -259,6 +285,9 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
   uint64_t* dready = pub + 2;                                                // [2] local: delta_b published
   uint64_t* dmask = dready + 2;                                              // [NB] bit l: row l is a data row
   double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [SW] current w slice
+  int64_t* iring = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(wsm + SW) + 15) & ~uintptr_t(15));  // [IA][L]
+  uint64_t* ifull = reinterpret_cast<uint64_t*>(iring + IA * L);             // [2][IA] (per producer)
+  uint64_t* wide = ifull + 2 * IA;                                           // [NB] fp32 rows widened
 
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
@@ -268,10 +297,15 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
   const int64_t nblk = (a.steps + L - 1) / L;
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) {
-      mbar_init(&full[q], 1);
+      mbar_init(&full[q], NP);  // one (expect_tx) arrival per row producer warp
       mbar_init(&empty[q], 1);
     }
-    for (int q = 0; q < 4; ++q) mbar_init(&ready[q], CS);
+    for (int q = 0; q < 4; ++q) {
+      // push: one local arrival (the arming expect_tx) + CS * L * 8 bytes of st.async
+      // partials; pull: one release arrive per rank from its signaller
+      mbar_init(&ready[q], PUSH ? 1 : CS);
+      if (PUSH) mbar_expect_tx(&ready[q], (uint32_t)(CS * L * 8));
+    }
     for (int q = 0; q < MXB; ++q) {
       mbar_init(&mx_full[q], 1);
       mbar_init(&mx_empty[q], 1);
@@ -280,11 +314,13 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
     mbar_init(&pub[1], NCW);
     mbar_init(&dready[0], 1);
     mbar_init(&dready[1], 1);
+    for (int q = 0; q < 2 * IA; ++q) mbar_init(&ifull[q], 1);
+    for (int q = 0; q < NB; ++q) mbar_init(&wide[q], 2);  // two widener warps
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // every CTA's barriers exist before any remote arrive
 
-  if (warp == WSIG) {
+  if (!PUSH && warp == WSIG) {
     // ---------------- signaller: once this CTA's partials of block j are pushed
     // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
     // release fence latency stays off the consumers' path.  pub is 2-deep: the
@@ -307,61 +343,67 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
         bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
       }
     }
-  } else if (warp == WROW) {
-    // ---------------- row producer warp ----------------
+  } else if (warp == WROW || (PUSH && warp == WSIG)) {
+    // ---------------- row producer warps ----------------
+    // NP warps gather the sampled rows, each RPP of them (push mode: the signaller
+    // warp is free and takes rows 16..31).  A bulk copy costs ~70 cycles of issue
+    // (an elect/broadcast loop per lane), so one warp issuing all 32 rows took
+    // ~2.2 K cycles per block — about the whole block.
+    const int h = warp == WROW ? 0 : 1;   // this producer's half
     const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);  // may be <= 0 past ld
-    // indices are loaded one block ahead (their L2 latency overlaps the copies)
-    int64_t nxt[L / 32];
-    auto load_idx = [&](int64_t b, int64_t (&dst)[L / 32]) {
-#pragma unroll
-      for (int h = 0; h < L / 32; ++h) {
-        const int64_t t = b * L + lane + 32 * h;
-        dst[h] = (b < nblk && t < a.steps) ? a.idx[t] : -1;
+    // The step indices of full blocks travel IA blocks ahead through a shared ring
+    // (one bulk copy per block): a register load one block ahead left the producer
+    // waiting a dependent global-load latency (~2 K cycles) per block.
+    const int64_t nfull = a.steps / L;  // blocks whose L indices all exist
+    int64_t* my_ring = iring + h * IA * RPP;
+    uint64_t* my_full = ifull + h * IA;
+    auto issue_idx = [&](int64_t b) {
+      if (b < nfull) {
+        const int q = (int)(b % IA);
+        mbar_expect_tx(&my_full[q], (uint32_t)(RPP * 8));
+        bulk_g2s(my_ring + q * RPP, a.idx + b * L + h * RPP, (uint32_t)(RPP * 8), &my_full[q]);
       }
     };
-    load_idx(0, nxt);
-    const bool pprof = a.prof && cr == 0 && lane == 0;
+    if (lane == 0)
+      for (int64_t b = 0; b < IA; ++b) issue_idx(b);
+    const bool pprof = a.prof && cr == 0 && lane == 0 && h == 0;
     unsigned long long pw = 0, pi = 0;
+    const bool mine = lane < RPP;  // lane owns row h * RPP + lane
     for (int64_t b = 0; b < nblk; ++b) {
       const int slot = (int)(b % NB);
       unsigned long long q0 = pprof ? clock64() : 0;
-      int64_t cur[L / 32];
-#pragma unroll
-      for (int h = 0; h < L / 32; ++h) cur[h] = nxt[h];
-      load_idx(b + 1, nxt);
+      int64_t i = -1;
+      if (b < nfull) {
+        const int q = (int)(b % IA);
+        mbar_wait(&my_full[q], (uint32_t)((b / IA) & 1));
+        if (mine) i = my_ring[q * RPP + lane];
+        __syncwarp();  // every lane has read slot q before it is refilled
+        if (lane == 0) issue_idx(b + IA);
+      } else if (mine) {  // the partial last block of the launch: direct loads
+        const int64_t t = b * L + h * RPP + lane;
+        i = t < a.steps ? a.idx[t] : -1;
+      }
       if (b >= NB) mbar_wait(&empty[slot], (uint32_t)(((b / NB) - 1) & 1));
       unsigned long long q1 = pprof ? clock64() : 0;
-      // row indices -> smem, data-row mask, then one bulk copy (1-D TMA) per row slice
-      uint32_t bytes = 0;
-      uint64_t mask = 0;
-#pragma unroll
-      for (int h = 0; h < L / 32; ++h) {
-        const int64_t i = cur[h];
-        if (i >= 0 && slice_elems > 0) bytes += (uint32_t)(slice_elems * (i < R.n ? (int64_t)sizeof(T) : 8));
-        const unsigned bal = __ballot_sync(0xffffffffu, i >= 0 && i < R.n);
-        mask |= (uint64_t)bal << (32 * h);
-      }
+      // data-row mask (this half), then one bulk copy (1-D TMA) per row slice
+      uint32_t bytes = (i >= 0 && slice_elems > 0) ? (uint32_t)(slice_elems * (i < R.n ? (int64_t)sizeof(T) : 8)) : 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, i >= 0 && i < R.n);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
       if (lane == 0) {
-        dmask[slot] = mask;
+        if (NP == 1) dmask[slot] = (uint64_t)bal;
+        else reinterpret_cast<uint16_t*>(&dmask[slot])[h] = (uint16_t)(bal & 0xFFFFu);  // rows 16h..16h+15
         if (bytes) mbar_expect_tx(&full[slot], bytes);
         else mbar_arrive_local(&full[slot]);
       }
       __syncwarp();
-      if (bytes) {
-#pragma unroll
-        for (int h = 0; h < L / 32; ++h) {
-          const int l = lane + 32 * h;
-          const int64_t i = cur[h];
-          if (i < 0 || slice_elems <= 0) continue;
-          unsigned char* dst = rows + ((size_t)slot * L + l) * ROWB;
-          if (i < R.n)
-            bulk_g2s(dst, static_cast<const T*>(R.Xt) + i * R.ld + slice0, (uint32_t)(slice_elems * sizeof(T)),
-                     &full[slot]);
-          else
-            bulk_g2s(dst, R.B + (i - R.n) * R.ld + slice0, (uint32_t)(slice_elems * 8), &full[slot]);
-        }
+      if (i >= 0 && slice_elems > 0) {
+        unsigned char* dst = rows + ((size_t)slot * L + h * RPP + lane) * ROWB;
+        if (i < R.n)
+          bulk_g2s(dst, static_cast<const T*>(R.Xt) + i * R.ld + slice0, (uint32_t)(slice_elems * sizeof(T)),
+                   &full[slot]);
+        else
+          bulk_g2s(dst, R.B + (i - R.n) * R.ld + slice0, (uint32_t)(slice_elems * 8), &full[slot]);
       }
       if (pprof) {
         const unsigned long long q2 = clock64();
@@ -372,6 +414,42 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
     if (pprof) {
       atomicAdd(a.prof + 7, pw);
       atomicAdd(a.prof + 8, pi);
+    }
+  } else if (PWIDEN && (warp == WWID || warp == WWID + 1)) {
+    // ---------------- two widener warps (rows 0..15 / 16..31): the fp32 data rows
+    // of each landed block -> fp64 in place (the slot is sized for fp64).  Lane l
+    // reads elements 2l, 2l+1 and 64+2l, 64+2l+1 (8-byte loads) and writes them
+    // as two 16-byte stores at 16 l and 512 + 16 l: conflict-free both ways; every
+    // lane reads a batch before any lane writes it ----------------
+    const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);
+    const bool act0 = 2 * lane < slice_elems, act1 = 64 + 2 * lane < slice_elems;
+    const int rbeg = (warp - WWID) * (L / 2);
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int slot = (int)(b % NB);
+      mbar_wait(&full[slot], (uint32_t)((b / NB) & 1));
+      const uint32_t dm = (uint32_t)dmask[slot];  // L = 32
+      unsigned char* base = rows + (size_t)slot * L * ROWB;
+      // all 16 rows loaded first, one warp barrier, then predicated stores: no
+      // per-row branches (the branchy version issued ~70 instructions per row)
+      float2 f[L / 2], g[L / 2];
+#pragma unroll
+      for (int r = 0; r < L / 2; ++r) {
+        const float2* src = reinterpret_cast<const float2*>(base + (size_t)(rbeg + r) * ROWB);
+        f[r] = act0 ? src[lane] : make_float2(0.f, 0.f);
+        g[r] = act1 ? src[32 + lane] : make_float2(0.f, 0.f);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < L / 2; ++r) {
+        const bool dr = (dm >> (rbeg + r)) & 1u;  // data row (regulariser rows are fp64 already)
+        double2* o = reinterpret_cast<double2*>(base + (size_t)(rbeg + r) * ROWB);
+        const double2 lo2 = make_double2(f32_to_f64(f[r].x), f32_to_f64(f[r].y));
+        const double2 hi2 = make_double2(f32_to_f64(g[r].x), f32_to_f64(g[r].y));
+        if (dr && act0) o[lane] = lo2;
+        if (dr && act1) o[32 + lane] = hi2;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&wide[slot]);
     }
   } else if (warp == DW || warp == DW + 1) {
     // ---------------- delta warps (64 threads): resolve block b while the consumers
@@ -400,7 +478,8 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
       }
       named_bar(2, 64);  // xterm visible
       // a_b: the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
-      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
+      if (PUSH) mbar_wait(&ready[b & 3], (uint32_t)((b >> 2) & 1));
+      else mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
       if (j < L) {
         double part[16];
 #pragma unroll
@@ -433,6 +512,9 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
       }
       named_bar(2, 64);  // delta_b complete, zbuf / M / X reads done
       if (j == 0) {
+        // push: slot b % 4 is read; arm it for block b + 4 (no rank can send those
+        // partials before every rank has consumed block b: they need delta_{b+3})
+        if (PUSH) mbar_expect_tx(&ready[b & 3], (uint32_t)(CS * L * 8));
         mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
         mbar_arrive_local(&dready[b & 1]);   // delta_b visible to the consumers (release.cta)
       }
@@ -459,7 +541,7 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
       const int slot = (int)(bb % NB);
       const int Lbb = (int)min((int64_t)L, a.steps - bb * L);
       const unsigned long long w0c = prof ? clock64() : 0;
-      mbar_wait(&full[slot], (uint32_t)((bb / NB) & 1));
+      mbar_wait(PWIDEN ? &wide[slot] : &full[slot], (uint32_t)((bb / NB) & 1));
       if (prof) tp[8] += clock64() - w0c;
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
       const uint64_t dm = dmask[slot];
@@ -479,7 +561,7 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
         const int l = warp * RPW + q;
         const unsigned char* rowp = rb + (size_t)l * ROWB;
         double s = 0.0;
-        if (sizeof(T) == 8 || ((dm >> l) & 1ull) == 0) {
+        if (sizeof(T) == 8 || PWIDEN || ((dm >> l) & 1ull) == 0) {
           const double* x = reinterpret_cast<const double*>(rowp) + lane;
 #pragma unroll
           for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? x[32 * c] : 0.0, wl[c], s);
@@ -489,7 +571,7 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
           const T* x = reinterpret_cast<const T*>(rowp) + lane;
           double xv[CPL];
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? (double)x[32 * c] : 0.0;
+          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? f32_to_f64(x[32 * c]) : 0.0;
           __syncwarp();  // every lane has read its fp32 values before any fp64 store lands
           double* xd = reinterpret_cast<double*>(const_cast<unsigned char*>(rowp)) + lane;
 #pragma unroll
@@ -508,16 +590,16 @@ __global__ void __launch_bounds__(NT + 160, 1) sstep_chain_kernel(ChainArgs a) {
       for (int r = 0; r < RPW; ++r) vals[r] = __shfl_sync(0xffffffffu, v[0], (32 / RPW) * r);
       if (PUSH) {
         if (lane < CS) {
-          double* dst = cluster.map_shared_rank(apub, lane) + ((bb & 3) * 16 + cr) * L + warp * RPW;
+          double* dst = apub + ((bb & 3) * 16 + cr) * L + warp * RPW;  // same offset in rank `lane`
 #pragma unroll
-          for (int r = 0; r < RPW; r += 2) *reinterpret_cast<double2*>(dst + r) = make_double2(vals[r], vals[r + 1]);
+          for (int r = 0; r < RPW; r += 2) st_async_v2(dst + r, &ready[bb & 3], (uint32_t)lane, vals[r], vals[r + 1]);
         }
       } else if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < RPW; ++r) apub[(bb & 3) * L + warp * RPW + r] = vals[r];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are pushed
+      if (!PUSH && lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are published
     };
     // prologue: a_0 = R_0 w_0 directly
     if (nblk > 0) {
@@ -594,7 +676,8 @@ template <int CPT, int L, int MXB, int NT>
 constexpr size_t sstep_chain_smem() {
   return (size_t)chain_nb(NT * CPT) * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
          sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 5 * L) +
-         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * NT * CPT + 128;
+         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * NT * CPT +
+         sizeof(int64_t) * kChainIdxAhead * L + sizeof(uint64_t) * (2 * kChainIdxAhead + chain_nb(NT * CPT)) + 128;
 }
 
 // w_avg = S / m ; zero padding.
