@@ -242,10 +242,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-// consumers + 2 delta warps + row producer + M/X producer + signaller (or second
-// row producer) [+ two wideners for fp32 rows in push mode]
+// consumers + 2 delta warps + row producer + M/X producer + signaller (push mode:
+// second row producer) [+ second row producer in pull mode | + two wideners for
+// fp32 rows in push mode]
 template <class T, int CPT, int NT>
-constexpr int chain_threads() { return NT + 160 + ((CPT == 1 && NT == 128 && sizeof(T) == 4) ? 64 : 0); }
+constexpr int chain_threads() {
+  return NT + 160 + (!(CPT == 1 && NT == 128) ? 32 : sizeof(T) == 4 ? 64 : 0);
+}
 
 template <class T, int CPT, int L, int MXB, int NT>
 __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_kernel(ChainArgs a) {
@@ -265,8 +268,9 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
   // ranks and gathers locally; pull (CPT = 2, where shared memory is tight): each
   // rank keeps its own apub[slot] and the gather reads the ranks remotely.
   constexpr bool PUSH = CPT == 1 && NT == 128;
-  constexpr int NP = PUSH ? 2 : 1;  // row producer warps
+  constexpr int NP = 2;             // row producer warps (each gathers 16 rows of a block)
   constexpr int RPP = L / NP;       // rows per producer warp
+  constexpr int WPR2 = PUSH ? WSIG : NCW + 5;  // second row producer
   // fp32 data rows are widened to fp64 in their ring slot by two widener warps as
   // soon as they land (push mode), so the consumers' dots and update read fp64
   // only; in pull mode the consumers widen them in the dots.
@@ -343,10 +347,10 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
         bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
       }
     }
-  } else if (warp == WROW || (PUSH && warp == WSIG)) {
+  } else if (warp == WROW || warp == WPR2) {
     // ---------------- row producer warps ----------------
     // NP warps gather the sampled rows, each RPP of them (push mode: the signaller
-    // warp is free and takes rows 16..31).  A bulk copy costs ~70 cycles of issue
+    // warp is free and takes rows 16..31; pull mode: an extra warp).  A bulk copy costs ~70 cycles of issue
     // (an elect/broadcast loop per lane), so one warp issuing all 32 rows took
     // ~2.2 K cycles per block — about the whole block.
     const int h = warp == WROW ? 0 : 1;   // this producer's half
@@ -391,8 +395,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
       if (lane == 0) {
-        if (NP == 1) dmask[slot] = (uint64_t)bal;
-        else reinterpret_cast<uint16_t*>(&dmask[slot])[h] = (uint16_t)(bal & 0xFFFFu);  // rows 16h..16h+15
+        reinterpret_cast<uint16_t*>(&dmask[slot])[h] = (uint16_t)(bal & 0xFFFFu);  // rows 16h..16h+15
         if (bytes) mbar_expect_tx(&full[slot], bytes);
         else mbar_arrive_local(&full[slot]);
       }
