@@ -88,20 +88,6 @@ inline NcclApi& nccl() {
     (ctx)->launches++;                                                                  \
   } while (0)
 
-// fp32 -> fp64 by integer ops (ALU pipe).  F2F.F64.F32 retires only ~4-5 lanes
-// per clock per SM on B200, which bounded every pass widening fp32 rows (K10's
-// fp32 dots: +930 cycles per 32 x 128 block).  Normal numbers: rebias the
-// exponent by 1023 - 127 and move the mantissa up 29 bits (exact); signed zero
-// by select (exact); subnormal inputs (|x| < 1.2e-38) come out with an absolute
-// error below 1.2e-38; inf / nan never reach here (the data is checked finite,
-// data_matrix.cpp:18-22).
-__device__ __forceinline__ double f32_to_f64(float f) {
-  const uint32_t u = __float_as_uint(f);
-  const uint32_t a = u & 0x7fffffffu;
-  const uint32_t hi = (a != 0u ? (a >> 3) + 0x38000000u : 0u) | (u & 0x80000000u);
-  return __hiloint2double((int)hi, (int)(u << 29));
-}
-
 // Buffers of >= 1 GiB bypass the stream-ordered pool: growing the pool maps
 // memory at ~17 GB/s on B200 (3.8 s for 64 GiB) while cudaMalloc maps 64 GiB in
 // ~5 ms (profiles/alloc_probe.py).  cudaFree synchronises the device, so the

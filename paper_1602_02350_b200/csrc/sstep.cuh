@@ -446,8 +446,8 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       for (int r = 0; r < L / 2; ++r) {
         const bool dr = (dm >> (rbeg + r)) & 1u;  // data row (regulariser rows are fp64 already)
         double2* o = reinterpret_cast<double2*>(base + (size_t)(rbeg + r) * ROWB);
-        const double2 lo2 = make_double2(f32_to_f64(f[r].x), f32_to_f64(f[r].y));
-        const double2 hi2 = make_double2(f32_to_f64(g[r].x), f32_to_f64(g[r].y));
+        const double2 lo2 = make_double2((double)f[r].x, (double)f[r].y);
+        const double2 hi2 = make_double2((double)g[r].x, (double)g[r].y);
         if (dr && act0) o[lane] = lo2;
         if (dr && act1) o[32 + lane] = hi2;
       }
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
           const T* x = reinterpret_cast<const T*>(rowp) + lane;
           double xv[CPL];
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? f32_to_f64(x[32 * c]) : 0.0;
+          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? (double)x[32 * c] : 0.0;
           __syncwarp();  // every lane has read its fp32 values before any fp64 store lands
           double* xd = reinterpret_cast<double*>(const_cast<unsigned char*>(rowp)) + lane;
 #pragma unroll
