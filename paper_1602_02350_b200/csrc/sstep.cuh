@@ -219,17 +219,6 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
-// 16-byte DSMEM store into CTA `rank` that completes `bytes` of the transaction
-// count of the mbarrier at the same offset there (no release fence, no signal:
-// the receiver's ordinary mbarrier wait makes the data visible)
-__device__ __forceinline__ void st_async_v2(double* local_dst, uint64_t* local_bar, uint32_t rank, double x, double y) {
-  uint32_t rdst, rbar;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(local_dst)), "r"(rank));
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(rank));
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(rdst),
-               "d"(x), "d"(y), "r"(rbar)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -242,19 +231,20 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-// consumers + 2 delta warps + row producer + M/X producer + signaller (push mode:
-// second row producer) [+ second row producer in pull mode | + two wideners for
-// fp32 rows in push mode]
+// consumers + 2 delta warps + row producer + M/X producer + signaller + second
+// row producer [+ two wideners for fp32 rows].  (A st.async exchange with
+// mbarrier complete_tx in place of the signaller was ~9 % faster per block but
+// not run-to-run deterministic at c3 (16 ranks): removed.)
 template <class T, int CPT, int NT>
 constexpr int chain_threads() {
-  return NT + 160 + (!(CPT == 1 && NT == 128) ? 32 : sizeof(T) == 4 ? 64 : 0);
+  return NT + 192 + ((CPT == 1 && NT == 128 && sizeof(T) == 4) ? 64 : 0);
 }
 
 template <class T, int CPT, int L, int MXB, int NT>
 __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_kernel(ChainArgs a) {
   // warps: NCW consumers | 2 delta warps | row producer | M/X producer | signaller
   constexpr int NCW = NT / 32;
-  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4, WWID = NCW + 5;
+  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4;
   static_assert(2 * L <= 64, "the two delta warps hold the M and X rows");
   constexpr int SW = NT * CPT, NB = chain_nb(NT * CPT);
   constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
@@ -270,11 +260,14 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
   constexpr bool PUSH = CPT == 1 && NT == 128;
   constexpr int NP = 2;             // row producer warps (each gathers 16 rows of a block)
   constexpr int RPP = L / NP;       // rows per producer warp
-  constexpr int WPR2 = PUSH ? WSIG : NCW + 5;  // second row producer
+  constexpr int WPR2 = NCW + 5;  // second row producer
+  constexpr int WWID = NCW + 6;  // first widener warp
+  constexpr int NWID = 2;        // widener warps
   // fp32 data rows are widened to fp64 in their ring slot by two widener warps as
-  // soon as they land (push mode), so the consumers' dots and update read fp64
-  // only; in pull mode the consumers widen them in the dots.
-  constexpr bool PWIDEN = PUSH && sizeof(T) == 4;
+  // soon as they land, so the consumers' dots and update read fp64 only.  With
+  // 256-column slices (d > 2048) the wideners cannot keep up (c4: 3.2 K -> 3.8 K
+  // cycles per block) and the consumers widen in the dots instead.
+  constexpr bool PWIDEN = sizeof(T) == 4 && PUSH;
   double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
   double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
   double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
@@ -291,7 +284,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
   double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [SW] current w slice
   int64_t* iring = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(wsm + SW) + 15) & ~uintptr_t(15));  // [IA][L]
   uint64_t* ifull = reinterpret_cast<uint64_t*>(iring + IA * L);             // [2][IA] (per producer)
-  uint64_t* wide = ifull + 2 * IA;                                           // [NB] fp32 rows widened
+  uint64_t* wide = ifull + 2 * IA;                                           // [NB][NWID] fp32 rows widened
 
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
@@ -307,8 +300,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
     for (int q = 0; q < 4; ++q) {
       // push: one local arrival (the arming expect_tx) + CS * L * 8 bytes of st.async
       // partials; pull: one release arrive per rank from its signaller
-      mbar_init(&ready[q], PUSH ? 1 : CS);
-      if (PUSH) mbar_expect_tx(&ready[q], (uint32_t)(CS * L * 8));
+      mbar_init(&ready[q], CS);  // one release arrive per rank (its signaller)
     }
     for (int q = 0; q < MXB; ++q) {
       mbar_init(&mx_full[q], 1);
@@ -319,12 +311,12 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
     mbar_init(&dready[0], 1);
     mbar_init(&dready[1], 1);
     for (int q = 0; q < 2 * IA; ++q) mbar_init(&ifull[q], 1);
-    for (int q = 0; q < NB; ++q) mbar_init(&wide[q], 2);  // two widener warps
+    for (int q = 0; q < NB * NWID; ++q) mbar_init(&wide[q], 1);  // [slot][widener warp]
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster.sync();  // every CTA's barriers exist before any remote arrive
 
-  if (!PUSH && warp == WSIG) {
+  if (warp == WSIG) {
     // ---------------- signaller: once this CTA's partials of block j are pushed
     // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
     // release fence latency stays off the consumers' path.  pub is 2-deep: the
@@ -349,8 +341,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
     }
   } else if (warp == WROW || warp == WPR2) {
     // ---------------- row producer warps ----------------
-    // NP warps gather the sampled rows, each RPP of them (push mode: the signaller
-    // warp is free and takes rows 16..31; pull mode: an extra warp).  A bulk copy costs ~70 cycles of issue
+    // NP warps gather the sampled rows, each RPP of them.  A bulk copy costs ~70 cycles of issue
     // (an elect/broadcast loop per lane), so one warp issuing all 32 rows took
     // ~2.2 K cycles per block — about the whole block.
     const int h = warp == WROW ? 0 : 1;   // this producer's half
@@ -418,41 +409,48 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       atomicAdd(a.prof + 7, pw);
       atomicAdd(a.prof + 8, pi);
     }
-  } else if (PWIDEN && (warp == WWID || warp == WWID + 1)) {
+  } else if (PWIDEN && warp >= WWID && warp < WWID + NWID) {
     // ---------------- two widener warps (rows 0..15 / 16..31): the fp32 data rows
     // of each landed block -> fp64 in place (the slot is sized for fp64).  Lane l
-    // reads elements 2l, 2l+1 and 64+2l, 64+2l+1 (8-byte loads) and writes them
-    // as two 16-byte stores at 16 l and 512 + 16 l: conflict-free both ways; every
-    // lane reads a batch before any lane writes it ----------------
+    // reads 8-byte float pairs l, l+32, ... and writes them as 16-byte double pairs
+    // at the same indices: conflict-free both ways.  Every lane reads a batch of
+    // rows before any lane writes it; no per-row branches ----------------
+    constexpr int NV = SW / 64;                  // float pairs per lane per row
+    constexpr int BR = SW <= 128 ? L / 2 : 4;    // rows per batch (register budget)
     const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);
-    const bool act0 = 2 * lane < slice_elems, act1 = 64 + 2 * lane < slice_elems;
-    const int rbeg = (warp - WWID) * (L / 2);
+    bool act[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) act[k] = 2 * (lane + 32 * k) < slice_elems;
+    const int rbeg = (warp - WWID) * (L / NWID);
     for (int64_t b = 0; b < nblk; ++b) {
       const int slot = (int)(b % NB);
       mbar_wait(&full[slot], (uint32_t)((b / NB) & 1));
       const uint32_t dm = (uint32_t)dmask[slot];  // L = 32
       unsigned char* base = rows + (size_t)slot * L * ROWB;
-      // all 16 rows loaded first, one warp barrier, then predicated stores: no
-      // per-row branches (the branchy version issued ~70 instructions per row)
-      float2 f[L / 2], g[L / 2];
 #pragma unroll
-      for (int r = 0; r < L / 2; ++r) {
-        const float2* src = reinterpret_cast<const float2*>(base + (size_t)(rbeg + r) * ROWB);
-        f[r] = act0 ? src[lane] : make_float2(0.f, 0.f);
-        g[r] = act1 ? src[32 + lane] : make_float2(0.f, 0.f);
-      }
-      __syncwarp();
+      for (int r0 = rbeg; r0 < rbeg + L / NWID; r0 += BR) {
+        float2 f[BR][NV];
 #pragma unroll
-      for (int r = 0; r < L / 2; ++r) {
-        const bool dr = (dm >> (rbeg + r)) & 1u;  // data row (regulariser rows are fp64 already)
-        double2* o = reinterpret_cast<double2*>(base + (size_t)(rbeg + r) * ROWB);
-        const double2 lo2 = make_double2((double)f[r].x, (double)f[r].y);
-        const double2 hi2 = make_double2((double)g[r].x, (double)g[r].y);
-        if (dr && act0) o[lane] = lo2;
-        if (dr && act1) o[32 + lane] = hi2;
+        for (int r = 0; r < BR; ++r) {
+          const float2* src = reinterpret_cast<const float2*>(base + (size_t)(r0 + r) * ROWB);
+#pragma unroll
+          for (int k = 0; k < NV; ++k) f[r][k] = act[k] ? src[lane + 32 * k] : make_float2(0.f, 0.f);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < BR; ++r) {
+          const bool dr = (dm >> (r0 + r)) & 1u;  // data row (regulariser rows are fp64 already)
+          double2* o = reinterpret_cast<double2*>(base + (size_t)(r0 + r) * ROWB);
+#pragma unroll
+          for (int k = 0; k < NV; ++k)
+            if (dr && act[k]) o[lane + 32 * k] = make_double2((double)f[r][k].x, (double)f[r][k].y);
+        }
+        __syncwarp();
       }
+      // order these generic-proxy stores before the bulk copy that refills the slot
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(&wide[slot]);
+      if (lane == 0) mbar_arrive_local(&wide[slot * NWID + (warp - WWID)]);
     }
   } else if (warp == DW || warp == DW + 1) {
     // ---------------- delta warps (64 threads): resolve block b while the consumers
@@ -481,8 +479,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       }
       named_bar(2, 64);  // xterm visible
       // a_b: the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
-      if (PUSH) mbar_wait(&ready[b & 3], (uint32_t)((b >> 2) & 1));
-      else mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
+      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
       if (j < L) {
         double part[16];
 #pragma unroll
@@ -517,7 +514,6 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       if (j == 0) {
         // push: slot b % 4 is read; arm it for block b + 4 (no rank can send those
         // partials before every rank has consumed block b: they need delta_{b+3})
-        if (PUSH) mbar_expect_tx(&ready[b & 3], (uint32_t)(CS * L * 8));
         mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
         mbar_arrive_local(&dready[b & 1]);   // delta_b visible to the consumers (release.cta)
       }
@@ -544,7 +540,12 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       const int slot = (int)(bb % NB);
       const int Lbb = (int)min((int64_t)L, a.steps - bb * L);
       const unsigned long long w0c = prof ? clock64() : 0;
-      mbar_wait(PWIDEN ? &wide[slot] : &full[slot], (uint32_t)((bb / NB) & 1));
+      if (PWIDEN) {
+#pragma unroll
+        for (int q = 0; q < NWID; ++q) mbar_wait(&wide[slot * NWID + q], (uint32_t)((bb / NB) & 1));
+      } else {
+        mbar_wait(&full[slot], (uint32_t)((bb / NB) & 1));
+      }
       if (prof) tp[8] += clock64() - w0c;
       const unsigned char* rb = rows + (size_t)slot * L * ROWB;
       const uint64_t dm = dmask[slot];
@@ -593,16 +594,16 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       for (int r = 0; r < RPW; ++r) vals[r] = __shfl_sync(0xffffffffu, v[0], (32 / RPW) * r);
       if (PUSH) {
         if (lane < CS) {
-          double* dst = apub + ((bb & 3) * 16 + cr) * L + warp * RPW;  // same offset in rank `lane`
+          double* dst = cluster.map_shared_rank(apub, lane) + ((bb & 3) * 16 + cr) * L + warp * RPW;
 #pragma unroll
-          for (int r = 0; r < RPW; r += 2) st_async_v2(dst + r, &ready[bb & 3], (uint32_t)lane, vals[r], vals[r + 1]);
+          for (int r = 0; r < RPW; r += 2) *reinterpret_cast<double2*>(dst + r) = make_double2(vals[r], vals[r + 1]);
         }
       } else if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < RPW; ++r) apub[(bb & 3) * L + warp * RPW + r] = vals[r];
       }
       __syncwarp();
-      if (!PUSH && lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are published
+      if (lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are published
     };
     // prologue: a_0 = R_0 w_0 directly
     if (nblk > 0) {
@@ -680,7 +681,7 @@ constexpr size_t sstep_chain_smem() {
   return (size_t)chain_nb(NT * CPT) * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
          sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 5 * L) +
          sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * NT * CPT +
-         sizeof(int64_t) * kChainIdxAhead * L + sizeof(uint64_t) * (2 * kChainIdxAhead + chain_nb(NT * CPT)) + 128;
+         sizeof(int64_t) * kChainIdxAhead * L + sizeof(uint64_t) * (2 * kChainIdxAhead + 2 * chain_nb(NT * CPT)) + 128;
 }
 
 // w_avg = S / m ; zero padding.
