@@ -623,3 +623,22 @@ def test_distributed_code_path_on_one_gpu_matches(O):
     assert rel(a[0], b[0]) < 1e-14 and rel(a[1], b[1]) < 1e-14
     assert rel(a[2], b[2]) < 1e-13 and abs(a[3] - b[3]) <= 1e-13 * abs(a[3])
     assert rel(a[4], b[4]) < 1e-12 and abs(a[5] - b[5]) <= 1e-13 * abs(a[5])
+
+
+@pytest.mark.parametrize("name,dtype", [("c3", "f32"), ("c3", "f64"), ("c5", "f32"), ("c2", "f64")])
+def test_svrg_chain_bitwise_deterministic(name, dtype):
+    """The s-step chain (one thread-block cluster of up to 16 CTAs exchanging partial
+    dots through distributed shared memory) gives bitwise-identical iterates across
+    repeated solves: no exchange or ring race.  c3 at 16 ranks is the case where an
+    st.async exchange once raced (K10)."""
+    import dataclasses
+    cfg = dataclasses.replace(configs.CONFIGS[name].scaled(16384), dtype=dtype)
+    X, y = configs.host_instance(cfg)
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, cfg.lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))
+    eta = configs.eta_for(cfg, pg.max_row_sq(), pg.mean_beta())
+    runs = [sk.svrg_solve(pg, sk.SvrgConfig(2, 2 * cfg.n, eta, cfg.seed), np.zeros(cfg.d)) for _ in range(4)]
+    for r in runs[1:]:
+        assert np.array_equal(np.asarray(r.iterate), np.asarray(runs[0].iterate))
+        assert [t.objective for t in r.trace] == [t.objective for t in runs[0].trace]
