@@ -281,8 +281,8 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
   uint64_t* pub = mx_empty + MXB;                                            // [2] local: partials pushed
   uint64_t* dready = pub + 2;                                                // [2] local: delta_b published
   uint64_t* dmask = dready + 2;                                              // [NB] bit l: row l is a data row
-  double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [SW] current w slice
-  int64_t* iring = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(wsm + SW) + 15) & ~uintptr_t(15));  // [IA][L]
+  double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [2][SW] w slice by block parity
+  int64_t* iring = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(wsm + 2 * SW) + 15) & ~uintptr_t(15));  // [IA][L]
   uint64_t* ifull = reinterpret_cast<uint64_t*>(iring + IA * L);             // [2][IA] (per producer)
   uint64_t* wide = ifull + 2 * IA;                                           // [NB][NWID] fp32 rows widened
 
@@ -529,7 +529,8 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       w[c] = act[c] ? a.state[col0 + c] : 0.0;
       S[c] = act[c] ? a.state[R.ld + col0 + c] : 0.0;
       mu[c] = act[c] ? a.mu[col0 + c] : 0.0;
-      wsm[tid * CPT + c] = w[c];
+      wsm[tid * CPT + c] = w[c];  // w at the start of block 0 in both buffers
+      wsm[SW + tid * CPT + c] = w[c];
     }
     named_bar(1, NT);
     unsigned long long tp[9] = {};
@@ -554,10 +555,14 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
       double wl[CPL];
       const int64_t valid = R.ld - slice0;  // columns past the copied slice hold stale smem
       bool lok[CPL];
+      // w at the start of block bb - 1 (the look-ahead dots), in buffer (bb - 1) & 1; the
+      // update of block bb - 1 writes the other buffer, so a warp that is already
+      // updating cannot overwrite values another warp is still loading here
+      const double* wb = wsm + ((bb + 1) & 1) * SW;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         lok[c] = (int64_t)(lane + 32 * c) < valid;
-        wl[c] = wsm[lane + 32 * c];
+        wl[c] = wb[lane + 32 * c];
       }
       double v[RPW];
 #pragma unroll
@@ -608,6 +613,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
     // prologue: a_0 = R_0 w_0 directly
     if (nblk > 0) {
       dots(0);
+      named_bar(1, NT);  // dots(0) read buffer 1, which the update of block 0 rewrites
     }
     for (int64_t b = 0; b < nblk; ++b) {
       const int slot = (int)(b % NB);
@@ -650,7 +656,7 @@ __global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_ke
         const double w0 = w[c];
         S[c] += (double)Lb * w0 - a.eta * v - a.eta * mu[c] * (0.5 * (double)Lb * (double)(Lb + 1));
         w[c] = w0 - a.eta * u - a.eta * (double)Lb * mu[c];
-        wsm[tid * CPT + c] = w[c];
+        wsm[((b + 1) & 1) * SW + tid * CPT + c] = w[c];  // w at the start of block b + 1
       }
       named_bar(1, NT);  // every consumer is done with rows[slot]; new w visible
       if (tid == 0) mbar_arrive_local(&empty[slot]);
@@ -680,7 +686,7 @@ template <int CPT, int L, int MXB, int NT>
 constexpr size_t sstep_chain_smem() {
   return (size_t)chain_nb(NT * CPT) * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
          sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 5 * L) +
-         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * NT * CPT +
+         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * 2 * NT * CPT +
          sizeof(int64_t) * kChainIdxAhead * L + sizeof(uint64_t) * (2 * kChainIdxAhead + 2 * chain_nb(NT * CPT)) + 128;
 }
 
