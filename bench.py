@@ -313,6 +313,8 @@ def run_ours(args, cfg):
 
     if not args.no_extras:
         out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
+        if world == 1:
+            out["lanczos_fp32"] = lanczos_fp32_extra(sk, ctx)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         X = data.download().astype(np.float64)
         dt, kk, thr, kind = cpu_full_gradient_sample(X, y, cfg.lam, sv.left, sv.singular_values,
@@ -353,6 +355,40 @@ def lanczos_flops(cfg, n):
     """2ndk + 4ndk(q-1) + 2nd*qk + n(qk)^2 algorithmic flops."""
     d, k, q = cfg.d, cfg.k, cfg.q
     return 2 * n * d * k + 4 * n * d * k * (q - 1) + 2 * n * d * q * k + n * (q * k) ** 2
+
+
+TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (B200_PROFILING.md table; not measured on this pool)
+
+
+def lanczos_fp32_extra(sk, ctx):
+    """The fp32-storage sketch on tcgen05 (3xTF32) at the c3 shape (configs[2]: n = 2^20,
+    d = 2048, k = 128, q = 3): warm block_lanczos wall time and the Krylov + Rayleigh-Ritz
+    products' device time (CUDA events around them), as fp32-algorithmic TFLOP/s and as
+    raw TF32 tensor throughput (3 MMAs per product) against the dense TF32 peak."""
+    from paper_1602_02350_b200 import configs
+    c3 = configs.CONFIGS["c3"]
+    data = sk.DataMatrix.generate(sk.SynthSpec(c3.n, c3.d, c3.dtype, c3.seed, c3.spectrum, c3.spectrum_param,
+                                               c3.t_scale, c3.tau), ctx)
+    a = data.scaled(1 / math.sqrt(c3.n))
+    lc = sk.LanczosConfig(c3.k, 0.5, c3.seed, c3.q)
+    sk.block_lanczos(a, lc, want_right=False)  # cold call: workspaces
+    ctx.synchronize()
+    ctx.profile(True)
+    t0 = time.perf_counter()
+    sk.block_lanczos(a, lc, want_right=False)
+    ctx.synchronize()
+    wall = time.perf_counter() - t0
+    gemm_ms, _ = ctx.profile_read("lanczos_gemm")
+    ctx.profile(False)
+    flops = lanczos_gemm_flops(c3, c3.n)
+    tf = flops / (gemm_ms * 1e-3) / 1e12
+    del a, data
+    return {"config": "c3 (fp32 storage, n=1048576, d=2048, k=128, q=3)", "seconds": round(wall, 4),
+            "gemm_ms": round(gemm_ms, 3), "gemm_tflops_fp32_equiv": round(tf, 1),
+            "tf32_raw_tflops": round(3 * tf, 1), "tf32_peak_tflops": TF32_DENSE_TFLOPS,
+            "tf32_frac": round(3 * tf / TF32_DENSE_TFLOPS, 3),
+            "note": "3xTF32 tcgen05 products (hi.hi + hi.lo + lo.hi); peak = dense TF32 nominal from "
+                    "B200_PROFILING.md (the measured bf16 burst is 0.74x its nominal)"}
 
 
 def solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx):
