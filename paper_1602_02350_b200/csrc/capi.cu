@@ -760,11 +760,11 @@ EncodeTiledFn encode_tiled() {
 // 2-D fp32 tensor map over a row-major matrix (rows x cols, row stride ld
 // elements), box = box_rows x 32 columns, 128-byte swizzle.
 CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int box_cols = 32) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
@@ -773,21 +773,47 @@ CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t 
   return m;
 }
 
+template <bool A_MN, int BN, int CS>
+void tc_launch_cs(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,
+                  int splits) {
+  // CS > 1: each CTA of a cluster loads BN / CS rows of B and multicasts them
+  const CUtensorMap mbh = make_tmap_f32(Bh, g.N, g.K, ldb, BN / CS);
+  const CUtensorMap mbl = make_tmap_f32(Bl, g.N, g.K, ldb, BN / CS);
+  constexpr size_t smem = tc_gemm_smem<BN>();
+  auto kern = tc_gemm_tf32x3_kernel<A_MN, BN, CS>;
+  static bool configured = false;
+  if (!configured) {
+    SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(ceil_div(g.M, TC_BM) * ceil_div(g.N, BN)), 1, splits);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SKR_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbh, mbl, g));
+  SKR_LAUNCHED(&c);
+}
+
+// B-tile multicast across clusters of 4 consecutive M tiles for the X^T products (B =
+// Pi^T / T^T streams from HBM, re-read by every M tile) when the M tiles come in
+// multiples of 4 and B is 128 rows wide: c3 12.3 -> 8.1 ms, c4 186 -> 132 ms.  Not for
+// the X Q^T products (B = Q is L2-resident; clustered they ran 0-20 % slower) nor at
+// BN = 64 (c5: B is half a stage; +16 %).  SKR_TC_CLUSTER=1 disables.
 template <bool A_MN, int BN>
 void tc_launch(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,
                int splits) {
-  const CUtensorMap mbh = make_tmap_f32(Bh, g.N, g.K, ldb, BN);
-  const CUtensorMap mbl = make_tmap_f32(Bl, g.N, g.K, ldb, BN);
-  constexpr size_t smem = tc_gemm_smem<BN>();
-  static bool configured = false;
-  if (!configured) {
-    SKR_CUDA(cudaFuncSetAttribute(tc_gemm_tf32x3_kernel<A_MN, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    configured = true;
-  }
-  dim3 grid((unsigned)(ceil_div(g.M, TC_BM) * ceil_div(g.N, BN)), 1, splits);
-  tc_gemm_tf32x3_kernel<A_MN, BN><<<grid, TC_THREADS, smem, c.stream>>>(ma, mbh, mbl, g);
-  SKR_LAUNCHED(&c);
+  static const int env_cs = getenv("SKR_TC_CLUSTER") ? atoi(getenv("SKR_TC_CLUSTER")) : 4;
+  const int64_t mtn = ceil_div(g.M, TC_BM);
+  if (A_MN && BN == 128 && env_cs == 4 && mtn % 4 == 0) tc_launch_cs<A_MN, BN, 4>(c, ma, Bh, Bl, ldb, g, splits);
+  else tc_launch_cs<A_MN, BN, 1>(c, ma, Bh, Bl, ldb, g, splits);
 }
 
 inline int tc_bn(int64_t N) { return N <= 64 ? 64 : 128; }
@@ -797,7 +823,10 @@ inline int tc_bn(int64_t N) { return N <= 64 ? 64 : 128; }
 template <bool A_MN>
 void tc_run(Ctx& c, const float* A, int64_t lda, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,
             int splits) {
-  const CUtensorMap ma = A_MN ? make_tmap_f32(A, g.K, g.M, lda, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+  // MN-major A (the data matrix read as its transpose) only feeds the converter warps
+  // (A_hi and A_lo both go to TMEM): one unswizzled 32 (K) x 128 (M) box per stage,
+  // 512 contiguous bytes per row of X
+  const CUtensorMap ma = A_MN ? make_tmap_f32(A, g.K, g.M, lda, TC_BK, CU_TENSOR_MAP_SWIZZLE_NONE, TC_BM)
                               : make_tmap_f32(A, g.M, g.K, lda, TC_BM);
   const int bn = tc_bn(g.N);
   if (bn == 64) tc_launch<A_MN, 64>(c, ma, Bh, Bl, ldb, g, splits);

@@ -19,7 +19,10 @@
 //     the stacked [B_hi; B_lo] tile, so A_hi is read once per K step; the two
 //     accumulator halves are summed in fp64 by the epilogue.
 // MN-major A (the X^T products) lets X serve both orientations from one copy:
-// no transposed duplicate of the data matrix is ever built.
+// no transposed duplicate of the data matrix is ever built.  Its converter warps
+// read the unswizzled 32 x 128 tile and put both A_hi and A_lo into TMEM, so every
+// MMA reads A as a K-major TMEM operand; clusters of 4 M tiles share the B tile
+// by TMA multicast (tc_launch).
 //
 // One CTA = one 128 x BN output tile over a K-range (split-K over gridDim.z);
 // N > 128 runs as several 128-wide tiles (stacked hi/lo needs 2N <= 256):
@@ -61,6 +64,17 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// the same box, written to the same shared offset of every CTA in ctaMask, each
+// CTA's mbarrier at `bar`'s offset receiving the bytes it got
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
 
@@ -130,6 +144,15 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// arrive on the barrier at `bar`'s offset in every CTA of ctaMask once the MMAs complete
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 __device__ __forceinline__ float tf32_lo(float v) { return v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
@@ -144,7 +167,12 @@ struct TcGemmArgs {
   int64_t ldt;     // row stride of out32 / out32lo
 };
 
-template <bool A_MN, int BN>
+// CS > 1: a cluster of CS CTAs with consecutive M tiles and the same N tile / K range
+// shares the B tiles — each CTA loads 1/CS of the rows and multicasts them to all, so
+// L2 -> SM traffic for B drops CS-fold (B was 2/3 of each stage's bytes, re-read by
+// every M tile); a stage is refilled once the MMAs of every CTA in the cluster are done
+// with it (the MMA commit arrives on all CTAs' empty barriers).
+template <bool A_MN, int BN, int CS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
                       const __grid_constant__ CUtensorMap mapBl, TcGemmArgs g) {
@@ -152,18 +180,35 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
   constexpr int STAGE = (int)tc_stage_bytes<BN>();
   constexpr int NST = tc_stages<BN>();
   constexpr uint32_t ACC = tc_acc_cols<BN>();
+  // TMEM columns per stage: A_lo (32); MN-major A also keeps A_hi in TMEM (32 more):
+  // every MMA then reads A as a K-major TMEM operand — the MN-major shared-memory
+  // A operand ran the tensor pipe at 45 % vs 61 % for K-major (ncu, c3)
+  constexpr uint32_t SLOT = A_MN ? 64u : 32u;
+  static_assert(tc_acc_cols<BN>() + SLOT * tc_stages<BN>() <= 512, "TMEM budget");
   constexpr uint32_t TMEM_COLS = 512;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by offsetting the shared array itself so the compiler keeps the shared address space (LDS, not LD)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t bar_tma[NST], bar_conv[NST], bar_empty[NST], bar_done;
+  // bar_tma: the A tile landed (the converters need only A); bar_tb: the B tiles landed
+  __shared__ __align__(8) uint64_t bar_tma[NST], bar_tb[NST], bar_conv[NST], bar_empty[NST], bar_done;
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // tiles linearised N-fastest: the CTAs sharing an A tile run side by side, so A
-  // comes from HBM once and from L2 for the other N tiles
+  // comes from HBM once and from L2 for the other N tiles.  Clusters (CS > 1): groups
+  // of CS consecutive M tiles, N tile next, then the next group — a cluster shares its
+  // B tile, consecutive clusters share their A tiles
   const int64_t ntn = (g.N + BN - 1) / BN;
-  const int64_t m0 = (int64_t)(blockIdx.x / ntn) * TC_BM, n0 = (int64_t)(blockIdx.x % ntn) * BN;
+  int64_t mt, nt;
+  if (CS > 1) {
+    const int64_t t = blockIdx.x / CS;
+    nt = t % ntn;
+    mt = (t / ntn) * CS + blockIdx.x % CS;
+  } else {
+    mt = blockIdx.x / ntn;
+    nt = blockIdx.x % ntn;
+  }
+  const int64_t m0 = mt * TC_BM, n0 = nt * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
   const int64_t kend = min(g.K, kbeg + g.kchunk);
   const int nk = kend > kbeg ? (int)((kend - kbeg + TC_BK - 1) / TC_BK) : 0;
@@ -171,8 +216,9 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&bar_tma[s], 1);
+      mbar_init(&bar_tb[s], 1);
       mbar_init(&bar_conv[s], 128);
-      mbar_init(&bar_empty[s], 1);
+      mbar_init(&bar_empty[s], CS);  // one MMA-commit arrival per CTA of the cluster
     }
     mbar_init(&bar_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -186,9 +232,13 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  if (CS > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast lands
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  uint32_t crank = 0;
+  if (CS > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  constexpr uint16_t CMASK = (uint16_t)((1u << CS) - 1u);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -196,39 +246,60 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
         const int s = kb % NST;
         if (kb >= NST) mbar_wait(&bar_empty[s], (uint32_t)(((kb / NST) - 1) & 1));
         unsigned char* st = smem + (size_t)s * STAGE;
-        mbar_expect_tx(&bar_tma[s], TC_A_BYTES + 2 * B_BYTES);
+        mbar_expect_tx(&bar_tma[s], TC_A_BYTES);
+        mbar_expect_tx(&bar_tb[s], 2 * B_BYTES);
         const int kc = (int)(kbeg + (int64_t)kb * TC_BK);
         if (A_MN) {
-          // A^T stored K x M row-major (the data matrix): four 32(M) x 32(K) boxes
-#pragma unroll
-          for (int b = 0; b < 4; ++b) tma_load_2d(st + 4096 * b, &mapA, &bar_tma[s], (int)m0 + 32 * b, kc);
+          // A^T stored K x M row-major (the data matrix): one unswizzled 128 (M) x 32 (K) box
+          tma_load_2d(st, &mapA, &bar_tma[s], (int)m0, kc);
         } else {
           tma_load_2d(st, &mapA, &bar_tma[s], kc, (int)m0);
         }
-        tma_load_2d(st + TC_A_BYTES, &mapBh, &bar_tma[s], kc, (int)n0);
-        tma_load_2d(st + TC_A_BYTES + B_BYTES, &mapBl, &bar_tma[s], kc, (int)n0);
+        if (CS > 1) {
+          // this CTA's BN/CS rows of B_hi and B_lo, to every CTA of the cluster
+          constexpr int SR = BN / CS;
+          const int off = (int)crank * SR;
+          tma_load_2d_mc(st + TC_A_BYTES + off * 128, &mapBh, &bar_tb[s], kc, (int)n0 + off, CMASK);
+          tma_load_2d_mc(st + TC_A_BYTES + B_BYTES + off * 128, &mapBl, &bar_tb[s], kc, (int)n0 + off, CMASK);
+        } else {
+          tma_load_2d(st + TC_A_BYTES, &mapBh, &bar_tb[s], kc, (int)n0);
+          tma_load_2d(st + TC_A_BYTES + B_BYTES, &mapBl, &bar_tb[s], kc, (int)n0);
+        }
       }
     }
   } else if (warp == 1) {
     const uint32_t id_w = tc_idesc_tf32(tc_concat<BN>() ? 2 * BN : BN, A_MN);  // A_hi x B (stacked when concat)
     const uint32_t id_n = tc_idesc_tf32(BN, A_MN);
     const uint32_t id_t = tc_idesc_tf32(BN, false);  // A from TMEM is K-major by construction
+    const uint32_t id_wt = tc_idesc_tf32(tc_concat<BN>() ? 2 * BN : BN, false);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % NST;
       mbar_wait(&bar_tma[s], (uint32_t)((kb / NST) & 1));
+      mbar_wait(&bar_tb[s], (uint32_t)((kb / NST) & 1));
       mbar_wait(&bar_conv[s], (uint32_t)((kb / NST) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (lane == 0) {
         const unsigned char* st = smem + (size_t)s * STAGE;
         const unsigned char* bhi = st + TC_A_BYTES;
         const unsigned char* blo = st + TC_A_BYTES + B_BYTES;
-        const uint32_t alo = tmem + ACC + 32u * (uint32_t)s;
+        const uint32_t alo = tmem + ACC + SLOT * (uint32_t)s;
+        const uint32_t ahi = alo + 32u;  // A_MN only
 #pragma unroll
         for (int k = 0; k < TC_BK / 8; ++k) {  // UMMA_K = 8 tf32
-          const uint64_t dah = A_MN ? umma_desc_mn_sw128_32b(st + 1024 * k) : umma_desc_k_sw128(st + 32 * k);
+          const uint64_t dah = umma_desc_k_sw128(st + 32 * k);  // K-major A (A_MN: unused)
           const uint64_t dbh = umma_desc_k_sw128(bhi + 32 * k);
           const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-          if (tc_concat<BN>()) {
+          if (A_MN) {
+            if (tc_concat<BN>()) {
+              tc_mma_ts(tmem, ahi + 8 * k, dbh, id_wt, acc0);  // [hi.hi | hi.lo] in columns [0, 2 BN)
+              tc_mma_ts(tmem, alo + 8 * k, dbh, id_t, 1u);     // + lo.hi into [0, BN)
+            } else {
+              const uint64_t dbl = umma_desc_k_sw128(blo + 32 * k);
+              tc_mma_ts(tmem, alo + 8 * k, dbh, id_t, acc0);
+              tc_mma_ts(tmem, ahi + 8 * k, dbl, id_t, 1u);
+              tc_mma_ts(tmem, ahi + 8 * k, dbh, id_t, 1u);
+            }
+          } else if (tc_concat<BN>()) {
             tc_mma_ss(tmem, dah, dbh, id_w, acc0);         // [hi.hi | hi.lo] in columns [0, 2 BN)
             tc_mma_ts(tmem, alo + 8 * k, dbh, id_t, 1u);   // + lo.hi into [0, BN)
           } else {
@@ -238,7 +309,8 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
             tc_mma_ss(tmem, dah, dbh, id_n, 1u);
           }
         }
-        tc_commit(&bar_empty[s]);                 // smem stage + TMEM A_lo slot reusable
+        if (CS > 1) tc_commit_mc(&bar_empty[s], CMASK);  // every CTA may refill this stage (its B slice lands everywhere)
+        else tc_commit(&bar_empty[s]);                 // smem stage + TMEM A_lo slot reusable
         if (kb == nk - 1) tc_commit(&bar_done);   // accumulator complete
       }
       __syncwarp();
@@ -252,14 +324,13 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
       const int s = kb % NST;
       mbar_wait(&bar_tma[s], (uint32_t)((kb / NST) & 1));
       const unsigned char* st = smem + (size_t)s * STAGE;
-      uint32_t v[32];
+      uint32_t v[32], h[32];
       if (A_MN) {
-        // element (r, k): box r/32, line k, 32-byte chunk ((r%32)/8) ^ (k%4), word r%8
-        const unsigned char* box = st + 4096 * (r >> 5);
-        const int cr = (r & 31) >> 3, wr = r & 7;
+        // element (r, k) at line k, word r (unswizzled 32 x 128 box): conflict-free per k
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          const float a = *reinterpret_cast<const float*>(box + 128 * k + 32 * (cr ^ (k & 3)) + 4 * wr);
+          const float a = *reinterpret_cast<const float*>(st + 512 * k + 4 * r);
+          h[k] = __float_as_uint(a);  // read as TF32 by the MMA, like the shared-memory operand
           v[k] = __float_as_uint(tf32_lo(a));
         }
       } else {
@@ -274,7 +345,16 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
           v[4 * j + 3] = __float_as_uint(tf32_lo(q.w));
         }
       }
-      const uint32_t taddr = tmem + ((uint32_t)(32 * quarter) << 16) + ACC + 32u * (uint32_t)s;
+      const uint32_t taddr = tmem + ((uint32_t)(32 * quarter) << 16) + ACC + SLOT * (uint32_t)s;
+      if (A_MN)
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr + 32u),
+            "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(h[8]),
+            "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(h[16]),
+            "r"(h[17]), "r"(h[18]), "r"(h[19]), "r"(h[20]), "r"(h[21]), "r"(h[22]), "r"(h[23]), "r"(h[24]),
+            "r"(h[25]), "r"(h[26]), "r"(h[27]), "r"(h[28]), "r"(h[29]), "r"(h[30]), "r"(h[31])
+            : "memory");
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
           "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
@@ -332,6 +412,7 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
+  if (CS > 1) cluster_sync_all();  // no CTA exits while peers may still multicast into it / arrive on it
 }
 
 // lo = x - trunc_tf32(x) of an fp32 matrix (the B operands' lo arrays)
