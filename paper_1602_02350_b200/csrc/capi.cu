@@ -117,7 +117,14 @@ struct skr_problem {
   DBuf<double> Pm, lz_r, lz_r2, lz_s, lz_g1, lz_g2, lz_v, lz_loss, lz_UT;
   // pinned host staging for the host-buffer entry points: [0, ld) w, [ld, 2 ld] mu and the objective
   double* io_host = nullptr;
+  // the host-buffer full gradient as one CUDA graph (H2D of w, the pass, D2H of mu and
+  // the objective), captured on the second call once the workspaces exist
+  cudaGraphExec_t fg_exec = nullptr;
+  int fg_mode = -1, fg_launches = 0;
+  int64_t fg_calls = 0;
+  const void* fg_ptrs[3] = {nullptr, nullptr, nullptr};  // workspaces the graph captured
   ~skr_problem() {
+    if (fg_exec) cudaGraphExecDestroy(fg_exec);
     if (io_host) cudaFreeHost(io_host);
   }
 };
@@ -2308,10 +2315,37 @@ int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) 
     const int64_t d = p->d, ld = p->ld;
     if (!p->io_host) SKR_CUDA(cudaMallocHost(&p->io_host, sizeof(double) * (2 * ld + 1)));  // first call only
     std::memcpy(p->io_host, w, sizeof(double) * d);
-    SKR_CUDA(cudaMemcpyAsync(p->wv.get(), p->io_host, sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
-    problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->muv.get() + ld : nullptr);
-    SKR_CUDA(cudaMemcpyAsync(p->io_host + ld, p->muv.get(), sizeof(double) * (obj ? ld + 1 : d),
-                             cudaMemcpyDeviceToHost, c.stream));
+    auto enqueue = [&] {
+      SKR_CUDA(cudaMemcpyAsync(p->wv.get(), p->io_host, sizeof(double) * d, cudaMemcpyHostToDevice, c.stream));
+      problem_fullgrad(p, p->wv.get(), p->muv.get(), obj ? p->muv.get() + ld : nullptr);
+      SKR_CUDA(cudaMemcpyAsync(p->io_host + ld, p->muv.get(), sizeof(double) * (obj ? ld + 1 : d),
+                               cudaMemcpyDeviceToHost, c.stream));
+    };
+    static const bool no_graph = getenv("SKR_NO_GRAPH") != nullptr;
+    const int mode = obj ? 1 : 0;
+    if (!no_graph && !c.dist && !c.prof_on && !p->lazy && p->fg_calls >= 1) {
+      const void* ptrs[3] = {p->part_g.get(), p->part_loss.get(), p->sums.get()};
+      if (!p->fg_exec || p->fg_mode != mode || !std::equal(ptrs, ptrs + 3, p->fg_ptrs)) {
+        if (p->fg_exec) SKR_CUDA(cudaGraphExecDestroy(p->fg_exec));
+        p->fg_exec = nullptr;
+        cudaGraph_t graph = nullptr;
+        const uint64_t l0 = c.launches;
+        SKR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        enqueue();
+        SKR_CUDA(cudaStreamEndCapture(c.stream, &graph));
+        SKR_CUDA(cudaGraphInstantiate(&p->fg_exec, graph, 0));
+        SKR_CUDA(cudaGraphDestroy(graph));
+        p->fg_mode = mode;
+        std::copy(ptrs, ptrs + 3, p->fg_ptrs);
+        p->fg_launches = (int)(c.launches - l0);
+        c.launches = l0;
+      }
+      SKR_CUDA(cudaGraphLaunch(p->fg_exec, c.stream));
+      c.launches += p->fg_launches;
+    } else {
+      enqueue();
+    }
+    ++p->fg_calls;
     c.sync();
     if (mu) std::memcpy(mu, p->io_host + ld, sizeof(double) * d);
     if (obj) *obj = p->io_host[2 * ld];
