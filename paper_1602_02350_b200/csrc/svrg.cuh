@@ -23,7 +23,7 @@ namespace skr {
 constexpr int CUM_T = 2048;
 __global__ void __launch_bounds__(512) cumulative_kernel(const double* __restrict__ beta, int64_t N,
                                                          double* __restrict__ cum, double* __restrict__ total_out) {
-  __shared__ double buf[2][CUM_T];
+  __shared__ __align__(16) double buf[2][CUM_T];
   __shared__ double s_total;
   const int t = threadIdx.x, nl = blockDim.x - 32;  // loader threads: t >= 32
   const int64_t ntile = (N + CUM_T - 1) / CUM_T;
@@ -51,7 +51,17 @@ __global__ void __launch_bounds__(512) cumulative_kernel(const double* __restric
     if (t == 0) {
       const int cnt = (int)min((int64_t)CUM_T, N - k * CUM_T);
       const double* b = buf[k & 1];
-      for (int j = 0; j < cnt; ++j) total = __dadd_rn(total, b[j]);
+      int j = 0;
+      // 16 operands staged in registers per group (8-byte aligned 16-byte loads), so the
+      // only serial dependence left is the add itself
+      for (; j + 16 <= cnt; j += 16) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) *reinterpret_cast<double2*>(&v[q]) = *reinterpret_cast<const double2*>(&b[j + q]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) total = __dadd_rn(total, v[q]);
+      }
+      for (; j < cnt; ++j) total = __dadd_rn(total, b[j]);
     }
     __syncthreads();
   }
@@ -70,7 +80,20 @@ __global__ void __launch_bounds__(512) cumulative_kernel(const double* __restric
     if (t == 0) {
       const int cnt = (int)min((int64_t)CUM_T, N - k * CUM_T);
       double* b = buf[k & 1];
-      for (int j = 0; j < cnt; ++j) {
+      int j = 0;
+      for (; j + 16 <= cnt; j += 16) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) *reinterpret_cast<double2*>(&v[q]) = *reinterpret_cast<const double2*>(&b[j + q]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          run = __dadd_rn(run, v[q]);
+          v[q] = run;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) *reinterpret_cast<double2*>(&b[j + q]) = *reinterpret_cast<const double2*>(&v[q]);
+      }
+      for (; j < cnt; ++j) {
         run = __dadd_rn(run, b[j]);
         b[j] = run;
       }
