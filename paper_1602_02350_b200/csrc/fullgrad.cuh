@@ -464,6 +464,7 @@ fullgrad_rowring_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const do
   bool act[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) act[c] = (int64_t)lane + 32 * c < chunks_per_row;
+  const bool all_act = chunks_per_row >= 32 * CH;  // uniform: the fast path below needs no selects
   double acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.0;
@@ -475,31 +476,58 @@ fullgrad_rowring_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const do
     mbar_wait(&bars[s], (uint32_t)((j / NB) & 1));
     const unsigned char* slot = mine + (size_t)s * row_bytes;
     T x[E];
-    if constexpr (sizeof(T) == 8) {
-      const double2* src = reinterpret_cast<const double2*>(slot);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const double2 v = act[c] ? src[lane + 32 * c] : make_double2(0.0, 0.0);
-        x[2 * c] = v.x;
-        x[2 * c + 1] = v.y;
-      }
-    } else {
-      const float4* src = reinterpret_cast<const float4*>(slot);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const float4 v = act[c] ? src[lane + 32 * c] : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[4 * c] = v.x;
-        x[4 * c + 1] = v.y;
-        x[4 * c + 2] = v.z;
-        x[4 * c + 3] = v.w;
-      }
-    }
     double sdot = 0.0;
+    if (all_act) {
+      // every chunk of every lane is inside the row: no per-element selects
+      if constexpr (sizeof(T) == 8) {
+        const double2* src = reinterpret_cast<const double2*>(slot);
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if (!act[c]) continue;
+        for (int c = 0; c < CH; ++c) {
+          const double2 v = src[lane + 32 * c];
+          x[2 * c] = v.x;
+          x[2 * c + 1] = v.y;
+        }
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(slot);
 #pragma unroll
-      for (int e = 0; e < PER; ++e) sdot = fma((double)x[c * PER + e], sw[(lane + 32 * c) * PER + e], sdot);
+        for (int c = 0; c < CH; ++c) {
+          const float4 v = src[lane + 32 * c];
+          x[4 * c] = v.x;
+          x[4 * c + 1] = v.y;
+          x[4 * c + 2] = v.z;
+          x[4 * c + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int e = 0; e < PER; ++e) sdot = fma((double)x[c * PER + e], sw[(lane + 32 * c) * PER + e], sdot);
+    } else {
+      if constexpr (sizeof(T) == 8) {
+        const double2* src = reinterpret_cast<const double2*>(slot);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const double2 v = act[c] ? src[lane + 32 * c] : make_double2(0.0, 0.0);
+          x[2 * c] = v.x;
+          x[2 * c + 1] = v.y;
+        }
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(slot);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const float4 v = act[c] ? src[lane + 32 * c] : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[4 * c] = v.x;
+          x[4 * c + 1] = v.y;
+          x[4 * c + 2] = v.z;
+          x[4 * c + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        if (!act[c]) continue;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) sdot = fma((double)x[c * PER + e], sw[(lane + 32 * c) * PER + e], sdot);
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
