@@ -72,6 +72,11 @@ int64_t skr_ctx_kernel_launches(const skr_ctx* ctx);
  * streaming kernel; "svrg_epoch": the K10 inner loop). */
 int skr_ctx_profile(skr_ctx* ctx, int enable);
 int skr_ctx_profile_read(skr_ctx* ctx, const char* key, double* total_ms, int64_t* launches);
+/* cap the grid of the SVRG inner loop's PREP kernel (blocks are grid-strided);
+ * 0 = one CTA per block (default).  Concurrent chains on one GPU (the eta-grid
+ * protocol of bench.cpp:140-193, one context per lane) keep SMs for each
+ * other's clusters this way. */
+int skr_ctx_set_prep_cap(skr_ctx* ctx, int ctas);
 
 /* ---- data: DataMatrix (data_matrix.hpp:18-61) -------------------------- */
 /* rows: n x d row-major host array of `dtype`.  On a distributed context the

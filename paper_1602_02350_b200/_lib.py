@@ -48,6 +48,7 @@ SIGNATURES = {
     "skr_ctx_kernel_launches": (i64, [vp]),
     "skr_ctx_profile": (cint, [vp, cint]),
     "skr_ctx_profile_read": (cint, [vp, cp, P(f64), P(i64)]),
+    "skr_ctx_set_prep_cap": (cint, [vp, cint]),
     "skr_data_create": (cint, [vp, vp, i64, i64, cint, P(vp)]),
     "skr_data_create_device": (cint, [vp, vp, i64, i64, i64, cint, P(vp)]),
     "skr_data_scaled": (cint, [vp, f64, P(vp)]),

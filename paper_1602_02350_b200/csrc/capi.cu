@@ -965,7 +965,8 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     const int64_t steps = std::min(chunk_steps, m - s0);
     const int64_t nblk = (steps + L - 1) / L;
     if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
-    prep<<<(unsigned)nblk, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
+    const int64_t pgrid = c.prep_cap > 0 ? std::min<int64_t>(nblk, c.prep_cap) : nblk;
+    prep<<<(unsigned)pgrid, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
                                                      p->reg_coef, mu, snap, eta, Mb, pb, Xb);
     SKR_LAUNCHED(&c);
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
@@ -1474,6 +1475,13 @@ int skr_ctx_destroy(skr_ctx* ctx) {
 }
 
 int skr_ctx_synchronize(skr_ctx* ctx) { return guard([&] { C_(ctx).sync(); }); }
+
+int skr_ctx_set_prep_cap(skr_ctx* ctx, int ctas) {
+  return guard([&] {
+    if (ctas < 0) raise(SKR_EPARAM, "prep cap must be >= 0");
+    C_(ctx).prep_cap = ctas;
+  });
+}
 
 int skr_ctx_profile(skr_ctx* ctx, int enable) {
   return guard([&] {

@@ -145,6 +145,7 @@ struct Ctx {
   cusolverDnHandle_t solver = nullptr;
   ncclComm_t comm = nullptr;
   int sm_count = 148;
+  int prep_cap = 0;  // K10 PREP grid cap (0: one CTA per block)
   int64_t launches = 0;
   DBuf<uint64_t> mt_polys;  // mt19937_64 jump polynomials per tree level (device copy)
 

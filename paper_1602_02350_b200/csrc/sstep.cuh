@@ -72,92 +72,98 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
   __shared__ double cvec[L];
   __shared__ int64_t ridx[2 * L];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t t0 = (int64_t)blockIdx.x * L;
-  const bool look = blockIdx.x > 0;  // the previous block of this launch exists (and is full)
-  if (tid < L) {
-    const int64_t t = t0 + tid;
-    const int64_t i = t < steps ? idx[t] : -1;
-    ridx[tid] = i;
-    ridx[L + tid] = look ? idx[t0 - L + tid] : -1;
-    cvec[tid] = i < 0 ? 0.0 : (i < R.n ? data_coef : reg_coef) * inv_nq[i];
-  }
-  __syncthreads();
-  auto fetch = [&](int64_t c0, double (&v)[PER]) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * 256, r = e / KC;
-      const int64_t col = c0 + e % KC;
-      double x = 0.0;
-      if (col < R.d) {
-        if (r < 2 * L) {
-          const int64_t i = ridx[r];
-          if (i >= 0) x = row_elem<T>(R, i, col);
-        } else if (r == 2 * L) {
-          x = mu[col];
-        } else if (r == 2 * L + 1) {
-          x = wbar[col];
+  // grid-strided over the chunk's blocks: a capped grid (skr_ctx_set_prep_cap) leaves
+  // SMs to concurrent chains (eta-grid lanes)
+  const int64_t nblk = (steps + L - 1) / L;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t t0 = (int64_t)blk * L;
+    const bool look = blk > 0;  // the previous block of this launch exists (and is full)
+    if (tid < L) {
+      const int64_t t = t0 + tid;
+      const int64_t i = t < steps ? idx[t] : -1;
+      ridx[tid] = i;
+      ridx[L + tid] = look ? idx[t0 - L + tid] : -1;
+      cvec[tid] = i < 0 ? 0.0 : (i < R.n ? data_coef : reg_coef) * inv_nq[i];
+    }
+    __syncthreads();
+    auto fetch = [&](int64_t c0, double (&v)[PER]) {
+  #pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = tid + q * 256, r = e / KC;
+        const int64_t col = c0 + e % KC;
+        double x = 0.0;
+        if (col < R.d) {
+          if (r < 2 * L) {
+            const int64_t i = ridx[r];
+            if (i >= 0) x = row_elem<T>(R, i, col);
+          } else if (r == 2 * L) {
+            x = mu[col];
+          } else if (r == 2 * L + 1) {
+            x = wbar[col];
+          }
+        }
+        v[q] = x;
+      }
+    };
+    const int mt = warp & 3, nb = warp >> 2;  // m-tile; n-tiles nb, nb+2, ...
+    double acc[5][2] = {};
+    double v[PER];
+    fetch(0, v);
+    for (int64_t c0 = 0; c0 < R.d; c0 += KC) {
+      __syncthreads();
+  #pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = tid + q * 256;
+        st[(e / KC) * SP + e % KC] = v[q];
+      }
+      __syncthreads();
+      if (c0 + KC < R.d) fetch(c0 + KC, v);  // next chunk in flight during the products
+  #pragma unroll
+      for (int k4 = 0; k4 < KC; k4 += 4) {
+        const double a = st[(8 * mt + (lane >> 2)) * SP + k4 + (lane & 3)];
+  #pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const int nt = nb + 2 * j;
+          if (nt < NTN) dmma_884(acc[j][0], acc[j][1], a, st[(8 * nt + (lane >> 2)) * SP + k4 + (lane & 3)]);
         }
       }
-      v[q] = x;
-    }
-  };
-  const int mt = warp & 3, nb = warp >> 2;  // m-tile; n-tiles nb, nb+2, ...
-  double acc[5][2] = {};
-  double v[PER];
-  fetch(0, v);
-  for (int64_t c0 = 0; c0 < R.d; c0 += KC) {
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * 256;
-      st[(e / KC) * SP + e % KC] = v[q];
     }
     __syncthreads();
-    if (c0 + KC < R.d) fetch(c0 + KC, v);  // next chunk in flight during the products
-#pragma unroll
-    for (int k4 = 0; k4 < KC; k4 += 4) {
-      const double a = st[(8 * mt + (lane >> 2)) * SP + k4 + (lane & 3)];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        const int nt = nb + 2 * j;
-        if (nt < NTN) dmma_884(acc[j][0], acc[j][1], a, st[(8 * nt + (lane >> 2)) * SP + k4 + (lane & 3)]);
+    double* res = st;  // res[i*RS + n]: n < L: G, L..2L-1: X, 2L: e, 2L+1: b
+  #pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int nt = nb + 2 * j;
+      if (nt < NTN) {
+        const int i = 8 * mt + (lane >> 2), n = 8 * nt + 2 * (lane & 3);
+        res[i * RS + n] = acc[j][0];
+        res[i * RS + n + 1] = acc[j][1];
       }
     }
-  }
-  __syncthreads();
-  double* res = st;  // res[i*RS + n]: n < L: G, L..2L-1: X, 2L: e, 2L+1: b
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    const int nt = nb + 2 * j;
-    if (nt < NTN) {
-      const int i = 8 * mt + (lane >> 2), n = 8 * nt + 2 * (lane & 3);
-      res[i * RS + n] = acc[j][0];
-      res[i * RS + n + 1] = acc[j][1];
+    __syncthreads();
+    if (look) {  // X = R_b R_{b-1}^T stored transposed: Xt[j*L + i] = X[i][j]
+      double* Xb = Xout + (int64_t)blk * L * L;
+      for (int e = tid; e < L * L; e += blockDim.x) Xb[e] = res[(e % L) * RS + L + e / L];
     }
-  }
-  __syncthreads();
-  if (look) {  // X = R_b R_{b-1}^T stored transposed: Xt[j*L + i] = X[i][j]
-    double* Xb = Xout + (int64_t)blockIdx.x * L * L;
-    for (int e = tid; e < L * L; e += blockDim.x) Xb[e] = res[(e % L) * RS + L + e / L];
-  }
-  // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward
-  // substitution (thread j), then M = T^{-1} C  (M[i][j] = Tinv[i][j] c_j).
-  double* Mb = Mout + (int64_t)blockIdx.x * L * L;
-  if (tid < L) {
-    const int j = tid;
-    for (int i = 0; i < L; ++i) Xs[i][j] = i == j ? 1.0 : 0.0;
-    for (int i = j + 1; i < L; ++i) {
-      double s = 0.0;
-      for (int k2 = j; k2 < i; ++k2) s = fma(res[i * RS + k2], Xs[k2][j], s);
-      Xs[i][j] = -eta * cvec[i] * s;
+    // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward
+    // substitution (thread j), then M = T^{-1} C  (M[i][j] = Tinv[i][j] c_j).
+    double* Mb = Mout + (int64_t)blk * L * L;
+    if (tid < L) {
+      const int j = tid;
+      for (int i = 0; i < L; ++i) Xs[i][j] = i == j ? 1.0 : 0.0;
+      for (int i = j + 1; i < L; ++i) {
+        double s = 0.0;
+        for (int k2 = j; k2 < i; ++k2) s = fma(res[i * RS + k2], Xs[k2][j], s);
+        Xs[i][j] = -eta * cvec[i] * s;
+      }
+      // p_j = eta (j-1) e_j + b_j (1-based), + eta L e_j when a_b is formed by look-ahead
+      pout[(int64_t)blk * L + j] = eta * (double)(look ? j + L : j) * res[j * RS + 2 * L] + res[j * RS + 2 * L + 1];
     }
-    // p_j = eta (j-1) e_j + b_j (1-based), + eta L e_j when a_b is formed by look-ahead
-    pout[(int64_t)blockIdx.x * L + j] = eta * (double)(look ? j + L : j) * res[j * RS + 2 * L] + res[j * RS + 2 * L + 1];
-  }
-  __syncthreads();
-  for (int e = tid; e < L * L; e += blockDim.x) {  // stored transposed: Mt[j][i] = M[i][j]
-    const int j = e / L, i = e % L;
-    Mb[e] = Xs[i][j] * cvec[j];
+    __syncthreads();
+    for (int e = tid; e < L * L; e += blockDim.x) {  // stored transposed: Mt[j][i] = M[i][j]
+      const int j = e / L, i = e % L;
+      Mb[e] = Xs[i][j] * cvec[j];
+    }
+    __syncthreads();  // shared staging / results are reused by the next block
   }
 }
 

@@ -113,6 +113,10 @@ class Context:
         """Enable (and reset) CUDA-event timing of the hot kernels."""
         _check(_lib.load().skr_ctx_profile(self.h, int(enable)))
 
+    def set_prep_cap(self, ctas: int):
+        """Cap the inner loop's PREP grid (0 = uncapped); see skr_ctx_set_prep_cap."""
+        _check(_lib.load().skr_ctx_set_prep_cap(self.h, int(ctas)))
+
     def profile_read(self, key: str):
         """(total device ms, launches) of a profiled kernel key."""
         ms, cnt = f64(), i64()
@@ -829,7 +833,7 @@ def _clone_problem(pre: PreconditionedRidge, ctx: Context) -> PreconditionedRidg
     return c
 
 
-def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7) -> list:
+def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7, prep_cap: Optional[int] = None) -> list:
     """bench.cpp:140-193: both methods, one row per (method, seed, epoch) with the
     suboptimality against one shared reference solve; epoch length 2(n+d); eta
     tuned over eta_grid (bench.cpp:96-100) unless fixed — the grid point with the
@@ -846,6 +850,9 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7) -> list:
     start = max(objective(problem, np.zeros(d)) - ref.minimum, 0.0)
     plain = preconditioned_components(problem, Preconditioner.identity(d, cfg.lam))
     ctxs = [Context(p.data.ctx.device) for _ in range(max(1, int(lanes)))]
+    if prep_cap is not None:  # optional PREP grid cap per lane (measured: no gain at c2, see DESIGN)
+        for cx in ctxs:
+            cx.set_prep_cap(prep_cap)
     rows = []
 
     def run_once(job):
