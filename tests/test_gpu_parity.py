@@ -642,3 +642,22 @@ def test_svrg_chain_bitwise_deterministic(name, dtype):
     for r in runs[1:]:
         assert np.array_equal(np.asarray(r.iterate), np.asarray(runs[0].iterate))
         assert [t.objective for t in r.trace] == [t.objective for t in runs[0].trace]
+
+
+def test_prep_cap_grid_strided_identical():
+    """skr_ctx_set_prep_cap: the inner loop's PREP kernel strides over the blocks of a
+    chunk with a capped grid; iterates must be bitwise those of the uncapped grid."""
+    cfg = configs.CONFIGS["c2"].scaled(8192)
+    X, y = configs.host_instance(cfg)
+    ctx = sk.Context(0)
+    p = sk.RidgeProblem(sk.DataMatrix(X, ctx=ctx), y, cfg.lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
+    pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))
+    eta = configs.eta_for(cfg, pg.max_row_sq(), pg.mean_beta())
+    runs = []
+    for cap in (0, 7, 64):
+        ctx.set_prep_cap(cap)
+        runs.append(sk.svrg_solve(pg, sk.SvrgConfig(2, 2 * cfg.n, eta, cfg.seed), np.zeros(cfg.d)))
+    ctx.set_prep_cap(0)
+    for r in runs[1:]:
+        assert np.array_equal(np.asarray(r.iterate), np.asarray(runs[0].iterate))
