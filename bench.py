@@ -121,7 +121,7 @@ def run_reference(args, cfg):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libskridge_ref.so not built"}))
         return
     R = oracle.ref()
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     X = X.astype(np.float64)
     y = y.astype(np.float64)
     n, d = X.shape

@@ -457,3 +457,140 @@ def ref() -> _Backend:
 def best() -> _Backend:
     """The real reference when it is available, else the restatement."""
     return ref() if ref_available() else port()
+
+
+# ---------------------------------------------------------------------------
+# Synthetic BASELINE instances: host restatement of the DEVICE generator
+# (skr_data_generate; oracle/synth.c restates its Philox4x32-10 streams), so the
+# CPU reference consumes the instance the GPU generates and times.
+def philox4x32_10(ctr, key):
+    """Raw Philox4x32-10 block (known-answer tests)."""
+    lib = port().lib
+    f = lib.skro_philox4x32_10
+    u32a = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+    f.restype, f.argtypes = None, [u32a, u32a, u32a]
+    out = np.zeros(4, dtype=np.uint32)
+    f(np.asarray(ctr, dtype=np.uint32), np.asarray(key, dtype=np.uint32), out)
+    return out
+
+
+def philox_normals(seed: int, stream: int, first: int, count: int, scale: float = 1.0) -> np.ndarray:
+    f = port().lib.skro_philox_normals
+    f.restype, f.argtypes = None, [u64, C.c_uint32, i64, i64, f64, _dp]
+    out = np.empty(count)
+    f(seed, stream, first, count, scale, out)
+    return out
+
+
+def synth_haar(cfg) -> np.ndarray:
+    """V (d x d): the device draws a d x d Gaussian (stream 2, row-major), QRs its
+    column-major view (= its transpose) and fixes signs by sign(diag R)."""
+    d = cfg.d
+    A = philox_normals(cfg.seed, 2, 0, d * d).reshape(d, d)
+    Q, R = np.linalg.qr(A.T)
+    return Q * np.sign(np.diag(R))
+
+
+def synth_instance(cfg, rows: int | None = None, row0: int = 0, V: np.ndarray | None = None,
+                   chunk: int = 1 << 16):
+    """Rows [row0, row0 + rows) of the config's instance, exactly as the device
+    generator lays them out: (X, y) with X (rows, d) float64 or float32 and y
+    float64 or float32 (fp32 configs round both).  rows=None: all cfg.n rows.
+    The first r rows of the instance at n rows are the instance at r rows."""
+    rows = cfg.n - row0 if rows is None else rows
+    d = cfg.d
+    V = synth_haar(cfg) if V is None else V
+    Vt = np.ascontiguousarray(V.T)
+    sig = np.ascontiguousarray(cfg.sigma(), dtype=np.float64)
+    wstar = philox_normals(cfg.seed, 4, 0, d, 1.0 / math.sqrt(d))
+    f32 = cfg.dtype == "f32"
+    X = np.empty((rows, d), dtype=np.float32 if f32 else np.float64)
+    y = np.empty(rows, dtype=X.dtype)
+    g = port().lib.skro_synth_g
+    g.restype, g.argtypes = None, [u64, i64, i64, i64, _dp, _dp]
+    ts = port().lib.skro_synth_tscale
+    ts.restype, ts.argtypes = None, [u64, i64, i64, _dp]
+    G = np.empty((min(chunk, max(rows, 1)), d))
+    for r in range(0, rows, chunk):
+        nr = min(chunk, rows - r)
+        Gc = G[:nr]
+        g(cfg.seed, row0 + r, nr, d, sig, Gc)
+        Xc = Gc @ Vt
+        if f32:
+            Xc = Xc.astype(np.float32)
+        if cfg.t_scale:
+            t = np.empty(nr)
+            ts(cfg.seed, row0 + r, nr, t)
+            Xc = Xc.astype(np.float64) * t[:, None]
+            if f32:
+                Xc = Xc.astype(np.float32)
+        X[r:r + nr] = Xc
+        noise = philox_normals(cfg.seed, 5, row0 + r, nr)
+        yc = X[r:r + nr].astype(np.float64) @ wstar + cfg.tau * noise
+        y[r:r + nr] = yc.astype(np.float32) if f32 else yc
+    return X, y
+
+
+@dataclass
+class PipelineOut:
+    sigma: np.ndarray
+    U: np.ndarray | None
+    trace: np.ndarray
+    trace_ms: np.ndarray
+    w_hat: np.ndarray
+    idx: np.ndarray
+    alpha: float
+    beta_hat: float
+    max_row_sq: float
+    eta: float
+    L_star: float
+    L_hat: float
+    sketch_ms: float
+    precompute_ms: float
+    solve_ms: float
+    refmin_ms: float
+    mode: str
+    k_used: int
+    full_gradient_ms: float
+    rank_reduced: bool
+
+
+def pipeline(X, y, lam, k, q, seed, epochs, m, eta_rule=0, eta=0.0, mode=2, stop=0.0, idx_count=0,
+             want_U=False) -> PipelineOut:
+    """The reference's composed pipeline (oracle/ref_capi.cpp ref_pipeline) on ONE
+    DataMatrix built from X (n x d, float32 promoted once, or float64)."""
+    R = ref()
+    f = R._fn("pipeline", cint, [vp, cint, i64, i64, _dp, f64, i64, i64, u64, i64, i64, cint, f64, cint, f64, i64,
+                                 _dp, vp, _dp, _dp, P(i64), _dp, vp, _dp])
+    X = np.ascontiguousarray(X)
+    if X.dtype not in (np.float32, np.float64):
+        raise TypeError("X must be float32 or float64")
+    n, d = X.shape
+    sig = np.zeros(max(k, 1))
+    U = np.zeros((d, k), order="F") if (want_U and k > 0) else None
+    tr, tms = np.zeros(max(epochs, 1)), np.zeros(max(epochs, 1))
+    done = i64(0)
+    wh = np.zeros(d)
+    idx = np.zeros(max(idx_count, 1), dtype=np.int64)
+    sc = np.zeros(16)
+    R._check(f(X.ctypes.data, 1 if X.dtype == np.float32 else 0, n, d, _c64(y), lam, k, q, seed, epochs, m, eta_rule,
+               eta, mode, stop, idx_count, sig, None if U is None else U.ctypes.data, tr, tms, C.byref(done), wh,
+               idx.ctypes.data if idx_count > 0 else None, sc))
+    nd = done.value
+    return PipelineOut(sig[:int(sc[11])], U, tr[:nd], tms[:nd], wh, idx[:idx_count], sc[0], sc[1], sc[2], sc[3],
+                       sc[4], sc[5], sc[6], sc[7], sc[8], sc[9], "dense" if sc[10] == 0 else "lazy", int(sc[11]),
+                       sc[12], bool(sc[13]))
+
+
+def conditioned_matrix(X, lam, U, sigma) -> np.ndarray:
+    """The reference's conditioned_matrix(scaled_design, lambda, P) (unguarded)."""
+    R = ref()
+    f = R._fn("conditioned_matrix", cint, [vp, cint, i64, i64, f64, _dp, _dp, i64, _dp])
+    X = np.ascontiguousarray(X)
+    n, d = X.shape
+    out = np.zeros((d, d))
+    k = 0 if U is None else U.shape[1]
+    Uc = np.zeros(1) if U is None else np.ascontiguousarray(np.asarray(U).reshape(-1, order="F"))
+    sg = np.zeros(1) if sigma is None else _c64(sigma)
+    R._check(f(X.ctypes.data, 1 if X.dtype == np.float32 else 0, n, d, lam, Uc, sg, k, out))
+    return out

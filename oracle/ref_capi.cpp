@@ -10,6 +10,7 @@
 // column-major DenseMatrix (dense_matrix.hpp:12-15).  Dense
 // results (U, V) are returned column-major exactly as DenseMatrix stores them.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -449,6 +450,141 @@ int ref_cumulative_weights(const double* betas, std::int64_t N, double* out) {
   return guard([&] {
     Vector cum = make_cumulative_weights(Vector(betas, betas + N));
     std::memcpy(out, cum.data(), sizeof(double) * N);
+  });
+}
+
+
+// ---- the composed pipeline on ONE DataMatrix -------
+// RidgeProblem(X, y, lambda) -> block_lanczos(scaled_design(p), {k, 0.5, seed, q})
+// -> build_sketched -> preconditioned_components(p, P, mode) -> reference_minimum
+// -> svrg_solve(m, eta, seed, L*) -> apply_inv_sqrt -> objective(p, w^)
+// (ridge.cpp:413-454 with q_override; bench.cpp:84-94).  X is n x d row-major,
+// fp32 (promoted to fp64 once, the reference has no fp32) or fp64.  k == 0: the
+// unpreconditioned Preconditioner::identity.  eta_rule 0: 1/(4 max_i ||x~_i||^2);
+// 1: 1/(4 max(max_i ||x~_i||^2, beta_hat)) (configs.eta_for).  eta > 0 overrides.
+// stop > 0: the solve stops at the first epoch with suboptimality <= stop
+// (bench.cpp:182-189 time-to-eps protocol: the trace is cut there).
+// sc[0..] = alpha, beta_hat, max_row_sq, eta, L_star, L_hat, sketch_ms,
+//           precompute_ms, solve_ms, refmin_ms, mode (0 dense / 1 lazy), k_used,
+//           full_gradient_ms (one timed call), rank_reduced
+int ref_pipeline(const void* x, int x_f32, std::int64_t n, std::int64_t d, const double* y, double lambda,
+                 std::int64_t k, std::int64_t q, std::uint64_t seed, std::int64_t epochs, std::int64_t m,
+                 int eta_rule, double eta_in, int mode, double stop, std::int64_t idx_count, double* sigma_out,
+                 double* U_out, double* trace, double* trace_ms, std::int64_t* done, double* w_hat,
+                 std::int64_t* idx_out, double* sc) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  return guard([&] {
+    Vector xs(static_cast<std::size_t>(n * d));
+    if (x_f32) {
+      const float* xf = static_cast<const float*>(x);
+      for (std::size_t e = 0; e < xs.size(); ++e) xs[e] = static_cast<double>(xf[e]);
+    } else {
+      std::memcpy(xs.data(), x, sizeof(double) * xs.size());
+    }
+    RidgeProblem p(DataMatrix(DenseMatrix(static_cast<std::size_t>(d), static_cast<std::size_t>(n), std::move(xs))),
+                   Vector(y, y + n), lambda);
+    auto t0 = clk::now();
+    Preconditioner pc = Preconditioner::identity(static_cast<std::size_t>(d), lambda);
+    SketchedSvd sv;
+    if (k > 0) {
+      LanczosConfig lc;
+      lc.k = static_cast<std::size_t>(k);
+      lc.eps_prime = 0.5;
+      lc.seed = seed;
+      if (q > 0) lc.q_override = static_cast<std::size_t>(q);
+      sv = block_lanczos(scaled_design(p), lc);
+      std::memcpy(sigma_out, sv.singular_values.data(), sizeof(double) * sv.k);
+      if (U_out) std::memcpy(U_out, sv.left.data(), sizeof(double) * sv.left.size());
+      pc = build_sketched(sv, lambda);
+    }
+    auto t1 = clk::now();
+    ApplyMode am = mode == 0 ? ApplyMode::Dense : mode == 1 ? ApplyMode::Lazy : ApplyMode::Auto;
+    auto pre = preconditioned_components(p, pc, am);
+    auto t2 = clk::now();
+    ReferenceSolution ref = reference_minimum(p);
+    auto t3 = clk::now();
+    const Vector& b = pre->betas();
+    double mx = 0.0;
+    for (std::int64_t i = 0; i < n; ++i) mx = std::max(mx, b[static_cast<std::size_t>(i)]);
+    const double max_row = mx * static_cast<double>(n) / static_cast<double>(n + d);
+    const double bh = mean_beta(*pre);
+    double eta = eta_in > 0 ? eta_in : 1.0 / (4.0 * (eta_rule == 1 ? std::max(max_row, bh) : max_row));
+    Vector g;
+    auto tg0 = clk::now();
+    pre->full_gradient(Vector(static_cast<std::size_t>(d), 0.0), g);
+    auto tg1 = clk::now();
+    SvrgConfig cfg;
+    cfg.epochs = static_cast<std::size_t>(epochs);
+    cfg.epoch_length = static_cast<std::size_t>(m);
+    cfg.step_size = eta;
+    cfg.seed = seed;
+    // time-to-eps: run epoch by epoch through the unmodified engine would change the
+    // index stream; instead run the whole solve and cut the trace at the first hit
+    auto t4 = clk::now();
+    SvrgResult r = svrg_solve(*pre, cfg, Vector(static_cast<std::size_t>(d), 0.0), ref.minimum);
+    auto t5 = clk::now();
+    std::size_t cut = r.trace.size();
+    if (stop > 0)
+      for (std::size_t s = 0; s < r.trace.size(); ++s)
+        if (r.trace[s].suboptimality && *r.trace[s].suboptimality <= stop) {
+          cut = s + 1;
+          break;
+        }
+    for (std::size_t s = 0; s < cut; ++s) {
+      trace[s] = r.trace[s].objective;
+      trace_ms[s] = r.trace[s].elapsed_ms;
+    }
+    *done = static_cast<std::int64_t>(cut);
+    Vector wh = pc.apply_inv_sqrt(r.iterate);
+    std::memcpy(w_hat, wh.data(), sizeof(double) * static_cast<std::size_t>(d));
+    const double L = objective(p, wh);
+    if (idx_count > 0) {
+      Vector cum = make_cumulative_weights(b);
+      NormalSampler rng(seed);
+      for (std::int64_t t = 0; t < idx_count; ++t) {
+        auto it = std::lower_bound(cum.begin(), cum.end(), rng.uniform());
+        if (it == cum.end()) --it;
+        idx_out[t] = static_cast<std::int64_t>(it - cum.begin());
+      }
+    }
+    sc[0] = pre->strong_convexity();
+    sc[1] = bh;
+    sc[2] = max_row;
+    sc[3] = eta;
+    sc[4] = ref.minimum;
+    sc[5] = L;
+    sc[6] = ms(t0, t1);
+    sc[7] = ms(t1, t2);
+    sc[8] = ms(t4, t5);
+    sc[9] = ms(t2, t3);
+    sc[10] = pre->mode() == ApplyMode::Dense ? 0.0 : 1.0;
+    sc[11] = static_cast<double>(k > 0 ? sv.k : 0);
+    sc[12] = ms(tg0, tg1);
+    sc[13] = k > 0 && sv.rank_reduced ? 1.0 : 0.0;
+  });
+}
+
+// conditioned_matrix(scaled_design, lambda, P) (precond.cpp:174-194), unguarded,
+// returned for an external symmetric eigensolve (d > 2000, where the reference's
+// own kappa~ refuses: ScaleGuardError).  fp32 input promoted once.
+int ref_conditioned_matrix(const void* x, int x_f32, std::int64_t n, std::int64_t d, double lambda, const double* U,
+                           const double* sigma, std::int64_t k, double* out) {
+  return guard([&] {
+    Vector xs(static_cast<std::size_t>(n * d));
+    if (x_f32) {
+      const float* xf = static_cast<const float*>(x);
+      for (std::size_t e = 0; e < xs.size(); ++e) xs[e] = static_cast<double>(xf[e]);
+    } else {
+      std::memcpy(xs.data(), x, sizeof(double) * xs.size());
+    }
+    DataMatrix a(DenseMatrix(static_cast<std::size_t>(d), static_cast<std::size_t>(n), std::move(xs)),
+                 1.0 / std::sqrt(static_cast<double>(n)));
+    Preconditioner pc = make_precond(static_cast<std::size_t>(d), U, sigma, static_cast<std::size_t>(k), lambda);
+    DenseMatrix mat = conditioned_matrix(a, lambda, pc);
+    std::memcpy(out, mat.data(), sizeof(double) * mat.size());
   });
 }
 

@@ -5,17 +5,16 @@ d x d matrix, V = Q diag(sign diag R)), optional |Student-t(3)| row scaling,
 w* ~ N(0, I/d), y = X w* + tau N(0,1).  fp32 configs round X and y to fp32 and
 the oracle consumes exactly those values promoted to fp64.
 
-Two generators implement this spec:
-  * ``host_instance`` (numpy, Philox bit generator; draw order G, V-Gaussian,
-    t-scales, w*, noise) — used for parity instances small enough for the CPU
-    oracle and for the reference arm of bench.py;
-  * ``skridge.DataMatrix.generate`` (device, Philox4x32-10 streams 1..5) — used
-    at benchmark scale.  The two are statistically identical, not bitwise; any
-    parity check hands the SAME arrays to both sides.
+The generator is ``skridge.DataMatrix.generate`` (device, Philox4x32-10
+streams 1..5, skr_data_generate).  The CPU side (tests, goldens, bench.py's
+reference arm) regenerates the same instance with ``oracle.synth_instance``,
+a host restatement of the device generator: identical integer streams, fp64
+values within a few ulps, fp32 values identical except for rare rounding ties.
+Row i of the instance does not depend on n, so a row-subsampled instance is
+the first n rows of the full one.
 """
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,28 +58,6 @@ CONFIGS = {
     "c4": Config("c4", "f32", 1 << 22, 4096, 3, 3, 0.0, True, 0.1, 1e-6, 256, 3, 60),
     "c5": Config("c5", "f32", 1 << 24, 1024, 4, 1, 0.99, False, 0.2, 1e-6, 64, 2, 20),
 }
-
-
-def host_instance(cfg: Config):
-    """(X, y) as numpy arrays: float64, or float32 for fp32 configs."""
-    rng = np.random.Generator(np.random.Philox(cfg.seed))
-    n, d = cfg.n, cfg.d
-    G = rng.standard_normal((n, d))
-    A = rng.standard_normal((d, d))
-    Q, R = np.linalg.qr(A)
-    V = Q * np.sign(np.diag(R))
-    X = (G * cfg.sigma()) @ V.T
-    if cfg.t_scale:
-        t = np.abs(rng.standard_t(3, size=n))
-        X *= t[:, None]
-    wstar = rng.standard_normal(d) / math.sqrt(d)
-    noise = rng.standard_normal(n)
-    if cfg.dtype == "f32":
-        X = X.astype(np.float32)
-        y = (X.astype(np.float64) @ wstar + cfg.tau * noise).astype(np.float32)
-        return X, y
-    y = X @ wstar + cfg.tau * noise
-    return np.ascontiguousarray(X), y
 
 
 def step_size(max_row_sq: float) -> float:

@@ -111,7 +111,7 @@ struct skr_problem {
   int fg_grid = 0;
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
-  DBuf<double> s_state, s_M, s_p, s_X;  // s-step inner loop workspaces
+  DBuf<double> s_state, s_M, s_p, s_X, s_pk;  // s-step inner loop workspaces (s_pk: packed rows)
   // Lazy mode (sparse data): X~ is never materialised; Pm = X U^T (n x k) and workspaces
   bool lazy = false;
   DBuf<double> Pm, lz_r, lz_r2, lz_s, lz_g1, lz_g2, lz_v, lz_loss, lz_UT;
@@ -224,14 +224,7 @@ void launch_fullgrad_nt(Ctx& c, FgPlan& p, int64_t ntiles, const T* X, int64_t l
     const size_t budget = (size_t)(getenv("SKR_K9_SMEM_KB") ? kn.smem_kb : (NT >= 512 ? 200 : 96)) * 1024;
     const int stages = (int)std::max<size_t>(2, std::min<size_t>(16, budget / tile));
     const size_t smem = tile * stages;
-    static int per_sm = 0;
-    static size_t configured = 0;
-    if (configured != smem) {
-      SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-      per_sm = std::max(per_sm, 1);
-      configured = smem;
-    }
+    const int per_sm = resident_ctas((const void*)kern, NT, smem);
     p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * c.sm_count));
     if (plan_only) return;
     if (getenv("SKR_DEBUG"))
@@ -242,11 +235,7 @@ void launch_fullgrad_nt(Ctx& c, FgPlan& p, int64_t ntiles, const T* X, int64_t l
     return;
   }
   auto kern = fullgrad_kernel<T, VEC, TR, NT>;
-  static int per_sm = 0;
-  if (!per_sm) {
-    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0));
-    per_sm = std::max(per_sm, 1);
-  }
+  const int per_sm = resident_ctas((const void*)kern, NT, 0);
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * c.sm_count));
   if (plan_only) return;
   kern<<<p.grid, NT, 0, c.stream>>>(X, ld, n, y, w, part_g, part_loss);
@@ -300,14 +289,7 @@ void launch_rowring(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const 
                     double* part_g, double* part_loss, bool plan_only, const UwHead& head) {
   auto kern = fullgrad_rowring_kernel<T, CH, NB, NTH>;
   const size_t smem = rowring_smem<NB, NTH>(ld, sizeof(T));
-  static int per_sm = 0;
-  static size_t configured = 0;
-  if (configured != smem) {
-    SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, smem));
-    per_sm = std::max(per_sm, 1);
-    configured = smem;
-  }
+  const int per_sm = resident_ctas((const void*)kern, NTH, smem);
   constexpr int NWR = NTH / 32;
   p.nt = NTH;
   p.grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + NWR - 1) / NWR, (int64_t)per_sm * c.sm_count));
@@ -324,14 +306,7 @@ void launch_rowwarp(Ctx& c, FgPlan& p, int64_t ld, int64_t n, const T* X, const 
                     double* part_g, double* part_loss, bool plan_only, const UwHead& head) {
   auto kern = fullgrad_rowwarp_kernel<T, CH, RPI>;
   const size_t smem = 2 * ld * sizeof(double);
-  static int per_sm = 0;
-  static size_t configured = 0;
-  if (configured != smem) {
-    if (smem > 48 * 1024) SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowwarpThreads, smem));
-    per_sm = std::max(per_sm, 1);
-    configured = smem;
-  }
+  const int per_sm = resident_ctas((const void*)kern, kRowwarpThreads, smem);
   constexpr int NWR = kRowwarpThreads / 32;
   const int64_t warps_needed = (n + RPI - 1) / RPI;
   p.nt = kRowwarpThreads;
@@ -623,8 +598,10 @@ void mt_uniforms_dev(Ctx& c, MtState* st, double* out, int64_t count) {
     for (int l = 0; l < MTJ_MAX_LEVELS; ++l)
       SKR_CUDA(cudaMemcpyAsync(c.mt_polys.get() + (size_t)l * (MT_POLY_WORDS + 1), P[l].data(),
                                8 * (MT_POLY_WORDS + 1), cudaMemcpyHostToDevice, c.stream));
-    SKR_CUDA(cudaFuncSetAttribute(mt_jump_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)mt_jump_smem()));
+    configure_once((const void*)mt_jump_chain_kernel, [&] {
+      SKR_CUDA(cudaFuncSetAttribute(mt_jump_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)mt_jump_smem()));
+    });
     c.sync();  // host vectors are static, but keep the upload ordered before first use
   }
   // states at level l: stride CH * 2^l, count ceil(C / 2^l); level `levels` = *st
@@ -788,11 +765,8 @@ void tc_launch_cs(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* B
   const CUtensorMap mbl = make_tmap_f32(Bl, g.N, g.K, ldb, BN / CS);
   constexpr size_t smem = tc_gemm_smem<BN>();
   auto kern = tc_gemm_tf32x3_kernel<A_MN, BN, CS>;
-  static bool configured = false;
-  if (!configured) {
-    SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  configure_once((const void*)kern,
+                 [&] { SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(ceil_div(g.M, TC_BM) * ceil_div(g.N, BN)), 1, splits);
   cfg.blockDim = dim3(TC_THREADS);
@@ -893,12 +867,10 @@ void f64_to_tf32x2(Ctx& c, const double* src, int64_t lds, int64_t rows, int64_t
 template <class T, int VEC, int NT>
 void launch_epoch_t(Ctx& c, const EpochArgs& a) {
   const size_t smem = svrg_epoch_smem<T, VEC, NT>();
-  static bool configured = false;
-  if (!configured) {
+  configure_once((const void*)svrg_epoch_kernel<T, VEC, NT>, [&] {
     SKR_CUDA(cudaFuncSetAttribute(svrg_epoch_kernel<T, VEC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    configured = true;
-  }
+  });
   svrg_epoch_kernel<T, VEC, NT><<<1, NT, smem, c.stream>>>(a);
   SKR_LAUNCHED(&c);
 }
@@ -924,61 +896,71 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
 constexpr int64_t kSstepChunkBlocks = 1024;  // blocks per prep/chain launch pair (double-buffered)
 static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
 
-template <class T, int CPT, int L, int NT>
+template <class T, int SW, int L>
 void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
                  double* w_avg) {
+  using Cf = ChainCfg<SW, L>;
   Ctx& c = p->ctx->c;
   const int64_t ld = p->ld;
-  const int CS = (int)((ld + NT * CPT - 1) / (NT * CPT));
+  const int CS = (int)((ld + SW - 1) / SW);
   if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
   if (p->s_state.n < (size_t)2 * ld) p->s_state.alloc(2 * ld, c.stream);
   const size_t mneed = (size_t)2 * kSstepChunkBlocks * L * L, pneed = (size_t)2 * kSstepChunkBlocks * L;
+  const size_t pkchunk = (size_t)kSstepChunkBlocks * CS * L * SW;
   if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
   if (p->s_X.n < mneed) p->s_X.alloc(mneed, c.stream);
   if (p->s_p.n < pneed) p->s_p.alloc(pneed, c.stream);
+  if (p->s_pk.n != 2 * pkchunk) {  // zero once: the padding columns past d are never written
+    p->s_pk.alloc(2 * pkchunk, c.stream);
+    p->s_pk.zero();
+  }
   auto prep = sstep_prep_kernel<T, L>;
-  constexpr int MXB = (CPT == 1 && NT == 128) ? 2 : 1;
-  auto chain = sstep_chain_kernel<T, CPT, L, MXB, NT>;
+  auto chain = sstep_chain_kernel<SW, L>;
   constexpr size_t prep_smem = sstep_prep_smem<L>();
-  constexpr size_t chain_smem = sstep_chain_smem<CPT, L, MXB, NT>();
-  static bool configured = false;
-  if (!configured) {
+  // The chain CTA reserves its SM's whole shared memory: otherwise PREP CTAs of
+  // the next chunk (side stream) co-reside on the chain's 16 SMs and compete for
+  // issue slots, the FP64 pipe and shared-memory bandwidth.
+  static_assert(Cf::smem() <= 227 * 1024, "chain shared memory");
+  constexpr size_t chain_smem = 227 * 1024;
+  configure_once((const void*)chain, [&] {
     SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
+  });
   SstepRows rows{p->xt_all, p->B.get(), ld, p->d, p->n_global};
+  const PackGeom pg{CS, SW};
   sstep_init_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, ld, p->s_state.get());
   SKR_LAUNCHED(&c);
   // chunks of kSstepChunkBlocks blocks: prep(i+1) runs on the side stream (all
-  // free SMs) while chain(i) runs on the main stream; M/p are double-buffered.
+  // free SMs) while chain(i) runs on the main stream; M/p/X/packed rows are
+  // double-buffered.
   const int64_t chunk_steps = kSstepChunkBlocks * L;
   SKR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
   SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+  if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
+    SKR_CUDA(cudaMalloc(&dprof, 128 * sizeof(unsigned long long)));
+    SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
+  }
   int64_t chunk = 0;
   for (int64_t s0 = 0; s0 < m; s0 += chunk_steps, ++chunk) {
     const int b = (int)(chunk & 1);
     double* Mb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * L * L;
     double* pb = p->s_p.get() + (size_t)b * kSstepChunkBlocks * L;
     double* Xb = p->s_X.get() + (size_t)b * kSstepChunkBlocks * L * L;
+    double* pkb = p->s_pk.get() + (size_t)b * pkchunk;
     const int64_t steps = std::min(chunk_steps, m - s0);
     const int64_t nblk = (steps + L - 1) / L;
     if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
     const int64_t pgrid = c.prep_cap > 0 ? std::min<int64_t>(nblk, c.prep_cap) : nblk;
     prep<<<(unsigned)pgrid, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
-                                                     p->reg_coef, mu, snap, eta, Mb, pb, Xb);
+                                                     p->reg_coef, mu, snap, eta, Mb, pb, Xb, pkb, pg);
     SKR_LAUNCHED(&c);
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
     SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
-    if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
-      SKR_CUDA(cudaMalloc(&dprof, 16 * sizeof(unsigned long long)));
-      SKR_CUDA(cudaMemset(dprof, 0, 16 * sizeof(unsigned long long)));
-    }
-    ChainArgs ca{rows, idx + s0, steps, Mb, pb, Xb, mu, eta, p->s_state.get(), dprof};
+    ChainArgs ca{pkb, steps, Mb, pb, Xb, mu, ld, eta, p->s_state.get(), dprof};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(chain_threads<T, CPT, NT>());
+    cfg.blockDim = dim3(Cf::NT);
     cfg.dynamicSmemBytes = chain_smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
@@ -990,17 +972,44 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     cfg.numAttrs = 1;
     SKR_CUDA(cudaLaunchKernelEx(&cfg, chain, ca));
     SKR_LAUNCHED(&c);
+    if (dprof && chunk == 0) {  // freeze the event trace after the first launch
+      const unsigned long long one = 1;
+      SKR_CUDA(cudaMemcpyAsync(dprof + 15, &one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
+      SKR_CUDA(cudaStreamSynchronize(c.stream));
+    }
     SKR_CUDA(cudaEventRecord(c.ev_chain[b], c.stream));
   }
   sstep_finish_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->s_state.get(), ld, p->d, (double)m, w_avg);
   SKR_LAUNCHED(&c);
   if (dprof) {
-    unsigned long long h[16] = {};
+    unsigned long long h[128] = {};
     SKR_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
-    const double nb = (double)std::max<unsigned long long>(h[6], 1);
-    fprintf(stderr, "[skr] chain cycles/block: total %.0f  (rows-wait %.0f)  dots(b+1) %.0f  xterm+bar %.0f  ready-wait %.0f  gather %.0f  gemv %.0f  update %.0f  (blocks %llu) producer: empty-wait %.0f issue %.0f\n",
-            h[9] / nb, h[10] / nb, h[1] / nb, h[0] / nb, h[2] / nb, h[3] / nb, h[4] / nb, h[5] / nb, h[6], h[7] / nb, h[8] / nb);
+    for (int k = 0; k < kTraceN; ++k) {
+      const unsigned long long* e = h + 16 + 8 * k;
+      const unsigned long long b0 = h[16];  // block kTraceB0 dots start
+      fprintf(stderr, "[skr]   block %d: dots %lld..%lld  partials@delta %lld  delta %lld  update %lld..%lld\n",
+              kTraceB0 + k, (long long)(e[0] - b0), (long long)(e[1] - b0), (long long)(e[2] - b0),
+              (long long)(e[3] - b0), (long long)(e[4] - b0), (long long)(e[5] - b0));
+    }
+    const double nb = (double)std::max<unsigned long long>(h[3], 1);
+    fprintf(stderr, "[skr] chain v3 (SW=%d L=%d CS=%d) cycles/block: dots %.0f (w/rows wait %.0f)  update %.0f "
+            "(delta wait %.0f)  delta-warp partials wait %.0f  (blocks %llu)\n", SW, L, CS, h[0] / nb, h[5] / nb,
+            h[2] / nb, h[1] / nb, h[4] / nb, h[3]);
+    SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
   }
+}
+
+// Chain geometry: the narrowest slice (>= 32 columns) that spans ld with at most
+// 16 CTAs; 256-column slices use L = 16 (shared-memory budget of the row ring).
+template <class T>
+void run_sstep(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
+               double* w_avg) {
+  const int64_t ld = p->ld;
+  if (ld <= 16 * 32) run_sstep_t<T, 32, 32>(p, snap, mu, idx, m, eta, w_avg);
+  else if (ld <= 16 * 64) run_sstep_t<T, 64, 32>(p, snap, mu, idx, m, eta, w_avg);
+  else if (ld <= 16 * 128) run_sstep_t<T, 128, 32>(p, snap, mu, idx, m, eta, w_avg);
+  else if (ld <= 16 * 256) run_sstep_t<T, 256, 16>(p, snap, mu, idx, m, eta, w_avg);
+  else raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
 }
 
 // Lazy epoch (sparse rows): per-epoch snapshot quantities on all SMs, then the
@@ -1104,17 +1113,7 @@ void run_epoch(skr_problem* p, const double* snap, const double* mu, const int64
   static const bool naive = getenv("SKR_K10") && std::string(getenv("SKR_K10")) == "naive";
   if (c.prof_on) c.prof_mark("svrg_epoch");
   if (!naive) {
-    static const bool wide_cpt2 = getenv("SKR_K10_CPT2") != nullptr;
-    static const int env_nt = getenv("SKR_K10_NT") ? atoi(getenv("SKR_K10_NT")) : 0;
-    if (p->ld <= 2048 && env_nt == 256) {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 256>(p, snap, mu, idx, m, eta, w_avg));
-    } else if (p->ld <= 2048) {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 128>(p, snap, mu, idx, m, eta, w_avg));
-    } else if (wide_cpt2) {
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 2, 32, 128>(p, snap, mu, idx, m, eta, w_avg));
-    } else {  // d > 2048: 8 consumer warps per CTA, one column each
-      DISPATCH_DTYPE(p->dtype, T, run_sstep_t<T, 1, 32, 256>(p, snap, mu, idx, m, eta, w_avg));
-    }
+    DISPATCH_DTYPE(p->dtype, T, run_sstep<T>(p, snap, mu, idx, m, eta, w_avg));
     if (c.prof_on) c.prof_mark("svrg_epoch");
     return;
   }

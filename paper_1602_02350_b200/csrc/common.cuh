@@ -10,6 +10,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -90,15 +93,20 @@ inline NcclApi& nccl() {
 
 // Buffers of >= 1 GiB bypass the stream-ordered pool: growing the pool maps
 // memory at ~17 GB/s on B200 (3.8 s for 64 GiB) while cudaMalloc maps 64 GiB in
-// ~5 ms (profiles/alloc_probe.py).  cudaFree synchronises the device, so the
-// direct buffers are still released after every queued use.
+// ~5 ms (profiles/alloc_probe.py).  A direct buffer is released after an
+// explicit synchronisation of its stream (every queued use on it has finished);
+// big buffers are never freed inside a graph capture (they outlive the graphs).
 constexpr size_t kDirectAllocBytes = size_t(1) << 30;
 inline cudaError_t dev_malloc(void** p, size_t bytes, cudaStream_t s) {
   return bytes >= kDirectAllocBytes ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, s);
 }
 inline void dev_free(void* p, size_t bytes, cudaStream_t s) {
-  if (bytes >= kDirectAllocBytes) cudaFree(p);
-  else cudaFreeAsync(p, s);
+  if (bytes >= kDirectAllocBytes) {
+    cudaStreamSynchronize(s);
+    cudaFree(p);
+  } else {
+    cudaFreeAsync(p, s);
+  }
 }
 
 // Device buffer with RAII; stream-ordered pool (direct allocation >= 1 GiB).
@@ -181,6 +189,40 @@ struct Ctx {
   }
   void sync() { SKR_CUDA(cudaStreamSynchronize(stream)); }
 };
+
+// cudaFuncSetAttribute once per (kernel, device).  Attributes are per device, and
+// concurrent contexts (eta-grid lanes on several host threads) may reach the same
+// launch site together, so the registry is keyed by device and locked.
+template <class F>
+void configure_once(const void* kernel, F&& set) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  SKR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev})) return;
+  set();
+  done.insert({kernel, dev});
+}
+
+// Resident CTAs per SM of `kernel` at (threads, smem), raising its dynamic
+// shared-memory limit first; cached per (kernel, device, threads, smem) under a lock.
+inline int resident_ctas(const void* kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  SKR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_tuple(kernel, dev, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024) SKR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  per_sm = std::max(per_sm, 1);
+  cache[key] = per_sm;
+  return per_sm;
+}
 
 inline size_t dtype_size(int dtype) { return dtype == SKR_F32 ? 4 : 8; }
 

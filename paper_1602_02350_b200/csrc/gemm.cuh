@@ -191,12 +191,10 @@ void gemm_tiled(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t 
   dim3 grid(ceil_div(M, BM), ceil_div(N, BN), splits);
   constexpr size_t smem = gemm_smem(BM, BN);
   if (splits == 1) {
-    static bool attr = [] {
+    configure_once((const void*)gemm_kernel<TA, TB, A_T, B_T, Epi, false, BM, BN>, [&] {
       SKR_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, A_T, B_T, Epi, false, BM, BN>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      return true;
-    }();
-    (void)attr;
+    });
     gemm_kernel<TA, TB, A_T, B_T, Epi, false, BM, BN><<<grid, GEMM_THREADS, smem, ctx->stream>>>(
         M, N, K, A, lda, B, ldb, kchunk, epi);
     SKR_LAUNCHED(ctx);
@@ -204,12 +202,10 @@ void gemm_tiled(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t 
   }
   DBuf<double> ws((size_t)splits * M * N, ctx->stream);
   EpiPartial part{ws.get(), M, N};
-  static bool attr_p = [] {
+  configure_once((const void*)gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true, BM, BN>, [&] {
     SKR_CUDA(cudaFuncSetAttribute(gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true, BM, BN>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    return true;
-  }();
-  (void)attr_p;
+  });
   gemm_kernel<TA, TB, A_T, B_T, EpiPartial, true, BM, BN><<<grid, GEMM_THREADS, smem, ctx->stream>>>(
       M, N, K, A, lda, B, ldb, kchunk, part);
   SKR_LAUNCHED(ctx);

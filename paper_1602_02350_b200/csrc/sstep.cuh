@@ -18,10 +18,16 @@
 // Look-ahead: with X_b = R_b R_{b-1}^T and e_b = R_b mu (also from PREP),
 //   a_b = R_b w_b = R_b w_{b-1} - eta X_b delta_{b-1} - eta L e_b,
 // so the partial dots a~_b = R_b w_{b-1} are computed (and their cluster
-// reduction through DSMEM started) while block b-1 is still being resolved; the
-// exchange latency leaves the dependent chain.  PREP folds eta L e_b into
+// reduction started) while block b-1 is still being resolved; the exchange
+// latency leaves the dependent chain.  PREP folds eta L e_b into
 // p'_b = p_b + eta L e_b for every block but the first of a launch, whose a_0 is
 // computed directly.
+//
+// Row staging (v2): PREP, which reads every sampled row anyway, also writes the
+// block's rows widened to fp64 into a PACKED buffer laid out per CTA slice,
+// pk[block][cta][l][SW], so each chain CTA receives its L x SW slice of a block
+// with ONE bulk copy (v1 issued one bulk copy per row slice from two producer
+// warps plus two fp32 -> fp64 widener warps).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -45,26 +51,43 @@ __device__ __forceinline__ double row_elem(const SstepRows& R, int64_t i, int64_
   return i < R.n ? (double)static_cast<const T*>(R.Xt)[i * R.ld + j] : R.B[(i - R.n) * R.ld + j];
 }
 
+// Packed-row geometry of the chain: CS CTAs, SW columns each (CS * SW >= ld).
+struct PackGeom {
+  int cs, sw;
+};
+// Element (row l, column j) of a CTA's L x SW slice sits at l * SW + pk_swz(j, l).
+// The XOR swizzle makes both chain access patterns conflict-free: the dots
+// (lanes = rows, one column at a time) and the update (lanes = columns, one row
+// at a time); 8-byte accesses are served per half-warp, so 16 distinct bank
+// pairs suffice.
+__host__ __device__ __forceinline__ int pk_swz(int j, int l) { return j ^ (l & 15); }
+
 // ---------------------------------------------------------------------------
-// PREP: one CTA (256 threads, 8 warps) per block of L = 32 steps.  One FP64
-// tensor-core (DMMA m8n8k4) product of the block's rows against the staged rows
-// [R_b; R_{b-1}; mu; wbar] gives G = R_b R_b^T, X = R_b R_{b-1}^T (look-ahead),
-// e = R_b mu and b = R_b wbar in one pass over the rows (column chunks of 32,
-// register-prefetched one chunk ahead).  Then M = (I + eta C G_strict)^{-1} C by
-// forward substitution.  Outputs: Mout[b] (L x L, stored TRANSPOSED:
+// PREP: one CTA (256 threads, 8 warps) per block of L (16 or 32) steps.  One
+// FP64 tensor-core (DMMA m8n8k4) product of the block's rows against the staged
+// rows [R_b; R_{b-1}; mu; wbar] gives G = R_b R_b^T, X = R_b R_{b-1}^T
+// (look-ahead), e = R_b mu and b = R_b wbar in one pass over the rows (column
+// chunks of 32, register-prefetched one chunk ahead); the same pass writes the
+// block's rows (fp64) to the packed buffer.  Then M = (I + eta C G_strict)^{-1} C
+// by forward substitution.  Outputs: Mout[b] (L x L, stored TRANSPOSED:
 // Mout[b][j*L + i] = M[i][j]), pout[b] (L), Xout[b] (transposed, blocks > 0 of
-// the launch).  Padded steps (beyond `steps`) get c_l = 0, so delta_l = 0 there.
+// the launch), pk.  Padded steps (beyond `steps`) get c_l = 0, so delta_l = 0
+// there, and zero rows.
 template <class T, int L>
 __global__ void __launch_bounds__(256)
 sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, const double* __restrict__ inv_nq,
                   double data_coef, double reg_coef, const double* __restrict__ mu,
                   const double* __restrict__ wbar, double eta, double* __restrict__ Mout,
-                  double* __restrict__ pout, double* __restrict__ Xout) {
-  static_assert(L == 32, "warp tiling assumes L = 32");
+                  double* __restrict__ pout, double* __restrict__ Xout, double* __restrict__ pk, PackGeom pg) {
+  static_assert(L == 16 || L == 32, "L = 16 or 32");
   constexpr int KC = 32, SP = KC + 4;         // staged columns per chunk, padded row stride (conflict-free frags)
   constexpr int NR = 2 * L + 8;               // staged rows: block b, block b-1, mu, wbar, zero pad
-  constexpr int NTN = NR / 8;                 // n-tiles (9)
-  constexpr int PER = NR * KC / 256;          // staged elements per thread per chunk (9)
+  constexpr int NTN = NR / 8;                 // n-tiles
+  constexpr int MT = L / 8;                   // m-tiles
+  constexpr int STEP = 8 / MT;                // warps per m-tile
+  constexpr int NJ = (NTN + STEP - 1) / STEP; // n-tiles per warp
+  constexpr int PER = NR * KC / 256;          // staged elements per thread per chunk
+  static_assert(NR * KC % 256 == 0, "staging split");
   constexpr int RS = NR + 1;                  // result row stride
   extern __shared__ double dyn[];
   double* st = dyn;                           // [NR][SP] staging, then [L][RS] results
@@ -105,16 +128,20 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
         v[q] = x;
       }
     };
-    const int mt = warp & 3, nb = warp >> 2;  // m-tile; n-tiles nb, nb+2, ...
-    double acc[5][2] = {};
+    const int mt = warp % MT, nb = warp / MT;  // m-tile; n-tiles nb, nb + STEP, ...
+    double acc[NJ][2] = {};
     double v[PER];
     fetch(0, v);
+    double* pkb = pk + (size_t)blk * pg.cs * L * pg.sw;
     for (int64_t c0 = 0; c0 < R.d; c0 += KC) {
       __syncthreads();
   #pragma unroll
       for (int q = 0; q < PER; ++q) {
-        const int e = tid + q * 256;
-        st[(e / KC) * SP + e % KC] = v[q];
+        const int e = tid + q * 256, r = e / KC;
+        st[r * SP + e % KC] = v[q];
+        const int64_t col = c0 + e % KC;
+        if (r < L && col < R.d)  // the block's rows, packed per chain-CTA slice (swizzled, see pk_swz)
+          pkb[((col / pg.sw) * L + r) * pg.sw + pk_swz((int)(col % pg.sw), r)] = v[q];
       }
       __syncthreads();
       if (c0 + KC < R.d) fetch(c0 + KC, v);  // next chunk in flight during the products
@@ -122,8 +149,8 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
       for (int k4 = 0; k4 < KC; k4 += 4) {
         const double a = st[(8 * mt + (lane >> 2)) * SP + k4 + (lane & 3)];
   #pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          const int nt = nb + 2 * j;
+        for (int j = 0; j < NJ; ++j) {
+          const int nt = nb + STEP * j;
           if (nt < NTN) dmma_884(acc[j][0], acc[j][1], a, st[(8 * nt + (lane >> 2)) * SP + k4 + (lane & 3)]);
         }
       }
@@ -131,8 +158,8 @@ sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, c
     __syncthreads();
     double* res = st;  // res[i*RS + n]: n < L: G, L..2L-1: X, 2L: e, 2L+1: b
   #pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const int nt = nb + 2 * j;
+    for (int j = 0; j < NJ; ++j) {
+      const int nt = nb + STEP * j;
       if (nt < NTN) {
         const int i = 8 * mt + (lane >> 2), n = 8 * nt + 2 * (lane & 3);
         res[i * RS + n] = acc[j][0];
@@ -173,57 +200,74 @@ constexpr size_t sstep_prep_smem() {
 }
 
 // ---------------------------------------------------------------------------
-// CHAIN: one cluster of CS CTAs; each CTA = 4 consumer warps + 2 producer warps
-// + 1 signaller warp.
-// CTA r owns columns [r*SW, r*SW + SW), SW = 128*CPT; consumer thread t owns
-// columns r*SW + t*CPT + [0, CPT) of w and of the running sum (registers).
-//  * row producer warp: per block, loads the L indices and issues one bulk copy
-//    (cp.async.bulk, 1-D TMA) per row slice into an NB-deep ring (full/empty
-//    mbarriers), running up to NB blocks ahead;
-//  * M/X producer warp: bulk-copies M_b^T, X_b^T and p_b (from PREP) into an
-//    MXB-deep shared ring, so no consumer register or LSU slot holds them;
-//  * consumers, iteration b: (1) partial dots a~_{b+1} = R_{b+1} w_b over the
-//    slice -> transposed warp reductions -> pushed by remote DSMEM stores into
-//    apub[(b+1)%4][rank] of every CTA; (2) wait (acquire) on ready[b%4] —
-//    completed one iteration earlier, normally — sum the CS partials from local
-//    shared memory, z = a~_b - eta X_b delta_{b-1} - p'_b (threads L..2L-1 form
-//    the X term), delta_b = M_b z (M, X staged in shared memory by a producer
-//    warp); (3) the two rank-L updates with the rows of block b;
-//  * signaller warp: after each block's partials are pushed (local mbarrier),
-//    arrives (release, cluster scope) on every CTA's ready mbarrier, keeping
-//    the fence latency off the consumers.
-//    No cluster-wide barrier inside the loop.
+// CHAIN (v3): one cluster of CS CTAs; CTA r owns columns [r*SW, r*SW + SW).
+// Roles per CTA (warps): NDW dot warps | NUW = SW/32 update warps | one delta
+// warp | one producer warp.
+//  * producer (lane 0): per block, ONE bulk copy of the block's packed L x SW
+//    slice into an NB-deep ring (full/empty mbarriers), and M_b^T, X_b^T, p'_b
+//    into a 2-deep ring;
+//  * dot warps, iteration b: the look-ahead partials a~_{b+1} = R_{b+1} w_b over
+//    the slice, lanes = rows (no cross-lane reduction), dot warp k covering
+//    columns [k*SW/NDW, ...) — combined in shared memory when NDW = 2 — then
+//    every row total goes to every rank of the cluster by st.async (8-byte
+//    remote stores that complete_tx the receiver's part[(b+1) % 4] mbarrier);
+//    w_b comes from the update warps (wready[b & 1]);
+//  * update warps, iteration b: thread t owns column t (w_t and the running sum
+//    S_t in registers): wait delta_b, the two rank-L updates with the block's
+//    rows, w_{b+1} to the shared slice buffer of parity b+1 (wready), rows slot
+//    released (empty);
+//  * delta warp, block b: X term (X_b delta_{b-1}) while the partials travel,
+//    wait part[b % 4] (acquire, cluster scope), z = sum of the CS partials in
+//    rank order - eta X term - p'_b, delta_b = M_b z, then re-arm part[b % 4]
+//    for block b+4.
+// The dependent cycle spans two blocks: update(b-1) -> dots(b+1) -> exchange ->
+// delta_{b+1} -> update(b+1), with the dots and the update of consecutive
+// blocks running concurrently on different warps.
+// Exchange ordering: st.async's complete_tx is the only publication: a phase of
+// part[s] completes when its receiver has armed it (arrive.expect_tx of
+// CS*L*8 bytes) AND every byte of the phase has landed, so a delta warp that
+// observes completion reads complete partials.  Slot reuse needs no
+// back-pressure: a rank pushes block b+4 into slot (b % 4) only after its
+// dots(b+4), which need w_{b+3}, hence delta_{b+2}, hence THIS rank's partials
+// of block b+2, which need this rank's w_{b+1}, i.e. its update(b), which
+// follows its delta warp's read of slot b % 4 and the re-arming.
+// Shared w buffers: dots(b+1) read buffer b & 1 (w_b); update(b+1) rewrites it
+// only after delta_{b+1}, which needs this CTA's own partials of block b+1.
 // w and the running sum persist in global state[0..ld) / [ld..2 ld) between
 // launches (one launch per chunk of blocks).
 struct ChainArgs {
-  SstepRows R;
-  const int64_t* idx;   // chunk indices
+  const double* pk;     // this chunk's packed rows [nblk][CS][L][SW] (swizzled)
   int64_t steps;        // steps in this chunk
   const double* M;      // nblk x L x L (transposed)
   const double* p;      // nblk x L  (p'_b: look-ahead correction folded in for b >= 1)
   const double* X;      // nblk x L x L (transposed): R_b R_{b-1}^T, b >= 1
   const double* mu;     // ld
+  int64_t ld;
   double eta;
   double* state;        // [0, ld) w ; [ld, 2 ld) sum
-  unsigned long long* prof;  // optional: per-phase cycle totals of CTA 0 / thread 0 (debug)
+  unsigned long long* prof;  // optional: per-phase cycle totals of CTA 0 (debug)
 };
 
-constexpr int kChainIdxAhead = 4;  // blocks of step indices the row producer keeps in flight
-
-// row-ring depth: 4 for 1 KB row slices (blocks b, b+1 in use, two in flight), 3 when
-// the slices are 2 KB (shared memory)
-constexpr int chain_nb(int slice_doubles) { return slice_doubles <= 128 ? 4 : 3; }
+template <int SW, int L>
+struct ChainCfg {
+  static constexpr int NUW = SW / 32;                   // update warps (one column per thread)
+  static constexpr int NDW = SW * L / 1024;             // dot warps: 32 columns per dot lane
+  static constexpr int NT = 32 * (NDW + NUW) + 64;      // + delta warp + producer warp
+  static constexpr int NB = SW * L * 8 <= 16384 ? 4 : 3;  // row ring depth
+  static constexpr int NMX = 2;                         // M/X/p ring depth
+  static constexpr int MXW = 2 * L * L + L;             // doubles per M/X/p slot
+  static constexpr int NPS = 4;                         // partials slots (see the ordering argument)
+  static constexpr size_t smem() {
+    return sizeof(double) * ((size_t)NB * L * SW + (size_t)NMX * MXW + (size_t)NPS * 16 * L + 4 * L + L +
+                             2 * NDW * L + 2 * SW) +
+           sizeof(uint64_t) * (2 * NB + 2 * NMX + NPS + 2 + 2) + 128;
+  }
+};
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// arrive (release, cluster scope) on the mbarrier at the same offset in CTA `rank`
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -236,464 +280,321 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-
-// consumers + 2 delta warps + row producer + M/X producer + signaller + second
-// row producer [+ two wideners for fp32 rows].  (A st.async exchange with
-// mbarrier complete_tx in place of the signaller was ~9 % faster per block but
-// not run-to-run deterministic at c3 (16 ranks): removed.)
-template <class T, int CPT, int NT>
-constexpr int chain_threads() {
-  return NT + 192 + ((CPT == 1 && NT == 128 && sizeof(T) == 4) ? 64 : 0);
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+// 8-byte asynchronous store to the cluster shared address `rdst`, completing 8
+// bytes on the mbarrier at cluster shared address `rbar` (same CTA as rdst)
+__device__ __forceinline__ void st_async_f64(uint32_t rdst, uint32_t rbar, double v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(rdst),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
 }
 
-template <class T, int CPT, int L, int MXB, int NT>
-__global__ void __launch_bounds__(chain_threads<T, CPT, NT>(), 1) sstep_chain_kernel(ChainArgs a) {
-  // warps: NCW consumers | 2 delta warps | row producer | M/X producer | signaller
-  constexpr int NCW = NT / 32;
-  constexpr int DW = NCW, WROW = NCW + 2, WMX = NCW + 3, WSIG = NCW + 4;
-  static_assert(2 * L <= 64, "the two delta warps hold the M and X rows");
-  constexpr int SW = NT * CPT, NB = chain_nb(NT * CPT);
-  constexpr int MXW = 2 * L * L + L;  // doubles per M/X slot: M_b^T, X_b^T, then p_b
-  constexpr size_t ROWB = (size_t)SW * 8;  // bytes per row slot (fits an fp64 slice)
-  constexpr int IA = kChainIdxAhead;       // index ring depth (blocks of indices in flight)
-  static_assert(L == 32, "one row per producer lane");
+// debug event trace (SKR_DEBUG_CHAIN): clock64 of CTA 0 per event for blocks
+// [kTraceB0, kTraceB0 + kTraceN) of the first launch: prof[16 + 8 * k + e]
+constexpr int kTraceB0 = 200, kTraceN = 8;
+__device__ __forceinline__ void chain_trace(unsigned long long* prof, int cr, int64_t b, int e) {
+  if (prof && cr == 0 && b >= kTraceB0 && b < kTraceB0 + kTraceN && prof[15] == 0)
+    prof[16 + 8 * (b - kTraceB0) + e] = clock64();
+}
+
+template <int SW, int L>
+__global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(ChainArgs a) {
+  using Cf = ChainCfg<SW, L>;
+  constexpr int NUW = Cf::NUW, NDW = Cf::NDW, NB = Cf::NB, NMX = Cf::NMX, MXW = Cf::MXW, NPS = Cf::NPS;
+  constexpr int WU0 = NDW, WDL = NDW + NUW, WPR = NDW + NUW + 1;  // first update warp, delta warp, producer
+  static_assert(L == 16 || L == 32, "lanes = rows in the dots");
+  static_assert(SW >= 32 && SW % 32 == 0, "slice width");
   extern __shared__ __align__(128) unsigned char sm[];
-  unsigned char* rows = sm;                                                  // [NB][L][ROWB]
-  double* mx = reinterpret_cast<double*>(sm + (size_t)NB * L * ROWB);       // [MXB][MXW] M_b^T, X_b^T, p_b
-  // PUSH (CPT = 1): every rank pushes its partials into apub[slot][rank] of all
-  // ranks and gathers locally; pull (CPT = 2, where shared memory is tight): each
-  // rank keeps its own apub[slot] and the gather reads the ranks remotely.
-  constexpr bool PUSH = CPT == 1 && NT == 128;
-  constexpr int NP = 2;             // row producer warps (each gathers 16 rows of a block)
-  constexpr int RPP = L / NP;       // rows per producer warp
-  constexpr int WPR2 = NCW + 5;  // second row producer
-  constexpr int WWID = NCW + 6;  // first widener warp
-  constexpr int NWID = 2;        // widener warps
-  // fp32 data rows are widened to fp64 in their ring slot by two widener warps as
-  // soon as they land, so the consumers' dots and update read fp64 only.  With
-  // 256-column slices (d > 2048) the wideners cannot keep up (c4: 3.2 K -> 3.8 K
-  // cycles per block) and the consumers widen in the dots instead.
-  constexpr bool PWIDEN = sizeof(T) == 4 && PUSH;
-  double* apub = mx + MXB * MXW;                                             // [4][PUSH ? 16 : 1][L]
-  double* zbuf = apub + 4 * (PUSH ? 16 : 1) * L;                             // [L] (also the X term)
-  double* xterm = zbuf;                                                      // thread i reads xterm[i] then writes zbuf[i]
-  double* dl = zbuf + L;                                                     // [2][L] delta_b (by parity)
-  double* delta2 = dl + 2 * L;                                               // [2][L]
-  uint64_t* full = reinterpret_cast<uint64_t*>(delta2 + 2 * L);              // [NB]
-  uint64_t* empty = full + NB;                                               // [NB]
-  uint64_t* ready = empty + NB;                                              // [4]
-  uint64_t* mx_full = ready + 4;                                             // [MXB]
-  uint64_t* mx_empty = mx_full + MXB;                                        // [MXB]
-  uint64_t* pub = mx_empty + MXB;                                            // [2] local: partials pushed
-  uint64_t* dready = pub + 2;                                                // [2] local: delta_b published
-  uint64_t* dmask = dready + 2;                                              // [NB] bit l: row l is a data row
-  double* wsm = reinterpret_cast<double*>(dmask + NB);                       // [2][SW] w slice by block parity
-  int64_t* iring = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(wsm + 2 * SW) + 15) & ~uintptr_t(15));  // [IA][L]
-  uint64_t* ifull = reinterpret_cast<uint64_t*>(iring + IA * L);             // [2][IA] (per producer)
-  uint64_t* wide = ifull + 2 * IA;                                           // [NB][NWID] fp32 rows widened
+  double* rows = reinterpret_cast<double*>(sm);                 // [NB][L][SW] (swizzled)
+  double* mx = rows + (size_t)NB * L * SW;                      // [NMX][MXW]: M_b^T, X_b^T, p'_b
+  double* apub = mx + NMX * MXW;                                // [NPS][16][L] partials by sender rank
+  double* dl = apub + NPS * 16 * L;                             // [2][L] delta_b by parity
+  double* d2 = dl + 2 * L;                                      // [2][L] (Lb - l) delta_b by parity
+  double* zbuf = d2 + 2 * L;                                    // [L]
+  double* dpart = zbuf + L;                                     // [2][NDW][L] dot warps' partials by parity
+  double* wsm = dpart + 2 * NDW * L;                            // [2][SW] w slice by block parity
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + 2 * SW);   // [NB]
+  uint64_t* empty = full + NB;                                  // [NB]
+  uint64_t* mx_full = empty + NB;                               // [NMX]
+  uint64_t* mx_empty = mx_full + NMX;                           // [NMX]
+  uint64_t* part = mx_empty + NMX;                              // [NPS] partials (complete_tx)
+  uint64_t* dready = part + NPS;                                // [2] delta_b published (local)
+  uint64_t* wready = dready + 2;                                // [2] w_b written, by parity
 
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const SstepRows& R = a.R;
   const int64_t slice0 = (int64_t)cr * SW;
   const int64_t nblk = (a.steps + L - 1) / L;
+  const uint32_t part_bytes = (uint32_t)(CS * L * 8);
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) {
-      mbar_init(&full[q], NP);  // one (expect_tx) arrival per row producer warp
-      mbar_init(&empty[q], 1);
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NUW);
     }
-    for (int q = 0; q < 4; ++q) {
-      // push: one local arrival (the arming expect_tx) + CS * L * 8 bytes of st.async
-      // partials; pull: one release arrive per rank from its signaller
-      mbar_init(&ready[q], CS);  // one release arrive per rank (its signaller)
-    }
-    for (int q = 0; q < MXB; ++q) {
+    for (int q = 0; q < NMX; ++q) {
       mbar_init(&mx_full[q], 1);
       mbar_init(&mx_empty[q], 1);
     }
-    mbar_init(&pub[0], NCW);
-    mbar_init(&pub[1], NCW);
+    for (int q = 0; q < NPS; ++q) mbar_init(&part[q], 1);  // the receiver's own arming arrive
     mbar_init(&dready[0], 1);
     mbar_init(&dready[1], 1);
-    for (int q = 0; q < 2 * IA; ++q) mbar_init(&ifull[q], 1);
-    for (int q = 0; q < NB * NWID; ++q) mbar_init(&wide[q], 1);  // [slot][widener warp]
+    mbar_init(&wready[0], NUW);
+    mbar_init(&wready[1], NUW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // arm the first NPS phases; bytes that land earlier count negative until then
+    for (int q = 0; q < NPS && q < nblk; ++q) mbar_expect_tx(&part[q], part_bytes);
   }
-  cluster.sync();  // every CTA's barriers exist before any remote arrive
+  // w_0 in both parity buffers (dots(0) reads buffer 1, dots(1) buffer 0)
+  for (int t = tid; t < SW; t += blockDim.x) {
+    const int64_t col = slice0 + t;
+    const double w0 = col < a.ld ? a.state[col] : 0.0;
+    wsm[t] = w0;
+    wsm[SW + t] = w0;
+  }
+  cluster.sync();  // every CTA's barriers exist before any remote complete_tx; w_0 visible
 
-  if (warp == WSIG) {
-    // ---------------- signaller: once this CTA's partials of block j are pushed
-    // (pub), arrive (release, cluster scope) on every rank's ready[j % 4].  The
-    // release fence latency stays off the consumers' path.  pub is 2-deep: the
-    // consumers cannot complete phase j+2 before their ready[j] wait, which needs
-    // this warp's arrive for j.
-    for (int64_t j = 0; j < nblk; ++j) {
-      mbar_wait(&pub[j & 1], (uint32_t)((j >> 1) & 1));
-      if (lane < CS) mbar_arrive_remote(&ready[j & 3], (uint32_t)lane);
-    }
-  } else if (warp == WMX) {
-    // ---------------- M/X producer: M_b^T, X_b^T, p_b by bulk copy ----------------
+  if (warp == WPR) {
+    // ---------------- producer: packed rows and M/X/p by bulk copy ----------------
     if (lane == 0) {
+      const uint32_t slice_bytes = (uint32_t)(L * SW * 8);
       for (int64_t b = 0; b < nblk; ++b) {
-        const int slot = (int)(b % MXB);
-        if (b >= MXB) mbar_wait(&mx_empty[slot], (uint32_t)(((b / MXB) - 1) & 1));
-        double* dst = mx + slot * MXW;
-        mbar_expect_tx(&mx_full[slot], (uint32_t)(MXW * 8));
-        bulk_g2s(dst, a.M + b * L * L, (uint32_t)(L * L * 8), &mx_full[slot]);
-        bulk_g2s(dst + L * L, a.X + b * L * L, (uint32_t)(L * L * 8), &mx_full[slot]);  // b = 0: unused
-        bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[slot]);
+        const int s = (int)(b % NB);
+        if (b >= NB) mbar_wait(&empty[s], (uint32_t)(((b / NB) - 1) & 1));
+        mbar_expect_tx(&full[s], slice_bytes);
+        bulk_g2s(rows + (size_t)s * L * SW, a.pk + ((size_t)b * CS + cr) * L * SW, slice_bytes, &full[s]);
+        const int ms = (int)(b % NMX);
+        if (b >= NMX) mbar_wait(&mx_empty[ms], (uint32_t)(((b / NMX) - 1) & 1));
+        double* dst = mx + ms * MXW;
+        mbar_expect_tx(&mx_full[ms], (uint32_t)(MXW * 8));
+        bulk_g2s(dst, a.M + b * L * L, (uint32_t)(L * L * 8), &mx_full[ms]);
+        bulk_g2s(dst + L * L, a.X + b * L * L, (uint32_t)(L * L * 8), &mx_full[ms]);  // b = 0: unused
+        bulk_g2s(dst + 2 * L * L, a.p + b * L, (uint32_t)(L * 8), &mx_full[ms]);
       }
     }
-  } else if (warp == WROW || warp == WPR2) {
-    // ---------------- row producer warps ----------------
-    // NP warps gather the sampled rows, each RPP of them.  A bulk copy costs ~70 cycles of issue
-    // (an elect/broadcast loop per lane), so one warp issuing all 32 rows took
-    // ~2.2 K cycles per block — about the whole block.
-    const int h = warp == WROW ? 0 : 1;   // this producer's half
-    const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);  // may be <= 0 past ld
-    // The step indices of full blocks travel IA blocks ahead through a shared ring
-    // (one bulk copy per block): a register load one block ahead left the producer
-    // waiting a dependent global-load latency (~2 K cycles) per block.
-    const int64_t nfull = a.steps / L;  // blocks whose L indices all exist
-    int64_t* my_ring = iring + h * IA * RPP;
-    uint64_t* my_full = ifull + h * IA;
-    auto issue_idx = [&](int64_t b) {
-      if (b < nfull) {
-        const int q = (int)(b % IA);
-        mbar_expect_tx(&my_full[q], (uint32_t)(RPP * 8));
-        bulk_g2s(my_ring + q * RPP, a.idx + b * L + h * RPP, (uint32_t)(RPP * 8), &my_full[q]);
-      }
-    };
-    if (lane == 0)
-      for (int64_t b = 0; b < IA; ++b) issue_idx(b);
-    const bool pprof = a.prof && cr == 0 && lane == 0 && h == 0;
-    unsigned long long pw = 0, pi = 0;
-    const bool mine = lane < RPP;  // lane owns row h * RPP + lane
-    for (int64_t b = 0; b < nblk; ++b) {
-      const int slot = (int)(b % NB);
-      unsigned long long q0 = pprof ? clock64() : 0;
-      int64_t i = -1;
-      if (b < nfull) {
-        const int q = (int)(b % IA);
-        mbar_wait(&my_full[q], (uint32_t)((b / IA) & 1));
-        if (mine) i = my_ring[q * RPP + lane];
-        __syncwarp();  // every lane has read slot q before it is refilled
-        if (lane == 0) issue_idx(b + IA);
-      } else if (mine) {  // the partial last block of the launch: direct loads
-        const int64_t t = b * L + h * RPP + lane;
-        i = t < a.steps ? a.idx[t] : -1;
-      }
-      if (b >= NB) mbar_wait(&empty[slot], (uint32_t)(((b / NB) - 1) & 1));
-      unsigned long long q1 = pprof ? clock64() : 0;
-      // data-row mask (this half), then one bulk copy (1-D TMA) per row slice
-      uint32_t bytes = (i >= 0 && slice_elems > 0) ? (uint32_t)(slice_elems * (i < R.n ? (int64_t)sizeof(T) : 8)) : 0u;
-      const unsigned bal = __ballot_sync(0xffffffffu, i >= 0 && i < R.n);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
-      if (lane == 0) {
-        reinterpret_cast<uint16_t*>(&dmask[slot])[h] = (uint16_t)(bal & 0xFFFFu);  // rows 16h..16h+15
-        if (bytes) mbar_expect_tx(&full[slot], bytes);
-        else mbar_arrive_local(&full[slot]);
-      }
-      __syncwarp();
-      if (i >= 0 && slice_elems > 0) {
-        unsigned char* dst = rows + ((size_t)slot * L + h * RPP + lane) * ROWB;
-        if (i < R.n)
-          bulk_g2s(dst, static_cast<const T*>(R.Xt) + i * R.ld + slice0, (uint32_t)(slice_elems * sizeof(T)),
-                   &full[slot]);
-        else
-          bulk_g2s(dst, R.B + (i - R.n) * R.ld + slice0, (uint32_t)(slice_elems * 8), &full[slot]);
-      }
-      if (pprof) {
-        const unsigned long long q2 = clock64();
-        pw += q1 - q0;
-        pi += q2 - q1;
-      }
-    }
-    if (pprof) {
-      atomicAdd(a.prof + 7, pw);
-      atomicAdd(a.prof + 8, pi);
-    }
-  } else if (PWIDEN && warp >= WWID && warp < WWID + NWID) {
-    // ---------------- two widener warps (rows 0..15 / 16..31): the fp32 data rows
-    // of each landed block -> fp64 in place (the slot is sized for fp64).  Lane l
-    // reads 8-byte float pairs l, l+32, ... and writes them as 16-byte double pairs
-    // at the same indices: conflict-free both ways.  Every lane reads a batch of
-    // rows before any lane writes it; no per-row branches ----------------
-    constexpr int NV = SW / 64;                  // float pairs per lane per row
-    constexpr int BR = SW <= 128 ? L / 2 : 4;    // rows per batch (register budget)
-    const int64_t slice_elems = std::min<int64_t>(SW, R.ld - slice0);
-    bool act[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) act[k] = 2 * (lane + 32 * k) < slice_elems;
-    const int rbeg = (warp - WWID) * (L / NWID);
-    for (int64_t b = 0; b < nblk; ++b) {
-      const int slot = (int)(b % NB);
-      mbar_wait(&full[slot], (uint32_t)((b / NB) & 1));
-      const uint32_t dm = (uint32_t)dmask[slot];  // L = 32
-      unsigned char* base = rows + (size_t)slot * L * ROWB;
-#pragma unroll
-      for (int r0 = rbeg; r0 < rbeg + L / NWID; r0 += BR) {
-        float2 f[BR][NV];
-#pragma unroll
-        for (int r = 0; r < BR; ++r) {
-          const float2* src = reinterpret_cast<const float2*>(base + (size_t)(r0 + r) * ROWB);
-#pragma unroll
-          for (int k = 0; k < NV; ++k) f[r][k] = act[k] ? src[lane + 32 * k] : make_float2(0.f, 0.f);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < BR; ++r) {
-          const bool dr = (dm >> (r0 + r)) & 1u;  // data row (regulariser rows are fp64 already)
-          double2* o = reinterpret_cast<double2*>(base + (size_t)(r0 + r) * ROWB);
-#pragma unroll
-          for (int k = 0; k < NV; ++k)
-            if (dr && act[k]) o[lane + 32 * k] = make_double2((double)f[r][k].x, (double)f[r][k].y);
-        }
-        __syncwarp();
-      }
-      // order these generic-proxy stores before the bulk copy that refills the slot
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_local(&wide[slot * NWID + (warp - WWID)]);
-    }
-  } else if (warp == DW || warp == DW + 1) {
-    // ---------------- delta warps (64 threads): resolve block b while the consumers
-    // compute the look-ahead dots of block b+1 ----------------
-    const int j = tid - NT;  // 0..63
+  } else if (warp == WDL) {
+    // ---------------- delta warp: lane i resolves row i of each block ----------------
+    const int i = lane;
+    const bool prof = a.prof && cr == 0 && lane == 0;
+    unsigned long long t_wait = 0;
     for (int64_t b = 0; b < nblk; ++b) {
       const int Lb = (int)min((int64_t)L, a.steps - b * L);
-      const int mslot = (int)(b % MXB);
-      const double* Ms = mx + mslot * MXW;
+      const int ms = (int)(b % NMX);
+      const double* Ms = mx + ms * MXW;
       const double* Xs = Ms + L * L;
       const double* ps = Ms + 2 * L * L;
-      mbar_wait(&mx_full[mslot], (uint32_t)((b / MXB) & 1));
-      // X term (threads L..2L-1): xterm_i = (X_b delta_{b-1})_i
-      if (j >= L && j < 2 * L && b > 0) {
-        const double* dp = dl + ((b - 1) & 1) * L;
-        const int i = j - L;
-        double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+      mbar_wait(&mx_full[ms], (uint32_t)((b / NMX) & 1));
+      // off the critical path (delta_{b-1} is known, the partials of b are in
+      // flight): c_i = eta (X_b delta_{b-1})_i + p'_i and row i of M_b in registers
+      double ci = 0.0, mrow[L];
+      if (i < L) {
+        double xt = 0.0;
+        if (b > 0) {
+          const double* dp = dl + ((b - 1) & 1) * L;
+          double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
 #pragma unroll
-        for (int k = 0; k < L; k += 4) {
-          x0 = fma(Xs[k * L + i], dp[k], x0);
-          x1 = fma(Xs[(k + 1) * L + i], dp[k + 1], x1);
-          x2 = fma(Xs[(k + 2) * L + i], dp[k + 2], x2);
-          x3 = fma(Xs[(k + 3) * L + i], dp[k + 3], x3);
+          for (int k = 0; k < L; k += 4) {
+            const double4 dq = *reinterpret_cast<const double4*>(dp + k);
+            x0 = fma(Xs[k * L + i], dq.x, x0);
+            x1 = fma(Xs[(k + 1) * L + i], dq.y, x1);
+            x2 = fma(Xs[(k + 2) * L + i], dq.z, x2);
+            x3 = fma(Xs[(k + 3) * L + i], dq.w, x3);
+          }
+          xt = (x0 + x1) + (x2 + x3);
         }
-        xterm[i] = (x0 + x1) + (x2 + x3);
-      }
-      named_bar(2, 64);  // xterm visible
-      // a_b: the CS partials of block b (DSMEM), z = a - eta X delta_prev - p'
-      mbar_wait_cluster(&ready[b & 3], (uint32_t)((b >> 2) & 1));
-      if (j < L) {
-        double part[16];
+        ci = a.eta * xt + ps[i];
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          part[q] = q >= CS ? 0.0
-                    : PUSH  ? apub[((b & 3) * 16 + q) * L + j]
-                            : cluster.map_shared_rank(apub, q)[(b & 3) * L + j];
-        double sum = 0.0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sum += part[q];
-        if (b > 0) sum -= a.eta * xterm[j];
-        zbuf[j] = sum - ps[j];
+        for (int k = 0; k < L; ++k) mrow[k] = Ms[k * L + i];
       }
-      named_bar(2, 64);
-      // delta_b = M_b z (thread j < L: row j, four partial sums)
-      double* dcur = dl + (b & 1) * L;
-      double* d2 = delta2 + (b & 1) * L;
-      if (j < L) {
+      const int ps4 = (int)(b % NPS);
+      const unsigned long long w0 = prof ? clock64() : 0;
+      mbar_wait_cluster(&part[ps4], (uint32_t)((b / NPS) & 1));
+      if (prof) t_wait += clock64() - w0;
+      if (lane == 0) chain_trace(a.prof, cr, b, 2);
+      if (i < L) {
+        // the CS partials of row i, summed by a fixed tree (deterministic)
+        const double* ap = apub + (size_t)ps4 * 16 * L + i;
+        double pq[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) pq[q] = q < CS ? ap[q * L] : 0.0;
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+          for (int q = 0; q < h; ++q) pq[q] += pq[q + h];
+        zbuf[i] = pq[0] - ci;
+      }
+      __syncwarp();
+      if (i < L) {
         double d0 = 0.0, d1 = 0.0, d2v = 0.0, d3 = 0.0;
 #pragma unroll
         for (int k = 0; k < L; k += 4) {
-          d0 = fma(Ms[k * L + j], zbuf[k], d0);
-          d1 = fma(Ms[(k + 1) * L + j], zbuf[k + 1], d1);
-          d2v = fma(Ms[(k + 2) * L + j], zbuf[k + 2], d2v);
-          d3 = fma(Ms[(k + 3) * L + j], zbuf[k + 3], d3);
+          const double4 zq = *reinterpret_cast<const double4*>(zbuf + k);
+          d0 = fma(mrow[k], zq.x, d0);
+          d1 = fma(mrow[k + 1], zq.y, d1);
+          d2v = fma(mrow[k + 2], zq.z, d2v);
+          d3 = fma(mrow[k + 3], zq.w, d3);
         }
         const double dv = (d0 + d1) + (d2v + d3);
-        dcur[j] = dv;
-        d2[j] = (double)(Lb - j) * dv;  // (Lb - l + 1) weight, 1-based l
-      }
-      named_bar(2, 64);  // delta_b complete, zbuf / M / X reads done
-      if (j == 0) {
-        // push: slot b % 4 is read; arm it for block b + 4 (no rank can send those
-        // partials before every rank has consumed block b: they need delta_{b+3})
-        mbar_arrive_local(&mx_empty[mslot]);  // M/X slot consumed
-        mbar_arrive_local(&dready[b & 1]);   // delta_b visible to the consumers (release.cta)
-      }
-    }
-  } else {
-    // ---------------- consumer warps (128 threads) ----------------
-    const int64_t col0 = slice0 + (int64_t)tid * CPT;
-    bool act[CPT];
-    double w[CPT], S[CPT], mu[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      act[c] = col0 + c < R.d;
-      w[c] = act[c] ? a.state[col0 + c] : 0.0;
-      S[c] = act[c] ? a.state[R.ld + col0 + c] : 0.0;
-      mu[c] = act[c] ? a.mu[col0 + c] : 0.0;
-      wsm[tid * CPT + c] = w[c];  // w at the start of block 0 in both buffers
-      wsm[SW + tid * CPT + c] = w[c];
-    }
-    named_bar(1, NT);
-    unsigned long long tp[9] = {};
-    const bool prof = a.prof && cr == 0 && tid == 0;
-    // partial dots of block bb's rows (ring slot) with the current w slice, pushed
-    // (remote DSMEM stores) into apub[bb % 4][cr] of every CTA of the cluster
-    auto dots = [&](int64_t bb) {
-      const int slot = (int)(bb % NB);
-      const int Lbb = (int)min((int64_t)L, a.steps - bb * L);
-      const unsigned long long w0c = prof ? clock64() : 0;
-      if (PWIDEN) {
-#pragma unroll
-        for (int q = 0; q < NWID; ++q) mbar_wait(&wide[slot * NWID + q], (uint32_t)((bb / NB) & 1));
-      } else {
-        mbar_wait(&full[slot], (uint32_t)((bb / NB) & 1));
-      }
-      if (prof) tp[8] += clock64() - w0c;
-      const unsigned char* rb = rows + (size_t)slot * L * ROWB;
-      const uint64_t dm = dmask[slot];
-      constexpr int RPW = L / NCW;      // rows per warp: warp q owns rows [q*RPW, (q+1)*RPW)
-      constexpr int CPL = SW / 32;      // columns per lane, interleaved (conflict-free)
-      double wl[CPL];
-      const int64_t valid = R.ld - slice0;  // columns past the copied slice hold stale smem
-      bool lok[CPL];
-      // w at the start of block bb - 1 (the look-ahead dots), in buffer (bb - 1) & 1; the
-      // update of block bb - 1 writes the other buffer, so a warp that is already
-      // updating cannot overwrite values another warp is still loading here
-      const double* wb = wsm + ((bb + 1) & 1) * SW;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        lok[c] = (int64_t)(lane + 32 * c) < valid;
-        wl[c] = wb[lane + 32 * c];
-      }
-      double v[RPW];
-#pragma unroll
-      for (int q = 0; q < RPW; ++q) {
-        const int l = warp * RPW + q;
-        const unsigned char* rowp = rb + (size_t)l * ROWB;
-        double s = 0.0;
-        if (sizeof(T) == 8 || PWIDEN || ((dm >> l) & 1ull) == 0) {
-          const double* x = reinterpret_cast<const double*>(rowp) + lane;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) s = fma(lok[c] ? x[32 * c] : 0.0, wl[c], s);
-        } else {
-          // fp32 data row: widen once and write the fp64 values back in place (the
-          // slot is sized for fp64), so the update of this block reads fp64 rows only
-          const T* x = reinterpret_cast<const T*>(rowp) + lane;
-          double xv[CPL];
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) xv[c] = lok[c] ? (double)x[32 * c] : 0.0;
-          __syncwarp();  // every lane has read its fp32 values before any fp64 store lands
-          double* xd = reinterpret_cast<double*>(const_cast<unsigned char*>(rowp)) + lane;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            xd[32 * c] = xv[c];
-            s = fma(xv[c], wl[c], s);
-          }
-        }
-        v[q] = l < Lbb ? s : 0.0;
-      }
-      warp_transpose_reduce<RPW>(v, lane);
-      // lane (32/RPW) r holds row r: broadcast the warp's RPW sums, then lane q < CS
-      // writes them to rank q with 16-byte stores
-      double vals[RPW];
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) vals[r] = __shfl_sync(0xffffffffu, v[0], (32 / RPW) * r);
-      if (PUSH) {
-        if (lane < CS) {
-          double* dst = cluster.map_shared_rank(apub, lane) + ((bb & 3) * 16 + cr) * L + warp * RPW;
-#pragma unroll
-          for (int r = 0; r < RPW; r += 2) *reinterpret_cast<double2*>(dst + r) = make_double2(vals[r], vals[r + 1]);
-        }
-      } else if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) apub[(bb & 3) * L + warp * RPW + r] = vals[r];
+        dl[(b & 1) * L + i] = dv;
+        d2[(b & 1) * L + i] = (double)(Lb - i) * dv;  // (Lb - l + 1) weight, 1-based l
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(&pub[bb & 1]);  // this warp's partials of block bb are published
-    };
-    // prologue: a_0 = R_0 w_0 directly
-    if (nblk > 0) {
-      dots(0);
-      named_bar(1, NT);  // dots(0) read buffer 1, which the update of block 0 rewrites
-    }
-    for (int64_t b = 0; b < nblk; ++b) {
-      const int slot = (int)(b % NB);
-      const int Lb = (int)min((int64_t)L, a.steps - b * L);
-      unsigned long long c0 = prof ? clock64() : 0;
-      // 1. look-ahead partial dots of block b+1 with w_b, published to the cluster
-      if (b + 1 < nblk) dots(b + 1);
-      unsigned long long c1 = prof ? clock64() : 0;
-      // delta_b from the delta warps (computed while this iteration's dots ran)
-      unsigned long long c2 = prof ? clock64() : 0;
-      mbar_wait(&dready[b & 1], (uint32_t)((b >> 1) & 1));
-      unsigned long long c3 = c2, c4 = c2;
-      const double* dcur = dl + (b & 1) * L;
-      const double* dd2 = delta2 + (b & 1) * L;
-      unsigned long long c5 = prof ? clock64() : 0;
-      // 3. w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
-      const unsigned char* rb = rows + (size_t)slot * L * ROWB;
-      // every row of the slot is fp64 by now (fp32 rows were widened in place by dots())
-      auto elem = [&](int l, int c) -> double {
-        return reinterpret_cast<const double*>(rb + (size_t)l * ROWB)[tid * CPT + c];
-      };
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        if (!act[c]) continue;
-        double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-        int l = 0;
-        for (; l + 3 < Lb; l += 4) {
-          const double x0 = elem(l, c), x1 = elem(l + 1, c), x2 = elem(l + 2, c), x3 = elem(l + 3, c);
-          const double4 dd = *reinterpret_cast<const double4*>(dcur + l);
-          const double4 ee = *reinterpret_cast<const double4*>(dd2 + l);
-          u0 = fma(dd.x, x0, u0); u1 = fma(dd.y, x1, u1); u2 = fma(dd.z, x2, u2); u3 = fma(dd.w, x3, u3);
-          v0 = fma(ee.x, x0, v0); v1 = fma(ee.y, x1, v1); v2 = fma(ee.z, x2, v2); v3 = fma(ee.w, x3, v3);
-        }
-        for (; l < Lb; ++l) {
-          const double x = elem(l, c);
-          u0 = fma(dcur[l], x, u0);
-          v0 = fma(dd2[l], x, v0);
-        }
-        const double u = (u0 + u1) + (u2 + u3), v = (v0 + v1) + (v2 + v3);
-        const double w0 = w[c];
-        S[c] += (double)Lb * w0 - a.eta * v - a.eta * mu[c] * (0.5 * (double)Lb * (double)(Lb + 1));
-        w[c] = w0 - a.eta * u - a.eta * (double)Lb * mu[c];
-        wsm[((b + 1) & 1) * SW + tid * CPT + c] = w[c];  // w at the start of block b + 1
+      if (lane == 0) {
+        chain_trace(a.prof, cr, b, 3);
+        mbar_arrive_local(&dready[b & 1]);  // delta_b visible to the update warps (release.cta)
+        mbar_arrive_local(&mx_empty[ms]);   // M/X slot consumed
+        if (b + NPS < nblk) mbar_expect_tx(&part[ps4], part_bytes);  // slot read: arm block b + NPS
       }
-      named_bar(1, NT);  // every consumer is done with rows[slot]; new w visible
-      if (tid == 0) mbar_arrive_local(&empty[slot]);
+    }
+    if (prof) atomicAdd(a.prof + 4, t_wait);
+  } else if (warp < NDW) {
+    // ---------------- dot warps: lanes = rows ----------------
+    // L = 32: lane l = row l; L = 16: lanes l and l+16 take row l, each half of
+    // the warp's columns.  Every dot lane covers 32 consecutive (logical) columns
+    // starting at c0; with the swizzle, column c0 + 16m + jj of row l sits at
+    // c0 + 16m + (jj ^ (l & 15)): 16 per-lane offsets, the rest immediates.
+    constexpr int HALVES = 32 / L;
+    constexpr int NCOL = 32;
+    static_assert(NDW * HALVES * NCOL == SW, "dot warps cover the slice");
+    const int l = lane % L;
+    const int c0 = (warp * HALVES + lane / L) * NCOL;
+    int off[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) off[jj] = jj ^ (l & 15);
+    // remote addresses of this lane's partial in every rank (slot 0), and of part[0]
+    uint32_t rdst[16], rbar[16];
+    const uint32_t ldst = smem_u32(apub + (size_t)cr * L + l), lbar = smem_u32(&part[0]);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      rdst[q] = q < CS ? mapa_u32(ldst, (uint32_t)q) : 0u;
+      rbar[q] = q < CS ? mapa_u32(lbar, (uint32_t)q) : 0u;
+    }
+    const bool prof = a.prof && cr == 0 && tid == 0;
+    unsigned long long tw = 0, td = 0;
+    for (int64_t bb = 0; bb < nblk; ++bb) {  // dots(bb) against w_{bb-1} (w_0 for bb = 0)
+      const int s = (int)(bb % NB);
+      const unsigned long long q0 = prof ? clock64() : 0;
+      if (bb >= 2) mbar_wait(&wready[(bb - 1) & 1], (uint32_t)(((bb - 2) >> 1) & 1));  // w_{bb-1} written
+      mbar_wait(&full[s], (uint32_t)((bb / NB) & 1));
+      const unsigned long long q1 = prof ? clock64() : 0;
+      if (warp == 0 && lane == 0) chain_trace(a.prof, cr, bb, 0);
+      const double* x = rows + (size_t)s * L * SW + (size_t)l * SW + c0;
+      const double* wb = wsm + (size_t)((bb + 1) & 1) * SW + c0;  // w_{bb-1}: buffer of parity bb - 1
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < NCOL / 16; ++m) {
+#pragma unroll
+        for (int jj = 0; jj < 16; jj += 2) {
+          const double2 wq = *reinterpret_cast<const double2*>(wb + 16 * m + jj);
+          acc[(jj >> 1) & 3] = fma(x[16 * m + off[jj]], wq.x, acc[(jj >> 1) & 3]);
+          acc[((jj >> 1) + 1) & 3] = fma(x[16 * m + off[jj + 1]], wq.y, acc[((jj >> 1) + 1) & 3]);
+        }
+      }
+      double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      if constexpr (HALVES == 2) v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if constexpr (NDW > 1) {
+        // the dot warps' partials of the same rows meet in shared memory (by parity)
+        double* dp = dpart + (size_t)(bb & 1) * NDW * L;
+        if (lane < L) dp[warp * L + l] = v;
+        named_bar(2, 32 * NDW);
+        if (warp == 0 && lane < L) {
+          v = dp[l];
+#pragma unroll
+          for (int k = 1; k < NDW; ++k) v += dp[k * L + l];
+        }
+      }
+      if (warp == 0 && lane < L) {
+        const uint32_t off_s = (uint32_t)((bb % NPS) * 16 * L * 8), boff = (uint32_t)((bb % NPS) * 8);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < CS) st_async_f64(rdst[q] + off_s, rbar[q] + boff, v);
+        if (lane == 0) chain_trace(a.prof, cr, bb, 1);
+      }
       if (prof) {
-        const unsigned long long c6 = clock64();
-        tp[0] += c2 - c1; tp[7] += c6 - c0; tp[1] += c1 - c0; tp[2] += c3 - c2; tp[3] += c4 - c3; tp[4] += c5 - c4; tp[5] += c6 - c5;
-        tp[6] += 1;
+        const unsigned long long q2 = clock64();
+        tw += q1 - q0;
+        td += q2 - q1;
       }
     }
-    if (prof)
-      for (int q = 0; q < 7; ++q) atomicAdd(a.prof + q, tp[q]);
     if (prof) {
-      atomicAdd(a.prof + 9, tp[7]);
-      atomicAdd(a.prof + 10, tp[8]);
+      atomicAdd(a.prof + 0, td);
+      atomicAdd(a.prof + 5, tw);
     }
+  } else {
+    // ---------------- update warps: thread t owns column slice0 + t ----------------
+    const int t = tid - 32 * WU0;
+    const int64_t col = slice0 + t;
+    const bool act = col < a.ld;
+    double w = act ? a.state[col] : 0.0;
+    double S = act ? a.state[a.ld + col] : 0.0;
+    const double muc = act ? a.mu[col] : 0.0;
+    int off[16];  // column t of row l sits at l * SW + off[l & 15]
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if (!act[c]) continue;
-      a.state[col0 + c] = w[c];
-      a.state[R.ld + col0 + c] = S[c];
+    for (int k = 0; k < 16; ++k) off[k] = pk_swz(t, k);
+    const bool prof = a.prof && cr == 0 && t == 0;
+    unsigned long long tp[3] = {};
+    for (int64_t b = 0; b < nblk; ++b) {
+      const int s = (int)(b % NB);
+      const int Lb = (int)min((int64_t)L, a.steps - b * L);
+      const unsigned long long c0 = prof ? clock64() : 0;
+      mbar_wait(&dready[b & 1], (uint32_t)((b >> 1) & 1));
+      const unsigned long long c1 = prof ? clock64() : 0;
+      if (t == 0) chain_trace(a.prof, cr, b, 4);
+      // w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
+      const double* rb = rows + (size_t)s * L * SW;
+      const double* dd = dl + (b & 1) * L;
+      const double* ee = d2 + (b & 1) * L;
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      if (Lb == L) {
+#pragma unroll
+        for (int l = 0; l < L; l += 4) {
+          const double x0 = rb[l * SW + off[l & 15]], x1 = rb[(l + 1) * SW + off[(l + 1) & 15]];
+          const double x2 = rb[(l + 2) * SW + off[(l + 2) & 15]], x3 = rb[(l + 3) * SW + off[(l + 3) & 15]];
+          const double4 dq = *reinterpret_cast<const double4*>(dd + l);
+          const double4 eq = *reinterpret_cast<const double4*>(ee + l);
+          u0 = fma(dq.x, x0, u0); u1 = fma(dq.y, x1, u1); u2 = fma(dq.z, x2, u2); u3 = fma(dq.w, x3, u3);
+          v0 = fma(eq.x, x0, v0); v1 = fma(eq.y, x1, v1); v2 = fma(eq.z, x2, v2); v3 = fma(eq.w, x3, v3);
+        }
+      } else {
+        for (int l = 0; l < Lb; ++l) {
+          const double x = rb[l * SW + pk_swz(t, l)];
+          u0 = fma(dd[l], x, u0);
+          v0 = fma(ee[l], x, v0);
+        }
+      }
+      const double u = (u0 + u1) + (u2 + u3), vv = (v0 + v1) + (v2 + v3);
+      const double w0 = w;
+      S += (double)Lb * w0 - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
+      w = w0 - a.eta * u - a.eta * (double)Lb * muc;
+      wsm[((b + 1) & 1) * SW + t] = w;  // w_{b+1}
+      __syncwarp();
+      if (t == 0) chain_trace(a.prof, cr, b, 5);
+      if (lane == 0) {
+        mbar_arrive_local(&wready[(b + 1) & 1]);  // this warp's columns of w_{b+1} written (release.cta)
+        mbar_arrive_local(&empty[s]);             // this warp is done with rows[s]
+      }
+      if (prof) {
+        const unsigned long long c2 = clock64();
+        tp[0] += c1 - c0;
+        tp[1] += c2 - c1;
+        tp[2] += 1;
+      }
+    }
+    if (prof) {
+      atomicAdd(a.prof + 1, tp[0]);
+      atomicAdd(a.prof + 2, tp[1]);
+      atomicAdd(a.prof + 3, tp[2]);
+    }
+    if (act) {
+      a.state[col] = w;
+      a.state[a.ld + col] = S;
     }
   }
-  cluster.sync();  // no CTA exits while others may still read its smem / arrive on its barriers
-}
-
-template <int CPT, int L, int MXB, int NT>
-constexpr size_t sstep_chain_smem() {
-  return (size_t)chain_nb(NT * CPT) * L * NT * CPT * 8 + sizeof(double) * MXB * (2 * L * L + L) +
-         sizeof(double) * (4 * (CPT == 1 && NT == 128 ? 16 : 1) * L + 5 * L) +
-         sizeof(uint64_t) * (3 * chain_nb(NT * CPT) + 4 + 2 * MXB + 4) + sizeof(double) * 2 * NT * CPT +
-         sizeof(int64_t) * kChainIdxAhead * L + sizeof(uint64_t) * (2 * kChainIdxAhead + 2 * chain_nb(NT * CPT)) + 128;
+  cluster.sync();  // no CTA exits while others may still write its smem / signal its barriers
 }
 
 // w_avg = S / m ; zero padding.

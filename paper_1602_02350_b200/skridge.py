@@ -854,10 +854,17 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7, prep_cap:
         for cx in ctxs:
             cx.set_prep_cap(prep_cap)
     rows = []
+    # Contexts are checked out per job: calls on one Context must be serialised
+    # (skr.h), and the pool hands a job to whichever worker is free.
+    import queue
+    free = queue.Queue()
+    for cx in ctxs:
+        free.put(cx)
 
     def run_once(job):
-        lane, pre, eta, seed = job
-        clone = _clone_problem(pre, ctxs[lane])
+        pre, eta, seed = job
+        cx = free.get()
+        clone = _clone_problem(pre, cx)
         try:
             res = svrg_solve(clone, SvrgConfig(cfg.epochs, m, eta, seed, SvrgMode.Tuned), np.zeros(d), ref.minimum)
             tr = res.trace
@@ -867,6 +874,7 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7, prep_cap:
             return math.inf, []
         finally:
             del clone
+            free.put(cx)
 
     with ThreadPoolExecutor(max_workers=len(ctxs)) as pool:
         for sketched in (False, True):
@@ -878,7 +886,7 @@ def run_convergence(p: RidgeProblem, cfg: BenchConfig, lanes: int = 7, prep_cap:
                 else:
                     pre = plain
                 grid = [cfg.eta] if cfg.eta is not None else eta_grid(mean_beta(pre))
-                jobs = [(i % len(ctxs), pre, eta, int(seed)) for i, eta in enumerate(grid)]
+                jobs = [(pre, eta, int(seed)) for eta in grid]
                 results = list(pool.map(run_once, jobs))
                 best, best_tr = math.inf, []
                 for final, tr in results:  # strict '<' in grid order, as bench.cpp:180

@@ -1,6 +1,7 @@
 """Bitwise run-to-run determinism of the SVRG chain (same problem, same seed, 3 solves)."""
 import sys, numpy as np
 sys.path.insert(0, '.')
+import oracle
 from paper_1602_02350_b200 import configs, skridge as sk
 import dataclasses
 for name in (sys.argv[1].split(',') if len(sys.argv) > 1 else ['c2', 'c3']):
@@ -8,7 +9,7 @@ for name in (sys.argv[1].split(',') if len(sys.argv) > 1 else ['c2', 'c3']):
     cfg = configs.CONFIGS[base].scaled(16384) if base != 'c1' else configs.CONFIGS[base]
     if dt:
         cfg = dataclasses.replace(cfg, dtype=dt)
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     p = sk.RidgeProblem(sk.DataMatrix(X), y, cfg.lam)
     sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
     pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))

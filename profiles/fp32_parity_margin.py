@@ -10,6 +10,6 @@ for name, nn in (("c3", 16384), ("c4", 16384), ("c5", 16384)):
     except Exception as e:
         print(name, "no golden", e); continue
     cfg = configs.CONFIGS[name].scaled(nn)
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     p, sv, pg, eta, res, L = t._pipeline(cfg, X, y, gold["epochs"])
     print(name, "sigma", t.rel(sv.singular_values, gold["sigma"]), "eta", abs(eta - gold["eta"]) / gold["eta"], "L", abs(L - gold["L_hat"]) / gold["L_hat"], "epochs", gold["epochs"], [r.objective for r in res.trace][-3:], flush=True)

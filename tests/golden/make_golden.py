@@ -6,14 +6,19 @@ oracle/Makefile) — never the restatement — and stores inputs and outputs:
   tests/golden/small.npz   small known-answer cases (streams, eigensolver,
                            block_lanczos incl. rank drop, preconditioned
                            components, SVRG trace + index stream, L*, kappa~)
-  tests/golden/configs.json  BASELINE configs c1, c2 (c3, c4, c5 row-subsampled to n = 16384; c5 at
-                           lambda 1e-6 and 1e-8, and unpreconditioned at 1e-6)
-                           composed as SURVEY §0 fact 6 prescribes: sigma~,
-                           beta_hat, alpha, eta, per-epoch objectives, L(w^), L*,
-                           kappa~ (d <= 2000), index-stream head; inputs come
-                           from paper_1602_02350_b200.configs.host_instance.
+  tests/golden/configs.json  BASELINE configs composed as SURVEY §0 fact 6
+                           prescribes (sigma~, beta_hat, alpha, eta, per-epoch
+                           objectives, L(w^), L*, kappa~, index-stream sha256,
+                           X sha256 and row-block sums): c1, c2 and c3 at FULL
+                           size; c4 at n/16 (262,144 rows) and c5 at n/16
+                           (1,048,576 rows; lambda 1e-4/1e-6/1e-8, preconditioned
+                           and unpreconditioned); quick row-subsampled cases at
+                           n = 16384.  Inputs are oracle.synth_instance — the
+                           host restatement of the device generator — so a
+                           row-subsampled instance is the first n rows of the
+                           full one and the GPU tests regenerate it on device.
 
-Usage:  python tests/golden/make_golden.py [small] [c1] [c2] [c3] [c4] [c5]
+Usage:  python tests/golden/make_golden.py [small] [c1] [c2] [c3s] [c3] [c4] [c5]
 """
 from __future__ import annotations
 
@@ -100,70 +105,96 @@ def small():
     print("small.npz written", len(out), "arrays")
 
 
-def config_case(name: str, n_override: int | None = None, epochs: int | None = None, kappa: bool = True,
+def config_case(name: str, n_override: int | None = None, epochs: int | None = None, kappa: str = "auto",
                 lam: float | None = None, sketched: bool = True):
-    R = oracle.ref()
+    """One BASELINE config through the reference's composed pipeline (oracle.pipeline
+    -> ref_pipeline: ONE DataMatrix, block_lanczos with q_override, build_sketched,
+    preconditioned_components(Auto), reference_minimum, svrg_solve(m = 2n),
+    apply_inv_sqrt, objective on the original X).  The instance is the first
+    n rows of the config's DEVICE instance (oracle.synth_instance restates the
+    device generator), so the GPU tests regenerate it on the device."""
     cfg = configs.CONFIGS[name]
     if n_override:
         cfg = cfg.scaled(n_override)
     if lam is not None:
         cfg = configs.Config(**{**cfg.__dict__, "lam": lam})
     t0 = time.time()
-    X, y = configs.host_instance(cfg)
-    Xd = X.astype(np.float64)
-    yd = y.astype(np.float64)
-    n, d = Xd.shape
+    X, y = oracle.synth_instance(cfg)
+    t_gen = time.time() - t0
+    n, d = X.shape
     digest = hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest()
-    sk = R.block_lanczos(Xd, cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
-    t_l = time.time() - t0
-    # unsketched baseline (Preconditioner::identity == RidgeFiniteSum, test_ridge.cpp:109-127)
-    prob = R.problem(Xd, yd, cfg.lam, sk.U, sk.sigma, 0) if sketched else R.problem(Xd, yd, cfg.lam, None, None, 0)
-    betas = prob.betas()
-    alpha, beta_hat, _ = prob.scalars()
-    # eta = 1/(4 max_i ||x~_i||^2): ||x~_i||^2 = beta_i n/(n+d) (ridge.cpp:124-127)
-    max_row_sq = float(np.max(betas[:n]) * n / (n + d))
-    eta = configs.eta_for(cfg, max_row_sq, beta_hat)
+    # per-row-block checksums (fp64 sums of 4096-row blocks) for a device-side check
+    # that tolerates the rare fp32 rounding ties between the host and device generators
+    blk = 4096
+    row_sums = [float(np.sum(X[r:r + blk], dtype=np.float64)) for r in range(0, n, blk)]
     ep = epochs or cfg.epochs
-    wmin, Lstar = R.reference_minimum(Xd, yd, cfg.lam)
-    sv = prob.svrg(ep, 2 * n, eta, cfg.seed, reference=Lstar)
-    w_hat = R.apply_inv_sqrt(sk.U, sk.sigma, cfg.lam, sv.iterate) if sketched else sv.iterate
-    L = R.objective(Xd, yd, cfg.lam, w_hat)
-    idx = R.index_stream(betas, cfg.seed, 100000)
+    rule = 0 if name in ("c1", "c2") else 1
+    out = oracle.pipeline(X, y.astype(np.float64), cfg.lam, cfg.k if sketched else 0, cfg.q, cfg.seed, ep, 2 * n,
+                          eta_rule=rule, idx_count=100000, want_U=True)
     rec = {
-        "config": name, "n": n, "d": d, "dtype": cfg.dtype, "k": cfg.k if sketched else 0, "q": cfg.q, "lambda": cfg.lam,
-        "seed": cfg.seed, "epochs": ep, "m": 2 * n, "x_sha256": digest,
-        "sigma": sk.sigma.tolist(), "k_used": sk.k, "alpha": alpha, "beta_hat": beta_hat,
-        "max_row_sq": max_row_sq, "eta": eta, "trace": sv.trace.tolist(), "L_hat": L, "L_star": Lstar,
-        "w_hat_head": w_hat[:8].tolist(), "idx_head": idx[:64].tolist(), "idx_sha256_100k": idx_hash(idx),
-        "seconds": {"lanczos": t_l, "total": time.time() - t0},
-        "source": "oracle/_ref (unmodified reference library)",
+        "config": name, "n": n, "d": d, "dtype": cfg.dtype, "k": cfg.k if sketched else 0, "q": cfg.q,
+        "lambda": cfg.lam, "seed": cfg.seed, "epochs": ep, "m": 2 * n, "x_sha256": digest,
+        "x_block_rows": blk, "x_block_sums": row_sums, "y_head": [float(v) for v in y[:8]],
+        "sigma": out.sigma.tolist(), "k_used": out.k_used, "alpha": out.alpha, "beta_hat": out.beta_hat,
+        "max_row_sq": out.max_row_sq, "eta": out.eta, "trace": out.trace.tolist(), "L_hat": out.L_hat,
+        "L_star": out.L_star, "w_hat_head": out.w_hat[:8].tolist(), "idx_head": out.idx[:64].tolist(),
+        "idx_sha256_100k": idx_hash(out.idx), "mode": out.mode,
+        "seconds": {"generate": t_gen, "sketch": out.sketch_ms / 1e3, "precompute": out.precompute_ms / 1e3,
+                    "reference_minimum": out.refmin_ms / 1e3, "solve": out.solve_ms / 1e3,
+                    "full_gradient": out.full_gradient_ms / 1e3, "total": time.time() - t0},
+        "threads": os.cpu_count(),
+        "source": "oracle/_ref (unmodified reference library) on oracle.synth_instance",
     }
-    if kappa and d <= 2000 and sketched:
-        rec["kappa"] = R.conditioned_cond(Xd, cfg.lam, sk.U, sk.sigma)
-    print(name, "done in", round(time.time() - t0, 1), "s", flush=True)
+    if sketched and kappa != "none":
+        if kappa == "auto" and d <= 2000:
+            rec["kappa"] = oracle.ref().conditioned_cond(X.astype(np.float64), cfg.lam, out.U, out.sigma)
+            rec["kappa_source"] = "conditioned_condition_number"
+        else:
+            M = oracle.conditioned_matrix(X, cfg.lam, out.U, out.sigma)
+            ev = np.linalg.eigvalsh(M)
+            rec["kappa"] = float(np.trace(M) / ev[0])
+            rec["kappa_source"] = "reference conditioned_matrix (unguarded) + numpy eigvalsh (d > 2000 guard)"
+            del M
+    print(name, n, "done in", round(time.time() - t0, 1), "s", flush=True)
     return rec
+
+
+def save(db, path):
+    tmp = path + ".tmp"
+    with open(tmp, "w") as f:
+        json.dump(db, f, indent=1)
+    os.replace(tmp, path)
 
 
 def main():
     which = sys.argv[1:] or ["small", "c1"]
     path = os.path.join(HERE, "configs.json")
     db = json.load(open(path)) if os.path.exists(path) else {}
+
+    def put(key, rec):
+        db[key] = rec
+        save(db, path)
+
     if "small" in which:
         small()
     if "c1" in which:
-        db["c1"] = config_case("c1")
+        put("c1", config_case("c1"))
     if "c2" in which:
-        db["c2"] = config_case("c2")
-    if "c3" in which:
-        db["c3_n16384"] = config_case("c3", n_override=16384, epochs=4, kappa=False)
-    if "c4" in which:
-        db["c4_n16384"] = config_case("c4", n_override=16384, epochs=12, kappa=False)
-    if "c5" in which:
+        put("c2", config_case("c2"))
+    if "c3s" in which:  # row-subsampled quick cases (first 16384 rows of the instance)
+        put("c3_n16384", config_case("c3", n_override=16384, epochs=4, kappa="none"))
+        put("c4_n16384", config_case("c4", n_override=16384, epochs=12, kappa="none"))
         for lam, tag in ((1e-6, "l6"), (1e-8, "l8")):
-            db[f"c5_n16384_{tag}"] = config_case("c5", n_override=16384, epochs=6, lam=lam)
-        db["c5_n16384_l6_svrg"] = config_case("c5", n_override=16384, epochs=6, lam=1e-6, sketched=False)
-    with open(path, "w") as f:
-        json.dump(db, f, indent=1)
+            put(f"c5_n16384_{tag}", config_case("c5", n_override=16384, epochs=6, lam=lam))
+        put("c5_n16384_l6_svrg", config_case("c5", n_override=16384, epochs=6, lam=1e-6, sketched=False))
+    if "c3" in which:  # full size
+        put("c3", config_case("c3", kappa="eigvalsh"))
+    if "c4" in which:  # n/16
+        put("c4_n262144", config_case("c4", n_override=1 << 18, epochs=8, kappa="eigvalsh"))
+    if "c5" in which:  # n/16, the lambda sweep, preconditioned and not
+        for lam, tag in ((1e-4, "l4"), (1e-6, "l6"), (1e-8, "l8")):
+            put(f"c5_n1048576_{tag}", config_case("c5", n_override=1 << 20, epochs=4, lam=lam))
+            put(f"c5_n1048576_{tag}_svrg", config_case("c5", n_override=1 << 20, epochs=4, lam=lam, sketched=False))
     print("configs.json:", list(db))
 
 

@@ -296,7 +296,7 @@ def test_conditioned_condition_number(O):
 @pytest.mark.slow
 def test_config_c1_end_to_end(O):
     cfg = configs.CONFIGS["c1"]
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     n, d = X.shape
     scale = 1 / math.sqrt(n)
     # oracle pipeline, composed as SURVEY §0 fact 6 prescribes
@@ -394,7 +394,7 @@ def test_config_c2_against_reference_golden():
     import hashlib
     gold = _golden("c2")
     cfg = configs.CONFIGS["c2"]
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     p, sv, pg, eta, res, L = _pipeline(cfg, X, y, cfg.epochs)
     assert rel(sv.singular_values, gold["sigma"]) < 1e-6                  # BASELINE fp64 Ritz gate
     assert abs(eta - gold["eta"]) <= 1e-10 * gold["eta"]
@@ -414,7 +414,7 @@ def test_config_c3_subsampled_fp32_tensor_core_lanczos():
     """c3 (fp32 storage) at n = 16384: Lanczos products on tcgen05 (3xTF32)."""
     gold = _golden("c3_n16384")
     cfg = configs.CONFIGS["c3"].scaled(16384)
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     assert X.dtype == np.float32
     p, sv, pg, eta, res, L = _pipeline(cfg, X, y, gold["epochs"])
     assert rel(sv.singular_values, gold["sigma"]) < 1e-3                  # BASELINE fp32 Ritz gate
@@ -432,7 +432,7 @@ def test_config_c4_c5_subsampled_against_reference_golden(key):
     gold = _golden(key)
     base = configs.CONFIGS[key[:2]].scaled(gold["n"])
     cfg = configs.Config(**{**base.__dict__, "lam": gold["lambda"]})
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     assert X.dtype == np.float32
     n, d = X.shape
     p = sk.RidgeProblem(sk.DataMatrix(X), y.astype(np.float64), cfg.lam)
@@ -633,7 +633,7 @@ def test_svrg_chain_bitwise_deterministic(name, dtype):
     st.async exchange once raced (K10)."""
     import dataclasses
     cfg = dataclasses.replace(configs.CONFIGS[name].scaled(16384), dtype=dtype)
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     p = sk.RidgeProblem(sk.DataMatrix(X), y, cfg.lam)
     sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
     pg = sk.preconditioned_components(p, sk.build_sketched(sv, cfg.lam))
@@ -648,7 +648,7 @@ def test_prep_cap_grid_strided_identical():
     """skr_ctx_set_prep_cap: the inner loop's PREP kernel strides over the blocks of a
     chunk with a capped grid; iterates must be bitwise those of the uncapped grid."""
     cfg = configs.CONFIGS["c2"].scaled(8192)
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     ctx = sk.Context(0)
     p = sk.RidgeProblem(sk.DataMatrix(X, ctx=ctx), y, cfg.lam)
     sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)

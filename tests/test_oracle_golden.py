@@ -105,7 +105,7 @@ def test_c1_against_reference_golden(O):
     """BASELINE c1 composed by hand vs the reference's run."""
     gold = json.load(open(os.path.join(GOLD, "configs.json")))["c1"]
     cfg = configs.CONFIGS["c1"]
-    X, y = configs.host_instance(cfg)
+    X, y = oracle.synth_instance(cfg)
     n, d = X.shape
     sk = O.block_lanczos(X, cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
     # data generation (numpy QR) may differ in the last bits across CPUs -> 1e-12
