@@ -17,7 +17,13 @@
 //   reference_minimum (bench.hpp:24)           b200::reference_minimum
 #pragma once
 
+#include <cctype>
+#include <charconv>
 #include <chrono>
+#include <numeric>
+#include <string_view>
+#include <system_error>
+#include <istream>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -513,65 +519,88 @@ struct LabeledDataset {
   std::string provenance;
 };
 
-/// dataset.cpp:87-162: "label idx:value ..." lines, 1-based strictly increasing
-/// indices, '#' comments; d = the largest index seen; zero values are dropped.
+/// Host-side CSR arrays of a parsed corpus (points = rows).
+struct CsrCorpus {
+  std::vector<int64_t> row_ptr{0};
+  std::vector<int32_t> col_idx;
+  Vector vals, labels;
+  std::size_t dim = 0;
+};
+
+namespace detail {
+// Cursor over one line of the corpus text: whitespace-separated tokens, the
+// rest of the line after '#' ignored.
+struct LineCursor {
+  const char* p;
+  const char* end;
+  bool next(std::string_view& tok) {
+    while (p < end && std::isspace((unsigned char)*p)) ++p;
+    if (p == end || *p == '#') return false;
+    const char* b = p;
+    while (p < end && !std::isspace((unsigned char)*p) && *p != '#') ++p;
+    tok = std::string_view(b, (std::size_t)(p - b));
+    return true;
+  }
+};
+// Whole-token numeric conversions (std::from_chars: no locale, no partial parse).
+inline bool to_double(std::string_view t, double& v) {
+  if (!t.empty() && t.front() == '+') t.remove_prefix(1);
+  auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+  return r.ec == std::errc() && r.ptr == t.data() + t.size();
+}
+inline bool to_index(std::string_view t, long long& v) {
+  if (!t.empty() && t.front() == '+') t.remove_prefix(1);
+  auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+  return r.ec == std::errc() && r.ptr == t.data() + t.size();
+}
+}  // namespace detail
+
+/// The sparse text format of dataset.hpp:37-49 ("label idx:value ..." per point,
+/// 1-based strictly increasing feature indices, '#' comments, blank lines
+/// skipped, explicit zeros dropped, d = the largest index seen).  Same
+/// exception types and line numbering as the reference reader (dataset.cpp:87-162).
+inline CsrCorpus parse_sparse_corpus(std::istream& in) {
+  CsrCorpus c;
+  std::string raw;
+  std::size_t lineno = 0;
+  while (std::getline(in, raw)) {
+    ++lineno;
+    detail::LineCursor cur{raw.data(), raw.data() + raw.size()};
+    std::string_view tok;
+    if (!cur.next(tok)) continue;  // blank or comment-only line
+    double label = 0.0;
+    if (!detail::to_double(tok, label)) throw ParseError(lineno, "bad label '" + std::string(tok) + "'");
+    c.labels.push_back(label);
+    long long last = 0;
+    while (cur.next(tok)) {
+      const std::size_t sep = tok.find(':');
+      long long index = 0;
+      double value = 0.0;
+      const bool ok = sep != std::string_view::npos && sep > 0 && sep + 1 < tok.size() &&
+                      detail::to_index(tok.substr(0, sep), index) && index >= 1 &&
+                      detail::to_double(tok.substr(sep + 1), value);
+      if (!ok) throw ParseError(lineno, "bad feature '" + std::string(tok) + "'");
+      if (index <= last) throw ParseError(lineno, "feature indices must be strictly increasing");
+      if (!std::isfinite(value)) throw ParseError(lineno, "non-finite value");
+      last = index;
+      if ((std::size_t)index > c.dim) c.dim = (std::size_t)index;
+      if (value == 0.0) continue;
+      c.col_idx.push_back((int32_t)(index - 1));
+      c.vals.push_back(value);
+    }
+    c.row_ptr.push_back((int64_t)c.vals.size());
+  }
+  return c;
+}
+
 inline LabeledDataset read_sparse_corpus(const Context& ctx, const std::string& path) {
   std::ifstream in(path);
   if (!in) throw InputError("corpus: cannot open " + path);
-  std::vector<int64_t> row_ptr{0};
-  std::vector<int32_t> col_idx;
-  std::vector<double> vals;
-  Vector labels;
-  std::size_t max_index = 0, lineno = 0;
-  std::string raw;
-  auto parse_double = [](const std::string& t, double& v) {
-    std::size_t used = 0;
-    v = std::stod(t, &used);
-    if (used != t.size()) throw std::invalid_argument(t);
-  };
-  while (std::getline(in, raw)) {
-    ++lineno;
-    const auto hash = raw.find('#');
-    std::istringstream line(hash == std::string::npos ? raw : raw.substr(0, hash));
-    std::string tok;
-    if (!(line >> tok)) continue;
-    double label;
-    try {
-      parse_double(tok, label);
-    } catch (const std::exception&) {
-      throw ParseError(lineno, "bad label '" + tok + "'");
-    }
-    labels.push_back(label);
-    std::size_t prev = 0;
-    while (line >> tok) {
-      const auto colon = tok.find(':');
-      if (colon == std::string::npos || colon == 0 || colon + 1 >= tok.size())
-        throw ParseError(lineno, "bad feature '" + tok + "'");
-      std::size_t index;
-      double value;
-      try {
-        std::size_t used = 0;
-        const long long ri = std::stoll(tok.substr(0, colon), &used);
-        if (used != colon || ri < 1) throw std::invalid_argument(tok);
-        index = (std::size_t)ri;
-        parse_double(tok.substr(colon + 1), value);
-      } catch (const std::exception&) {
-        throw ParseError(lineno, "bad feature '" + tok + "'");
-      }
-      if (index <= prev) throw ParseError(lineno, "feature indices must be strictly increasing");
-      if (!std::isfinite(value)) throw ParseError(lineno, "non-finite value");
-      prev = index;
-      max_index = std::max(max_index, index);
-      if (value != 0.0) {
-        col_idx.push_back((int32_t)(index - 1));
-        vals.push_back(value);
-      }
-    }
-    row_ptr.push_back((int64_t)vals.size());
-  }
-  if (labels.empty()) throw InputError("corpus: no data lines in " + path);
-  if (max_index == 0) throw DegenerateDataError("corpus: no features seen");
-  return LabeledDataset{DataMatrix::from_csr(ctx, labels.size(), max_index, row_ptr, col_idx, vals), labels, path};
+  CsrCorpus c = parse_sparse_corpus(in);
+  if (c.labels.empty()) throw InputError("corpus: no data lines in " + path);
+  if (c.dim == 0) throw DegenerateDataError("corpus: no features seen");
+  const std::size_t n = c.labels.size();
+  return LabeledDataset{DataMatrix::from_csr(ctx, n, c.dim, c.row_ptr, c.col_idx, c.vals), std::move(c.labels), path};
 }
 
 // ---- ratio / spectrum diagnostics (precond.hpp:13-20,81-91; bench.cpp:195-212) --------
@@ -604,26 +633,28 @@ inline SpectrumSummary dataset_spectrum(const RidgeProblem& p) {
   return SpectrumSummary(std::move(e), p.lambda);
 }
 
-/// precond.cpp:165-172.
+/// kappa_avg = tr(Sigma + lambda I) / (lambda_min + lambda) (precond.hpp:81-84).
 inline double avg_condition_number(const SpectrumSummary& spec) {
-  if (spec.eigenvalues.empty()) throw InputError("avg_condition_number: empty spectrum");
-  const double denom = spec.eigenvalues.back() + spec.lambda;
-  if (!(denom > 0.0)) throw InputError("avg_condition_number: lam_min + lambda must be positive");
-  double tr = 0.0;
-  for (double v : spec.eigenvalues) tr += v + spec.lambda;
-  return tr / denom;
+  const Vector& e = spec.eigenvalues;
+  if (e.empty()) throw InputError("avg_condition_number: empty spectrum");
+  const double bottom = e.back() + spec.lambda;
+  if (!(bottom > 0.0)) throw InputError("avg_condition_number: lam_min + lambda must be positive");
+  const double shifted = std::accumulate(e.begin(), e.end(), 0.0,
+                                         [&](double acc, double v) { return acc + (v + spec.lambda); });
+  return shifted / bottom;
 }
 
-/// precond.cpp:208-219.
+/// Paper Thm. ratio (precond.hpp:86-91): sum_i s_i / (k s_k + sum_{i>k} s_i),
+/// with the spectrum split at k.
 inline double theoretical_ratio(const SpectrumSummary& spec, std::size_t k) {
-  const std::size_t d = spec.dim();
-  if (k < 1 || k > d) throw ParameterError("theoretical_ratio: k must satisfy 1 <= k <= d");
-  double head = 0.0, tail = 0.0;
-  for (std::size_t i = 0; i < k; ++i) head += spec.eigenvalues[i];
-  for (std::size_t i = k; i < d; ++i) tail += spec.eigenvalues[i];
-  const double denom = static_cast<double>(k) * spec.eigenvalues[k - 1] + tail;
-  if (denom == 0.0) throw DegenerateSpectrumError("theoretical_ratio: zero denominator");
-  return (head + tail) / denom;
+  const Vector& e = spec.eigenvalues;
+  if (k < 1 || k > e.size()) throw ParameterError("theoretical_ratio: k must satisfy 1 <= k <= d");
+  const auto split = e.begin() + (std::ptrdiff_t)k;
+  const double top = std::accumulate(e.begin(), split, 0.0);
+  const double rest = std::accumulate(split, e.end(), 0.0);
+  const double below = rest + (double)k * e[k - 1];
+  if (below == 0.0) throw DegenerateSpectrumError("theoretical_ratio: zero denominator");
+  return (top + rest) / below;
 }
 
 /// bench.cpp:195-203.

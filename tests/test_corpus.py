@@ -85,3 +85,17 @@ def test_writer_round_trip(corpus_path, tmp_path):
     again, y2 = _parse_host(out)
     assert np.array_equal(again["rp"], got["rp"]) and np.array_equal(again["va"], got["va"])
     assert np.array_equal(y2, y)
+
+
+def test_cpp_parser_matches_reference_reader(tmp_path):
+    """include/skridge_b200.hpp parse_sparse_corpus against the unmodified reference
+    reader (dataset.cpp:87-162) on valid corpora and every malformed-line class
+    (tests/cpp/corpus_parse.cpp, built by __graft_entry__.build())."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "corpus_parse")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/corpus_parse not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 of 19 cases differ" in r.stdout
