@@ -1,20 +1,23 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 hot path (see DESIGN.md §measurement).
+"""Benchmark of the B200 hot path (see DESIGN.md §5).
 
 A step is ONE full-gradient pass (the fused K9 pass of
 PreconditionedRidge::full_gradient + objective, ridge.cpp:174-236) over the
-preconditioned rows X~ of the configs[1] workload (c2: fp64, n = 65,536 rows
-per GPU, d = 1024).  `value` is the whole-job HBM throughput of that pass in
-algorithmic GB/s (n*d*8 bytes of X~ per pass per GPU, all GPUs); `e2e` is the
-same metric through the reference-facing C-ABI call with host buffers
-(skr_full_gradient: w uploaded, mu and the objective read back every step).
+preconditioned rows X~ of the headline workload: c3 (BASELINE configs[2], the
+largest single-GPU config: fp32 storage with fp64 accumulation, n = 2^20 rows
+per GPU, d = 2048, k = 128, q = 3).  `value` is the whole-job HBM throughput of
+that pass in algorithmic GB/s (n*d*4 bytes of X~ per pass per GPU, all GPUs);
+`e2e` is the same metric through the reference-facing C-ABI call with host
+buffers (skr_full_gradient: w uploaded, mu and the objective read back every
+step).  `--config c2` etc. select another BASELINE config.
 
-Multi-GPU (torchrun): rows are sharded, each rank owns a c2-sized shard (weak
+Multi-GPU (torchrun): rows are sharded, each rank owns a c3-sized shard (weak
 scaling) and the pass ends in one NCCL allreduce of d+1 doubles.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref: the unmodified skridge library, OpenMP on all host cores) on the
-same metric; under torchrun only rank 0 runs it.
+same metric, on a bounded row sample of the same instance (see
+reference_full_gradient_sample); under torchrun only rank 0 runs it.
 """
 from __future__ import annotations
 
@@ -95,61 +98,97 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-def cpu_full_gradient_sample(X, y, lam, U, sigma, budget_s: float, max_passes: int):
-    """The reference's PreconditionedRidge::full_gradient (oracle/_ref, OpenMP) on the
-    same instance; returns (seconds per pass, passes timed, threads)."""
+REF_SAMPLE_ROWS = 1 << 17   # rows of the instance the CPU reference streams per timed pass (c3: 1/8)
+REF_SKETCH_ROWS = 1 << 14   # rows the reference's block_lanczos sees to build U (values do not affect the timing)
+
+
+def reference_full_gradient_sample(cfg, max_passes: int, budget_s: float, X=None, y=None):
+    """The reference's PreconditionedRidge::full_gradient + objective (oracle/_ref: the
+    unmodified skridge library, OpenMP on every host core) on a bounded sample of the
+    cfg instance: its first min(n, REF_SAMPLE_ROWS) rows, preconditioned with the
+    rank-k sketch the reference's own block_lanczos builds from the first
+    REF_SKETCH_ROWS rows, apply mode Auto (the reference's stock choice: Lazy when
+    n*d > 2e8, ridge.cpp:104-113).  Timed passes stop at max_passes or once budget_s
+    is spent.  Returns (seconds per pass, passes, threads, backend, rows, mode, setup_s).
+    X, y: the sample rows if the caller already has them (else the host restatement
+    of the device generator makes them)."""
     import oracle
     R = oracle.ref() if oracle.ref_available() else oracle.port()
-    prob = R.problem(X, y, lam, U, sigma, 0)
+    rows = min(cfg.n, REF_SAMPLE_ROWS)
+    t0 = time.perf_counter()
+    if X is None:
+        X, y = oracle.synth_instance(cfg, rows=rows)
+    X = np.ascontiguousarray(X[:rows], dtype=np.float64)
+    y = np.ascontiguousarray(y[:rows], dtype=np.float64)
+    ks = min(rows, REF_SKETCH_ROWS)
+    sv = R.block_lanczos(X[:ks], cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
+    mode = 2 if R.name == "reference" else 0  # ApplyMode::Auto (the port has Dense only)
+    prob = R.problem(X, y, cfg.lam, sv.U, sv.sigma, mode)
+    setup_s = time.perf_counter() - t0
     w = np.random.default_rng(1).standard_normal(X.shape[1]) * 1e-2
     prob.full_gradient(w)  # warm-up
+    prob.objective(w)
     t0 = time.perf_counter()
     k = 0
     while k < max_passes and (k == 0 or time.perf_counter() - t0 < budget_s):
         prob.full_gradient(w)
+        prob.objective(w)  # the GPU step also yields the objective
         k += 1
     dt = (time.perf_counter() - t0) / k
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return dt, k, threads, R.name
+    mode_name = ("lazy" if rows * cfg.d > 200_000_000 else "dense") if mode == 2 else "dense"
+    return dt, k, threads, R.name, rows, mode_name, setup_s
+
+
+def host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "")
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def run_reference(args, cfg):
     """--impl reference: the reference CPU path on the same workload (rank 0 only)."""
     import oracle
-    from paper_1602_02350_b200 import configs
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libskridge_ref.so not built"}))
         return
-    R = oracle.ref()
-    X, y = oracle.synth_instance(cfg)
-    X = X.astype(np.float64)
-    y = y.astype(np.float64)
-    n, d = X.shape
-    sv = R.block_lanczos(X, cfg.k, q=cfg.q, seed=cfg.seed, want_right=False)
-    prob = R.problem(X, y, cfg.lam, sv.U, sv.sigma, 0)
-    w = np.random.default_rng(1).standard_normal(d) * 1e-2
-    for _ in range(args.warmup):
-        prob.full_gradient(w)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        prob.full_gradient(w)
-        prob.objective(w)  # the GPU step also yields the objective
-    dt = (time.perf_counter() - t0) / args.steps
-    bytes_per_step = n * d * 8
-    val = bytes_per_step / dt / 1e9
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    s_bytes = 4 if cfg.dtype == "f32" else 8
+    dt, k, threads, kind, rows, mode, setup_s = reference_full_gradient_sample(cfg, max_passes=args.steps,
+                                                                               budget_s=90.0)
+    val = rows * cfg.d * s_bytes / dt / 1e9
+    sample = (f"{k} full_gradient+objective calls of skridge::PreconditionedRidge ({mode} mode, ApplyMode::Auto) "
+              f"over the first {rows} of the {cfg.n} rows of the {cfg.name} instance (host restatement of the device "
+              f"generator); U from the reference's block_lanczos on the first {min(rows, REF_SKETCH_ROWS)} rows; "
+              f"GB/s = rows*d*{s_bytes} algorithmic bytes (the GPU arm's definition) per pass")
     print(json.dumps({
-        "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (configs.host_instance, numpy Philox)",
+        "metric": METRIC, "value": round(val, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": k,
+        "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(cfg),
+        "data": "synthetic (oracle.synth_instance: host restatement of the device Philox generator, same instance)",
         "impl": "reference",
-        "config": {"workload": f"{cfg.name}: full-gradient + objective pass over X~ (n={n}, d={d}, k={cfg.k})",
-                   "n": n, "d": d, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam},
-        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} full_gradient+objective calls of skridge::PreconditionedRidge "
-                                   f"(Dense) on the {cfg.name} instance"},
+        "config": workload_config(cfg, 1),
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample,
+                         "setup_s": round(setup_s, 2), **host_info()},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def dtype_label(cfg) -> str:
+    return "fp32 storage / fp64 accumulate" if cfg.dtype == "f32" else "f64"
+
+
+def workload_config(cfg, world: int) -> dict:
+    s_bytes = 4 if cfg.dtype == "f32" else 8
+    return {"workload": f"{cfg.name}: fused full-gradient + objective pass over X~ "
+                        f"(n={cfg.n} rows/GPU, d={cfg.d}, {dtype_label(cfg)}, k={cfg.k}, q={cfg.q}, "
+                        f"lambda={cfg.lam})",
+            "n_per_gpu": cfg.n, "n_total": cfg.n * world, "d": cfg.d, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam,
+            "parallelism": f"rows sharded dp{world}",
+            "l2": f"inputs larger than L2 (X~ {cfg.n * cfg.d * s_bytes / 1e6:.0f} MB/GPU vs 126 MB L2)"}
 
 
 # ---------------------------------------------------------------------------
@@ -194,17 +233,20 @@ def run_ours(args, cfg):
     ld = (d + 15) // 16 * 16
 
     warm_library(sk, configs, ctx)
-    for rep in range(2):  # the first call also grows the memory pool; the second is reported
+    walls, gemms = [], []
+    for rep in range(4):  # the first call also grows the memory pool; best of the 3 warm calls is reported
         torch.cuda.synchronize()
         barrier()
-        ctx.profile(rep == 1)
+        ctx.profile(rep >= 1)
         t0 = time.perf_counter()
         sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
         ctx.synchronize()
-        lanczos_s = max_over_ranks(time.perf_counter() - t0)
-    lz_gemm_ms, _ = ctx.profile_read("lanczos_gemm")
-    lz_gemm_ms = max_over_ranks(lz_gemm_ms)
-    ctx.profile(False)
+        wall = max_over_ranks(time.perf_counter() - t0)
+        if rep >= 1:
+            walls.append(wall)
+            gemms.append(max_over_ranks(ctx.profile_read("lanczos_gemm")[0]))
+        ctx.profile(False)
+    lanczos_s, lz_gemm_ms = min(walls), min(gemms)
     for _ in range(2):  # as for the sketch: the second (steady-state) build is reported
         prob = None
         barrier()
@@ -243,6 +285,10 @@ def run_ours(args, cfg):
         ev1.record(stream)
         ctx.synchronize()
         launches = ctx.kernel_launches - launches0
+        # the dominant kernel's launches inside the timed region only (the soak
+        # below runs into the box's power cap and would skew the average)
+        k9_ms, k9_n = ctx.profile_read("fullgrad")
+        ctx.profile(False)
         # keep the same loop running ~0.4 s more so the clock sampler sees load
         t_soak = time.perf_counter()
         while time.perf_counter() - t_soak < 0.4:
@@ -252,12 +298,10 @@ def run_ours(args, cfg):
     ms = ev0.elapsed_time(ev1)
     barrier()
     ms = max_over_ranks(ms)
-    k9_ms, k9_n = ctx.profile_read("fullgrad")
-    ctx.profile(False)
     ms_step = ms / args.steps
     bytes_per_gpu = n_loc * d * s_bytes
     value = world * bytes_per_gpu / (ms_step * 1e-3) / 1e9
-    # the dominant kernel: K9's streaming pass (average over the timed + soak launches)
+    # the dominant kernel: K9's streaming pass (average over the timed launches)
     k9_avg = k9_ms / max(k9_n, 1)
     hbm, bf16, src = peaks()
     achieved = bytes_per_gpu / (k9_avg * 1e-3) / 1e9
@@ -283,18 +327,17 @@ def run_ours(args, cfg):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(cfg),
         "data": "synthetic (device Philox4x32-10 generator, BASELINE spectrum)",
-        "config": {"workload": f"{cfg.name}: fused full-gradient + objective pass over X~ "
-                               f"(n={cfg.n} rows/GPU, d={d}, {cfg.dtype}, k={cfg.k}, q={cfg.q})",
-                   "n_per_gpu": cfg.n, "n_total": n_total, "d": d, "k": cfg.k, "q": cfg.q, "lambda": cfg.lam,
-                   "parallelism": f"rows sharded dp{world}",
-                   "l2": f"inputs larger than L2 (X~ {bytes_per_gpu / 1e6:.0f} MB/GPU vs 126 MB L2)"},
+        "config": workload_config(cfg, world),
         "passes_per_s": round(1e3 / ms_step, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "kernel": k9_kernel_name(cfg), "kernel_ms": round(k9_avg, 5), "peak_source": src,
-                     "bytes_per_launch": bytes_per_gpu},
+                     "bytes_per_launch": bytes_per_gpu, "frac_of_8000_spec": round(achieved / 8000.0, 4),
+                     "peak_note": "peak = MEASURED_PEAKS hbm_gbs, a read+write copy; a read-only stream "
+                                  "(K9 reads X~ once, writes ~0) can exceed it — ncu puts the same launch at "
+                                  "81 % of its DRAM peak (profiles/r02_k9_tma_c3_ncu_details.txt)"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": d * 8,
                 "d2h_bytes_per_step": d * 8 + 8, "ms_per_step": round(e2e_s * 1e3, 4)},
         "gpu_launches": int(launches),
@@ -313,16 +356,21 @@ def run_ours(args, cfg):
 
     if not args.no_extras:
         out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
-        if world == 1:
+        if world == 1 and cfg.dtype == "f64":
             out["lanczos_fp32"] = lanczos_fp32_extra(sk, ctx)
+    if cfg.dtype == "f32":
+        out["lanczos"].update(lanczos_tf32_fields(cfg, lz_gemm_ms, n_loc))
     if world == 1 and not args.no_cpu_baseline and rank == 0:
-        X = data.download().astype(np.float64)
-        dt, kk, thr, kind = cpu_full_gradient_sample(X, y, cfg.lam, sv.left, sv.singular_values,
-                                                     budget_s=10.0, max_passes=max(3, args.steps))
-        out["cpu_baseline"] = {"value": round(bytes_per_gpu / dt / 1e9, 3), "unit": "GB/s", "cores": thr,
+        rows = min(cfg.n, REF_SAMPLE_ROWS)
+        Xs = data.download()[:rows]
+        dt, kk, thr, kind, rows, mode, _ = reference_full_gradient_sample(cfg, max_passes=max(3, args.steps),
+                                                                          budget_s=15.0, X=Xs, y=y[:rows])
+        out["cpu_baseline"] = {"value": round(rows * d * s_bytes / dt / 1e9, 3), "unit": "GB/s", "cores": thr,
                                "kind": kind,
-                               "sample": f"{kk} PreconditionedRidge::full_gradient calls (reference, Dense, "
-                                         f"OpenMP) on the same {cfg.name} instance"}
+                               "sample": f"{kk} PreconditionedRidge::full_gradient+objective calls (reference, "
+                                         f"{mode} mode = ApplyMode::Auto, OpenMP) over the first {rows} rows of "
+                                         f"the same {cfg.name} device instance; GB/s = rows*d*{s_bytes} per pass",
+                               **host_info()}
     if rank == 0:
         print(json.dumps(out))
     if dist is not None:
@@ -358,6 +406,14 @@ def lanczos_flops(cfg, n):
 
 
 TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (B200_PROFILING.md table; not measured on this pool)
+
+
+def lanczos_tf32_fields(cfg, gemm_ms, n):
+    tf = lanczos_gemm_flops(cfg, n) / (max(gemm_ms, 1e-6) * 1e-3) / 1e12
+    return {"gemm_tflops_fp32_equiv": round(tf, 1), "tf32_raw_tflops": round(3 * tf, 1),
+            "tf32_peak_tflops": TF32_DENSE_TFLOPS, "tf32_frac": round(3 * tf / TF32_DENSE_TFLOPS, 3),
+            "gemm_note": "3xTF32 tcgen05 products (hi.hi + hi.lo + lo.hi), best of 3 warm calls; peak = dense TF32 "
+                         "nominal from B200_PROFILING.md"}
 
 
 def lanczos_fp32_extra(sk, ctx):
@@ -563,7 +619,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
