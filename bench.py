@@ -233,7 +233,7 @@ def run_ours(args, cfg):
     ld = (d + 15) // 16 * 16
 
     warm_library(sk, configs, ctx)
-    walls, gemms = [], []
+    walls, gemms, gemms_tc = [], [], []
     for rep in range(4):  # the first call also grows the memory pool; best of the 3 warm calls is reported
         torch.cuda.synchronize()
         barrier()
@@ -245,8 +245,9 @@ def run_ours(args, cfg):
         if rep >= 1:
             walls.append(wall)
             gemms.append(max_over_ranks(ctx.profile_read("lanczos_gemm")[0]))
+            gemms_tc.append(max_over_ranks(ctx.profile_read("lanczos_gemm_tc")[0]))
         ctx.profile(False)
-    lanczos_s, lz_gemm_ms = min(walls), min(gemms)
+    lanczos_s, lz_gemm_ms, lz_tc_ms = min(walls), min(gemms), min(gemms_tc)
     for _ in range(2):  # as for the sketch: the second (steady-state) build is reported
         prob = None
         barrier()
@@ -343,23 +344,14 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "gpu_launches_per_step": round(launches / max(1, args.steps), 2),
         "clocks": clk.summary(),
-        "lanczos": {"seconds": round(lanczos_s, 4),
-                    "tflops": round(lanczos_flops(cfg, n_total) / lanczos_s / 1e12 / world, 4),
-                    "note": "whole block_lanczos call incl. Pi stream, ortho, RR, eigensolve",
-                    "gemm_ms": round(lz_gemm_ms, 4),
-                    "gemm_tflops_per_gpu": round(lanczos_gemm_flops(cfg, n_loc) / (max(lz_gemm_ms, 1e-6) * 1e-3) / 1e12, 3),
-                    "gemm_peak_tflops": FP64_DMMA_TFLOPS if cfg.dtype == "f64" else None,
-                    "gemm_note": "Krylov + Rayleigh-Ritz products only (device events); fp64 peak = measured cuBLAS "
-                                 "DGEMM 8192^3 on this B200 (profiles/fp64_peak.py)"},
+        "lanczos": lanczos_fields(cfg, n_total, n_loc, world, lanczos_s, lz_gemm_ms, lz_tc_ms),
         "precompute_s": round(precompute_s, 4),
     }
 
     if not args.no_extras:
         out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
-        if world == 1 and cfg.dtype == "f64":
-            out["lanczos_fp32"] = lanczos_fp32_extra(sk, ctx)
-    if cfg.dtype == "f32":
-        out["lanczos"].update(lanczos_tf32_fields(cfg, lz_gemm_ms, n_loc))
+        if world == 1:
+            out["lanczos_tf32"] = lanczos_tf32_extra(sk, ctx)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         rows = min(cfg.n, REF_SAMPLE_ROWS)
         Xs = data.download()[:rows]
@@ -408,25 +400,46 @@ def lanczos_flops(cfg, n):
 TF32_DENSE_TFLOPS = 1100.0  # B200 dense TF32 tensor peak (B200_PROFILING.md table; not measured on this pool)
 
 
-def lanczos_tf32_fields(cfg, gemm_ms, n):
-    tf = lanczos_gemm_flops(cfg, n) / (max(gemm_ms, 1e-6) * 1e-3) / 1e12
-    return {"gemm_tflops_fp32_equiv": round(tf, 1), "tf32_raw_tflops": round(3 * tf, 1),
-            "tf32_peak_tflops": TF32_DENSE_TFLOPS, "tf32_frac": round(3 * tf / TF32_DENSE_TFLOPS, 3),
-            "gemm_note": "3xTF32 tcgen05 products (hi.hi + hi.lo + lo.hi), best of 3 warm calls; peak = dense TF32 "
-                         "nominal from B200_PROFILING.md"}
+def lanczos_fields(cfg, n_total, n_loc, world, wall_s, gemm_ms, tc_ms):
+    """The sketch's path and throughput.  fp64 data: DMMA products.  fp32 storage:
+    3xTF32 tcgen05 products, redone on the fp64 DMMA path when the Rayleigh-Ritz
+    spectrum is too ill-conditioned for fp32 accumulation (capi.cu rr_needs_fp64;
+    c3: lambda_1 / lambda_128 = 2e6)."""
+    if cfg.dtype == "f64":
+        path = "fp64 DMMA (mma.sync m8n8k4)"
+    elif gemm_ms > 0.0:
+        path = "3xTF32 tcgen05 attempt, redone on fp64 DMMA (ill-conditioned Ritz spectrum)"
+    else:
+        path = "3xTF32 tcgen05"
+    final_ms = gemm_ms if gemm_ms > 0.0 else tc_ms
+    tf = lanczos_gemm_flops(cfg, n_loc) / (max(final_ms, 1e-6) * 1e-3) / 1e12
+    dmma = gemm_ms > 0.0
+    out = {"seconds": round(wall_s, 4), "path": path,
+           "tflops": round(lanczos_flops(cfg, n_total) / wall_s / 1e12 / world, 4),
+           "note": "whole block_lanczos call incl. Pi stream, ortho, RR, eigensolve (and a discarded tc attempt)",
+           "gemm_ms": round(final_ms, 4), "gemm_tflops_per_gpu": round(tf if dmma else 3 * tf, 3),
+           "gemm_peak_tflops": FP64_DMMA_TFLOPS if dmma else TF32_DENSE_TFLOPS,
+           "gemm_frac": round((tf if dmma else 3 * tf) / (FP64_DMMA_TFLOPS if dmma else TF32_DENSE_TFLOPS), 3),
+           "gemm_note": "Krylov + Rayleigh-Ritz products only (device events); fp64 peak = measured cuBLAS DGEMM "
+                        "8192^3 on this B200 (profiles/fp64_peak.py); TF32 = raw 3xTF32 throughput vs the dense TF32 "
+                        "nominal"}
+    if tc_ms > 0.0 and dmma:
+        out["tc_attempt_ms"] = round(tc_ms, 4)
+    return out
 
 
-def lanczos_fp32_extra(sk, ctx):
-    """The fp32-storage sketch on tcgen05 (3xTF32) at the c3 shape (configs[2]: n = 2^20,
-    d = 2048, k = 128, q = 3): warm block_lanczos wall time and the Krylov + Rayleigh-Ritz
-    products' device time (CUDA events around them), as fp32-algorithmic TFLOP/s and as
-    raw TF32 tensor throughput (3 MMAs per product) against the dense TF32 peak."""
+def lanczos_tf32_extra(sk, ctx):
+    """The tensor-core sketch where it is the one used: c5 (configs[4]: fp32 storage,
+    n = 2^24, d = 1024, k = 64, q = 2, well-conditioned 0.99^j spectrum): warm
+    block_lanczos wall time and the Krylov + Rayleigh-Ritz products' device time (CUDA
+    events), as raw TF32 tensor throughput (3 MMAs per 3xTF32 product) against the
+    dense TF32 peak."""
     from paper_1602_02350_b200 import configs
-    c3 = configs.CONFIGS["c3"]
-    data = sk.DataMatrix.generate(sk.SynthSpec(c3.n, c3.d, c3.dtype, c3.seed, c3.spectrum, c3.spectrum_param,
-                                               c3.t_scale, c3.tau), ctx)
-    a = data.scaled(1 / math.sqrt(c3.n))
-    lc = sk.LanczosConfig(c3.k, 0.5, c3.seed, c3.q)
+    c5 = configs.CONFIGS["c5"]
+    data = sk.DataMatrix.generate(sk.SynthSpec(c5.n, c5.d, c5.dtype, c5.seed, c5.spectrum, c5.spectrum_param,
+                                               c5.t_scale, c5.tau), ctx)
+    a = data.scaled(1 / math.sqrt(c5.n))
+    lc = sk.LanczosConfig(c5.k, 0.5, c5.seed, c5.q)
     sk.block_lanczos(a, lc, want_right=False)  # cold call: workspaces
     ctx.synchronize()
     walls, gemms = [], []
@@ -436,14 +449,13 @@ def lanczos_fp32_extra(sk, ctx):
         sk.block_lanczos(a, lc, want_right=False)
         ctx.synchronize()
         walls.append(time.perf_counter() - t0)
-        gemms.append(ctx.profile_read("lanczos_gemm")[0])
+        gemms.append(ctx.profile_read("lanczos_gemm_tc")[0])
         ctx.profile(False)
     wall, gemm_ms = min(walls), min(gemms)
-    flops = lanczos_gemm_flops(c3, c3.n)
-    tf = flops / (gemm_ms * 1e-3) / 1e12
+    tf = lanczos_gemm_flops(c5, c5.n) / (max(gemm_ms, 1e-6) * 1e-3) / 1e12
     del a, data
-    return {"config": "c3 (fp32 storage, n=1048576, d=2048, k=128, q=3)", "seconds": round(wall, 4),
-            "gemm_ms": round(gemm_ms, 3), "gemm_tflops_fp32_equiv": round(tf, 1),
+    return {"config": "c5 (fp32 storage, n=16777216, d=1024, k=64, q=2)", "path": "3xTF32 tcgen05",
+            "seconds": round(wall, 4), "gemm_ms": round(gemm_ms, 3), "gemm_tflops_fp32_equiv": round(tf, 1),
             "tf32_raw_tflops": round(3 * tf, 1), "tf32_peak_tflops": TF32_DENSE_TFLOPS,
             "tf32_frac": round(3 * tf / TF32_DENSE_TFLOPS, 3),
             "note": "3xTF32 tcgen05 products (hi.hi + hi.lo + lo.hi); peak = dense TF32 nominal from "

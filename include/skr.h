@@ -62,6 +62,14 @@ int skr_ctx_create(int device, skr_ctx** out);
 /* NCCL bootstrap for row sharding across ranks (one process per GPU). */
 int skr_nccl_unique_id(char id_out[128]);
 int skr_ctx_create_dist(int device, int rank, int world, const char id[128], skr_ctx** out);
+
+/* Row sharding of the distributed path (host only, no device needed).
+ * skr_shard_rows: the shard skr_data_generate gives `rank` of `world` for n rows:
+ *   n_local = n / world + (rank < n % world), row0 = rank * (n / world) + min(rank, n % world).
+ * skr_shard_layout: (n_global, row0) of `rank` from every rank's local row count in rank
+ *   order (skr_data_create gathers the counts; shards are concatenated in rank order). */
+int skr_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* n_local);
+int skr_shard_layout(const int64_t* counts, int world, int rank, int64_t* n_global, int64_t* row0);
 int skr_ctx_destroy(skr_ctx* ctx);
 int skr_ctx_synchronize(skr_ctx* ctx);
 void* skr_ctx_stream(skr_ctx* ctx); /* cudaStream_t the context orders work on */

@@ -42,6 +42,8 @@ SIGNATURES = {
     "skr_ctx_create": (cint, [cint, P(vp)]),
     "skr_nccl_unique_id": (cint, [C.c_char_p]),
     "skr_ctx_create_dist": (cint, [cint, cint, cint, C.c_char_p, P(vp)]),
+    "skr_shard_rows": (cint, [i64, cint, cint, P(i64), P(i64)]),
+    "skr_shard_layout": (cint, [i64ptr, cint, cint, P(i64), P(i64)]),
     "skr_ctx_destroy": (cint, [vp]),
     "skr_ctx_synchronize": (cint, [vp]),
     "skr_ctx_stream": (vp, [vp]),

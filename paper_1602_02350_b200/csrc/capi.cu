@@ -157,6 +157,22 @@ void download_rows(Ctx& c, double* dst, const double* src, int64_t rows, int64_t
                                rows, cudaMemcpyDeviceToHost, c.stream));
 }
 
+// Host-side shard arithmetic (also exported: skr_shard_rows / skr_shard_layout).
+void shard_rows_host(int64_t n, int world, int rank, int64_t* row0, int64_t* n_local) {
+  const int64_t base = n / world, extra = n % world;
+  *n_local = base + (rank < extra ? 1 : 0);
+  *row0 = rank * base + std::min<int64_t>(rank, extra);
+}
+void shard_layout_host(const int64_t* counts, int world, int rank, int64_t* n_global, int64_t* row0) {
+  int64_t tot = 0, r0 = 0;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) r0 = tot;
+    tot += counts[r];
+  }
+  *n_global = tot;
+  *row0 = r0;
+}
+
 // Shard layout across ranks: gather every rank's local row count.
 void shard_layout(Ctx& c, int64_t n_local, int64_t* n_global, int64_t* row0,
                   std::vector<int64_t>* counts = nullptr) {
@@ -168,13 +184,7 @@ void shard_layout(Ctx& c, int64_t n_local, int64_t* n_global, int64_t* row0,
     SKR_CUDA(cudaMemcpyAsync(all.data(), recv.get(), sizeof(int64_t) * c.world, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
   }
-  int64_t tot = 0, r0 = 0;
-  for (int r = 0; r < c.world; ++r) {
-    if (r == c.rank) r0 = tot;
-    tot += all[r];
-  }
-  *n_global = tot;
-  *row0 = r0;
+  shard_layout_host(all.data(), c.world, c.rank, n_global, row0);
   if (counts) *counts = all;
 }
 
@@ -1459,6 +1469,22 @@ int skr_nccl_unique_id(char id_out[128]) {
   });
 }
 
+int skr_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* n_local) {
+  return guard([&] {
+    if (n < 0 || world < 1 || rank < 0 || rank >= world || !row0 || !n_local) raise(SKR_EPARAM, "bad shard arguments");
+    shard_rows_host(n, world, rank, row0, n_local);
+  });
+}
+
+int skr_shard_layout(const int64_t* counts, int world, int rank, int64_t* n_global, int64_t* row0) {
+  return guard([&] {
+    if (!counts || world < 1 || rank < 0 || rank >= world || !n_global || !row0) raise(SKR_EPARAM, "bad layout arguments");
+    for (int r = 0; r < world; ++r)
+      if (counts[r] < 0) raise(SKR_EPARAM, "negative shard size");
+    shard_layout_host(counts, world, rank, n_global, row0);
+  });
+}
+
 int skr_ctx_create_dist(int device, int rank, int world, const char id[128], skr_ctx** out) {
   return guard([&] {
     if (!out || world < 1 || rank < 0 || rank >= world) raise(SKR_EPARAM, "bad rank/world");
@@ -1748,8 +1774,8 @@ int skr_data_generate(skr_ctx* ctx, const skr_synth_spec* spec, skr_data** out) 
       SKR_CUDA(cudaMemcpyAsync(Qt.get(), A.get(), sizeof(double) * d * ld, cudaMemcpyDeviceToDevice, c.stream));
     }
     // shard
-    int64_t n_local = n / c.world + (c.rank < n % c.world ? 1 : 0);
-    int64_t row0 = c.rank * (n / c.world) + std::min<int64_t>(c.rank, n % c.world);
+    int64_t n_local = 0, row0 = 0;
+    shard_rows_host(n, c.world, c.rank, &row0, &n_local);
     auto st = new_storage(c, spec->dtype, n_local, d);
     // X = (G diag sigma) V^T in row chunks: X_chunk = G_chunk Qt
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_local, (int64_t)(1 << 30) / ld));
@@ -1847,9 +1873,10 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       Qh.alloc((size_t)k * ld, c.stream);
       Ql.alloc((size_t)k * ld, c.stream);
     }
-    // "lanczos_gemm" marks bracket the Krylov / Rayleigh-Ritz products only (bench: GEMM TFLOP/s)
+    // "lanczos_gemm" marks bracket the Krylov / Rayleigh-Ritz products only (bench: GEMM TFLOP/s);
+    // "lanczos_gemm_tc" those of a tensor-core (3xTF32) attempt
     auto gmark = [&] {
-      if (c.prof_on) c.prof_mark("lanczos_gemm");
+      if (c.prof_on) c.prof_mark(tc ? "lanczos_gemm_tc" : "lanczos_gemm");
     };
     // block = A Pi  -> Vt (k x ld) = scale * Pi^T X   (sketch.cpp:25)
     Vt.zero();
@@ -2153,7 +2180,23 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
                                                               p->betas.get() + ng);
       SKR_LAUNCHED(&c);
     }
-    c.allreduce_sum(p->betas.get(), N);
+    if (c.dist) {
+      // every rank's data betas (its own rows) and rank 0's regulariser betas [ng, N)
+      // land in place on every rank (the table is replicated for the sampling stream)
+      std::vector<int64_t> counts;
+      int64_t ngl = 0, r0 = 0;
+      shard_layout(c, n, &ngl, &r0, &counts);
+      std::vector<size_t> off(c.world), byt(c.world), roff(c.world, (size_t)ng * sizeof(double)), rbyt(c.world, 0);
+      size_t o = 0;
+      for (int r = 0; r < c.world; ++r) {
+        off[r] = o * sizeof(double);
+        byt[r] = (size_t)counts[r] * sizeof(double);
+        o += counts[r];
+      }
+      rbyt[0] = (size_t)d * sizeof(double);
+      c.gather_in_place(p->betas.get(), p->betas.get() + p->row0, off, byt);
+      c.gather_in_place(p->betas.get(), p->betas.get() + ng, roff, rbyt);
+    }
     c.allreduce_max(rowmax.get(), 1);
     DBuf<double> top(1, c.stream);
     top.zero();
@@ -2175,24 +2218,28 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
       std::vector<int64_t> counts;
       int64_t ngl = 0, r0 = 0;
       shard_layout(c, n, &ngl, &r0, &counts);
-      const int64_t mx = *std::max_element(counts.begin(), counts.end());
       const size_t s = dtype_size(S.dtype), row_bytes = (size_t)ld * s;
-      DBuf<unsigned char> send((size_t)mx * row_bytes, c.stream), recv((size_t)mx * row_bytes * c.world, c.stream);
-      SKR_CUDA(cudaMemcpyAsync(send.get(), p->xt->ptr, (size_t)n * row_bytes, cudaMemcpyDeviceToDevice, c.stream));
-      c.allgather_bytes(send.get(), recv.get(), (size_t)mx * row_bytes);
+      // memory budget: the replica of all ng rows of X~ (the sequential inner loop
+      // reads any sampled row) on top of this rank's X and X~ shards
+      size_t free_b = 0, total_b = 0;
+      SKR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t need = (size_t)ng * row_bytes + (size_t)ng * sizeof(double) + (256ull << 20);
+      if (need > free_b)
+        raise(SKR_ECUDA, "preconditioned components: the replicated X~ needs " + std::to_string(need >> 20) +
+                             " MiB, " + std::to_string(free_b >> 20) + " MiB free on this GPU");
       p->xt_all_buf.alloc((size_t)ng * row_bytes, c.stream);
-      DBuf<double> ysend(mx, c.stream), yrecv((size_t)mx * c.world, c.stream);
-      SKR_CUDA(cudaMemcpyAsync(ysend.get(), p->y.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
-      c.allgather_bytes(ysend.get(), yrecv.get(), sizeof(double) * mx);
       p->y_all_buf.alloc(ng, c.stream);
-      int64_t off = 0;
+      std::vector<size_t> xoff(c.world), xbyt(c.world), yoff(c.world), ybyt(c.world);
+      size_t o = 0;
       for (int r = 0; r < c.world; ++r) {
-        SKR_CUDA(cudaMemcpyAsync(p->xt_all_buf.get() + off * row_bytes, recv.get() + (size_t)r * mx * row_bytes,
-                                 (size_t)counts[r] * row_bytes, cudaMemcpyDeviceToDevice, c.stream));
-        SKR_CUDA(cudaMemcpyAsync(p->y_all_buf.get() + off, yrecv.get() + (size_t)r * mx, sizeof(double) * counts[r],
-                                 cudaMemcpyDeviceToDevice, c.stream));
-        off += counts[r];
+        xoff[r] = o * row_bytes;
+        xbyt[r] = (size_t)counts[r] * row_bytes;
+        yoff[r] = o * sizeof(double);
+        ybyt[r] = (size_t)counts[r] * sizeof(double);
+        o += counts[r];
       }
+      c.gather_in_place(p->xt_all_buf.get(), p->xt->ptr, xoff, xbyt);
+      c.gather_in_place(p->y_all_buf.get(), p->y.get(), yoff, ybyt);
       p->xt_all = p->xt_all_buf.get();
       p->y_all = p->y_all_buf.get();
     }

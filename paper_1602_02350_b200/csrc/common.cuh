@@ -54,6 +54,9 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 inline NcclApi& nccl() {
@@ -70,6 +73,9 @@ inline NcclApi& nccl() {
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
       api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+      api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+      api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     }
   }
@@ -186,6 +192,23 @@ struct Ctx {
   }
   void allgather_bytes(const void* send, void* recv, size_t bytes_per_rank) {
     if (dist) SKR_NCCL(nccl().AllGather(send, recv, bytes_per_rank, ncclChar, comm, stream));
+  }
+  // Variable-size all-gather straight into place: rank r's `bytes[r]` bytes land at
+  // base + offset[r] on every rank (one grouped ncclBroadcast per rank, rooted at r;
+  // the root reads `mine`, which may alias its own destination).  No staging
+  // buffers and no repacking, so a replica costs exactly its own size.
+  void gather_in_place(void* base, const void* mine, const std::vector<size_t>& offset,
+                       const std::vector<size_t>& bytes) {
+    if (!dist) return;
+    if (!nccl().Broadcast || !nccl().GroupStart || !nccl().GroupEnd)
+      raise(SKR_ENCCL, "libnccl.so.2 lacks ncclBroadcast / ncclGroupStart");
+    SKR_NCCL(nccl().GroupStart());
+    for (int r = 0; r < world; ++r) {
+      if (!bytes[r]) continue;
+      char* dst = static_cast<char*>(base) + offset[r];
+      SKR_NCCL(nccl().Broadcast(r == rank ? mine : dst, dst, bytes[r], ncclChar, r, comm, stream));
+    }
+    SKR_NCCL(nccl().GroupEnd());
   }
   void sync() { SKR_CUDA(cudaStreamSynchronize(stream)); }
 };

@@ -138,6 +138,23 @@ class Context:
 _default_ctx: Optional[Context] = None
 
 
+def shard_rows(n: int, world: int, rank: int) -> tuple:
+    """(row0, n_local) of `rank` when the library shards n rows over `world` ranks
+    (skr_shard_rows: the layout skr_data_generate uses; host only)."""
+    r0, nl = C.c_int64(), C.c_int64()
+    _check(_lib.load().skr_shard_rows(int(n), int(world), int(rank), C.byref(r0), C.byref(nl)))
+    return r0.value, nl.value
+
+
+def shard_layout(counts, rank: int) -> tuple:
+    """(n_global, row0) of `rank` from every rank's local row count in rank order
+    (skr_shard_layout: what skr_data_create derives after gathering the counts)."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    ng, r0 = C.c_int64(), C.c_int64()
+    _check(_lib.load().skr_shard_layout(c, len(c), int(rank), C.byref(ng), C.byref(r0)))
+    return ng.value, r0.value
+
+
 def default_context() -> Context:
     global _default_ctx
     if _default_ctx is None:

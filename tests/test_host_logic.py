@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle  # noqa: E402  (checker: the host restatement of the device generator)
-from paper_1602_02350_b200 import configs, sharding
+from paper_1602_02350_b200 import configs, skridge as sk_mod
 from paper_1602_02350_b200 import skridge as sk
 
 
@@ -74,14 +74,18 @@ def test_step_size_rule():
 
 @pytest.mark.parametrize("n,world", [(10, 3), (65536, 8), (5, 8), (1 << 20, 2)])
 def test_shard_rows_partition(n, world):
-    rows = [sharding.shard_rows(n, world, r) for r in range(world)]
+    """The library's host shard arithmetic (skr_shard_rows / skr_shard_layout, the
+    layout capi.cu uses for skr_data_generate and skr_data_create)."""
+    rows = [sk_mod.shard_rows(n, world, r) for r in range(world)]
     assert sum(c for _, c in rows) == n
     for r in range(world - 1):
         assert rows[r][0] + rows[r][1] == rows[r + 1][0]
     assert max(c for _, c in rows) - min(c for _, c in rows) <= 1
     counts = [c for _, c in rows]
     for r in range(world):
-        assert sharding.layout_from_counts(counts, r) == (n, rows[r][0])
+        assert sk_mod.shard_layout(counts, r) == (n, rows[r][0])
+    with pytest.raises(sk_mod.ParameterError):
+        sk_mod.shard_rows(n, world, world)
 
 
 def test_ratio_host_functions_match_reference():
