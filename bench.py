@@ -500,16 +500,59 @@ def warm_library(sk, configs, ctx):
     ctx.synchronize()
 
 
+class DistEnv:
+    """One process per GPU (torchrun): NCCL process group for the timing plumbing,
+    the library's own distributed context for the data path."""
+
+    def __init__(self, sk, force: bool = False):
+        import torch
+        self.torch = torch
+        self.rank, self.world, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1 or force:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            nid = [sk.Context.nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(nid, src=0)
+            self.ctx = sk.Context(self.local, self.rank, self.world, nid[0])
+            self.dist = dist
+        else:
+            self.ctx = sk.Context(self.local)
+        sk._default_ctx = self.ctx
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
 def run_solve(args):
-    """End-to-end time-to-eps (eps = 1e-6 absolute suboptimality) per config on
-    this GPU: sketch (block_lanczos) + precompute (preconditioned_components) +
-    SVRG epochs until the first epoch with L(w_s) - L* <= eps (cap: cfg.epochs),
-    as SketchedSolveDiagnostics and bench.cpp:182-189 time it.  c5 adds the
-    BASELINE lambda sweep, preconditioned vs unpreconditioned, with one sketch
-    reused across lambdas (block_lanczos is lambda-independent)."""
+    """End-to-end time-to-eps (eps = 1e-6 absolute suboptimality) per config on N
+    GPUs (torchrun, one process per GPU; N = 1 without it): the config's instance
+    (fixed size: strong scaling) is row-sharded across the ranks; sketch
+    (block_lanczos: NCCL allreduce of the Krylov partials) + precompute
+    (preconditioned_components: sharded X~, grouped in-place broadcast of the
+    replica) + SVRG epochs (the sequential chain replicated on every rank, the
+    full gradient row-sharded) until the first epoch with L(w_s) - L* <= eps (cap:
+    cfg.epochs), as SketchedSolveDiagnostics and bench.cpp:182-189 time it; every
+    phase is the max over ranks.  c5 adds the BASELINE lambda sweep, preconditioned
+    vs unpreconditioned, with one sketch reused across lambdas.  With --cpu-ref,
+    rank 0 then times the reference's own pipeline (oracle/_ref, OpenMP on every
+    host core) on the first n/--cpu-ref-frac rows of the same instance."""
     from paper_1602_02350_b200 import configs, skridge as sk
-    ctx = sk.Context(0)
-    sk._default_ctx = ctx
+    E = DistEnv(sk, force=os.environ.get("SKR_BENCH_DIST") == "1")
+    ctx = E.ctx
     eps = 1e-6
     warm_library(sk, configs, ctx)
     for name in args.solve.split(","):
@@ -521,28 +564,36 @@ def run_solve(args):
         # this size; the second (reported) is the steady-state cost
         for _ in range(2):
             ctx.synchronize()
+            E.barrier()
             t0 = time.perf_counter()
             sv = sk.block_lanczos(sk.scaled_design(sk.RidgeProblem(data, y, cfg.lam)),
                                   sk.LanczosConfig(cfg.k, 0.5, cfg.seed, cfg.q), want_right=False)
             ctx.synchronize()
-            sketch_s = time.perf_counter() - t0
+            sketch_s = E.max(time.perf_counter() - t0)
         lams = [1e-4, 1e-6, 1e-8] if name == "c5" else [cfg.lam]
         if args.lambdas:
             lams = [float(x) for x in args.lambdas.split(",")]
         for lam in lams:
             p = sk.RidgeProblem(data, y, lam)
+            E.barrier()
             t0 = time.perf_counter()
             ref = sk.reference_minimum(p)
-            refmin_s = time.perf_counter() - t0
+            refmin_s = E.max(time.perf_counter() - t0)
             for method in (["sketched-svrg", "svrg"] if name == "c5" else ["sketched-svrg"]):
-                t0 = time.perf_counter()
-                pc = sk.build_sketched(sv, lam) if method == "sketched-svrg" else sk.Preconditioner.identity(cfg.d, lam)
-                prob = sk.preconditioned_components(p, pc)
-                ctx.synchronize()
-                pre_s = time.perf_counter() - t0
+                prob = None
+                for _ in range(2):  # as for the sketch: the first build also grows the memory pool
+                    prob = None
+                    E.barrier()
+                    t0 = time.perf_counter()
+                    pc = (sk.build_sketched(sv, lam) if method == "sketched-svrg"
+                          else sk.Preconditioner.identity(cfg.d, lam))
+                    prob = sk.preconditioned_components(p, pc)
+                    ctx.synchronize()
+                    pre_s = E.max(time.perf_counter() - t0)
                 eta = configs.eta_for(cfg, prob.max_row_sq(), prob.mean_beta())
                 m = 2 * cfg.n
                 row = {"solve": name, "method": method, "lambda": lam, "n": cfg.n, "d": cfg.d, "dtype": cfg.dtype,
+                       "n_gpus": E.world, "scaling": "strong (rows of one instance sharded)",
                        "k": cfg.k if method == "sketched-svrg" else 0, "q": cfg.q, "m": m, "eta": eta,
                        "beta_hat": prob.mean_beta(), "alpha": prob.strong_convexity(),
                        "sketch_s": round(sketch_s, 4) if method == "sketched-svrg" else 0.0,
@@ -550,6 +601,7 @@ def run_solve(args):
                        "L_star": ref.minimum}
                 try:
                     ctx.profile(True)
+                    E.barrier()
                     res = sk.svrg_solve(prob, sk.SvrgConfig(cfg.epochs, m, eta, cfg.seed), None, ref.minimum,
                                         stop_suboptimality=eps)
                     k10_ms, k10_n = ctx.profile_read("svrg_epoch")
@@ -562,18 +614,68 @@ def run_solve(args):
                                 "inner_loop_ms_per_epoch": round(k10_ms / max(k10_n, 1), 3)})
                     hit = next((r for r in res.trace if r.suboptimality is not None and r.suboptimality <= eps), None)
                     setup = row["sketch_s"] + pre_s
+                    solve_s = E.max((hit.elapsed_ms if hit else res.trace[-1].elapsed_ms) / 1e3)
                     row.update({
                         "epochs_run": len(res.trace), "epochs_to_eps": hit.epoch if hit else None,
-                        "time_to_eps_s": round(setup + hit.elapsed_ms / 1e3, 4) if hit else None,
+                        "time_to_eps_s": round(setup + solve_s, 4) if hit else None,
                         "epoch_ms": round(res.trace[-1].elapsed_ms / len(res.trace), 3),
                         "inner_loop_ns_per_step": round(k10_ms / max(k10_n, 1) * 1e6 / m, 2),
                         "suboptimality": [r.suboptimality for r in res.trace]})
                 except sk.DivergenceError as e:
                     ctx.profile(False)
                     row.update({"diverged": str(e), "suboptimality": [r.suboptimality for r in e.trace]})
-                print(json.dumps(row), flush=True)
+                if E.rank == 0:
+                    print(json.dumps(row), flush=True)
                 del prob
         del data
+    if args.cpu_ref and E.rank == 0:
+        for name in args.solve.split(","):
+            for row in reference_solve_rows(configs.CONFIGS[name], args.cpu_ref_frac, eps, args.lambdas):
+                print(json.dumps(row), flush=True)
+    E.close()
+
+
+def reference_solve_rows(cfg, frac: int, eps: float, lambdas: str = ""):
+    """The reference's own time-to-eps protocol (ridge.cpp:413-454 + bench.cpp:182-189:
+    block_lanczos (q_override) -> build_sketched -> preconditioned_components(Auto)
+    -> reference_minimum -> svrg_solve until suboptimality <= eps) with
+    SketchedSolveDiagnostics-style phase timings, on the first n / frac rows of the
+    cfg instance (host restatement of the device generator), OpenMP on every host
+    core.  Sketch and precompute scale ~linearly in n, epochs cost ~2n steps, so the
+    full-size figure is extrapolated linearly in n and labelled so."""
+    import oracle
+    if not oracle.ref_available():
+        return [{"solve": cfg.name, "impl": "reference", "unavailable": "oracle/_ref not built"}]
+    from paper_1602_02350_b200 import configs
+    rows = max(1, cfg.n // frac)
+    sub = cfg.scaled(rows)
+    X, y = oracle.synth_instance(sub)
+    lams = [1e-4, 1e-6, 1e-8] if cfg.name == "c5" else [cfg.lam]
+    if lambdas:
+        lams = [float(x) for x in lambdas.split(",")]
+    out = []
+    for lam in lams:
+        for method in (["sketched-svrg", "svrg"] if cfg.name == "c5" else ["sketched-svrg"]):
+            t0 = time.perf_counter()
+            epochs = min(cfg.epochs, 6 if cfg.name == "c5" else 12)  # the solve runs whole; the trace is cut at eps
+            po = oracle.pipeline(X, y.astype(np.float64), lam, cfg.k if method == "sketched-svrg" else 0, cfg.q,
+                                 cfg.seed, epochs, 2 * rows, eta_rule=0 if cfg.name in ("c1", "c2") else 1,
+                                 stop=eps)
+            wall = time.perf_counter() - t0
+            hit = next((i for i, v in enumerate(po.trace) if v - po.L_star <= eps), None)
+            t_eps = None if hit is None else (po.sketch_ms + po.precompute_ms + float(po.trace_ms[hit])) / 1e3
+            out.append({"solve": cfg.name, "impl": "reference", "method": method, "lambda": lam,
+                        "rows": rows, "n": cfg.n, "sample": f"first n/{frac} rows of the {cfg.name} instance",
+                        "threads": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), **host_info(),
+                        "mode": po.mode, "sketch_s": round(po.sketch_ms / 1e3, 3),
+                        "precompute_s": round(po.precompute_ms / 1e3, 3),
+                        "reference_minimum_s": round(po.refmin_ms / 1e3, 3), "solve_s": round(po.solve_ms / 1e3, 3),
+                        "epochs_to_eps": None if hit is None else hit + 1,
+                        "time_to_eps_s_at_sample": None if t_eps is None else round(t_eps, 3),
+                        "time_to_eps_s_full_extrapolated": None if t_eps is None else round(t_eps * frac, 2),
+                        "extrapolation": f"linear in n (x{frac}); measured at n/{frac}",
+                        "wall_s": round(wall, 2)})
+    return out
 
 
 def run_sweep(args):
@@ -627,6 +729,8 @@ def main():
     ap.add_argument("--sweep", default="", help="comma list of configs: K9 alone at each shape")
     ap.add_argument("--solve", default="", help="comma list of configs: end-to-end time-to-eps per config")
     ap.add_argument("--lambdas", default="", help="--solve: override the lambda list")
+    ap.add_argument("--cpu-ref", action="store_true", help="--solve: also time the reference pipeline (rank 0)")
+    ap.add_argument("--cpu-ref-frac", type=int, default=16, help="--solve --cpu-ref: rows sample n / frac")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
