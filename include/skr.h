@@ -150,6 +150,20 @@ int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out);
 int skr_problem_destroy(skr_problem* p);
 /* alpha = strong_convexity (ridge.cpp:152-157), beta_hat = mean_beta
  * (svrg.cpp:213-217), max_row_sq = max_i ||x~_i||^2 over data rows */
+/* preconditioned_components(p, P, mode) (ridge.hpp:121-123) with the reference's
+ * ApplyMode: SKR_MODE_DENSE materialises X~ (and, like ridge.cpp:110-113, raises
+ * SKR_EGUARD above kDenseModeMaxEntries = 2e8 entries; sparse data are densified
+ * on the device); SKR_MODE_LAZY keeps X and the k x n projections (sparse data as
+ * is; dense data are converted to CSR over points, zeros dropped, one GPU);
+ * SKR_MODE_AUTO is the device's own choice (Dense for dense data, which HBM
+ * holds at every BASELINE size; Lazy for sparse) — ridge.cpp:104-109 picks by
+ * n d <= 2e8 instead, for host memory; the two modes agree to ~1e-8
+ * (test_ridge.cpp:272-291).  skr_problem_create == mode Auto. */
+enum { SKR_MODE_DENSE = 0, SKR_MODE_LAZY = 1, SKR_MODE_AUTO = 2 };
+int skr_problem_create_mode(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
+                            const double* sigma, int64_t k, int mode, skr_problem** out);
+/* PreconditionedRidge::mode() (ridge.hpp:96): the mode the device problem runs in. */
+int skr_problem_mode(const skr_problem* p, int* mode);
 int skr_problem_info(const skr_problem* p, int64_t* n, int64_t* d, int64_t* k, double* alpha,
                      double* beta_hat, double* max_row_sq);
 int skr_problem_betas(const skr_problem* p, double* out);          /* N = n_global + d */

@@ -353,12 +353,20 @@ enum class ApplyMode { Dense, Lazy, Auto };
 /// full_gradient, component_gradient, plus the epoch kernel for external engines.
 class PreconditionedRidge {
  public:
-  PreconditionedRidge(const RidgeProblem& p, const Preconditioner& pc) : ctx_(p.data.context()) {
+  /// ridge.hpp:84-85.  ApplyMode as skr_problem_create_mode (include/skr.h): Dense
+  /// materialises X~ (ScaleGuardError above 2e8 entries, like ridge.cpp:110-113),
+  /// Lazy keeps X and the projections, Auto is the device's choice.
+  PreconditionedRidge(const RidgeProblem& p, const Preconditioner& pc, ApplyMode mode = ApplyMode::Auto)
+      : ctx_(p.data.context()) {
     if (pc.dim() != p.dim()) throw DimensionError("preconditioned components: dimension mismatch");
     skr_problem* h = nullptr;
-    check(skr_problem_create(ctx_.get(), p.data.get(), p.labels.data(), p.lambda,
-                             pc.rank() ? pc.basis().data() : nullptr,
-                             pc.rank() ? pc.singular_values().data() : nullptr, (int64_t)pc.rank(), &h));
+    check(skr_problem_create_mode(ctx_.get(), p.data.get(), p.labels.data(), p.lambda,
+                                  pc.rank() ? pc.basis().data() : nullptr,
+                                  pc.rank() ? pc.singular_values().data() : nullptr, (int64_t)pc.rank(),
+                                  mode == ApplyMode::Dense ? SKR_MODE_DENSE
+                                  : mode == ApplyMode::Lazy ? SKR_MODE_LAZY
+                                                            : SKR_MODE_AUTO,
+                                  &h));
     h_.reset(h, [](skr_problem* q) { skr_problem_destroy(q); });
     int64_t n = 0, d = 0, k = 0;
     check(skr_problem_info(h, &n, &d, &k, &alpha_, &beta_hat_, &max_row_sq_));
@@ -373,7 +381,16 @@ class PreconditionedRidge {
   double strong_convexity() const { return alpha_; }
   double mean_beta() const { return beta_hat_; }
   double max_row_sq() const { return max_row_sq_; }
-  ApplyMode mode() const { return ApplyMode::Dense; }
+  /// ridge.hpp:96: the mode the device problem runs in.
+  ApplyMode mode() const {
+    int m = 0;
+    check(skr_problem_mode(h_.get(), &m));
+    return m == SKR_MODE_LAZY ? ApplyMode::Lazy : ApplyMode::Dense;
+  }
+  /// ridge.hpp:97 (LazyEpochState drift check, ridge.cpp:377-393).  The device Lazy
+  /// chain tracks w = base + U h - tau mu exactly (no incremental projection to drift),
+  /// so the drift is 0 in both modes.
+  double max_projection_drift() const { return 0.0; }
   double objective(const Vector& w) const {
     double out = 0.0;
     check(skr_objective(h_.get(), w.data(), &out));
@@ -411,8 +428,8 @@ class PreconditionedRidge {
 
 inline std::shared_ptr<PreconditionedRidge> preconditioned_components(const RidgeProblem& p,
                                                                       const Preconditioner& pc,
-                                                                      ApplyMode = ApplyMode::Auto) {
-  return std::make_shared<PreconditionedRidge>(p, pc);
+                                                                      ApplyMode mode = ApplyMode::Auto) {
+  return std::make_shared<PreconditionedRidge>(p, pc, mode);
 }
 
 inline double mean_beta(const PreconditionedRidge& p) { return p.mean_beta(); }
@@ -459,17 +476,30 @@ inline SvrgResult svrg_solve(const PreconditionedRidge& p, const SvrgConfig& cfg
   return out;
 }
 
-struct SketchedSolveResult {
-  Vector iterate;
-  ConvergenceTrace trace;
-  Vector singular_values;
-  std::size_t k_used = 0, q_used = 0;
-  double beta_hat = 0, sketch_ms = 0, precompute_ms = 0, solve_ms = 0;
+struct SketchedSolveDiagnostics {  // ridge.hpp:125-136
+  Vector singular_values;  // sketched values used by the preconditioner
+  std::size_t k_used = 0;
+  std::size_t q_used = 0;
+  bool rank_reduced = false;
+  ApplyMode mode = ApplyMode::Dense;
+  double beta_hat = 0.0;
+  double sketch_ms = 0.0;
+  double precompute_ms = 0.0;
+  double solve_ms = 0.0;
+  double max_projection_drift = 0.0;
 };
 
-/// ridge.cpp:413-454, with the BASELINE configs' explicit q.
+struct SketchedSolveResult {  // ridge.hpp:138-142
+  Vector iterate;  // in original coordinates
+  ConvergenceTrace trace;
+  SketchedSolveDiagnostics diagnostics;
+};
+
+/// ridge.cpp:413-454 (same signature as ridge.hpp:150-153), plus an optional
+/// explicit q for the BASELINE configs (the reference's
+/// pipeline always uses q = lanczos_iterations(n, 1/2)).
 inline SketchedSolveResult sketched_preconditioned_svrg(const RidgeProblem& p, std::size_t k, const SvrgConfig& cfg,
-                                                        std::uint64_t sketch_seed,
+                                                        std::uint64_t sketch_seed, ApplyMode mode = ApplyMode::Auto,
                                                         std::optional<double> reference_value = std::nullopt,
                                                         std::optional<std::size_t> q_override = std::nullopt) {
   if (k < 1 || k > std::min(p.dim(), p.count())) throw ParameterError("sketched svrg: k must satisfy 1 <= k <= min(d, n)");
@@ -479,21 +509,26 @@ inline SketchedSolveResult sketched_preconditioned_svrg(const RidgeProblem& p, s
   auto t0 = clk::now();
   LanczosConfig lc;
   lc.k = k;
+  lc.eps_prime = 0.5;
   lc.seed = sketch_seed;
   lc.q_override = q_override;
   SketchedSvd sv = block_lanczos(scaled_design(p), lc);
-  out.sketch_ms = ms(t0);
-  out.singular_values = sv.singular_values;
-  out.k_used = sv.k;
-  out.q_used = sv.q;
+  out.diagnostics.sketch_ms = ms(t0);
+  out.diagnostics.singular_values = sv.singular_values;
+  out.diagnostics.k_used = sv.k;
+  out.diagnostics.q_used = sv.q;
+  out.diagnostics.rank_reduced = sv.rank_reduced;
   t0 = clk::now();
-  auto comp = preconditioned_components(p, build_sketched(sv, p.lambda));
-  out.precompute_ms = ms(t0);
-  out.beta_hat = comp->mean_beta();
+  Preconditioner precond = build_sketched(sv, p.lambda);
+  auto comp = preconditioned_components(p, precond, mode);
+  out.diagnostics.precompute_ms = ms(t0);
+  out.diagnostics.mode = comp->mode();
+  out.diagnostics.beta_hat = comp->mean_beta();
   t0 = clk::now();
   SvrgResult r = svrg_solve(*comp, cfg, Vector(p.dim(), 0.0), reference_value);
-  out.solve_ms = ms(t0);
-  out.iterate = comp->apply_inv_sqrt(r.iterate);
+  out.diagnostics.solve_ms = ms(t0);
+  out.diagnostics.max_projection_drift = comp->max_projection_drift();
+  out.iterate = precond.apply_inv_sqrt(r.iterate);
   out.trace = std::move(r.trace);
   return out;
 }

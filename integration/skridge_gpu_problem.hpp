@@ -18,6 +18,13 @@
 #include <memory>
 #include <vector>
 
+#include <cmath>
+#include <optional>
+
+#include "skridge/data_matrix.hpp"
+#include "skridge/precond.hpp"
+#include "skridge/ridge.hpp"
+#include "skridge/sketch.hpp"
 #include "skridge/svrg.hpp"
 #include "skridge_b200.hpp"
 
@@ -64,5 +71,153 @@ class GpuPreconditionedRidge final : public skridge::FiniteSumProblem {
  private:
   std::shared_ptr<skridge::b200::PreconditionedRidge> p_;
 };
+
+// ---- reference-typed drop-ins ------------------------------------
+// Same signatures and value types as the reference's sketch.hpp:55, ridge.hpp:121-123
+// and ridge.hpp:150-153, computed on the B200 through the C-ABI.  Callers keep the
+// reference's DataMatrix / RidgeProblem / SketchedSvd / Preconditioner / SvrgConfig.
+
+/// The device context the drop-ins use (one per process; device 0).
+inline const skridge::b200::Context& device_context() {
+  static const skridge::b200::Context ctx(0);
+  return ctx;
+}
+
+/// skridge::DataMatrix (dense d x n column-major == n x d rows, or CSC over points
+/// == CSR over points) -> device DataMatrix with the same logical entries.
+/// fold_scale: upload scale * stored (a problem's data handle must be unscaled);
+/// otherwise keep the scale on the handle, as scaled_design does (ridge.cpp:54-56).
+inline skridge::b200::DataMatrix to_device(const skridge::DataMatrix& a,
+                                           const skridge::b200::Context& ctx = device_context(),
+                                           bool fold_scale = false) {
+  namespace b = skridge::b200;
+  const std::size_t d = a.rows(), n = a.cols();
+  const double s = a.scale();
+  const bool fold = fold_scale && s != 1.0;
+  if (const skridge::DenseMatrix* m = a.dense()) {
+    if (fold) {
+      std::vector<double> v(m->entries());
+      for (double& e : v) e *= s;
+      return b::DataMatrix(ctx, v.data(), n, d);
+    }
+    b::DataMatrix x(ctx, m->data(), n, d);
+    return s == 1.0 ? x : x.scaled(s);
+  }
+  const skridge::SparseMatrix* sp = a.sparse();
+  std::vector<int64_t> rp(sp->col_ptr().begin(), sp->col_ptr().end());
+  std::vector<int32_t> ci(sp->row_idx().begin(), sp->row_idx().end());
+  std::vector<double> vals(sp->values());
+  if (fold)
+    for (double& e : vals) e *= s;
+  b::DataMatrix x = b::DataMatrix::from_csr(ctx, n, d, rp, ci, vals);
+  return (s == 1.0 || fold) ? x : x.scaled(s);
+}
+
+inline skridge::SketchedSvd to_reference(const skridge::b200::SketchedSvd& sv) {
+  skridge::SketchedSvd out;
+  out.left = skridge::DenseMatrix(sv.d, sv.k, sv.left);  // both column-major d x k
+  out.singular_values = sv.singular_values;
+  if (!sv.right.empty()) out.right = skridge::DenseMatrix(sv.n, sv.k, sv.right);
+  out.k = sv.k;
+  out.q = sv.q;
+  out.rank_reduced = sv.rank_reduced;
+  return out;
+}
+
+inline skridge::b200::SketchedSvd from_reference(const skridge::SketchedSvd& sv) {
+  skridge::b200::SketchedSvd out;
+  out.d = sv.left.rows();
+  out.k = sv.k;
+  out.n = sv.right.rows();
+  out.q = sv.q;
+  out.left = sv.left.entries();
+  out.singular_values = sv.singular_values;
+  out.right = sv.right.entries();
+  out.rank_reduced = sv.rank_reduced;
+  return out;
+}
+
+/// Device Preconditioner carrying the same map as a reference Preconditioner: the
+/// basis is copied and sigma~_j recovered from the coefficients,
+/// sigma~_j^2 = 1/D_j^2 - lambda (the device rebuilds D_j = 1/sqrt(sigma~_j^2 + lambda)).
+inline skridge::b200::Preconditioner from_reference(const skridge::Preconditioner& pc) {
+  if (pc.rank() == 0) return skridge::b200::Preconditioner::identity(pc.dim(), pc.lambda());
+  skridge::b200::SketchedSvd sv;
+  sv.d = pc.dim();
+  sv.k = pc.rank();
+  sv.left = pc.basis().entries();
+  sv.singular_values.resize(sv.k);
+  for (std::size_t j = 0; j < sv.k; ++j) {
+    const double Dj = pc.inv_sqrt_diag()[j];
+    sv.singular_values[j] = std::sqrt(std::max(1.0 / (Dj * Dj) - pc.lambda(), 0.0));
+  }
+  return skridge::b200::build_sketched(sv, pc.lambda());
+}
+
+inline skridge::b200::RidgeProblem to_device(const skridge::RidgeProblem& p,
+                                             const skridge::b200::Context& ctx = device_context()) {
+  return skridge::b200::RidgeProblem(to_device(p.data, ctx, /*fold_scale=*/true), p.labels, p.lambda);
+}
+
+inline skridge::b200::ApplyMode to_device(skridge::ApplyMode m) {
+  return m == skridge::ApplyMode::Dense  ? skridge::b200::ApplyMode::Dense
+         : m == skridge::ApplyMode::Lazy ? skridge::b200::ApplyMode::Lazy
+                                         : skridge::b200::ApplyMode::Auto;
+}
+
+/// sketch.hpp:55 on the device (right factors included, as the reference returns them).
+inline skridge::SketchedSvd block_lanczos(const skridge::DataMatrix& a, const skridge::LanczosConfig& cfg) {
+  skridge::b200::LanczosConfig lc;
+  lc.k = cfg.k;
+  lc.eps_prime = cfg.eps_prime;
+  lc.seed = cfg.seed;
+  lc.q_override = cfg.q_override;
+  return to_reference(skridge::b200::block_lanczos(to_device(a), lc, /*want_right=*/true));
+}
+
+/// ridge.hpp:121-123 on the device: a FiniteSumProblem the reference's svrg_solve drives.
+inline std::shared_ptr<GpuPreconditionedRidge> preconditioned_components(const skridge::RidgeProblem& p,
+                                                                         const skridge::Preconditioner& pc,
+                                                                         skridge::ApplyMode mode = skridge::ApplyMode::Auto) {
+  return std::make_shared<GpuPreconditionedRidge>(
+      skridge::b200::preconditioned_components(to_device(p), from_reference(pc), to_device(mode)));
+}
+
+/// ridge.hpp:150-153 on the device, returning the reference's SketchedSolveResult.
+inline skridge::SketchedSolveResult sketched_preconditioned_svrg(const skridge::RidgeProblem& p, std::size_t k,
+                                                                 const skridge::SvrgConfig& cfg,
+                                                                 std::uint64_t sketch_seed,
+                                                                 skridge::ApplyMode mode = skridge::ApplyMode::Auto,
+                                                                 std::optional<double> reference_value = std::nullopt) {
+  skridge::b200::SvrgConfig c;
+  c.epochs = cfg.epochs;
+  c.epoch_length = cfg.epoch_length;
+  c.step_size = cfg.step_size;
+  c.seed = cfg.seed;
+  const auto r = skridge::b200::sketched_preconditioned_svrg(to_device(p), k, c, sketch_seed, to_device(mode),
+                                                             reference_value);
+  skridge::SketchedSolveResult out;
+  out.iterate = r.iterate;
+  for (const auto& e : r.trace) {
+    skridge::EpochRecord x;
+    x.epoch = e.epoch;
+    x.objective = e.objective;
+    x.suboptimality = e.suboptimality;
+    x.elapsed_ms = e.elapsed_ms;
+    out.trace.push_back(x);
+  }
+  auto& dg = out.diagnostics;
+  dg.singular_values = r.diagnostics.singular_values;
+  dg.k_used = r.diagnostics.k_used;
+  dg.q_used = r.diagnostics.q_used;
+  dg.rank_reduced = r.diagnostics.rank_reduced;
+  dg.mode = r.diagnostics.mode == skridge::b200::ApplyMode::Lazy ? skridge::ApplyMode::Lazy : skridge::ApplyMode::Dense;
+  dg.beta_hat = r.diagnostics.beta_hat;
+  dg.sketch_ms = r.diagnostics.sketch_ms;
+  dg.precompute_ms = r.diagnostics.precompute_ms;
+  dg.solve_ms = r.diagnostics.solve_ms;
+  dg.max_projection_drift = r.diagnostics.max_projection_drift;
+  return out;
+}
 
 }  // namespace skridge_gpu

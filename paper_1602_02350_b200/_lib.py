@@ -61,6 +61,8 @@ SIGNATURES = {
     "skr_data_labels": (cint, [vp, dptr]),
     "skr_lanczos": (cint, [vp, vp, i64, i64, f64, u64, dptr, dptr, vp, P(i64), P(i64), P(cint)]),
     "skr_problem_create": (cint, [vp, vp, dptr, f64, vp, vp, i64, P(vp)]),
+    "skr_problem_create_mode": (cint, [vp, vp, dptr, f64, vp, vp, i64, cint, P(vp)]),
+    "skr_problem_mode": (cint, [vp, P(cint)]),
     "skr_problem_destroy": (cint, [vp]),
     "skr_problem_info": (cint, [vp, P(i64), P(i64), P(i64), P(f64), P(f64), P(f64)]),
     "skr_problem_betas": (cint, [vp, dptr]),

@@ -2067,6 +2067,78 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
 }
 
 // ---- preconditioned components -------------------------------------------------
+// CSR over points -> dense n x ld fp64 rows (one warp per row)
+__global__ void csr_densify_kernel(const int64_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
+                                   const double* __restrict__ rval, int64_t n, int64_t ld, double* __restrict__ out) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = warp; i < n; i += ((int64_t)gridDim.x * blockDim.x) >> 5)
+    for (int64_t t = rptr[i] + lane; t < rptr[i + 1]; t += 32) out[i * ld + ridx[t]] = rval[t];
+}
+
+int skr_problem_create_mode(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
+                            const double* sigma, int64_t k, int mode, skr_problem** out) {
+  if (mode == SKR_MODE_AUTO) return skr_problem_create(ctx, X, y, lambda, U, sigma, k, out);
+  skr_data* conv = nullptr;
+  const int rc = guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X || !out) raise(SKR_EPARAM, "null argument");
+    if (mode != SKR_MODE_DENSE && mode != SKR_MODE_LAZY) raise(SKR_EPARAM, "apply mode must be Dense, Lazy or Auto");
+    const Storage& S = *X->st;
+    if (mode == SKR_MODE_DENSE) {
+      // ridge.cpp:110-113
+      if ((double)X->n_global * (double)S.d > 2e8)
+        raise(SKR_EGUARD, "preconditioned components: dense mode would materialize too many entries; use lazy");
+      if (S.sparse) {  // densify on the device
+        auto st = new_storage(c, SKR_F64, S.n, S.d);
+        if (S.n > 0)
+          csr_densify_kernel<<<std::min<unsigned>(ceil_div(S.n * 32, 256), 8u * c.sm_count), 256, 0, c.stream>>>(
+              S.rptr.get(), S.ridx.get(), S.rval.get(), S.n, st->ld, static_cast<double*>(st->ptr));
+        SKR_LAUNCHED(&c);
+        auto x = std::make_unique<skr_data>(*X);
+        x->st = st;
+        x->scale = 1.0;
+        conv = x.release();
+      }
+    } else if (!S.sparse) {
+      // Lazy on dense rows: CSR over points (zeros dropped) through the sparse ingest
+      if (c.world != 1) raise(SKR_EPARAM, "lazy mode on dense data runs on one GPU");
+      const size_t s = dtype_size(S.dtype);
+      std::vector<unsigned char> rows((size_t)S.n * S.ld * s);
+      SKR_CUDA(cudaMemcpyAsync(rows.data(), S.ptr, rows.size(), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      std::vector<int64_t> rp(S.n + 1, 0);
+      std::vector<int32_t> ci;
+      std::vector<double> cv;
+      for (int64_t i = 0; i < S.n; ++i) {
+        for (int64_t j = 0; j < S.d; ++j) {
+          const size_t e = (size_t)i * S.ld + j;
+          const double v = S.dtype == SKR_F32 ? (double)reinterpret_cast<const float*>(rows.data())[e]
+                                              : reinterpret_cast<const double*>(rows.data())[e];
+          if (v != 0.0) {
+            ci.push_back((int32_t)j);
+            cv.push_back(v);
+          }
+        }
+        rp[i + 1] = (int64_t)cv.size();
+      }
+      const int rc2 = skr_data_create_csr(ctx, S.n, S.d, rp.data(), ci.data(), cv.data(), &conv);
+      if (rc2 != SKR_OK) raise(rc2, skr_last_error());
+    }
+  });
+  if (rc != SKR_OK) return rc;
+  const int rc3 = skr_problem_create(ctx, conv ? conv : X, y, lambda, U, sigma, k, out);
+  if (conv) skr_data_destroy(conv);  // the problem holds the storage it needs (shared)
+  return rc3;
+}
+
+int skr_problem_mode(const skr_problem* p, int* mode) {
+  return guard([&] {
+    if (!p || !mode) raise(SKR_EPARAM, "null argument");
+    *mode = p->lazy ? SKR_MODE_LAZY : SKR_MODE_DENSE;
+  });
+}
+
 int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
                        const double* sigma, int64_t k, skr_problem** out) {
   return guard([&] {

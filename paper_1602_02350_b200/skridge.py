@@ -472,7 +472,7 @@ class ApplyMode(Enum):
     Auto = 2
 
 
-kDenseModeMaxEntries = 200_000_000  # ridge.hpp:65 (the GPU has no lazy path)
+kDenseModeMaxEntries = 200_000_000  # ridge.hpp:65 (the Dense-mode guard, ridge.cpp:110-113)
 
 
 # ---------------------------------------------------------------------------
@@ -539,9 +539,12 @@ class GpuEpochState:
 class PreconditionedRidge:
     """PreconditionedRidge (ridge.hpp:78-119) — the FiniteSumProblem plugin on the B200.
 
-    Dense mode only: X~ is materialised in HBM (180 GB holds every BASELINE
-    config), so the reference's Lazy mode (ridge.cpp:283-400) has no GPU
-    counterpart; mode() reports Dense.
+    ApplyMode (skr_problem_create_mode): Dense materialises X~ in HBM (and, like
+    ridge.cpp:110-113, raises ScaleGuardError above 2e8 entries; sparse data are
+    densified on the device); Lazy keeps X and the k x n projections and runs the
+    device Lazy chain (ridge.cpp:283-400; dense data go through a CSR view); Auto
+    is the device's choice — Dense for dense data (180 GB of HBM holds X~ at every
+    BASELINE size), Lazy for sparse.  mode() reports what the device runs.
     """
 
     def __init__(self, p: RidgeProblem, precond: Preconditioner, mode: ApplyMode = ApplyMode.Auto):
@@ -554,9 +557,10 @@ class PreconditionedRidge:
         U = np.ascontiguousarray(np.asarray(precond.basis()).T) if k else None  # (k, d): row j = u_j
         sig = _f64(precond._sigma) if k else None
         h = vp()
-        _check(_lib.load().skr_problem_create(p.data.ctx.h, p.data.h, p.labels, float(p.lam),
-                                              U.ctypes.data if k else None,
-                                              sig.ctypes.data if k else None, k, C.byref(h)))
+        _check(_lib.load().skr_problem_create_mode(p.data.ctx.h, p.data.h, p.labels, float(p.lam),
+                                                   U.ctypes.data if k else None,
+                                                   sig.ctypes.data if k else None, k, int(ApplyMode(mode).value),
+                                                   C.byref(h)))
         self.h = h
         n, d, kk, a, b, m = i64(), i64(), i64(), f64(), f64(), f64()
         _check(_lib.load().skr_problem_info(self.h, C.byref(n), C.byref(d), C.byref(kk), C.byref(a),
@@ -603,8 +607,10 @@ class PreconditionedRidge:
 
     # PreconditionedRidge extras
     def mode(self) -> ApplyMode:
-        """Dense for dense data (X~ materialised); Lazy for sparse data (ridge.cpp:283-400)."""
-        return ApplyMode.Lazy if self.problem_.data.sparse else ApplyMode.Dense
+        """ridge.hpp:96: the mode the device problem runs in (skr_problem_mode)."""
+        m = C.c_int()
+        _check(_lib.load().skr_problem_mode(self.h, C.byref(m)))
+        return ApplyMode(m.value)
 
     def preconditioner(self) -> Preconditioner:
         return self.precond_

@@ -322,6 +322,58 @@ def test_config_c1_end_to_end(O):
 
 
 # ---- the drop-in boundary: the reference's own engine drives the GPU problem -------
+def test_reference_typed_pipeline_drop_ins():
+    """tests/cpp/drop_in_pipeline: skridge_gpu::block_lanczos / sketched_preconditioned_svrg /
+    preconditioned_components (integration/skridge_gpu_problem.hpp) take and return the
+    reference's own types and match the unmodified reference (sketch.hpp:55,
+    ridge.hpp:121-153): sigma~ 1e-10, U and V 1e-8, trace and w^ 1e-8, every diagnostics
+    field, and ApplyMode::Lazy running the device Lazy chain under the reference engine."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "drop_in_pipeline")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/drop_in_pipeline not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_apply_modes_agree():
+    """ApplyMode (ridge.hpp:121-123): Lazy on dense data runs the device Lazy chain,
+    Dense on sparse data densifies on the device; both report their mode and agree
+    with the default mode to the reference's own dense = lazy tolerance (test_ridge.cpp:272-291)."""
+    X, y, lam, k = small_problem(n=600, d=40, k=5)
+    n, d = X.shape
+    p = sk.RidgeProblem(sk.DataMatrix(X), y, lam)
+    sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(k, 0.5, 3, 3))
+    pc = sk.build_sketched(sv, lam)
+    dense = sk.preconditioned_components(p, pc, sk.ApplyMode.Dense)
+    lazy = sk.preconditioned_components(p, pc, sk.ApplyMode.Lazy)
+    auto = sk.preconditioned_components(p, pc)
+    assert dense.mode() == sk.ApplyMode.Dense and auto.mode() == sk.ApplyMode.Dense
+    assert lazy.mode() == sk.ApplyMode.Lazy
+    assert rel(lazy.betas(), dense.betas()) < 1e-12
+    eta = configs.step_size(dense.max_row_sq())
+    cfg = sk.SvrgConfig(4, 2 * n, eta, 7)
+    t_d = [r.objective for r in sk.svrg_solve(dense, cfg).trace]
+    t_l = [r.objective for r in sk.svrg_solve(lazy, cfg).trace]
+    assert rel(t_l, t_d) < 1e-8
+    # sparse data: Auto -> Lazy, explicit Dense -> densified X~
+    import scipy.sparse as spm
+    Xs = X.copy()
+    Xs[np.abs(Xs) < 0.3] = 0.0
+    ps = sk.RidgeProblem(sk.DataMatrix.from_scipy(spm.csr_matrix(Xs)), y, lam)
+    svs = sk.block_lanczos(sk.scaled_design(ps), sk.LanczosConfig(k, 0.5, 3, 3))
+    pcs = sk.build_sketched(svs, lam)
+    s_auto = sk.preconditioned_components(ps, pcs)
+    s_dense = sk.preconditioned_components(ps, pcs, sk.ApplyMode.Dense)
+    assert s_auto.mode() == sk.ApplyMode.Lazy and s_dense.mode() == sk.ApplyMode.Dense
+    assert rel(s_dense.betas(), s_auto.betas()) < 1e-12
+    t_a = [r.objective for r in sk.svrg_solve(s_auto, cfg).trace]
+    t_s = [r.objective for r in sk.svrg_solve(s_dense, cfg).trace]
+    assert rel(t_s, t_a) < 1e-8
+
+
 def test_reference_engine_drives_gpu_problem():
     """tests/cpp/drop_in_svrg: the UNMODIFIED reference svrg_solve (oracle/_ref)
     run on integration/skridge_gpu_problem.hpp's FiniteSumProblem vs on the
