@@ -383,12 +383,18 @@ def k9_kernel_name(cfg) -> str:
 FP64_DMMA_TFLOPS = 35.5  # cuBLAS DGEMM 8192^3 measured on this pool's B200 (profiles/fp64_peak.py)
 
 
-def lanczos_gemm_flops(cfg, n):
-    """The products skr_lanczos runs (no rank drop): Pi^T X, (q-1) x [X prev^T, T^T X],
-    Z = X Q^T and the full Gram Z^T Z."""
+def lanczos_gemm_flops(cfg, n, fp64_path=None):
+    """The products skr_lanczos executes (no rank drop).  3xTF32 path: Pi^T X,
+    (q-1) x [X prev^T, T^T X], Z = X Q^T for the last block and the Gram Z^T Z
+    (fp32-equivalent flops).  fp64 (DMMA) path: Pi^T X, q x [X Q_j^T, T^T X] (the
+    last pair gives V_q) and G = Q [V_1..V_q]^T (W x W x d)."""
     d, k, q = cfg.d, cfg.k, cfg.q
     W = q * k
-    return 2 * n * d * k + 4 * n * d * k * (q - 1) + 2 * n * d * W + 2 * n * W * W
+    if fp64_path is None:
+        fp64_path = cfg.dtype == "f64"
+    if fp64_path:
+        return 2 * n * d * k + 4 * n * d * k * q + 2 * W * W * d
+    return 2 * n * d * k + 4 * n * d * k * (q - 1) + 2 * n * d * k + 2 * n * W * W
 
 
 def lanczos_flops(cfg, n):
@@ -412,8 +418,8 @@ def lanczos_fields(cfg, n_total, n_loc, world, wall_s, gemm_ms, tc_ms):
     else:
         path = "3xTF32 tcgen05"
     final_ms = gemm_ms if gemm_ms > 0.0 else tc_ms
-    tf = lanczos_gemm_flops(cfg, n_loc) / (max(final_ms, 1e-6) * 1e-3) / 1e12
     dmma = gemm_ms > 0.0
+    tf = lanczos_gemm_flops(cfg, n_loc, fp64_path=dmma) / (max(final_ms, 1e-6) * 1e-3) / 1e12
     out = {"seconds": round(wall_s, 4), "path": path,
            "tflops": round(lanczos_flops(cfg, n_total) / wall_s / 1e12 / world, 4),
            "note": "whole block_lanczos call incl. Pi stream, ortho, RR, eigensolve (and a discarded tc attempt)",
@@ -452,7 +458,7 @@ def lanczos_tf32_extra(sk, ctx):
         gemms.append(ctx.profile_read("lanczos_gemm_tc")[0])
         ctx.profile(False)
     wall, gemm_ms = min(walls), min(gemms)
-    tf = lanczos_gemm_flops(c5, c5.n) / (max(gemm_ms, 1e-6) * 1e-3) / 1e12
+    tf = lanczos_gemm_flops(c5, c5.n, fp64_path=False) / (max(gemm_ms, 1e-6) * 1e-3) / 1e12
     del a, data
     return {"config": "c5 (fp32 storage, n=16777216, d=1024, k=64, q=2)", "path": "3xTF32 tcgen05",
             "seconds": round(wall, 4), "gemm_ms": round(gemm_ms, 3), "gemm_tflops_fp32_equiv": round(tf, 1),

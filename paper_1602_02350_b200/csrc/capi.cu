@@ -697,6 +697,18 @@ bool cholqr2_append(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t c
   return true;
 }
 
+// G <- (G + G^T) / 2 (W x W)
+__global__ void symmetrize_kernel(double* __restrict__ G, int64_t W) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= W * W) return;
+  const int64_t i = e / W, j = e % W;
+  if (i < j) {
+    const double v = 0.5 * (G[i * W + j] + G[j * W + i]);
+    G[i * W + j] = v;
+    G[j * W + i] = v;
+  }
+}
+
 // Whether the fp32-storage Rayleigh-Ritz Gram G (W x W, from the 3xTF32 tensor-core
 // products) must be recomputed in fp64: its eigenvalues (no vectors, on a copy)
 // give lambda_1 / lambda_kk; the 3xTF32 Gram's absolute error is ~2e-9 lambda_1
@@ -1905,6 +1917,13 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     DBuf<double> Tm(tc ? 1 : (size_t)std::max<int64_t>(n, 1) * k, c.stream);
     DBuf<double> prevT(S.sparse ? (size_t)d * k : 0, c.stream), tmpK(S.sparse ? (size_t)d * k : 0, c.stream);
     Pt.release();
+    // fp64 dense path: keep every Krylov product V_j = Xb^T Xb Q_j (before it is
+    // orthogonalised into the next block), so the Rayleigh-Ritz Gram is
+    // G = Q^T [V_1 .. V_q] — one more product pair for the last block instead of
+    // Z = Xb Q^T over all qk columns plus Z^T Z.
+    const bool kv_rr = !S.sparse && !tc;
+    DBuf<double> KV(kv_rr ? (size_t)cap * ld : 1, c.stream);
+    int64_t kv_done = 0;  // basis rows whose V rows exist
     for (int64_t j = 1; j < q && appended > 0; ++j) {
       const int64_t W = Wb;
       const double* prev = Qt.get() + (W - appended) * ld;
@@ -1939,9 +1958,13 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       }
       gmark();
       c.allreduce_sum(Vt.get(), (size_t)appended * ld);
+      if (kv_rr) {
+        SKR_CUDA(cudaMemcpyAsync(KV.get() + (W - appended) * ld, Vt.get(), sizeof(double) * appended * ld,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+        kv_done = W;
+      }
       appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), appended);
     }
-    Tm.release();
     const int64_t W = Wb;
     const int64_t kk = std::min<int64_t>(k, W);
     // Rayleigh-Ritz: G = (X Q)^T (X Q) scale^2 over row chunks (sketch.cpp:59-61)
@@ -1970,21 +1993,28 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
       Ql.release();
       tc_gemm_t(c, false, Zh.get(), np, Zh.get(), Zl.get(), np, W, W, n, 1.0, G.get(), W);
     } else {
-      const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)(1 << 28) / W));
-      DBuf<double> Z((size_t)chunk * W, c.stream);
-      for (int64_t r = 0; r < n; r += chunk) {
-        const int64_t rows = std::min(chunk, n - r);
+      // V rows of the blocks not yet multiplied (the last appended block, or all of
+      // them after a rank collapse): T = scale X Q_blk^T, V = scale T^T X
+      for (int64_t r0 = kv_done; r0 < W; r0 += k) {
+        const int64_t a = std::min<int64_t>(k, W - r0);
         DISPATCH_DTYPE(S.dtype, T, {
-          const T* X = static_cast<const T*>(S.ptr) + r * ld;
-          gemm<T, double, false, true>(&c, rows, W, d, X, ld, Qt.get(), ld, EpiStore{Z.get(), W, scale, 0.0});
+          const T* X = static_cast<const T*>(S.ptr);
+          gemm<T, double, false, true>(&c, n, a, d, X, ld, Qt.get() + r0 * ld, ld, EpiStore{Tm.get(), a, scale, 0.0});
+          gemm<double, T, true, false>(&c, a, d, n, Tm.get(), a, X, ld, EpiStore{KV.get() + r0 * ld, ld, scale, 0.0});
         });
-        gemm<double, double, true, false>(&c, W, W, rows, Z.get(), W, Z.get(), W, EpiStore{G.get(), W, 1.0, 1.0});
+        c.allreduce_sum(KV.get() + r0 * ld, (size_t)a * ld);
       }
+      // G = Q (Xb^T Xb) Q^T = Qt KV^T (W x W), symmetrised (the two triangles agree to rounding)
+      gemm<double, double, false, true>(&c, W, W, d, Qt.get(), ld, KV.get(), ld, EpiStore{G.get(), W, 1.0, 0.0});
+      symmetrize_kernel<<<ceil_div(W * W, 256), 256, 0, c.stream>>>(G.get(), W);
+      SKR_LAUNCHED(&c);
     }
     gmark();
+    Tm.release();
+    KV.release();
     Zh.release();  // >= 1 GiB at c3-c5: cudaFree synchronises, kept outside the timed products
     Zl.release();
-    c.allreduce_sum(G.get(), (size_t)W * W);
+    if (!kv_rr) c.allreduce_sum(G.get(), (size_t)W * W);  // KV rows are already global
     // The 3xTF32 products accumulate in fp32 (TMEM), so the Gram's absolute error is
     // ~eps32-class times lambda_1 and the smallest retained Ritz values lose
     // ~eps * lambda_1 / lambda_k relative accuracy (c3: lambda_1 / lambda_128 = 2e6
