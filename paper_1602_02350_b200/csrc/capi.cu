@@ -771,37 +771,6 @@ int append_block(Ctx& c, double* Qt, int64_t ld, int64_t d, int& W, int64_t cap,
 }
 
 // ---- tcgen05 3xTF32 GEMM host side --------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    SKR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (!p) raise(SKR_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-// 2-D fp32 tensor map over a row-major matrix (rows x cols, row stride ld
-// elements), box = box_rows x 32 columns, 128-byte swizzle.
-CUtensorMap make_tmap_f32(const float* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-                          CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, int box_cols = 32) {
-  CUtensorMap m;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  const cuuint32_t es[2] = {1, 1};
-  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
-                                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) raise(SKR_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  return m;
-}
 
 template <bool A_MN, int BN, int CS>
 void tc_launch_cs(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* Bl, int64_t ldb, const TcGemmArgs& g,

@@ -153,33 +153,7 @@ fullgrad_kernel(const T* __restrict__ X, int64_t ld, int64_t n, const double* __
 // stage it just drained S-1 tiles ahead.  Threads own interleaved 16-byte
 // column chunks (chunk j of thread t at byte 16*t + 16*NT*j of the row) so the
 // shared-memory reads are conflict-free; compute is identical to v2.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
+// (shared-memory address / mbarrier / bulk-copy helpers: common.cuh)
 template <class T, int VEC, int NT>
 __device__ __forceinline__ void lds_cols(const unsigned char* row, int tid, T (&v)[VEC]) {
   constexpr int PER = 16 / sizeof(T);  // elements per 16-byte chunk

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace skr {
 
@@ -160,6 +161,10 @@ gemm_kernel(int64_t M, int64_t N, int64_t K, const TA* __restrict__ A, int64_t l
   }
 }
 
+}  // namespace skr
+#include "gemm_tma.cuh"
+namespace skr {
+
 // Sum split-K partials in split order, then apply the final epilogue.
 template <class Epi>
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int64_t M, int64_t N,
@@ -214,10 +219,74 @@ void gemm_tiled(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t 
   SKR_LAUNCHED(ctx);
 }
 
+// TMA-staged DMMA GEMM (gemm_tma.cuh) for the large products: needs 16-byte aligned
+// bases and row strides (TMA), int32 coordinates.  Returns false when not eligible.
+template <class TA, class TB, bool A_T, bool B_T, class Epi>
+bool gemm_tma(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, const TB* B, int64_t ldb, Epi epi,
+              int splits) {
+  static const bool off = getenv("SKR_GEMM_LEGACY") != nullptr;
+  if (off) return false;
+  constexpr bool AK = !A_T, BK_ = B_T;  // K-major operands
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
+  if ((lda * (int64_t)sizeof(TA)) % 16 || (ldb * (int64_t)sizeof(TB)) % 16) return false;
+  if (M >= (1LL << 31) || N >= (1LL << 31) || K >= (1LL << 31)) return false;
+  // small products, and products narrower than the 128 x 128 tile in M or N (the
+  // register-staged kernel's 64 x 128 / 128 x 64 tiles waste less there)
+  if ((double)M * (double)N * (double)K < 3e8 || M < TG_BM || N < TG_BN) return false;
+  constexpr int EA = 128 / (int)sizeof(TA), EB = 128 / (int)sizeof(TB);
+  const CUtensorMap ma = AK ? make_tmap_2d(A, sizeof(TA), M, K, lda, TG_BM, EA, CU_TENSOR_MAP_SWIZZLE_128B)
+                            : make_tmap_2d(A, sizeof(TA), K, M, lda, TG_BK, EA, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap mb = BK_ ? make_tmap_2d(B, sizeof(TB), N, K, ldb, TG_BN, EB, CU_TENSOR_MAP_SWIZZLE_128B)
+                             : make_tmap_2d(B, sizeof(TB), K, N, ldb, TG_BK, EB, CU_TENSOR_MAP_SWIZZLE_128B);
+  const int64_t tiles = (int64_t)ceil_div(M, TG_BM) * ceil_div(N, TG_BN);
+  if (splits <= 0) {
+    // one CTA per SM: pick the split count whose last wave is fullest (fewest splits on ties)
+    const int64_t kmax = std::max<int64_t>(1, std::min<int64_t>(256, K / (8 * TG_BK)));
+    double best = -1.0;
+    splits = 1;
+    for (int64_t sp = 1; sp <= kmax; ++sp) {
+      const int64_t ctas = tiles * sp, waves = (ctas + ctx->sm_count - 1) / ctx->sm_count;
+      if (waves > 8 && sp > 1) break;
+      const double eff = (double)ctas / (double)(waves * ctx->sm_count);
+      if (eff > best + 0.02) {
+        best = eff;
+        splits = (int)sp;
+      }
+    }
+  }
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = std::max<int64_t>(TG_BK, (kchunk + TG_BK - 1) / TG_BK * TG_BK);
+  splits = (int)std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
+  const dim3 grid(ceil_div(M, TG_BM), ceil_div(N, TG_BN), splits);
+  constexpr size_t smem = tg_smem<TA, TB>();
+  if (splits == 1) {
+    auto k = dgemm_tma_kernel<TA, TB, AK, BK_, Epi, false>;
+    configure_once((const void*)k, [&] {
+      SKR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    k<<<grid, TG_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, epi);
+    SKR_LAUNCHED(ctx);
+    return true;
+  }
+  DBuf<double> ws((size_t)splits * M * N, ctx->stream);
+  EpiPartial part{ws.get(), M, N};
+  auto k = dgemm_tma_kernel<TA, TB, AK, BK_, EpiPartial, true>;
+  configure_once((const void*)k, [&] {
+    SKR_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  k<<<grid, TG_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, part);
+  SKR_LAUNCHED(ctx);
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(M * N, 256), 4LL * ctx->sm_count);
+  splitk_reduce_kernel<Epi><<<blocks, 256, 0, ctx->stream>>>(ws.get(), M, N, splits, epi);
+  SKR_LAUNCHED(ctx);
+  return true;
+}
+
 template <class TA, class TB, bool A_T, bool B_T, class Epi>
 void gemm(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t lda, const TB* B,
           int64_t ldb, Epi epi, int splits = 0) {
   if (M <= 0 || N <= 0) return;
+  if (gemm_tma<TA, TB, A_T, B_T, Epi>(ctx, M, N, K, A, lda, B, ldb, epi, splits)) return;
   if (M <= 64 && N > 64)
     gemm_tiled<TA, TB, A_T, B_T, Epi, 64, 128>(ctx, M, N, K, A, lda, B, ldb, epi, splits);
   else

@@ -38,7 +38,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
-#include "fullgrad.cuh"  // mbarrier / bulk-copy helpers
+#include "tma.cuh"  // tensor maps, TMA tile loads (mbarrier / bulk-copy helpers: common.cuh)
 
 namespace skr {
 
@@ -59,13 +59,6 @@ static_assert(tc_acc_cols<64>() + 32 * tc_stages<64>() <= 512, "TMEM budget");
 static_assert(tc_acc_cols<128>() + 32 * tc_stages<128>() <= 512, "TMEM budget");
 static_assert(tc_acc_cols<256>() + 32 * tc_stages<256>() <= 512, "TMEM budget");
 
-__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 
 // the same box, written to the same shared offset of every CTA in ctaMask, each
 // CTA's mbarrier at `bar`'s offset receiving the bytes it got
