@@ -1881,6 +1881,15 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
     }
     gmark();
     c.allreduce_sum(Vt.get(), (size_t)k * ld);
+    if (tc) {
+      // Early exit to the fp64 path: the first Krylov block K1 = Xb^T Pi has
+      // singular values ~ sigma_1..sigma_k of Xb (times a well-conditioned Gaussian
+      // factor, d >> k), so cond(K1)^2 ~ lambda_1 / lambda_k — the same test the
+      // Rayleigh-Ritz check applies at the end, decided before the remaining passes.
+      DBuf<double> K1g((size_t)k * k, c.stream);
+      gemm<double, double, false, true>(&c, k, k, d, Vt.get(), ld, Vt.get(), ld, EpiStore{K1g.get(), k, 1.0, 0.0});
+      if (rr_needs_fp64(c, K1g.get(), k, k)) return true;
+    }
     int appended = append_block(c, Qt.get(), ld, d, Wb, cap, Vt.get(), (int)k);
     if (Wb == 0) raise(SKR_EEMPTY, "krylov_block: A * Pi is numerically zero");
     DBuf<double> Tm(tc ? 1 : (size_t)std::max<int64_t>(n, 1) * k, c.stream);
