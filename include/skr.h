@@ -236,9 +236,17 @@ int skr_gram_eigs(skr_ctx* ctx, const skr_data* X, double* evals, double* evecs)
 /* objective(p, w) of the ORIGINAL ridge problem (ridge.cpp:33-43) */
 int skr_ridge_objective(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
                         const double* w, double* out);
-/* reference_minimum (bench.cpp:84-94): SYRK + Cholesky on the device */
+/* reference_minimum (bench.cpp:84-94): SYRK + Cholesky on the device for d <= 5000
+ * (kDirectSolveGuardDim, bench.cpp:19), the conjugate-gradient route of
+ * reference_minimum_cg(p, 1e-12, 20 d) above it (bench.cpp:56-82). */
 int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
                           double* w_out, double* min_out);
+/* reference_minimum_cg (bench.hpp:26, bench.cpp:56-82) on the device: CG on
+ * (Xb^T Xb + lambda I) w = X^T y / n from w = 0, stopping before the first
+ * iteration with ||r|| <= rel_residual_tol ||rhs|| or after max_iterations;
+ * *iterations (optional) = iterations run. */
+int skr_reference_minimum_cg(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
+                             double rel_residual_tol, int64_t max_iterations, double* w_out, int64_t* iterations);
 /* conditioned_condition_number (precond.cpp:196-206) without the d <= 2000
  * guard: tr(M) / lambda_min(M), M = P^{-1/2}(A^T A + lambda I)P^{-1/2} where A
  * is the handle as passed (the reference passes scaled_design(p)). */

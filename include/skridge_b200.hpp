@@ -538,7 +538,15 @@ struct ReferenceSolution {
   double minimum = 0.0;
 };
 
-/// bench.cpp:84-94 on the device.
+/// bench.hpp:26 / bench.cpp:56-82 on the device.
+inline Vector reference_minimum_cg(const RidgeProblem& p, double rel_residual_tol, std::size_t max_iterations) {
+  Vector w(p.dim());
+  check(skr_reference_minimum_cg(p.data.context().get(), p.data.get(), p.labels.data(), p.lambda, rel_residual_tol,
+                                 (int64_t)max_iterations, w.data(), nullptr));
+  return w;
+}
+
+/// bench.cpp:84-94 on the device (Cholesky for d <= 5000, the CG route above).
 inline ReferenceSolution reference_minimum(const RidgeProblem& p) {
   ReferenceSolution r;
   r.minimizer.resize(p.dim());

@@ -206,6 +206,15 @@ class _Backend:
             x, n, d, _c64(y), lam, w, C.byref(mn)))
         return w, mn.value
 
+    def reference_minimum_cg(self, x, y, lam, tol, max_it):
+        """bench.cpp:56-82 (reference backend only)."""
+        x = _c64(x)
+        n, d = x.shape
+        w = np.empty(d)
+        self._check(self._fn("reference_minimum_cg", cint, [_dp, i64, i64, _dp, f64, f64, i64, _dp])(
+            x, n, d, _c64(y), lam, tol, max_it, w))
+        return w
+
     def conditioned_cond(self, x, lam, U, sigma, unguarded=False) -> float:
         x = _c64(x)
         n, d = x.shape

@@ -168,6 +168,16 @@ int ref_reference_minimum(const double* x, std::int64_t n, std::int64_t d, const
   });
 }
 
+// reference_minimum_cg(p, tol, max_iterations) (bench.cpp:56-82) on dense rows
+int ref_reference_minimum_cg(const double* x, std::int64_t n, std::int64_t d, const double* y, double lambda,
+                             double tol, std::int64_t max_it, double* w_out) {
+  return guard([&] {
+    RidgeProblem p(DataMatrix(colmajor(x, d, n)), Vector(y, y + n), lambda);
+    Vector w = reference_minimum_cg(p, tol, static_cast<std::size_t>(max_it));
+    std::memcpy(w_out, w.data(), sizeof(double) * d);
+  });
+}
+
 // conditioned_condition_number on scaled_design(p) (precond.cpp:196-206);
 // unguarded=1 composes conditioned_matrix + sym_eigs directly (d > 2000).
 int ref_conditioned_cond(const double* x, std::int64_t n, std::int64_t d, double lambda,

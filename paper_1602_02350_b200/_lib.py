@@ -87,6 +87,7 @@ SIGNATURES = {
     "skr_gaussian_matrix": (cint, [vp, i64, i64, u64, dptr]),
     "skr_ridge_objective": (cint, [vp, vp, dptr, f64, dptr, P(f64)]),
     "skr_reference_minimum": (cint, [vp, vp, dptr, f64, dptr, P(f64)]),
+    "skr_reference_minimum_cg": (cint, [vp, vp, dptr, f64, f64, i64, dptr, P(i64)]),
     "skr_conditioned_cond": (cint, [vp, vp, f64, vp, vp, i64, P(f64)]),
 }
 

@@ -2075,15 +2075,6 @@ int skr_lanczos(skr_ctx* ctx, const skr_data* A, int64_t k, int64_t q, double ep
 }
 
 // ---- preconditioned components -------------------------------------------------
-// CSR over points -> dense n x ld fp64 rows (one warp per row)
-__global__ void csr_densify_kernel(const int64_t* __restrict__ rptr, const int32_t* __restrict__ ridx,
-                                   const double* __restrict__ rval, int64_t n, int64_t ld, double* __restrict__ out) {
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = warp; i < n; i += ((int64_t)gridDim.x * blockDim.x) >> 5)
-    for (int64_t t = rptr[i] + lane; t < rptr[i + 1]; t += 32) out[i * ld + ridx[t]] = rval[t];
-}
-
 int skr_problem_create_mode(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
                             const double* sigma, int64_t k, int mode, skr_problem** out) {
   if (mode == SKR_MODE_AUTO) return skr_problem_create(ctx, X, y, lambda, U, sigma, k, out);
@@ -2099,10 +2090,7 @@ int skr_problem_create_mode(skr_ctx* ctx, const skr_data* X, const double* y, do
         raise(SKR_EGUARD, "preconditioned components: dense mode would materialize too many entries; use lazy");
       if (S.sparse) {  // densify on the device
         auto st = new_storage(c, SKR_F64, S.n, S.d);
-        if (S.n > 0)
-          csr_densify_kernel<<<std::min<unsigned>(ceil_div(S.n * 32, 256), 8u * c.sm_count), 256, 0, c.stream>>>(
-              S.rptr.get(), S.ridx.get(), S.rval.get(), S.n, st->ld, static_cast<double*>(st->ptr));
-        SKR_LAUNCHED(&c);
+        csr_densify(c, S.rptr.get(), S.ridx.get(), S.rval.get(), S.n, static_cast<double*>(st->ptr), st->ld);
         auto x = std::make_unique<skr_data>(*X);
         x->st = st;
         x->scale = 1.0;
@@ -2772,6 +2760,23 @@ static double ridge_objective_dev(Ctx& c, const skr_data* X, const double* y_dev
       SKR_LAUNCHED(&c);
     }
     c.allreduce_sum(sums.get() + S.ld, 1);
+  } else if (S.ld > 4096) {
+    // wider than the fused pass (K9 keeps a row per thread group up to d = 4096):
+    // r = X w by a DMMA GEMV, loss = sum (r - y)^2 (single-CTA sum: deterministic)
+    if (sums.n < (size_t)S.ld + 1) sums.alloc(S.ld + 1, c.stream);
+    sums.zero();
+    if (S.n > 0) {
+      DBuf<double> r(S.n, c.stream);
+      DISPATCH_DTYPE(S.dtype, T, {
+        gemm<T, double, false, false>(&c, S.n, 1, S.d, static_cast<const T*>(S.ptr), S.ld, w_dev, 1,
+                                      EpiStore{r.get(), 1, X->scale, 0.0});
+      });
+      sq_residual_kernel<<<ceil_div(S.n, 256), 256, 0, c.stream>>>(r.get(), y_dev, S.n);
+      SKR_LAUNCHED(&c);
+      sum_kernel<<<1, 1024, 0, c.stream>>>(r.get(), S.n, sums.get() + S.ld);
+      SKR_LAUNCHED(&c);
+    }
+    c.allreduce_sum(sums.get() + S.ld, 1);
   } else {
     fullgrad_sums(c, S.dtype, S.ptr, S.ld, S.n, y_dev, w_dev, pg, pl, sums);
   }
@@ -2887,6 +2892,153 @@ int skr_gram_eigs(skr_ctx* ctx, const skr_data* X, double* evals, double* evecs)
   });
 }
 
+// ---- reference_minimum_cg (bench.cpp:56-82) on the device ----------------------
+// out += a v
+__global__ void axpy_kernel(int64_t d, double a, const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < d) out[j] = fma(a, v[j], out[j]);
+}
+// Deterministic single-block dot product (fixed-order tree), result on the device.
+__global__ void cg_dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                              double* __restrict__ out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) s = fma(a[j], b[j], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+// scalars: sc[0] rho, sc[1] dir.Ad, sc[2] rho_next, sc[3] threshold^2 (tol ||rhs||)^2; flag[0] done
+__global__ void cg_check_kernel(const double* sc, int* flag, int64_t* iters) {
+  if (!flag[0] && !(sc[0] > sc[3])) flag[0] = 1;  // sqrt(rho) <= tol ||rhs||: stop before this iteration
+  if (!flag[0]) ++*iters;
+}
+__global__ void cg_update_kernel(double* __restrict__ w, double* __restrict__ r, const double* __restrict__ dir,
+                                 const double* __restrict__ ad, int64_t d, const double* sc, const int* flag) {
+  if (flag[0]) return;
+  const double alpha = sc[0] / sc[1];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.x * blockDim.x) {
+    w[j] = fma(alpha, dir[j], w[j]);      // axpy(alpha, dir, w)
+    r[j] = fma(-alpha, ad[j], r[j]);      // axpy(-alpha, ad, r)
+  }
+}
+__global__ void cg_dir_kernel(const double* __restrict__ r, double* __restrict__ dir, int64_t d, double* sc,
+                              const int* flag) {
+  if (flag[0]) return;
+  const double beta = sc[2] / sc[0];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d; j += (int64_t)gridDim.x * blockDim.x)
+    dir[j] = r[j] + beta * dir[j];
+}
+__global__ void cg_rho_kernel(double* sc, const int* flag) {
+  if (!flag[0]) sc[0] = sc[2];
+}
+
+// out = Xb^T (Xb v) + lambda v, Xb = X / sqrt(n_global) (the reference's apply, bench.cpp:63-67)
+static void cg_apply(Ctx& c, const skr_data* X, const double* v, double lambda, double* t, double* out) {
+  const Storage& S = *X->st;
+  const int64_t n = S.n, d = S.d, ld = S.ld;
+  const double s = 1.0 / std::sqrt((double)X->n_global);
+  if (S.sparse) {
+    csr_spmv(c, S.rptr.get(), S.ridx.get(), S.rval.get(), n, v, s, t);
+    SKR_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * d, c.stream));
+    split_spmv(c, S.fsplit, S.fidx.get(), S.fval.get(), d, t, s, out);
+  } else {
+    DISPATCH_DTYPE(S.dtype, T, {
+      const T* Xp = static_cast<const T*>(S.ptr);
+      gemm<T, double, false, false>(&c, n, 1, d, Xp, ld, v, 1, EpiStore{t, 1, s, 0.0});
+      gemm<T, double, true, false>(&c, d, 1, n, Xp, ld, t, 1, EpiStore{out, 1, s, 0.0});
+    });
+  }
+  c.allreduce_sum(out, d);
+  axpy_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(d, lambda, v, out);
+  SKR_LAUNCHED(&c);
+}
+
+// rhs (device, d) = X^T y / n_global (bench.cpp:50-54)
+static void normal_rhs_dev(Ctx& c, const skr_data* X, const double* yd, double* rhs) {
+  const Storage& S = *X->st;
+  const int64_t n = S.n, d = S.d, ld = S.ld;
+  SKR_CUDA(cudaMemsetAsync(rhs, 0, sizeof(double) * d, c.stream));
+  if (S.sparse) {
+    split_spmv(c, S.fsplit, S.fidx.get(), S.fval.get(), d, yd, 1.0 / (double)X->n_global, rhs);
+  } else {
+    DISPATCH_DTYPE(S.dtype, T, {
+      gemm<T, double, true, false>(&c, d, 1, n, static_cast<const T*>(S.ptr), ld, yd, 1,
+                                   EpiStore{rhs, 1, 1.0 / (double)X->n_global, 0.0});
+    });
+  }
+  c.allreduce_sum(rhs, d);
+}
+
+// w (device, >= d) = reference_minimum_cg(p, tol, max_it); returns the iterations run.
+static int64_t reference_minimum_cg_dev(Ctx& c, const skr_data* X, const double* yd, double lambda, double tol,
+                                        int64_t max_it, double* w) {
+  const Storage& S = *X->st;
+  const int64_t d = S.d, n = S.n;
+  DBuf<double> rhs(d, c.stream), r(d, c.stream), dir(d, c.stream), ad(d, c.stream), t(std::max<int64_t>(n, 1), c.stream);
+  DBuf<double> sc(4, c.stream), tmp(1, c.stream);
+  DBuf<int> flag(1, c.stream);
+  DBuf<int64_t> iters(1, c.stream);
+  normal_rhs_dev(c, X, yd, rhs.get());
+  SKR_CUDA(cudaMemsetAsync(w, 0, sizeof(double) * d, c.stream));
+  SKR_CUDA(cudaMemcpyAsync(r.get(), rhs.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, c.stream));
+  SKR_CUDA(cudaMemcpyAsync(dir.get(), rhs.get(), sizeof(double) * d, cudaMemcpyDeviceToDevice, c.stream));
+  flag.zero();
+  iters.zero();
+  // rhs_norm = max(||rhs||, 1e-300); threshold^2 = (tol rhs_norm)^2
+  cg_dot_kernel<<<1, 1024, 0, c.stream>>>(rhs.get(), rhs.get(), d, tmp.get());
+  SKR_LAUNCHED(&c);
+  double rr = 0.0;
+  SKR_CUDA(cudaMemcpyAsync(&rr, tmp.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  const double rhs_norm = std::max(std::sqrt(rr), 1e-300);
+  const double hsc[4] = {rr, 0.0, 0.0, (tol * rhs_norm) * (tol * rhs_norm)};
+  SKR_CUDA(cudaMemcpyAsync(sc.get(), hsc, sizeof(hsc), cudaMemcpyHostToDevice, c.stream));
+  const unsigned gb = std::min<unsigned>(ceil_div(d, 256), 1024u);
+  for (int64_t it = 0; it < max_it;) {
+    const int64_t chunk = std::min<int64_t>(64, max_it - it);
+    for (int64_t q = 0; q < chunk; ++q) {
+      cg_check_kernel<<<1, 1, 0, c.stream>>>(sc.get(), flag.get(), iters.get());
+      cg_apply(c, X, dir.get(), lambda, t.get(), ad.get());
+      cg_dot_kernel<<<1, 1024, 0, c.stream>>>(dir.get(), ad.get(), d, sc.get() + 1);
+      cg_update_kernel<<<gb, 256, 0, c.stream>>>(w, r.get(), dir.get(), ad.get(), d, sc.get(), flag.get());
+      cg_dot_kernel<<<1, 1024, 0, c.stream>>>(r.get(), r.get(), d, sc.get() + 2);
+      cg_dir_kernel<<<gb, 256, 0, c.stream>>>(r.get(), dir.get(), d, sc.get(), flag.get());
+      cg_rho_kernel<<<1, 1, 0, c.stream>>>(sc.get(), flag.get());
+      SKR_LAUNCHED(&c);
+    }
+    it += chunk;
+    int done = 0;
+    SKR_CUDA(cudaMemcpyAsync(&done, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (done) break;
+  }
+  int64_t h_it = 0;
+  SKR_CUDA(cudaMemcpyAsync(&h_it, iters.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return h_it;
+}
+
+int skr_reference_minimum_cg(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
+                             double rel_residual_tol, int64_t max_iterations, double* w_out, int64_t* iterations) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!X || !w_out) raise(SKR_EPARAM, "null argument");
+    if (!(lambda > 0.0)) raise(SKR_EPARAM, "ridge problem: lambda must be positive");
+    const Storage& S = *X->st;
+    DBuf<double> yd(std::max<int64_t>(S.n, 1), c.stream), w(S.ld, c.stream);
+    if (S.n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * S.n, cudaMemcpyHostToDevice, c.stream));
+    const int64_t it = reference_minimum_cg_dev(c, X, yd.get(), lambda, rel_residual_tol, max_iterations, w.get());
+    SKR_CUDA(cudaMemcpyAsync(w_out, w.get(), sizeof(double) * S.d, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (iterations) *iterations = it;
+  });
+}
+
 int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, double* w_out,
                           double* min_out) {
   return guard([&] {
@@ -2895,6 +3047,17 @@ int skr_reference_minimum(skr_ctx* ctx, const skr_data* X, const double* y, doub
     if (!(lambda > 0.0)) raise(SKR_EPARAM, "ridge problem: lambda must be positive");
     const Storage& S = *X->st;
     const int64_t d = S.d, ld = S.ld, n = S.n;
+    if (d > 5000) {  // kDirectSolveGuardDim (bench.cpp:19): the CG route, tol 1e-12, 20 d iterations
+      DBuf<double> yd(std::max<int64_t>(n, 1), c.stream), w(ld, c.stream);
+      if (n) SKR_CUDA(cudaMemcpyAsync(yd.get(), y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      w.zero();
+      reference_minimum_cg_dev(c, X, yd.get(), lambda, 1e-12, 20 * d, w.get());
+      DBuf<double> pg, pl, sums;
+      *min_out = ridge_objective_dev(c, X, yd.get(), lambda, w.get(), pg, pl, sums);
+      SKR_CUDA(cudaMemcpyAsync(w_out, w.get(), sizeof(double) * d, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      return;
+    }
     DBuf<double> G;
     scaled_gram_dev(c, X, 1.0 / std::sqrt((double)X->n_global), G);  // scaled_design(p).gram()
     add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(G.get(), d, ld, lambda);

@@ -784,8 +784,19 @@ class ReferenceSolution:
     minimum: float
 
 
+def reference_minimum_cg(p: RidgeProblem, rel_residual_tol: float, max_iterations: int):
+    """bench.hpp:26 / bench.cpp:56-82 on the device: CG from w = 0 on the normal
+    equations; returns (w, iterations run)."""
+    w = np.empty(p.dim())
+    it = i64()
+    _check(_lib.load().skr_reference_minimum_cg(p.data.ctx.h, p.data.h, p.labels, float(p.lam),
+                                                float(rel_residual_tol), int(max_iterations), w, C.byref(it)))
+    return w, it.value
+
+
 def reference_minimum(p: RidgeProblem) -> ReferenceSolution:
-    """bench.cpp:84-94 on the device (SYRK + Cholesky)."""
+    """bench.cpp:84-94 on the device: SYRK + Cholesky for d <= 5000, else the CG
+    route reference_minimum_cg(p, 1e-12, 20 d)."""
     w = np.empty(p.dim())
     mn = f64()
     _check(_lib.load().skr_reference_minimum(p.data.ctx.h, p.data.h, p.labels, float(p.lam), w, C.byref(mn)))

@@ -281,6 +281,34 @@ def test_reference_minimum_and_objective(O):
     assert abs(sk.objective(p, w) - O.objective(X, y, lam, w)) <= 1e-12 * O.objective(X, y, lam, w)
 
 
+@pytest.mark.parametrize("storage", ["sparse", "dense"])
+def test_reference_minimum_cg_route_d_above_5000(storage):
+    """bench.cpp:84-94 takes reference_minimum_cg(p, 1e-12, 20 d) for d > 5000
+    (kDirectSolveGuardDim): the device CG route against the unmodified reference,
+    on RCV1-like sparse rows (CSR storage) and on the same rows stored dense; plus a
+    fixed-iteration-count run (reference_minimum_cg with max_iterations = 40)."""
+    import scipy.sparse as spm
+    R = oracle.ref()
+    n, d, lam = 1500, 6000, 1e-3
+    rng = np.random.default_rng(21)
+    A = spm.random(n, d, density=0.004, format="csr", random_state=3, data_rvs=rng.standard_normal)
+    A = A + spm.csr_matrix((rng.standard_normal(n), (np.arange(n), rng.integers(0, d, n))), shape=(n, d))
+    A.sum_duplicates()
+    A.eliminate_zeros()
+    Xd = A.toarray()
+    y = rng.standard_normal(n)
+    data = sk.DataMatrix.from_scipy(A) if storage == "sparse" else sk.DataMatrix(Xd)
+    p = sk.RidgeProblem(data, y, lam)
+    w_ref, L_ref = R.reference_minimum(Xd, y, lam)
+    got = sk.reference_minimum(p)
+    assert abs(got.minimum - L_ref) <= 1e-12 * abs(L_ref)
+    assert rel(got.minimizer, w_ref) < 1e-8
+    w40_ref = R.reference_minimum_cg(Xd, y, lam, 1e-12, 40)
+    w40, it = sk.reference_minimum_cg(p, 1e-12, 40)
+    assert it == 40
+    assert rel(w40, w40_ref) < 1e-10
+
+
 def test_conditioned_condition_number(O):
     X, y, lam, k = small_problem(n=400, d=50, k=6)
     sv = O.block_lanczos(X, k, q=3, seed=8)
