@@ -1023,7 +1023,7 @@ void run_sstep(skr_problem* p, const double* snap, const double* mu, const int64
   if (ld <= 16 * 32) run_sstep_t<T, 32, 32>(p, snap, mu, idx, m, eta, w_avg);
   else if (ld <= 16 * 64) run_sstep_t<T, 64, 32>(p, snap, mu, idx, m, eta, w_avg);
   else if (ld <= 16 * 128) run_sstep_t<T, 128, 32>(p, snap, mu, idx, m, eta, w_avg);
-  else if (ld <= 16 * 256) run_sstep_t<T, 256, 16>(p, snap, mu, idx, m, eta, w_avg);
+  else if (ld <= 16 * 256) run_sstep_t<T, 256, 16>(p, snap, mu, idx, m, eta, w_avg);  // L = 32 (2-deep ring): no gain
   else raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
 }
 

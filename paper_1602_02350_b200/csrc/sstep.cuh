@@ -253,7 +253,7 @@ struct ChainCfg {
   static constexpr int NUW = SW / 32;                   // update warps (one column per thread)
   static constexpr int NDW = SW * L / 1024;             // dot warps: 32 columns per dot lane
   static constexpr int NT = 32 * (NDW + NUW) + 64;      // + delta warp + producer warp
-  static constexpr int NB = SW * L * 8 <= 16384 ? 4 : 3;  // row ring depth
+  static constexpr int NB = SW * L * 8 <= 16384 ? 4 : SW * L * 8 <= 32768 ? 3 : 2;  // row ring depth (smem budget)
   static constexpr int NMX = 2;                         // M/X/p ring depth
   static constexpr int MXW = 2 * L * L + L;             // doubles per M/X/p slot
   static constexpr int NPS = 4;                         // partials slots (see the ordering argument)
