@@ -107,6 +107,8 @@ struct skr_problem {
   DBuf<double> B, y, y_all_buf, Ut, D, betas, cum, inv_nq, total;
   const double* y_all = nullptr;
   bool tables = false;
+  bool tables_pending = false;     // built on the side stream, ev_tables not yet waited on
+  cudaEvent_t ev_tables = nullptr;
   // full-gradient workspace
   int fg_grid = 0;
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
@@ -124,6 +126,10 @@ struct skr_problem {
   int64_t fg_calls = 0;
   const void* fg_ptrs[3] = {nullptr, nullptr, nullptr};  // workspaces the graph captured
   ~skr_problem() {
+    if (ev_tables) {
+      cudaEventSynchronize(ev_tables);  // the side-stream table build may still read betas
+      cudaEventDestroy(ev_tables);
+    }
     if (fg_exec) cudaGraphExecDestroy(fg_exec);
     if (io_host) cudaFreeHost(io_host);
   }
@@ -543,8 +549,35 @@ void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) 
 }
 
 // Exact sampling tables (svrg.cpp:90-106, :165-172), built once per problem.
+// Sampling tables (svrg.cpp:90-106, :167-172) on the side stream as soon as the
+// beta table is final; ensure_tables makes the main stream wait for them.
+void start_tables_async(skr_problem* p) {
+  Ctx& c = p->ctx->c;
+  const int64_t N = p->n_global + p->d;
+  p->cum.alloc(N, c.stream);
+  p->inv_nq.alloc(N, c.stream);
+  p->total.alloc(1, c.stream);
+  if (!p->ev_tables) SKR_CUDA(cudaEventCreateWithFlags(&p->ev_tables, cudaEventDisableTiming));
+  SKR_CUDA(cudaEventRecord(p->ev_tables, c.stream));  // the betas and the buffers above
+  SKR_CUDA(cudaStreamWaitEvent(c.aux, p->ev_tables, 0));
+  cumulative_kernel<<<1, 512, 0, c.aux>>>(p->betas.get(), N, p->cum.get(), p->total.get());
+  SKR_LAUNCHED(&c);
+  inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.aux>>>(p->betas.get(), N, p->total.get(),
+                                                                               p->inv_nq.get());
+  SKR_LAUNCHED(&c);
+  SKR_CUDA(cudaEventRecord(p->ev_tables, c.aux));
+  p->tables = true;
+  p->tables_pending = true;
+}
+
 void ensure_tables(skr_problem* p) {
-  if (p->tables) return;
+  if (p->tables) {
+    if (p->tables_pending) {
+      SKR_CUDA(cudaStreamWaitEvent(p->ctx->c.stream, p->ev_tables, 0));
+      p->tables_pending = false;
+    }
+    return;
+  }
   Ctx& c = p->ctx->c;
   const int64_t N = p->n_global + p->d;
   p->cum.alloc(N, c.stream);
@@ -2216,33 +2249,7 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
             Xp, ld, d, n, P.get(), k, p->D.get(), p->c, p->data_coef, p->betas.get() + p->row0, rowmax.get());
         SKR_LAUNCHED(&c);
       }
-      if (k > 0) {
-        auto xt = new_storage(c, S.dtype, n, d);
-        scale_cols_kernel<<<std::min<unsigned>(ceil_div(n * k, 256), 65535u), 256, 0, c.stream>>>(
-            P.get(), n, k, p->D.get(), p->c);
-        SKR_LAUNCHED(&c);
-        gemm<double, double, false, false>(&c, n, d, k, P.get(), k, p->Ut.get(), ld,
-                                           EpiXtilde<T>{Xp, static_cast<T*>(xt->ptr), ld, p->c}, 1);
-        p->xt = xt;
-      } else {
-        p->xt = X->st;  // identity: X~ = X exactly (c = 1)
-      }
     });
-    P.release();
-    // B = P^{-1/2} = c I + U (D - c) U^T  (d x ld); regulariser betas on rank 0 only (summed below)
-    p->B.alloc((size_t)d * ld, c.stream);
-    p->B.zero();
-    if (k > 0) {
-      DBuf<double> Us((size_t)k * ld, c.stream);
-      SKR_CUDA(cudaMemcpyAsync(Us.get(), p->Ut.get(), sizeof(double) * k * ld, cudaMemcpyDeviceToDevice, c.stream));
-      scale_rows_kernel<<<std::min<unsigned>(ceil_div(k * ld, 256), 65535u), 256, 0, c.stream>>>(Us.get(), k, ld,
-                                                                                                 p->D.get(), p->c);
-      SKR_LAUNCHED(&c);
-      gemm<double, double, true, false>(&c, d, d, k, Us.get(), ld, p->Ut.get(), ld, EpiBmat{p->B.get(), ld, p->c}, 1);
-    } else {
-      add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(p->B.get(), d, ld, 1.0);
-      SKR_LAUNCHED(&c);
-    }
     if (c.rank == 0) {
       reg_betas_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(p->Ut.get(), ld, d, k, p->D.get(), p->c, p->reg_coef,
                                                               p->betas.get() + ng);
@@ -2272,6 +2279,38 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     SKR_LAUNCHED(&c);
     floor_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096u), 256, 0, c.stream>>>(p->betas.get(), N, top.get());
     SKR_LAUNCHED(&c);
+    // the beta table is final: the sampling tables (two dependent fp64 chains over N,
+    // 158 ms at c5) build on the side stream while X~ and B are formed below
+    start_tables_async(p.get());
+    if (!S.sparse) DISPATCH_DTYPE(S.dtype, T, {
+      const T* Xp = static_cast<const T*>(S.ptr);
+      if (k > 0) {
+        auto xt = new_storage(c, S.dtype, n, d);
+        scale_cols_kernel<<<std::min<unsigned>(ceil_div(n * k, 256), 65535u), 256, 0, c.stream>>>(
+            P.get(), n, k, p->D.get(), p->c);
+        SKR_LAUNCHED(&c);
+        gemm<double, double, false, false>(&c, n, d, k, P.get(), k, p->Ut.get(), ld,
+                                           EpiXtilde<T>{Xp, static_cast<T*>(xt->ptr), ld, p->c}, 1);
+        p->xt = xt;
+      } else {
+        p->xt = X->st;  // identity: X~ = X exactly (c = 1)
+      }
+    });
+    if (!p->lazy) P.release();
+    // B = P^{-1/2} = c I + U (D - c) U^T  (d x ld); (the regulariser betas above)
+    p->B.alloc((size_t)d * ld, c.stream);
+    p->B.zero();
+    if (k > 0) {
+      DBuf<double> Us((size_t)k * ld, c.stream);
+      SKR_CUDA(cudaMemcpyAsync(Us.get(), p->Ut.get(), sizeof(double) * k * ld, cudaMemcpyDeviceToDevice, c.stream));
+      scale_rows_kernel<<<std::min<unsigned>(ceil_div(k * ld, 256), 65535u), 256, 0, c.stream>>>(Us.get(), k, ld,
+                                                                                                 p->D.get(), p->c);
+      SKR_LAUNCHED(&c);
+      gemm<double, double, true, false>(&c, d, d, k, Us.get(), ld, p->Ut.get(), ld, EpiBmat{p->B.get(), ld, p->c}, 1);
+    } else {
+      add_diag_kernel<<<ceil_div(d, 256), 256, 0, c.stream>>>(p->B.get(), d, ld, 1.0);
+      SKR_LAUNCHED(&c);
+    }
     DBuf<double> bsum(1, c.stream);
     sum_kernel<<<1, 1024, 0, c.stream>>>(p->betas.get(), N, bsum.get());
     SKR_LAUNCHED(&c);
@@ -2370,6 +2409,7 @@ int skr_problem_clone(const skr_problem* src, skr_ctx* ctx, skr_problem** out) {
     p->lazy = src->lazy;
     p->y_all = p->y.get();
     if (src->tables) {
+      if (src->tables_pending) SKR_CUDA(cudaStreamWaitEvent(c.stream, src->ev_tables, 0));
       copy(p->cum, src->cum);
       copy(p->inv_nq, src->inv_nq);
       copy(p->total, src->total);
