@@ -349,7 +349,10 @@ def run_ours(args, cfg):
     }
 
     if not args.no_extras:
-        out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
+        try:
+            out.update(solve_extras(args, cfg, sk, p, prob, sv, lanczos_s, precompute_s, ctx))
+        except Exception as e:  # the headline line must still print
+            out["svrg"] = {"error": repr(e)[:300]}
         if world == 1:
             out["lanczos_tf32"] = lanczos_tf32_extra(sk, ctx)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
