@@ -560,7 +560,13 @@ void start_tables_async(skr_problem* p) {
   if (!p->ev_tables) SKR_CUDA(cudaEventCreateWithFlags(&p->ev_tables, cudaEventDisableTiming));
   SKR_CUDA(cudaEventRecord(p->ev_tables, c.stream));  // the betas and the buffers above
   SKR_CUDA(cudaStreamWaitEvent(c.aux, p->ev_tables, 0));
-  cumulative_kernel<<<1, 512, 0, c.aux>>>(p->betas.get(), N, p->cum.get(), p->total.get());
+  // the two dependent chains are latency-bound: the CTA reserves its SM's shared memory
+  // (unused) so no GEMM CTA of the concurrent X~ product shares its issue slots
+  constexpr int kCumSmem = 180 * 1024;  // + its 32 KB of static tiles
+  configure_once((const void*)cumulative_kernel, [&] {
+    SKR_CUDA(cudaFuncSetAttribute(cumulative_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCumSmem));
+  });
+  cumulative_kernel<<<1, 512, kCumSmem, c.aux>>>(p->betas.get(), N, p->cum.get(), p->total.get());
   SKR_LAUNCHED(&c);
   inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.aux>>>(p->betas.get(), N, p->total.get(),
                                                                                p->inv_nq.get());
@@ -1289,8 +1295,18 @@ struct EpiXtilde {  // X~[m,n] = T(c X[m,n] + acc)   (ridge.cpp:133-149)
   T* Xt;
   int64_t ld;
   double c;
+  static constexpr bool kPair = true;  // columns n, n+1 in one 2-element access (n even, ld even)
   __device__ void operator()(int64_t m, int64_t n, double acc) const {
     Xt[m * ld + n] = (T)fma(c, (double)X[m * ld + n], acc);
+  }
+  __device__ void pair(int64_t m, int64_t n, double a0, double a1) const {
+    if constexpr (sizeof(T) == 4) {
+      const float2 x = *reinterpret_cast<const float2*>(X + m * ld + n);
+      *reinterpret_cast<float2*>(Xt + m * ld + n) = make_float2((float)fma(c, (double)x.x, a0), (float)fma(c, (double)x.y, a1));
+    } else {
+      const double2 x = *reinterpret_cast<const double2*>(X + m * ld + n);
+      *reinterpret_cast<double2*>(Xt + m * ld + n) = make_double2(fma(c, x.x, a0), fma(c, x.y, a1));
+    }
   }
 };
 struct EpiBmat {  // B[m,n] = acc + c [m == n]   (P^{-1/2} = c I + U (D - c) U^T)

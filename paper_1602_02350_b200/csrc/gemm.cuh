@@ -22,7 +22,13 @@ constexpr int GEMM_BK = 16, GEMM_THREADS = 256;
 template <class T>
 __device__ __forceinline__ double ld_as_double(const T* p) { return static_cast<double>(__ldg(p)); }
 
-// Epilogue receives the fp64 accumulator of one output element.
+// Epilogue receives the fp64 accumulator of one output element.  An epilogue with
+// `static constexpr bool kPair = true` also takes two adjacent columns (n even,
+// n + 1 < N) in one call, so it can use 2-element vector loads and stores.
+template <class E, class = void>
+struct epi_has_pair { static constexpr bool value = false; };
+template <class E>
+struct epi_has_pair<E, decltype((void)E::kPair)> { static constexpr bool value = E::kPair; };
 struct EpiStore {  // C = alpha*acc + beta*C  (beta ignored when 0)
   double* C;
   int64_t ldc;
@@ -232,7 +238,9 @@ bool gemm_tma(Ctx* ctx, int64_t M, int64_t N, int64_t K, const TA* A, int64_t ld
   if (M >= (1LL << 31) || N >= (1LL << 31) || K >= (1LL << 31)) return false;
   // small products, and products narrower than the 128 x 128 tile in M or N (the
   // register-staged kernel's 64 x 128 / 128 x 64 tiles waste less there)
-  if ((double)M * (double)N * (double)K < 3e8 || M < TG_BM || N < TG_BN) return false;
+  // and short K (the rank-k X~ product: with 1 CTA per SM the 3-4 stage ring never fills,
+  // while the register-staged kernel runs 2 CTAs per SM)
+  if ((double)M * (double)N * (double)K < 3e8 || M < TG_BM || N < TG_BN || K < 512) return false;
   constexpr int EA = 128 / (int)sizeof(TA), EB = 128 / (int)sizeof(TB);
   const CUtensorMap ma = AK ? make_tmap_2d(A, sizeof(TA), M, K, lda, TG_BM, EA, CU_TENSOR_MAP_SWIZZLE_128B)
                             : make_tmap_2d(A, sizeof(TA), K, M, lda, TG_BK, EA, CU_TENSOR_MAP_SWIZZLE_128B);

@@ -142,12 +142,18 @@ dgemm_tma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__
       if (m >= M) continue;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
+        const int64_t n = n0 + wn + 8 * j + 2 * fk;
+        if constexpr (!PARTIAL && epi_has_pair<Epi>::value) {
+          if (n + 1 < N) {  // n is even: one 2-element access for both columns
+            epi.pair(m, n, acc[i][j][0], acc[i][j][1]);
+            continue;
+          }
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int64_t n = n0 + wn + 8 * j + 2 * fk + h;
-          if (n >= N) continue;
-          if constexpr (PARTIAL) epi(m, n, acc[i][j][h], (int)blockIdx.z);
-          else epi(m, n, acc[i][j][h]);
+          if (n + h >= N) continue;
+          if constexpr (PARTIAL) epi(m, n + h, acc[i][j][h], (int)blockIdx.z);
+          else epi(m, n + h, acc[i][j][h]);
         }
       }
     }
