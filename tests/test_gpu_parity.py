@@ -402,6 +402,18 @@ def test_apply_modes_agree():
     assert rel(t_s, t_a) < 1e-8
 
 
+def test_dense_mode_scale_guard():
+    """ridge.cpp:110-113: explicit ApplyMode::Dense above kDenseModeMaxEntries (2e8) raises
+    ScaleGuardError; Auto (the device's choice) builds the problem."""
+    n, d = 200_704, 1000  # 2.007e8 entries
+    data = sk.DataMatrix.generate(sk.SynthSpec(n, d, "f32", 7, 0, 0.0, False, 0.1))
+    p = sk.RidgeProblem(data, data.labels(), 1e-3)
+    pc = sk.Preconditioner.identity(d, 1e-3)
+    with pytest.raises(sk.ScaleGuardError):
+        sk.preconditioned_components(p, pc, sk.ApplyMode.Dense)
+    assert sk.preconditioned_components(p, pc).mode() == sk.ApplyMode.Dense
+
+
 def test_reference_engine_drives_gpu_problem():
     """tests/cpp/drop_in_svrg: the UNMODIFIED reference svrg_solve (oracle/_ref)
     run on integration/skridge_gpu_problem.hpp's FiniteSumProblem vs on the
