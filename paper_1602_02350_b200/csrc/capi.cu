@@ -107,6 +107,7 @@ struct skr_problem {
   DBuf<double> B, y, y_all_buf, Ut, D, betas, cum, inv_nq, total;
   const double* y_all = nullptr;
   bool tables = false;
+  skr_ctx* own_ctx = nullptr;      // sparse data on a distributed context: the replicated problem's own context
   bool tables_pending = false;     // built on the side stream, ev_tables not yet waited on
   cudaEvent_t ev_tables = nullptr;
   // full-gradient workspace
@@ -2184,8 +2185,94 @@ int skr_problem_mode(const skr_problem* p, int* mode) {
   });
 }
 
+// Sparse data on a distributed context: the Lazy chain samples any row, so every rank
+// holds the whole problem.  The rank shards (CSR over points, labels) are gathered in
+// place on every rank and the problem is built on a private single-GPU context of the
+// same device; every call on it is then rank-local and identical on all ranks (the
+// sketch of the same data stays row-sharded on the distributed context).
+static int problem_create_replicated_sparse(skr_ctx* ctx, const skr_data* X, const double* y, double lambda,
+                                            const double* U, const double* sigma, int64_t k, skr_problem** out) {
+  skr_ctx* own = nullptr;
+  skr_data* full = nullptr;
+  const int rc = guard([&] {
+    Ctx& c = C_(ctx);
+    const Storage& S = *X->st;
+    const int64_t n = S.n, d = S.d, ng = X->n_global;
+    std::vector<int64_t> counts;
+    int64_t ngl = 0, r0 = 0;
+    shard_layout(c, n, &ngl, &r0, &counts);
+    // every rank's nnz
+    DBuf<int64_t> nz_send(1, c.stream), nz_all(c.world, c.stream);
+    SKR_CUDA(cudaMemcpyAsync(nz_send.get(), &S.nnz, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+    c.allgather_bytes(nz_send.get(), nz_all.get(), sizeof(int64_t));
+    std::vector<int64_t> nnz(c.world);
+    SKR_CUDA(cudaMemcpyAsync(nnz.data(), nz_all.get(), sizeof(int64_t) * c.world, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    int64_t nnz_tot = 0;
+    for (int64_t v : nnz) nnz_tot += v;
+    // row lengths, column indices, values and labels, each gathered in place by rank
+    DBuf<int64_t> rlen(std::max<int64_t>(ng, 1), c.stream);
+    DBuf<int32_t> cidx(std::max<int64_t>(nnz_tot, 1), c.stream);
+    DBuf<double> cval(std::max<int64_t>(nnz_tot, 1), c.stream), yall(std::max<int64_t>(ng, 1), c.stream);
+    std::vector<int64_t> hptr(n + 1);
+    if (n) SKR_CUDA(cudaMemcpyAsync(hptr.data(), S.rptr.get(), sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost,
+                                    c.stream));
+    c.sync();
+    std::vector<int64_t> hlen(std::max<int64_t>(n, 1));
+    for (int64_t i = 0; i < n; ++i) hlen[i] = hptr[i + 1] - hptr[i];
+    if (n) {
+      SKR_CUDA(cudaMemcpyAsync(rlen.get() + r0, hlen.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, c.stream));
+      SKR_CUDA(cudaMemcpyAsync(yall.get() + r0, y, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    }
+    std::vector<size_t> roff(c.world), rbyt(c.world), ioff(c.world), ibyt(c.world), voff(c.world), vbyt(c.world),
+        yoff(c.world), ybyt(c.world);
+    size_t ro = 0, zo = 0;
+    int64_t my_z = 0;
+    for (int r = 0; r < c.world; ++r) {
+      roff[r] = ro * sizeof(int64_t);
+      rbyt[r] = (size_t)counts[r] * sizeof(int64_t);
+      yoff[r] = ro * sizeof(double);
+      ybyt[r] = (size_t)counts[r] * sizeof(double);
+      ioff[r] = zo * sizeof(int32_t);
+      ibyt[r] = (size_t)nnz[r] * sizeof(int32_t);
+      voff[r] = zo * sizeof(double);
+      vbyt[r] = (size_t)nnz[r] * sizeof(double);
+      if (r == c.rank) my_z = (int64_t)zo;
+      ro += counts[r];
+      zo += nnz[r];
+    }
+    c.gather_in_place(rlen.get(), rlen.get() + r0, roff, rbyt);
+    c.gather_in_place(yall.get(), yall.get() + r0, yoff, ybyt);
+    c.gather_in_place(cidx.get(), S.ridx.get(), ioff, ibyt);
+    c.gather_in_place(cval.get(), S.rval.get(), voff, vbyt);
+    (void)my_z;
+    std::vector<int64_t> rl(std::max<int64_t>(ng, 1)), rp(ng + 1, 0);
+    std::vector<int32_t> hi(std::max<int64_t>(nnz_tot, 1));
+    std::vector<double> hv(std::max<int64_t>(nnz_tot, 1)), hy(std::max<int64_t>(ng, 1));
+    SKR_CUDA(cudaMemcpyAsync(rl.data(), rlen.get(), sizeof(int64_t) * ng, cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(hi.data(), cidx.get(), sizeof(int32_t) * nnz_tot, cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(hv.data(), cval.get(), sizeof(double) * nnz_tot, cudaMemcpyDeviceToHost, c.stream));
+    SKR_CUDA(cudaMemcpyAsync(hy.data(), yall.get(), sizeof(double) * ng, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    for (int64_t i = 0; i < ng; ++i) rp[i + 1] = rp[i] + rl[i];
+    int rc2 = skr_ctx_create(c.device, &own);
+    if (rc2 != SKR_OK) raise(rc2, skr_last_error());
+    rc2 = skr_data_create_csr(own, ng, d, rp.data(), hi.data(), hv.data(), &full);
+    if (rc2 != SKR_OK) raise(rc2, skr_last_error());
+    rc2 = skr_problem_create(own, full, hy.data(), lambda, U, sigma, k, out);
+    if (rc2 != SKR_OK) raise(rc2, skr_last_error());
+    (*out)->own_ctx = own;
+    own = nullptr;
+  });
+  if (full) skr_data_destroy(full);  // the problem keeps the storage it needs (shared)
+  if (own) skr_ctx_destroy(own);     // only on failure
+  return rc;
+}
+
 int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double lambda, const double* U,
                        const double* sigma, int64_t k, skr_problem** out) {
+  if (ctx && X && out && X->st && X->st->sparse && ctx->c.dist)
+    return problem_create_replicated_sparse(ctx, X, y, lambda, U, sigma, k, out);
   return guard([&] {
     Ctx& c = C_(ctx);
     if (!X || !out) raise(SKR_EPARAM, "null argument");
@@ -2241,7 +2328,6 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     if (S.sparse) {
       // Lazy mode (ridge.cpp:104-113 picks it for large n d; here for every sparse
       // input): P = X U^T by SpMM, betas from ||x_i||^2 and P, no X~
-      if (c.world != 1) raise(SKR_EPARAM, "sparse data: preconditioned problems run on one GPU");
       if (k > 0 && n > 0) {
         DBuf<double> UT((size_t)d * k, c.stream);
         transpose_f64(c, p->Ut.get(), k, d, ld, UT.get(), k);
@@ -2449,7 +2535,9 @@ int skr_problem_destroy(skr_problem* p) {
   return guard([&] {
     if (!p) return;
     cudaStreamSynchronize(p->ctx->c.stream);
+    skr_ctx* own = p->own_ctx;
     delete p;
+    if (own) skr_ctx_destroy(own);  // after the problem: its buffers free on that context's stream
   });
 }
 

@@ -717,6 +717,35 @@ def test_distributed_code_path_on_one_gpu_matches(O):
     assert rel(a[4], b[4]) < 1e-12 and abs(a[5] - b[5]) <= 1e-13 * abs(a[5])
 
 
+def test_distributed_sparse_problem_on_one_gpu_matches():
+    """Sparse data on a distributed context: the sketch runs row-sharded, the Lazy problem
+    is gathered in place and replicated on a private context of each rank (the chain
+    samples every row); as a 1-rank NCCL job it must reproduce the single-GPU run bit for
+    bit (same data, same private single-GPU code path)."""
+    import scipy.sparse as spm
+    rng = np.random.default_rng(8)
+    n, d, k, lam = 900, 300, 6, 1e-3
+    A = spm.random(n, d, density=0.05, format="csr", random_state=4, data_rvs=rng.standard_normal)
+    A = A + spm.csr_matrix((rng.standard_normal(n), (np.arange(n), rng.integers(0, d, n))), shape=(n, d))
+    A.sum_duplicates()
+    A.eliminate_zeros()
+    y = rng.standard_normal(n)
+    ctx1 = sk.Context(0, 0, 1, sk.Context.nccl_unique_id())
+    res = {}
+    for name, ctx in (("single", sk.default_context()), ("dist", ctx1)):
+        p = sk.RidgeProblem(sk.DataMatrix.from_scipy(A, ctx=ctx), y, lam)
+        sv = sk.block_lanczos(sk.scaled_design(p), sk.LanczosConfig(k, 0.5, 3, 3), want_right=False)
+        pg = sk.preconditioned_components(p, sk.build_sketched(sv, lam))
+        assert pg.mode() == sk.ApplyMode.Lazy
+        eta = configs.step_size(pg.max_row_sq())
+        w = np.random.default_rng(2).standard_normal(d)
+        tr = sk.svrg_solve(pg, sk.SvrgConfig(3, 2 * n, eta, 9), np.zeros(d)).trace
+        res[name] = (sv.singular_values, pg.betas(), pg.full_gradient(w), [r.objective for r in tr])
+    a, b = res["single"], res["dist"]
+    assert rel(a[0], b[0]) < 1e-14
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3]
+
+
 @pytest.mark.parametrize("name,dtype", [("c3", "f32"), ("c3", "f64"), ("c5", "f32"), ("c2", "f64")])
 def test_svrg_chain_bitwise_deterministic(name, dtype):
     """The s-step chain (one thread-block cluster of up to 16 CTAs exchanging partial
