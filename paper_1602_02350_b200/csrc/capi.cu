@@ -1,6 +1,21 @@
 // C-ABI implementation (include/skr.h): the host runtime that orders the
 // hot-path kernels on the context stream, owns device memory, and runs the
 // row-sharded collectives.  All reference citations are relative to proj/.
+//
+// One translation unit on purpose: every kernel template is instantiated once,
+// in whole-program device compilation, next to the launch that picks its
+// parameters.  The kernels themselves live in the headers (fullgrad.cuh: K9,
+// sstep.cuh: K10, gemm.cuh / gemm_tma.cuh: DMMA, tc_gemm.cuh: tcgen05, rng.cuh /
+// mt_jump.cuh: the reference streams, sparse.cuh: CSR paths, lanczos.cuh,
+// svrg.cuh); this file holds, in order:
+//   * handles and internal state ........ skr_ctx / Storage / skr_data / skr_problem
+//   * host orchestration (namespace {}) . shard layout, K9 dispatch, sampling tables,
+//                                          MT streams, index draws, Rayleigh-Ritz
+//                                          checks, tcgen05 host side, K10 dispatch,
+//                                          small elementwise kernels and epilogues
+//   * extern "C" entry points ........... context, data, block_lanczos, preconditioned
+//                                          components, full gradient / SVRG, diagnostics,
+//                                          reference_minimum (Cholesky and CG)
 #include <cmath>
 #include <chrono>
 #include <cstring>
