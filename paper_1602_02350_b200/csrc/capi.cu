@@ -129,7 +129,7 @@ struct skr_problem {
   int fg_grid = 0;
   DBuf<double> part_g, part_loss, sums, uw, half, uh, pinv, wv, muv, objv;
   DBuf<MtState> mt;
-  DBuf<double> s_state, s_M, s_p, s_X, s_pk;  // s-step inner loop workspaces (s_pk: packed rows)
+  DBuf<double> s_state, s_M, s_p, s_X, s_pk, s_vec;  // s-step inner loop workspaces (s_pk: packed rows)
   // Lazy mode (sparse data): X~ is never materialised; Pm = X U^T (n x k) and workspaces
   bool lazy = false;
   DBuf<double> Pm, lz_r, lz_r2, lz_s, lz_g1, lz_g2, lz_v, lz_loss, lz_UT;
@@ -833,13 +833,13 @@ void tc_launch_cs(Ctx& c, const CUtensorMap& ma, const float* Bh, const float* B
   // CS > 1: each CTA of a cluster loads BN / CS rows of B and multicasts them
   const CUtensorMap mbh = make_tmap_f32(Bh, g.N, g.K, ldb, BN / CS);
   const CUtensorMap mbl = make_tmap_f32(Bl, g.N, g.K, ldb, BN / CS);
-  constexpr size_t smem = tc_gemm_smem<BN>();
+  constexpr size_t smem = tc_gemm_smem<A_MN, BN>();
   auto kern = tc_gemm_tf32x3_kernel<A_MN, BN, CS>;
   configure_once((const void*)kern,
                  [&] { SKR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(ceil_div(g.M, TC_BM) * ceil_div(g.N, BN)), 1, splits);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads<A_MN, BN>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute attr[1];
@@ -985,8 +985,18 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     p->s_pk.zero();
   }
   auto prep = sstep_prep_kernel<T, L>;
+  auto pack = sstep_pack_kernel<T, L>;
+  auto gram = sstep_gram_kernel<L, 2>;
   auto chain = sstep_chain_kernel<SW, L>;
   constexpr size_t prep_smem = sstep_prep_smem<L>();
+  // PREP v2 (PACK + GRAM): ring of nstg stages of one column slice of the staged blocks
+  static const bool prep_v1 = getenv("SKR_PREP_V1") != nullptr;
+  using GC = GramCfg<L, 2>;
+  const size_t gstage = GC::stage_bytes(SW);
+  const int nstg = (int)std::max<size_t>(2, std::min<size_t>(std::min<size_t>(4, (size_t)CS), (200 * 1024) / gstage));
+  const size_t gram_smem = std::max((size_t)nstg * gstage, GC::epi_bytes());
+  if (gram_smem > 226 * 1024) raise(SKR_EDIM, "svrg: GRAM stage ring exceeds shared memory");
+  if (p->s_vec.n < (size_t)2 * CS * SW) p->s_vec.alloc((size_t)2 * CS * SW, c.stream);
   // The chain CTA reserves its SM's whole shared memory: otherwise PREP CTAs of
   // the next chunk (side stream) co-reside on the chain's 16 SMs and compete for
   // issue slots, the FP64 pipe and shared-memory bandwidth.
@@ -994,12 +1004,16 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   constexpr size_t chain_smem = 227 * 1024;
   configure_once((const void*)chain, [&] {
     SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
+    SKR_CUDA(cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   });
   SstepRows rows{p->xt_all, p->B.get(), ld, p->d, p->n_global};
   const PackGeom pg{CS, SW};
   sstep_init_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, ld, p->s_state.get());
+  SKR_LAUNCHED(&c);
+  const int64_t vw = (int64_t)CS * SW;
+  sstep_padvec_kernel<<<ceil_div(vw, 256), 256, 0, c.stream>>>(mu, snap, p->d, vw, p->s_vec.get());
   SKR_LAUNCHED(&c);
   // chunks of kSstepChunkBlocks blocks: prep(i+1) runs on the side stream (all
   // free SMs) while chain(i) runs on the main stream; M/p/X/packed rows are
@@ -1022,9 +1036,18 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     const int64_t nblk = (steps + L - 1) / L;
     if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
     const int64_t pgrid = c.prep_cap > 0 ? std::min<int64_t>(nblk, c.prep_cap) : nblk;
-    prep<<<(unsigned)pgrid, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
-                                                     p->reg_coef, mu, snap, eta, Mb, pb, Xb, pkb, pg);
-    SKR_LAUNCHED(&c);
+    if (prep_v1) {
+      prep<<<(unsigned)pgrid, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
+                                                       p->reg_coef, mu, snap, eta, Mb, pb, Xb, pkb, pg);
+      SKR_LAUNCHED(&c);
+    } else {
+      pack<<<(unsigned)pgrid, 256, 0, c.aux>>>(rows, idx + s0, steps, pkb, pg);
+      SKR_LAUNCHED(&c);
+      gram<<<(unsigned)pgrid, 256, gram_smem, c.aux>>>(pkb, pg, nstg, idx + s0, steps, p->n_global, p->inv_nq.get(),
+                                                       p->data_coef, p->reg_coef, p->s_vec.get(),
+                                                       p->s_vec.get() + vw, ld, eta, Mb, pb, Xb, nullptr);
+      SKR_LAUNCHED(&c);
+    }
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
     SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
     ChainArgs ca{pkb, steps, Mb, pb, Xb, mu, ld, eta, p->s_state.get(), dprof};

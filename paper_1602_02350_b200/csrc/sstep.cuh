@@ -200,6 +200,255 @@ constexpr size_t sstep_prep_smem() {
 }
 
 // ---------------------------------------------------------------------------
+// PREP v2 = PACK + GRAM (round 2).  The one-kernel PREP above issues one
+// dependent gather per 32-column chunk (64-128 global round trips per block,
+// ~5 B/clk/SM in flight): 0.81 ms per 1024 blocks at c3, as long as the chain
+// it is supposed to hide behind.  v2 splits it:
+//  * PACK (all SMs, many independent 16-byte loads in flight): gathers every
+//    sampled row ONCE, widens it to fp64 and writes it to the packed buffer
+//    pk[block][chain CTA][l][SW] (the layout the chain's bulk copies want);
+//  * GRAM: one CTA per block reads the packed tiles of blocks b, b-1 (, b-2)
+//    back with bulk copies (an NSTG-stage ring over the CS column slices, no
+//    register staging) and runs the DMMA products R_b [R_b; R_{b-1}; ..; mu;
+//    wbar]^T from shared memory, then the small triangular solve and products.
+// Fragment loads straight from the XOR-swizzled tiles are conflict-free when a
+// k-step of the m8n8k4 product takes the four columns {c, c+4, c+8, c+12} of a
+// 16-column group (any fixed order of the columns gives the same dot products).
+template <class E>
+__device__ __forceinline__ void pack_row(const E* __restrict__ src, int l, double* __restrict__ pkb, PackGeom pg,
+                                         int L, int64_t d, int64_t ld, int lane) {
+  constexpr int VE = 16 / (int)sizeof(E);  // elements per 16-byte load
+  const int x = l & 15;
+  constexpr int UN = 4;
+  for (int64_t c0 = (int64_t)lane * VE; c0 < ld; c0 += 32 * VE * UN) {
+    int4 raw[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int64_t c = c0 + (int64_t)u * 32 * VE;
+      raw[u] = make_int4(0, 0, 0, 0);
+      if (src && c < ld) raw[u] = __ldg(reinterpret_cast<const int4*>(src + c));
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int64_t c = c0 + (int64_t)u * 32 * VE;
+      if (c >= ld) continue;
+      double v[VE], o[VE];
+      const E* e = reinterpret_cast<const E*>(&raw[u]);
+#pragma unroll
+      for (int q = 0; q < VE; ++q) v[q] = c + q < d ? (double)e[q] : 0.0;
+#pragma unroll
+      for (int q = 0; q < VE; ++q) o[q] = v[q ^ (x & (VE - 1))];  // o[q ^ m] = v[q]
+      const int64_t slice = c / pg.sw;
+      const int j0 = (int)(c % pg.sw) ^ (x & ~(VE - 1));
+      double* dst = pkb + ((size_t)slice * L + l) * pg.sw + j0;
+#pragma unroll
+      for (int q = 0; q < VE; q += 2) *reinterpret_cast<double2*>(dst + q) = make_double2(o[q], o[q + 1]);
+    }
+  }
+}
+
+template <class T, int L>
+__global__ void __launch_bounds__(256)
+sstep_pack_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, double* __restrict__ pk, PackGeom pg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nblk = (steps + L - 1) / L;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    double* pkb = pk + (size_t)blk * pg.cs * L * pg.sw;
+    for (int l = warp; l < L; l += 8) {
+      const int64_t t = blk * L + l;
+      const int64_t i = t < steps ? idx[t] : -1;
+      if (i >= 0 && i < R.n)
+        pack_row<T>(static_cast<const T*>(R.Xt) + i * R.ld, l, pkb, pg, L, R.d, R.ld, lane);
+      else  // regulariser component, or a padded step (zero row)
+        pack_row<double>(i < 0 ? nullptr : R.B + (i - R.n) * R.ld, l, pkb, pg, L, R.d, R.ld, lane);
+    }
+  }
+}
+
+// Output layout of DEPTH = 3 (chain v7), per block MX7<L>::W doubles:
+//   [M | Y1 | Y2] each L x L "lane-major pairs": A[i][k] at (k >> 1) * 2L + 2i + (k & 1), so lane i
+//   reads its row with 16-byte loads, conflict-free; then p'' (L).
+template <int L>
+struct MX7 {
+  static constexpr int W = 3 * L * L + L;
+};
+__host__ __device__ __forceinline__ int lm_pair(int L, int i, int k) { return (k >> 1) * 2 * L + 2 * i + (k & 1); }
+
+template <int L, int DEPTH>
+struct GramCfg {
+  static constexpr int NRB = DEPTH * L;          // staged block rows
+  static constexpr int NTN = NRB / 8 + 1;        // n-tiles: block rows, then [mu; wbar; 0...]
+  static constexpr int MT = L / 8;               // m-tiles
+  static constexpr int STEP = 8 / MT;            // warps per m-tile
+  static constexpr int NJ = (NTN + STEP - 1) / STEP;
+  static constexpr int RS = NRB + 3;             // result row stride (odd: conflict-free column reads)
+  static constexpr size_t stage_bytes(int sw) { return sizeof(double) * ((size_t)NRB * sw + 2 * sw); }
+  static constexpr size_t epi_bytes() { return sizeof(double) * ((size_t)L * RS + 3 * (size_t)L * (L + 1) + L); }
+};
+
+// idx: this chunk's step indices; pk: this chunk's packed rows; outputs as the chain of the same DEPTH reads
+// them (DEPTH 2: Mout/pout/Xout as PREP v1; DEPTH 3: MXout, MX7 layout).
+template <int L, int DEPTH>
+__global__ void __launch_bounds__(256, 1)
+sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const int64_t* __restrict__ idx, int64_t steps,
+                  int64_t n_data, const double* __restrict__ inv_nq, double data_coef, double reg_coef,
+                  const double* __restrict__ mu, const double* __restrict__ wbar, int64_t ld, double eta,
+                  double* __restrict__ Mout, double* __restrict__ pout, double* __restrict__ Xout,
+                  double* __restrict__ MXout) {
+  using G = GramCfg<L, DEPTH>;
+  constexpr int NRB = G::NRB, NTN = G::NTN, MT = G::MT, STEP = G::STEP, NJ = G::NJ, RS = G::RS;
+  static_assert(L == 16 || L == 32, "L = 16 or 32");
+  static_assert(DEPTH == 2 || DEPTH == 3, "look-ahead depth");
+  extern __shared__ __align__(128) unsigned char gsm[];
+  __shared__ __align__(8) uint64_t full[4];
+  __shared__ double cvec[L];
+  const int SW = pg.sw, CS = pg.cs;
+  const size_t stage_d = (size_t)NRB * SW + 2 * SW;  // doubles per stage
+  double* stg = reinterpret_cast<double*>(gsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mt = warp % MT, nb = warp / MT;
+  const int64_t nblk = (steps + L - 1) / L;
+  if (tid == 0) {
+    for (int s = 0; s < 4; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t issued = 0, waited = 0;  // stage uses so far (ring position and phase parity)
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int nprev = (int)min((int64_t)(DEPTH - 1), blk);  // previous blocks of this launch that exist
+    if (tid < L) {
+      const int64_t t = blk * L + tid;
+      const int64_t i = t < steps ? idx[t] : -1;
+      cvec[tid] = i < 0 ? 0.0 : (i < n_data ? data_coef : reg_coef) * inv_nq[i];
+    }
+    auto issue = [&](int s) {  // slice s of blocks blk, blk-1, .. and of mu, wbar -> ring slot
+      const int slot = (int)(issued % (uint32_t)nstg);
+      double* dst = stg + (size_t)slot * stage_d;
+      const uint32_t tile_bytes = (uint32_t)(L * SW * 8), vec_bytes = (uint32_t)(SW * 8);
+      mbar_expect_tx(&full[slot], (uint32_t)(1 + nprev) * tile_bytes + 2 * vec_bytes);
+      for (int q = 0; q <= nprev; ++q)
+        bulk_g2s(dst + (size_t)q * L * SW, pk + ((size_t)(blk - q) * CS + s) * L * SW, tile_bytes, &full[slot]);
+      bulk_g2s(dst + (size_t)NRB * SW, mu + (size_t)s * SW, vec_bytes, &full[slot]);
+      bulk_g2s(dst + (size_t)NRB * SW + SW, wbar + (size_t)s * SW, vec_bytes, &full[slot]);
+      ++issued;
+    };
+    if (tid == 0) {
+      // the ring was last touched through the generic proxy (the previous block's results)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int s = 0; s < nstg - 1 && s < CS; ++s) issue(s);
+    }
+    double acc[NJ][2] = {};
+    // per-lane fragment geometry: row r8 = lane >> 2 of an 8-row tile, k index t4 = lane & 3
+    const int r8 = lane >> 2, t4 = lane & 3;
+    const int la = 8 * mt + r8;  // A row (block b)
+    for (int s = 0; s < CS; ++s) {
+      if (tid == 0 && s + nstg - 1 < CS) issue(s + nstg - 1);
+      const int slot = (int)(waited % (uint32_t)nstg);
+      mbar_wait(&full[slot], (waited / (uint32_t)nstg) & 1u);
+      ++waited;
+      const double* st = stg + (size_t)slot * stage_d;
+      const double* arow = st + (size_t)la * SW;
+      const int ax = la & 15;
+      for (int g16 = 0; g16 < SW; g16 += 16) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = g16 + c + 4 * t4;  // this lane's column of the k-step {c, c+4, c+8, c+12}
+          const double a = arow[j ^ ax];
+#pragma unroll
+          for (int q = 0; q < NJ; ++q) {
+            const int nt = nb + STEP * q;
+            if (nt < NTN - 1) {
+              const int rr = 8 * nt + r8, lb = rr % L;
+              if (rr / L <= nprev)  // warp-uniform: a tile covers rows of one block (L % 8 == 0)
+                dmma_884(acc[q][0], acc[q][1], a, st[(size_t)rr * SW + (j ^ (lb & 15))]);
+            } else if (nt == NTN - 1) {
+              const double bv = r8 < 2 ? st[(size_t)NRB * SW + (size_t)r8 * SW + j] : 0.0;
+              dmma_884(acc[q][0], acc[q][1], a, bv);
+            }
+          }
+        }
+      }
+      __syncthreads();  // the slot may be refilled
+    }
+    // ---- results: res[i * RS + n], n < L: G; L..2L: X1; (2L..3L: X2); NRB: e; NRB + 1: b ----
+    double* res = stg;                                   // aliases ring slot 0.. (all stages consumed)
+    double* Ti = res + (size_t)L * RS;                   // [L][L+1] T^{-1}, then M
+    double* W1 = Ti + (size_t)L * (L + 1);               // [L][L+1] scratch (Y1)
+    double* W2 = W1 + (size_t)L * (L + 1);               // [L][L+1] scratch (Y2)
+    double* pv = W2 + (size_t)L * (L + 1);               // [L]
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      const int nt = nb + STEP * q;
+      if (nt < NTN) {
+        const int i = 8 * mt + r8, n = 8 * nt + 2 * t4;
+        if (n < RS - 1) {
+          res[i * RS + n] = acc[q][0];
+          res[i * RS + n + 1] = acc[q][1];
+        }
+      }
+    }
+    __syncthreads();
+    // T = I + eta C G_strict (unit lower); column j of T^{-1} by forward substitution (thread j)
+    if (tid < L) {
+      const int j = tid;
+      for (int i = 0; i < L; ++i) Ti[i * (L + 1) + j] = i == j ? 1.0 : 0.0;
+      for (int i = j + 1; i < L; ++i) {
+        double sacc = 0.0;
+        for (int k2 = j; k2 < i; ++k2) sacc = fma(res[i * RS + k2], Ti[k2 * (L + 1) + j], sacc);
+        Ti[i * (L + 1) + j] = -eta * cvec[i] * sacc;
+      }
+      // p_j = eta j e_j + b_j (0-based j), + eta L nprev e_j: the dots of this block were taken nprev blocks early
+      pv[j] = eta * (double)(j + L * nprev) * res[j * RS + NRB] + res[j * RS + NRB + 1];
+    }
+    __syncthreads();
+    for (int e = tid; e < L * L; e += 256) {  // M = T^{-1} C in place
+      const int i = e / L, j = e % L;
+      Ti[i * (L + 1) + j] *= cvec[j];
+    }
+    __syncthreads();
+    if (DEPTH == 2) {
+      double* Mb = Mout + (int64_t)blk * L * L;
+      for (int e = tid; e < L * L; e += 256) Mb[e] = Ti[(e % L) * (L + 1) + e / L];  // transposed
+      if (nprev >= 1) {
+        double* Xb = Xout + (int64_t)blk * L * L;
+        for (int e = tid; e < L * L; e += 256) Xb[e] = res[(e % L) * RS + L + e / L];
+      }
+      if (tid < L) pout[(int64_t)blk * L + tid] = pv[tid];
+    } else {
+      double* out = MXout + (int64_t)blk * MX7<L>::W;
+      // Y_q = eta M X_q (zero when block b - q is not in this launch), p'' = M p
+      for (int e = tid; e < 2 * L * L; e += 256) {
+        const int q = e / (L * L), i = (e / L) % L, k = e % L;
+        double y = 0.0;
+        if (q < nprev) {
+          const double* xq = res + (size_t)(q + 1) * L + k;
+          for (int j = 0; j <= i; ++j) y = fma(Ti[i * (L + 1) + j], xq[j * RS], y);
+          y *= eta;
+        }
+        out[(size_t)(q + 1) * L * L + lm_pair(L, i, k)] = y;
+      }
+      for (int e = tid; e < L * L; e += 256) out[lm_pair(L, e / L, e % L)] = Ti[(e / L) * (L + 1) + e % L];
+      if (tid < L) {
+        double y = 0.0;
+        for (int j = 0; j <= tid; ++j) y = fma(Ti[tid * (L + 1) + j], pv[j], y);
+        out[3 * L * L + tid] = y;
+      }
+    }
+    __syncthreads();  // results alias the ring: done before the next block's copies land
+  }
+}
+
+// mu and wbar zero-padded to the chain's CS * SW columns (GRAM bulk-copies whole slices)
+__global__ void sstep_padvec_kernel(const double* __restrict__ mu, const double* __restrict__ wbar, int64_t d,
+                                    int64_t width, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < width) {
+    out[j] = j < d ? mu[j] : 0.0;
+    out[width + j] = j < d ? wbar[j] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CHAIN (v3): one cluster of CS CTAs; CTA r owns columns [r*SW, r*SW + SW).
 // Roles per CTA (warps): NDW dot warps | NUW = SW/32 update warps | one delta
 // warp | one producer warp.
@@ -252,7 +501,7 @@ template <int SW, int L>
 struct ChainCfg {
   static constexpr int NUW = SW / 32;                   // update warps (one column per thread)
   static constexpr int NDW = SW * L / 1024;             // dot warps: 32 columns per dot lane
-  static constexpr int NT = 32 * (NDW + NUW) + 64;      // + delta warp + producer warp
+  static constexpr int NT = 32 * (NDW + NUW) + 96;      // + delta warp + producer warp + sender warp
   static constexpr int NB = SW * L * 8 <= 16384 ? 4 : SW * L * 8 <= 32768 ? 3 : 2;  // row ring depth (smem budget)
   static constexpr int NMX = 2;                         // M/X/p ring depth
   static constexpr int MXW = 2 * L * L + L;             // doubles per M/X/p slot
@@ -260,7 +509,7 @@ struct ChainCfg {
   static constexpr size_t smem() {
     return sizeof(double) * ((size_t)NB * L * SW + (size_t)NMX * MXW + (size_t)NPS * 16 * L + 4 * L + L +
                              2 * NDW * L + 2 * SW) +
-           sizeof(uint64_t) * (2 * NB + 2 * NMX + NPS + 2 + 2) + 128;
+           sizeof(uint64_t) * (2 * NB + 2 * NMX + NPS + 2 + 2 + 2) + 128;
   }
 };
 
@@ -276,6 +525,30 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "WAITC_%=:\n"
       "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Non-suspending waits for the hand-offs on the chain's dependent cycle (try_wait may park
+// the warp; a parked warp resumes some hundred cycles after the phase completes).
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "SPIN_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra SPIN_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_spin_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "SPINC_%=:\n"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra SPINC_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -305,7 +578,7 @@ template <int SW, int L>
 __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(ChainArgs a) {
   using Cf = ChainCfg<SW, L>;
   constexpr int NUW = Cf::NUW, NDW = Cf::NDW, NB = Cf::NB, NMX = Cf::NMX, MXW = Cf::MXW, NPS = Cf::NPS;
-  constexpr int WU0 = NDW, WDL = NDW + NUW, WPR = NDW + NUW + 1;  // first update warp, delta warp, producer
+  constexpr int WU0 = NDW, WDL = NDW + NUW, WPR = NDW + NUW + 1, WSN = NDW + NUW + 2;  // update, delta, producer, sender
   static_assert(L == 16 || L == 32, "lanes = rows in the dots");
   static_assert(SW >= 32 && SW % 32 == 0, "slice width");
   extern __shared__ __align__(128) unsigned char sm[];
@@ -322,7 +595,8 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
   uint64_t* mx_full = empty + NB;                               // [NMX]
   uint64_t* mx_empty = mx_full + NMX;                           // [NMX]
   uint64_t* part = mx_empty + NMX;                              // [NPS] partials (complete_tx)
-  uint64_t* dready = part + NPS;                                // [2] delta_b published (local)
+  uint64_t* dotdone = part + NPS;                               // [2] the dot warps' partials of a block are in dpart
+  uint64_t* dready = dotdone + 2;                               // [2] delta_b published (local)
   uint64_t* wready = dready + 2;                                // [2] w_b written, by parity
 
   cg::cluster_group cluster = cg::this_cluster();
@@ -334,13 +608,15 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&empty[q], NUW);
+      mbar_init(&empty[q], NUW + NDW);  // update warps (column in registers) and dot warps (dots done)
     }
     for (int q = 0; q < NMX; ++q) {
       mbar_init(&mx_full[q], 1);
       mbar_init(&mx_empty[q], 1);
     }
     for (int q = 0; q < NPS; ++q) mbar_init(&part[q], 1);  // the receiver's own arming arrive
+    mbar_init(&dotdone[0], NDW);
+    mbar_init(&dotdone[1], NDW);
     mbar_init(&dready[0], 1);
     mbar_init(&dready[1], 1);
     mbar_init(&wready[0], NUW);
@@ -412,7 +688,7 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
       }
       const int ps4 = (int)(b % NPS);
       const unsigned long long w0 = prof ? clock64() : 0;
-      mbar_wait_cluster(&part[ps4], (uint32_t)((b / NPS) & 1));
+      mbar_spin_cluster(&part[ps4], (uint32_t)((b / NPS) & 1));
       if (prof) t_wait += clock64() - w0;
       if (lane == 0) chain_trace(a.prof, cr, b, 2);
       if (i < L) {
@@ -465,20 +741,12 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
     int off[16];
 #pragma unroll
     for (int jj = 0; jj < 16; ++jj) off[jj] = jj ^ (l & 15);
-    // remote addresses of this lane's partial in every rank (slot 0), and of part[0]
-    uint32_t rdst[16], rbar[16];
-    const uint32_t ldst = smem_u32(apub + (size_t)cr * L + l), lbar = smem_u32(&part[0]);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      rdst[q] = q < CS ? mapa_u32(ldst, (uint32_t)q) : 0u;
-      rbar[q] = q < CS ? mapa_u32(lbar, (uint32_t)q) : 0u;
-    }
     const bool prof = a.prof && cr == 0 && tid == 0;
     unsigned long long tw = 0, td = 0;
     for (int64_t bb = 0; bb < nblk; ++bb) {  // dots(bb) against w_{bb-1} (w_0 for bb = 0)
       const int s = (int)(bb % NB);
       const unsigned long long q0 = prof ? clock64() : 0;
-      if (bb >= 2) mbar_wait(&wready[(bb - 1) & 1], (uint32_t)(((bb - 2) >> 1) & 1));  // w_{bb-1} written
+      if (bb >= 2) mbar_spin(&wready[(bb - 1) & 1], (uint32_t)(((bb - 2) >> 1) & 1));  // w_{bb-1} written
       mbar_wait(&full[s], (uint32_t)((bb / NB) & 1));
       const unsigned long long q1 = prof ? clock64() : 0;
       if (warp == 0 && lane == 0) chain_trace(a.prof, cr, bb, 0);
@@ -495,24 +763,17 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
         }
       }
       double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[s]);  // this warp's reads of rows[s] are done
       if constexpr (HALVES == 2) v += __shfl_xor_sync(0xffffffffu, v, 16);
-      if constexpr (NDW > 1) {
-        // the dot warps' partials of the same rows meet in shared memory (by parity)
-        double* dp = dpart + (size_t)(bb & 1) * NDW * L;
-        if (lane < L) dp[warp * L + l] = v;
-        named_bar(2, 32 * NDW);
-        if (warp == 0 && lane < L) {
-          v = dp[l];
-#pragma unroll
-          for (int k = 1; k < NDW; ++k) v += dp[k * L + l];
-        }
-      }
-      if (warp == 0 && lane < L) {
-        const uint32_t off_s = (uint32_t)((bb % NPS) * 16 * L * 8), boff = (uint32_t)((bb % NPS) * 8);
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (q < CS) st_async_f64(rdst[q] + off_s, rbar[q] + boff, v);
-        if (lane == 0) chain_trace(a.prof, cr, bb, 1);
+      // hand the warp's row partials to the sender warp (by block parity): dots(bb + 2) needs
+      // delta_bb, hence this rank's partials of block bb on every rank, so the sender has read
+      // dpart[bb & 1] before it is rewritten
+      if (lane < L) dpart[(size_t)(bb & 1) * NDW * L + warp * L + l] = v;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_local(&dotdone[bb & 1]);
+        if (warp == 0) chain_trace(a.prof, cr, bb, 1);
       }
       if (prof) {
         const unsigned long long q2 = clock64();
@@ -523,6 +784,31 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
     if (prof) {
       atomicAdd(a.prof + 0, td);
       atomicAdd(a.prof + 5, tw);
+    }
+  } else if (warp == WSN) {
+    // ---------------- sender warp: lane l pushes row l's partial to every rank ----------------
+    // (its own warp: the 16 L remote stores of a block keep their issuer ~1 K cycles in the
+    // outbound queue, time the dot warps now spend on the next block)
+    uint32_t rdst[16], rbar[16];
+    const int l = lane % L;
+    const uint32_t ldst = smem_u32(apub + (size_t)cr * L + l), lbar = smem_u32(&part[0]);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      rdst[q] = q < CS ? mapa_u32(ldst, (uint32_t)q) : 0u;
+      rbar[q] = q < CS ? mapa_u32(lbar, (uint32_t)q) : 0u;
+    }
+    for (int64_t bb = 0; bb < nblk; ++bb) {
+      mbar_spin(&dotdone[bb & 1], (uint32_t)((bb >> 1) & 1));
+      if (lane < L) {
+        const double* dp = dpart + (size_t)(bb & 1) * NDW * L + l;
+        double v = dp[0];
+#pragma unroll
+        for (int k = 1; k < NDW; ++k) v += dp[k * L];
+        const uint32_t off_s = (uint32_t)((bb % NPS) * 16 * L * 8), boff = (uint32_t)((bb % NPS) * 8);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < CS) st_async_f64(rdst[q] + off_s, rbar[q] + boff, v);
+      }
     }
   } else {
     // ---------------- update warps: thread t owns column slice0 + t ----------------
@@ -541,41 +827,68 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
       const int s = (int)(b % NB);
       const int Lb = (int)min((int64_t)L, a.steps - b * L);
       const unsigned long long c0 = prof ? clock64() : 0;
-      mbar_wait(&dready[b & 1], (uint32_t)((b >> 1) & 1));
-      const unsigned long long c1 = prof ? clock64() : 0;
-      if (t == 0) chain_trace(a.prof, cr, b, 4);
       // w <- w0 - eta R^T delta - eta Lb mu ; S += Lb w0 - eta R^T((Lb-l+1) delta) - eta mu Lb(Lb+1)/2
+      // The column of the block's rows goes to registers BEFORE delta_b is known (the rows
+      // landed for dots(b)), the slot is released at once, and only the w half of the update
+      // sits between delta_b and w_{b+1}; the running sum follows off the dependent cycle.
       const double* rb = rows + (size_t)s * L * SW;
       const double* dd = dl + (b & 1) * L;
       const double* ee = d2 + (b & 1) * L;
-      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      double u, vv;
+      unsigned long long c1 = 0;
       if (Lb == L) {
+        double xr[L];
+        mbar_wait(&full[s], (uint32_t)((b / NB) & 1));
+#pragma unroll
+        for (int l = 0; l < L; ++l) xr[l] = rb[l * SW + off[l & 15]];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(&empty[s]);  // this warp is done with rows[s]
+        mbar_spin(&dready[b & 1], (uint32_t)((b >> 1) & 1));
+        c1 = prof ? clock64() : 0;
+        if (t == 0) chain_trace(a.prof, cr, b, 4);
+        double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
 #pragma unroll
         for (int l = 0; l < L; l += 4) {
-          const double x0 = rb[l * SW + off[l & 15]], x1 = rb[(l + 1) * SW + off[(l + 1) & 15]];
-          const double x2 = rb[(l + 2) * SW + off[(l + 2) & 15]], x3 = rb[(l + 3) * SW + off[(l + 3) & 15]];
           const double4 dq = *reinterpret_cast<const double4*>(dd + l);
-          const double4 eq = *reinterpret_cast<const double4*>(ee + l);
-          u0 = fma(dq.x, x0, u0); u1 = fma(dq.y, x1, u1); u2 = fma(dq.z, x2, u2); u3 = fma(dq.w, x3, u3);
-          v0 = fma(eq.x, x0, v0); v1 = fma(eq.y, x1, v1); v2 = fma(eq.z, x2, v2); v3 = fma(eq.w, x3, v3);
+          u0 = fma(dq.x, xr[l], u0); u1 = fma(dq.y, xr[l + 1], u1);
+          u2 = fma(dq.z, xr[l + 2], u2); u3 = fma(dq.w, xr[l + 3], u3);
         }
+        u = (u0 + u1) + (u2 + u3);
+        const double wn = w - a.eta * u - a.eta * (double)Lb * muc;
+        wsm[((b + 1) & 1) * SW + t] = wn;  // w_{b+1}
+        __syncwarp();
+        if (t == 0) chain_trace(a.prof, cr, b, 5);
+        if (lane == 0) mbar_arrive_local(&wready[(b + 1) & 1]);  // this warp's columns of w_{b+1} written
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < L; l += 4) {
+          const double4 eq = *reinterpret_cast<const double4*>(ee + l);
+          v0 = fma(eq.x, xr[l], v0); v1 = fma(eq.y, xr[l + 1], v1);
+          v2 = fma(eq.z, xr[l + 2], v2); v3 = fma(eq.w, xr[l + 3], v3);
+        }
+        vv = (v0 + v1) + (v2 + v3);
+        S += (double)Lb * w - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
+        w = wn;
       } else {
+        mbar_wait(&dready[b & 1], (uint32_t)((b >> 1) & 1));
+        c1 = prof ? clock64() : 0;
+        double u0 = 0.0, v0 = 0.0;
         for (int l = 0; l < Lb; ++l) {
           const double x = rb[l * SW + pk_swz(t, l)];
           u0 = fma(dd[l], x, u0);
           v0 = fma(ee[l], x, v0);
         }
-      }
-      const double u = (u0 + u1) + (u2 + u3), vv = (v0 + v1) + (v2 + v3);
-      const double w0 = w;
-      S += (double)Lb * w0 - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
-      w = w0 - a.eta * u - a.eta * (double)Lb * muc;
-      wsm[((b + 1) & 1) * SW + t] = w;  // w_{b+1}
-      __syncwarp();
-      if (t == 0) chain_trace(a.prof, cr, b, 5);
-      if (lane == 0) {
-        mbar_arrive_local(&wready[(b + 1) & 1]);  // this warp's columns of w_{b+1} written (release.cta)
-        mbar_arrive_local(&empty[s]);             // this warp is done with rows[s]
+        u = u0;
+        vv = v0;
+        const double w0 = w;
+        S += (double)Lb * w0 - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
+        w = w0 - a.eta * u - a.eta * (double)Lb * muc;
+        wsm[((b + 1) & 1) * SW + t] = w;  // w_{b+1}
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_local(&wready[(b + 1) & 1]);
+          mbar_arrive_local(&empty[s]);
+        }
       }
       if (prof) {
         const unsigned long long c2 = clock64();

@@ -30,9 +30,15 @@
 //             128-byte swizzle, or four 32 x 32 boxes MN-major with the 128-byte/
 //             32-byte-atom swizzle), B_hi and B_lo tiles (BN x 32), NST-stage ring;
 //   warp 1    TMEM allocator + MMA issuer (one elected lane);
-//   warps 2-5 A_lo converters (smem -> registers -> TMEM, one row per thread),
+//   warps 2-9 A_lo converters (smem -> registers -> TMEM, one row per thread):
+//             two groups of four warps (one per TMEM lane quarter) taking
+//             alternate K blocks, so each scheduler has a second converter warp
+//             to issue while the other waits on its shared-memory loads or on
+//             tcgen05.wait::st (with one group the skinny products ran at 55 % of
+//             the DRAM peak, half their stall samples on the loads' scoreboard);
 //             then the epilogue: tcgen05.ld of their TMEM lane quarter ->
-//             fp64 partials (transposed, split-K) or fp32 hi/lo transposed out.
+//             fp64 partials (transposed, split-K) or fp32 hi/lo transposed out,
+//             the 16-column chunks dealt over the groups.
 #pragma once
 
 #include <cuda.h>
@@ -42,22 +48,30 @@
 
 namespace skr {
 
-constexpr int TC_BM = 128, TC_BK = 32, TC_THREADS = 192;
+constexpr int TC_BM = 128, TC_BK = 32;
+// warp 0 producer, warp 1 MMA issuer, then TC_CG groups of 4 converter warps (one per TMEM lane quarter)
+// OCC = 2 (K-major A, BN = 64): two co-resident CTAs per SM, each with half the tensor
+// memory, 3 stages and one converter group, so one CTA's prologue / pipeline fill /
+// epilogue overlaps the other's steady state (the X Q^T products run one short-lived CTA
+// per 128-row tile: 32 K blocks of work against ~10 us of un-overlapped set-up and drain).
+template <bool A_MN, int BN>
+constexpr int tc_occ() { return (!A_MN && BN <= 64) ? 2 : 1; }
+template <bool A_MN, int BN>
+constexpr int tc_cg() { return tc_occ<A_MN, BN>() == 2 ? 1 : 2; }
+template <bool A_MN, int BN>
+constexpr int tc_threads() { return 64 + 128 * tc_cg<A_MN, BN>(); }
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 
-template <int BN>
-constexpr int tc_stages() { return BN <= 64 ? 6 : BN <= 128 ? 4 : 2; }
+template <bool A_MN, int BN>
+constexpr int tc_stages() { return tc_occ<A_MN, BN>() == 2 ? 3 : BN <= 64 ? 6 : BN <= 128 ? 4 : 2; }
 template <int BN>
 constexpr bool tc_concat() { return BN <= 128; }
 template <int BN>
 constexpr uint32_t tc_acc_cols() { return tc_concat<BN>() ? 2 * BN : BN; }
 template <int BN>
 constexpr size_t tc_stage_bytes() { return (size_t)TC_A_BYTES + 2 * (size_t)BN * TC_BK * 4; }
-template <int BN>
-constexpr size_t tc_gemm_smem() { return (size_t)tc_stages<BN>() * tc_stage_bytes<BN>() + 1024; }
-static_assert(tc_acc_cols<64>() + 32 * tc_stages<64>() <= 512, "TMEM budget");
-static_assert(tc_acc_cols<128>() + 32 * tc_stages<128>() <= 512, "TMEM budget");
-static_assert(tc_acc_cols<256>() + 32 * tc_stages<256>() <= 512, "TMEM budget");
+template <bool A_MN, int BN>
+constexpr size_t tc_gemm_smem() { return (size_t)tc_stages<A_MN, BN>() * tc_stage_bytes<BN>() + 1024; }
 
 
 // the same box, written to the same shared offset of every CTA in ctaMask, each
@@ -166,19 +180,20 @@ struct TcGemmArgs {
 // every M tile); a stage is refilled once the MMAs of every CTA in the cluster are done
 // with it (the MMA commit arrives on all CTAs' empty barriers).
 template <bool A_MN, int BN, int CS>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__((tc_threads<A_MN, BN>()), (tc_occ<A_MN, BN>()))
 tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
                       const __grid_constant__ CUtensorMap mapBl, TcGemmArgs g) {
   constexpr int B_BYTES = BN * TC_BK * 4;
   constexpr int STAGE = (int)tc_stage_bytes<BN>();
-  constexpr int NST = tc_stages<BN>();
+  constexpr int NST = tc_stages<A_MN, BN>();
+  constexpr int TC_CG = tc_cg<A_MN, BN>();
   constexpr uint32_t ACC = tc_acc_cols<BN>();
   // TMEM columns per stage: A_lo (32); MN-major A also keeps A_hi in TMEM (32 more):
   // every MMA then reads A as a K-major TMEM operand — the MN-major shared-memory
   // A operand ran the tensor pipe at 45 % vs 61 % for K-major (ncu, c3)
   constexpr uint32_t SLOT = A_MN ? 64u : 32u;
-  static_assert(tc_acc_cols<BN>() + SLOT * tc_stages<BN>() <= 512, "TMEM budget");
-  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t TMEM_COLS = 512 / tc_occ<A_MN, BN>();
+  static_assert(tc_acc_cols<BN>() + SLOT * NST <= TMEM_COLS, "TMEM budget");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by offsetting the shared array itself so the compiler keeps the shared address space (LDS, not LD)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -312,8 +327,9 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
   } else {
     // A_lo converters: thread owns A row (lane quarter of its warp) -> TMEM lane
     const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;    // converter group: K blocks grp, grp + TC_CG, ...
     const int r = 32 * quarter + lane;  // M index within the tile = TMEM lane
-    for (int kb = 0; kb < nk; ++kb) {
+    for (int kb = grp; kb < nk; kb += TC_CG) {
       const int s = kb % NST;
       mbar_wait(&bar_tma[s], (uint32_t)((kb / NST) & 1));
       const unsigned char* st = smem + (size_t)s * STAGE;
@@ -364,7 +380,7 @@ tc_gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_con
     mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int64_t row = m0 + r;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = 16 * grp; c0 < BN; c0 += 16 * TC_CG) {
       uint32_t a[16], b[16];
       const uint32_t taddr = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)c0;
       asm volatile(
