@@ -1050,7 +1050,7 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     }
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
     SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
-    ChainArgs ca{pkb, steps, Mb, pb, Xb, mu, ld, eta, p->s_state.get(), dprof};
+    ChainArgs ca{pkb, steps, Mb, pb, Xb, mu, ld, eta, p->s_state.get(), chunk == 0 ? dprof : nullptr};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(Cf::NT);
@@ -1065,11 +1065,6 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     cfg.numAttrs = 1;
     SKR_CUDA(cudaLaunchKernelEx(&cfg, chain, ca));
     SKR_LAUNCHED(&c);
-    if (dprof && chunk == 0) {  // freeze the event trace after the first launch
-      const unsigned long long one = 1;
-      SKR_CUDA(cudaMemcpyAsync(dprof + 15, &one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
-      SKR_CUDA(cudaStreamSynchronize(c.stream));
-    }
     SKR_CUDA(cudaEventRecord(c.ev_chain[b], c.stream));
   }
   sstep_finish_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->s_state.get(), ld, p->d, (double)m, w_avg);
@@ -1092,12 +1087,124 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   }
 }
 
+// K10 v7: PACK + GRAM (depth 3) per chunk on the side stream, chain v7 (one cluster) on the main stream.
+template <class T, int SW, int L>
+void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
+                  double* w_avg) {
+  using Cf = Chain7Cfg<SW, L>;
+  using GC = GramCfg<L, 3>;
+  Ctx& c = p->ctx->c;
+  const int64_t ld = p->ld;
+  const int CS = (int)((ld + SW - 1) / SW);
+  if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
+  constexpr int MXW = MX7<L>::W;
+  if (p->s_state.n < (size_t)3 * ld) p->s_state.alloc(3 * ld, c.stream);
+  const size_t mneed = (size_t)2 * kSstepChunkBlocks * MXW;
+  const size_t pkchunk = (size_t)kSstepChunkBlocks * CS * L * SW;
+  if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
+  if (p->s_pk.n != 2 * pkchunk) {  // zero once: the padding columns past d are never written
+    p->s_pk.alloc(2 * pkchunk, c.stream);
+    p->s_pk.zero();
+  }
+  if (p->s_vec.n < (size_t)2 * CS * SW) p->s_vec.alloc((size_t)2 * CS * SW, c.stream);
+  auto pack = sstep_pack_kernel<T, L>;
+  auto gram = sstep_gram_kernel<L, 3>;
+  auto chain = sstep_chain7_kernel<SW, L>;
+  const size_t gstage = GC::stage_bytes(SW);
+  const int nstg = (int)std::max<size_t>(2, std::min<size_t>(std::min<size_t>(4, (size_t)CS), (224 * 1024) / gstage));
+  const size_t gram_smem = std::max((size_t)nstg * gstage, GC::epi_bytes());
+  if (gram_smem > 226 * 1024) raise(SKR_EDIM, "svrg: GRAM stage ring exceeds shared memory");
+  // the chain CTA reserves its SM's whole shared memory (no PACK / GRAM CTA co-resides with it)
+  static_assert(Cf::smem() <= 227 * 1024, "chain shared memory");
+  constexpr size_t chain_smem = 227 * 1024;
+  configure_once((const void*)chain, [&] {
+    SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem));
+    SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  configure_once((const void*)gram, [&] {
+    SKR_CUDA(cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+  });
+  SstepRows rows{p->xt_all, p->B.get(), ld, p->d, p->n_global};
+  const PackGeom pg{CS, SW};
+  sstep_init_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(snap, ld, p->s_state.get());
+  SKR_LAUNCHED(&c);
+  const int64_t vw = (int64_t)CS * SW;
+  sstep_padvec_kernel<<<ceil_div(vw, 256), 256, 0, c.stream>>>(mu, snap, p->d, vw, p->s_vec.get());
+  SKR_LAUNCHED(&c);
+  const int64_t chunk_steps = kSstepChunkBlocks * L;
+  SKR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
+  if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
+    SKR_CUDA(cudaMalloc(&dprof, 128 * sizeof(unsigned long long)));
+    SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
+  }
+  int64_t chunk = 0;
+  for (int64_t s0 = 0; s0 < m; s0 += chunk_steps, ++chunk) {
+    const int b = (int)(chunk & 1);
+    double* MXb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * MXW;
+    double* pkb = p->s_pk.get() + (size_t)b * pkchunk;
+    const int64_t steps = std::min(chunk_steps, m - s0);
+    const int64_t nblk = (steps + L - 1) / L;
+    if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
+    const int64_t pgrid = c.prep_cap > 0 ? std::min<int64_t>(nblk, c.prep_cap) : nblk;
+    pack<<<(unsigned)pgrid, 256, 0, c.aux>>>(rows, idx + s0, steps, pkb, pg);
+    SKR_LAUNCHED(&c);
+    gram<<<(unsigned)pgrid, 256, gram_smem, c.aux>>>(pkb, pg, nstg, idx + s0, steps, p->n_global, p->inv_nq.get(),
+                                                     p->data_coef, p->reg_coef, p->s_vec.get(), p->s_vec.get() + vw,
+                                                     ld, eta, nullptr, nullptr, nullptr, MXb);
+    SKR_LAUNCHED(&c);
+    SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
+    SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
+    Chain7Args ca{pkb, steps, MXb, mu, ld, eta, p->s_state.get(), chunk == 0 ? dprof : nullptr};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(Cf::NT);
+    cfg.dynamicSmemBytes = chain_smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SKR_CUDA(cudaLaunchKernelEx(&cfg, chain, ca));
+    SKR_LAUNCHED(&c);
+    SKR_CUDA(cudaEventRecord(c.ev_chain[b], c.stream));
+  }
+  sstep_finish_kernel<<<ceil_div(ld, 256), 256, 0, c.stream>>>(p->s_state.get(), ld, p->d, (double)m, w_avg);
+  SKR_LAUNCHED(&c);
+  if (dprof) {
+    unsigned long long h[128] = {};
+    SKR_CUDA(cudaMemcpy(h, dprof, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[skr] chain v7 (SW=%d L=%d CS=%d)\n", SW, L, CS);
+    for (int k = 0; k < kTraceN; ++k) {
+      const unsigned long long* e = h + 16 + 8 * k;
+      const unsigned long long b0 = h[16];
+      fprintf(stderr, "[skr]   block %d: dots %lld..%lld  sent %lld  partials@postB %lld  delta %lld  update: column loaded %lld, "
+              "delta seen %lld, w out %lld\n",
+              kTraceB0 + k, (long long)(e[0] - b0), (long long)(e[1] - b0), (long long)(e[7] - b0), (long long)(e[2] - b0),
+              (long long)(e[3] - b0), (long long)(e[6] - b0), (long long)(e[4] - b0), (long long)(e[5] - b0));
+    }
+    SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
+  }
+}
+
 // Chain geometry: the narrowest slice (>= 32 columns) that spans ld with at most
 // 16 CTAs; 256-column slices use L = 16 (shared-memory budget of the row ring).
 template <class T>
 void run_sstep(skr_problem* p, const double* snap, const double* mu, const int64_t* idx, int64_t m, double eta,
                double* w_avg) {
   const int64_t ld = p->ld;
+  static const bool chain_v3 = getenv("SKR_CHAIN_V3") != nullptr;  // the depth-2 chain of round 1 / early round 2
+  if (!chain_v3) {
+    if (ld <= 16 * 32) run_sstep7_t<T, 32, 32>(p, snap, mu, idx, m, eta, w_avg);
+    else if (ld <= 16 * 64) run_sstep7_t<T, 64, 32>(p, snap, mu, idx, m, eta, w_avg);
+    else if (ld <= 16 * 128) run_sstep7_t<T, 128, 32>(p, snap, mu, idx, m, eta, w_avg);
+    else if (ld <= 16 * 256) run_sstep7_t<T, 256, 16>(p, snap, mu, idx, m, eta, w_avg);
+    else raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
+    return;
+  }
   if (ld <= 16 * 32) run_sstep_t<T, 32, 32>(p, snap, mu, idx, m, eta, w_avg);
   else if (ld <= 16 * 64) run_sstep_t<T, 64, 32>(p, snap, mu, idx, m, eta, w_avg);
   else if (ld <= 16 * 128) run_sstep_t<T, 128, 32>(p, snap, mu, idx, m, eta, w_avg);

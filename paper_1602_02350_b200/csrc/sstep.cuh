@@ -536,18 +536,34 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "SPIN_%=:\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n"
       "@!P1 bra SPIN_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// one non-blocking test: issue it early and look at the answer after independent work (a
+// phase check answers through the long scoreboard, some hundred cycles even when the phase is
+// complete; the answer "complete" stays valid while the ring arguments exclude a second flip)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void mbar_spin_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "SPINC_%=:\n"
-      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 0x989680;\n"
       "@!P1 bra SPINC_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
@@ -566,12 +582,20 @@ __device__ __forceinline__ void st_async_f64(uint32_t rdst, uint32_t rbar, doubl
                : "memory");
 }
 
+// 16-byte form: two doubles per store, one complete_tx of 16 bytes (the receiver's mbarrier
+// serialises its complete_tx updates: half as many per block)
+__device__ __forceinline__ void st_async_f64x2(uint32_t rdst, uint32_t rbar, double v0, double v1) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(rdst),
+               "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"(rbar)
+               : "memory");
+}
+
 // debug event trace (SKR_DEBUG_CHAIN): clock64 of CTA 0 per event for blocks
 // [kTraceB0, kTraceB0 + kTraceN) of the first launch: prof[16 + 8 * k + e]
 constexpr int kTraceB0 = 200, kTraceN = 8;
 __device__ __forceinline__ void chain_trace(unsigned long long* prof, int cr, int64_t b, int e) {
-  if (prof && cr == 0 && b >= kTraceB0 && b < kTraceB0 + kTraceN && prof[15] == 0)
-    prof[16 + 8 * (b - kTraceB0) + e] = clock64();
+  const unsigned long long t = clock64();
+  if (prof && cr == 0 && b >= kTraceB0 && b < kTraceB0 + kTraceN) prof[16 + 8 * (b - kTraceB0) + e] = t;
 }
 
 template <int SW, int L>
@@ -901,6 +925,373 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
       atomicAdd(a.prof + 1, tp[0]);
       atomicAdd(a.prof + 2, tp[1]);
       atomicAdd(a.prof + 3, tp[2]);
+    }
+    if (act) {
+      a.state[col] = w;
+      a.state[a.ld + col] = S;
+    }
+  }
+  cluster.sync();  // no CTA exits while others may still write its smem / signal its barriers
+}
+
+// ---------------------------------------------------------------------------
+// CHAIN v7 (round 2): look-ahead depth 3.  The partial dots of block b are taken
+// against w_{b-2}, two blocks early:
+//   a_b = R_b w_b = a~_b - eta X2_b delta_{b-2} - eta X1_b delta_{b-1} - 2 eta L e_b,
+//   delta_b = M_b (a_b - p_b) = [M_b a~_b - p''_b - Y2_b delta_{b-2}] - Y1_b delta_{b-1},
+// with Y_q = eta M_b X_q and p''_b = M_b (p_b + nprev eta L e_b) from GRAM (DEPTH = 3).
+// v3's dependent cycle (update -> dots -> all-to-all -> delta -> update, two blocks
+// long, ~1.1 K cycles of it the DSMEM exchange) now spans three blocks, and the
+// delta recurrence itself is one L x L product per block on its own warp:
+//   dot warps     a~_b against w_{b-2} (lanes = rows), partials to dpart
+//   sender warp   sums the dot warps' partials, st.async to every rank (complete_tx)
+//   postA warp    t_b = p''_b + Y2_b delta_{b-2}             (two blocks of slack)
+//   postB warp    waits the partials of b, tree-sums the CS ranks, s_b = M_b a~_b - t_b
+//   chain warp    delta_b = s_b - Y1_b delta_{b-1}           (Y1 delta_{b-1} before s_b lands)
+//   update warps  column in registers; w_{b+1} published first, running sum after
+//   two producer lanes (own warps): packed rows ring; [M | Y1 | Y2 | p''] ring.
+// Ring depths (each argued from the dependency chain dots(b) <- w_{b-2} <-
+// update(b-3) <- delta_{b-3} <- partials(b-3) of every rank):
+//   w slices 3, delta 4, t / s 4, dot partials 4, exchange slots 6 (a rank pushes
+//   block b+6 only after its w_{b+4}, i.e. delta_{b+3}, i.e. every rank's partials
+//   of b+3, whose sender needed its own w_{b+1} = update(b), after its postB(b)).
+template <int SW, int L>
+struct Chain7Cfg {
+  static constexpr int NUW = SW / 32;
+  static constexpr int NDW = SW * L / 1024;
+  static constexpr int NT = 32 * (NDW + NUW + 6);  // + sender, postA, postB, chain, rows producer, matrix producer
+  // ring depths are powers of two and block counters 32-bit: the 64-bit % 3, % 6 of the first
+  // version cost every role ~300 cycles of dependent integer arithmetic per block
+  static constexpr int NB = SW * L * 8 <= 16384 ? 8 : 4;
+  static constexpr int NMX = 2;
+  static constexpr int MXW = MX7<L>::W;
+  static constexpr int NPS = 8;   // >= 6 (see above)
+  static constexpr int NW = 4;    // w slices: w_b in slot b % 4 (>= 3)
+  static constexpr size_t smem() {
+    return sizeof(double) * ((size_t)NB * L * SW + (size_t)NMX * MXW + (size_t)NPS * 16 * L + 17 * L +
+                             4 * NDW * L + NW * SW) +
+           sizeof(uint64_t) * (2 * NB + 2 * NMX + NPS + 4 + 4 + NW + 4 + 4) + 128;
+  }
+};
+
+// lane's share of row i of an L x L matrix in the lane-major pair layout (MX7): KPL consecutive k from k0
+template <int L>
+struct LaneRow {
+  static constexpr int HALVES = 32 / L, KPL = L / HALVES;
+  double m[KPL];
+  __device__ __forceinline__ void load(const double* At, int i, int k0) {
+#pragma unroll
+    for (int kk = 0; kk < KPL; kk += 2) {
+      const double2 q = *reinterpret_cast<const double2*>(At + ((k0 + kk) >> 1) * 2 * L + 2 * i);
+      m[kk] = q.x;
+      m[kk + 1] = q.y;
+    }
+  }
+  // (row i) . vec, vec in shared memory; every lane of a row gets the full sum
+  __device__ __forceinline__ double dot(const double* vec, int k0) const {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0, a6 = 0.0, a7 = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KPL; kk += 8) {
+      const double2 v0 = *reinterpret_cast<const double2*>(vec + k0 + kk);
+      const double2 v1 = *reinterpret_cast<const double2*>(vec + k0 + kk + 2);
+      const double2 v2 = *reinterpret_cast<const double2*>(vec + k0 + kk + 4);
+      const double2 v3 = *reinterpret_cast<const double2*>(vec + k0 + kk + 6);
+      a0 = fma(m[kk], v0.x, a0); a1 = fma(m[kk + 1], v0.y, a1);
+      a2 = fma(m[kk + 2], v1.x, a2); a3 = fma(m[kk + 3], v1.y, a3);
+      a4 = fma(m[kk + 4], v2.x, a4); a5 = fma(m[kk + 5], v2.y, a5);
+      a6 = fma(m[kk + 6], v3.x, a6); a7 = fma(m[kk + 7], v3.y, a7);
+    }
+    double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if constexpr (HALVES == 2) r += __shfl_xor_sync(0xffffffffu, r, 16);
+    return r;
+  }
+};
+
+struct Chain7Args {
+  const double* pk;     // this chunk's packed rows [nblk][CS][L][SW] (swizzled)
+  int64_t steps;        // steps in this chunk
+  const double* MX;     // nblk x MX7<L>::W
+  const double* mu;     // ld
+  int64_t ld;
+  double eta;
+  double* state;        // [0, ld) w ; [ld, 2 ld) sum
+  unsigned long long* prof;  // optional event trace of CTA 0 (debug)
+};
+
+template <int SW, int L>
+__global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(Chain7Args a) {
+  using Cf = Chain7Cfg<SW, L>;
+  constexpr int NUW = Cf::NUW, NDW = Cf::NDW, NB = Cf::NB, NMX = Cf::NMX, MXW = Cf::MXW, NPS = Cf::NPS;
+  constexpr int NW = Cf::NW;
+  constexpr int WU0 = NDW, WSN = NDW + NUW, WPA = WSN + 1, WPB = WSN + 2, WCH = WSN + 3, WPR = WSN + 4, WPM = WSN + 5;
+  constexpr int HALVES = 32 / L, KPL = L / HALVES;
+  static_assert(L == 16 || L == 32, "lanes = rows in the dots");
+  static_assert(SW >= 32 && SW % 32 == 0, "slice width");
+  extern __shared__ __align__(128) unsigned char sm[];
+  double* rows = reinterpret_cast<double*>(sm);                 // [NB][L][SW] (swizzled)
+  double* mx = rows + (size_t)NB * L * SW;                      // [NMX][MXW]: M | Y1 | Y2 | p''
+  double* apub = mx + NMX * MXW;                                // [NPS][16][L] partials by sender rank
+  double* dl = apub + NPS * 16 * L;                             // [4][L] delta_b
+  double* d2 = dl + 4 * L;                                      // [4][L] (Lb - l) delta_b
+  double* tbuf = d2 + 4 * L;                                    // [4][L] t_b
+  double* sbuf = tbuf + 4 * L;                                  // [4][L] s_b
+  double* abuf = sbuf + 4 * L;                                  // [L] a~_b (postB)
+  double* dpart = abuf + L;                                     // [4][NDW][L] dot warps' partials
+  double* wsm = dpart + 4 * NDW * L;                            // [NW][SW] w slice: w_b in slot b % NW
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + NW * SW);  // [NB]
+  uint64_t* empty = full + NB;                                  // [NB]
+  uint64_t* mx_full = empty + NB;                               // [NMX]
+  uint64_t* mx_empty = mx_full + NMX;                           // [NMX]
+  uint64_t* part = mx_empty + NMX;                              // [NPS] partials (complete_tx)
+  uint64_t* dotdone = part + NPS;                               // [4]
+  uint64_t* dready = dotdone + 4;                               // [4] delta_b published
+  uint64_t* wready = dready + 4;                                // [NW] w_b written
+  uint64_t* tready = wready + NW;                               // [4]
+  uint64_t* sready = tready + 4;                                // [4]
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t slice0 = (int64_t)cr * SW;
+  const int nblk = (int)((a.steps + L - 1) / L);
+  const uint32_t part_bytes = (uint32_t)(CS * L * 8);
+  if (tid == 0) {
+    for (int q = 0; q < NB; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NUW + NDW);
+    }
+    for (int q = 0; q < NMX; ++q) {
+      mbar_init(&mx_full[q], 1);
+      mbar_init(&mx_empty[q], 3);  // postA, postB and chain each hold their matrix row in registers
+    }
+    for (int q = 0; q < NPS; ++q) mbar_init(&part[q], 1);
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&dotdone[q], NDW);
+      mbar_init(&dready[q], 1);
+      mbar_init(&tready[q], 1);
+      mbar_init(&sready[q], 1);
+    }
+    for (int q = 0; q < NW; ++q) mbar_init(&wready[q], NUW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < NPS && q < nblk; ++q) mbar_expect_tx(&part[q], part_bytes);
+  }
+  for (int t = tid; t < SW; t += blockDim.x) {
+    const int64_t col = slice0 + t;
+    wsm[t] = col < a.ld ? a.state[col] : 0.0;  // w_0
+  }
+  for (int t = tid; t < 8 * L; t += blockDim.x) dl[t] = 0.0;  // dl and d2
+  cluster.sync();
+
+  const int gi = lane % L, gk0 = (lane / L) * KPL;  // matrix-row lanes: row, first k
+  if (warp == WPR) {
+    if (lane == 0) {
+      const uint32_t slice_bytes = (uint32_t)(L * SW * 8);
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b & (NB - 1);
+        if (b >= NB) mbar_spin(&empty[s], (uint32_t)(((b / NB) - 1) & 1));
+        mbar_expect_tx(&full[s], slice_bytes);
+        bulk_g2s(rows + (size_t)s * L * SW, a.pk + ((size_t)b * CS + cr) * L * SW, slice_bytes, &full[s]);
+      }
+    }
+  } else if (warp == WPM) {
+    if (lane == 0) {
+      for (int b = 0; b < nblk; ++b) {
+        const int ms = b & (NMX - 1);
+        if (b >= NMX) mbar_spin(&mx_empty[ms], (uint32_t)(((b / NMX) - 1) & 1));
+        mbar_expect_tx(&mx_full[ms], (uint32_t)(MXW * 8));
+        bulk_g2s(mx + ms * MXW, a.MX + (size_t)b * MXW, (uint32_t)(MXW * 8), &mx_full[ms]);
+      }
+    }
+  } else if (warp == WPA) {
+    // ---------------- postA: t_b = p''_b + Y2_b delta_{b-2} ----------------
+    LaneRow<L> y2;
+    for (int b = 0; b < nblk; ++b) {
+      const int ms = b & (NMX - 1);
+      const double* Ms = mx + ms * MXW;
+      mbar_spin(&mx_full[ms], (uint32_t)((b / NMX) & 1));
+      y2.load(Ms + 2 * L * L, gi, gk0);
+      const double pp = Ms[3 * L * L + gi];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&mx_empty[ms]);
+      double t = pp;
+      if (b >= 2) {
+        mbar_spin(&dready[(b - 2) & 3], (uint32_t)(((b - 2) >> 2) & 1));
+        t += y2.dot(dl + ((b - 2) & 3) * L, gk0);
+      }
+      if (lane < L) tbuf[(b & 3) * L + gi] = t;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&tready[b & 3]);
+    }
+  } else if (warp == WPB) {
+    // ---------------- postB: s_b = M_b a~_b - t_b ----------------
+    LaneRow<L> mr;
+    for (int b = 0; b < nblk; ++b) {
+      const int ms = b & (NMX - 1);
+      if (!mbar_test(&mx_full[ms], (uint32_t)((b / NMX) & 1))) mbar_spin(&mx_full[ms], (uint32_t)((b / NMX) & 1));
+      mr.load(mx + ms * MXW, gi, gk0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&mx_empty[ms]);
+      const int ps = b & (NPS - 1);
+      mbar_spin_cluster(&part[ps], (uint32_t)((b / NPS) & 1));
+      if (lane == 0) chain_trace(a.prof, cr, b, 2);
+      if (lane < L) {
+        // the CS partials of row i, summed by a fixed tree (deterministic)
+        const double* ap = apub + (size_t)ps * 16 * L + gi;
+        double pq[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) pq[q] = q < CS ? ap[q * L] : 0.0;
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+          for (int q = 0; q < h; ++q) pq[q] += pq[q + h];
+        abuf[gi] = pq[0];
+      }
+      __syncwarp();
+      if (lane == 0 && b + NPS < nblk) mbar_expect_tx(&part[ps], part_bytes);  // slot read: arm block b + NPS
+      const bool tok = mbar_test(&tready[b & 3], (uint32_t)((b >> 2) & 1));  // t_b is two blocks early: normally there
+      const double ma = mr.dot(abuf, gk0);
+      if (!tok) mbar_spin(&tready[b & 3], (uint32_t)((b >> 2) & 1));
+      if (lane < L) sbuf[(b & 3) * L + gi] = ma - tbuf[(b & 3) * L + gi];
+      __syncwarp();  // also: every lane is done with abuf before the next block rewrites it
+      if (lane == 0) mbar_arrive_local(&sready[b & 3]);
+    }
+  } else if (warp == WCH) {
+    // ---------------- chain: delta_b = s_b - Y1_b delta_{b-1} ----------------
+    LaneRow<L> y1;
+    for (int b = 0; b < nblk; ++b) {
+      const int Lb = (int)min((int64_t)L, a.steps - (int64_t)b * L);
+      const int ms = b & (NMX - 1);
+      mbar_spin(&mx_full[ms], (uint32_t)((b / NMX) & 1));
+      y1.load(mx + ms * MXW + L * L, gi, gk0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&mx_empty[ms]);
+      const double yd = b >= 1 ? y1.dot(dl + ((b - 1) & 3) * L, gk0) : 0.0;  // before s_b is known
+      mbar_spin(&sready[b & 3], (uint32_t)((b >> 2) & 1));
+      const double dv = sbuf[(b & 3) * L + gi] - yd;
+      if (lane < L) {
+        dl[(b & 3) * L + gi] = dv;
+        d2[(b & 3) * L + gi] = (double)(Lb - gi) * dv;  // (Lb - l + 1) weight, 1-based l
+      }
+      __syncwarp();
+      if (lane == 0) {
+        chain_trace(a.prof, cr, b, 3);
+        mbar_arrive_local(&dready[b & 3]);
+      }
+    }
+  } else if (warp == WSN) {
+    // ---------------- sender: row l's partial to every rank ----------------
+    // lane j < L / 2 sends rows 2j, 2j + 1 as one 16-byte store per rank
+    uint32_t rdst[16], rbar[16];
+    const uint32_t ldst = smem_u32(apub + (size_t)cr * L + 2 * (lane % (L / 2))), lbar = smem_u32(&part[0]);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      rdst[q] = q < CS ? mapa_u32(ldst, (uint32_t)q) : 0u;
+      rbar[q] = q < CS ? mapa_u32(lbar, (uint32_t)q) : 0u;
+    }
+    for (int bb = 0; bb < nblk; ++bb) {
+      mbar_spin(&dotdone[bb & 3], (uint32_t)((bb >> 2) & 1));
+      const double* dp = dpart + (size_t)(bb & 3) * NDW * L + gi;
+      double v = dp[0];
+#pragma unroll
+      for (int k = 1; k < NDW; ++k) v += dp[k * L];
+      const double va = __shfl_sync(0xffffffffu, v, (2 * lane) & 31), vb = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 31);
+      if (lane < L / 2) {
+        const uint32_t off_s = (uint32_t)((bb & (NPS - 1)) * 16 * L * 8), boff = (uint32_t)((bb & (NPS - 1)) * 8);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q < CS) st_async_f64x2(rdst[q] + off_s, rbar[q] + boff, va, vb);
+      }
+      if (lane == 0) chain_trace(a.prof, cr, bb, 7);
+    }
+  } else if (warp < NDW) {
+    // ---------------- dot warps: a~_bb = R_bb w_{bb-2}, lanes = rows ----------------
+    constexpr int NCOL = 32;
+    static_assert(NDW * HALVES * NCOL == SW, "dot warps cover the slice");
+    const int l = lane % L;
+    const int c0 = (warp * HALVES + lane / L) * NCOL;
+    int off[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) off[jj] = jj ^ (l & 15);
+    for (int bb = 0; bb < nblk; ++bb) {
+      const int s = bb & (NB - 1);
+      const int wi = bb >= 2 ? bb - 2 : 0;  // w_{wi}
+      const bool fok = mbar_test(&full[s], (uint32_t)((bb / NB) & 1));
+      if (wi >= 1) mbar_spin(&wready[wi & (NW - 1)], (uint32_t)(((wi - 1) / NW) & 1));  // slot's k-th phase (slot 0: w_NW first)
+      if (!fok) mbar_spin(&full[s], (uint32_t)((bb / NB) & 1));
+      if (warp == 0 && lane == 0) chain_trace(a.prof, cr, bb, 0);
+      const double* x = rows + (size_t)s * L * SW + (size_t)l * SW + c0;
+      const double* wb = wsm + (size_t)(wi & (NW - 1)) * SW + c0;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < NCOL / 16; ++m) {
+#pragma unroll
+        for (int jj = 0; jj < 16; jj += 2) {
+          const double2 wq = *reinterpret_cast<const double2*>(wb + 16 * m + jj);
+          acc[(jj >> 1) & 3] = fma(x[16 * m + off[jj]], wq.x, acc[(jj >> 1) & 3]);
+          acc[((jj >> 1) + 1) & 3] = fma(x[16 * m + off[jj + 1]], wq.y, acc[((jj >> 1) + 1) & 3]);
+        }
+      }
+      double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[s]);  // this warp's reads of rows[s] are done
+      if constexpr (HALVES == 2) v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (lane < L) dpart[(size_t)(bb & 3) * NDW * L + warp * L + l] = v;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_local(&dotdone[bb & 3]);
+        if (warp == 0) chain_trace(a.prof, cr, bb, 1);
+      }
+    }
+  } else {
+    // ---------------- update warps: thread t owns column slice0 + t ----------------
+    const int t = tid - 32 * WU0;
+    const int64_t col = slice0 + t;
+    const bool act = col < a.ld;
+    double w = act ? a.state[col] : 0.0;
+    double S = act ? a.state[a.ld + col] : 0.0;
+    const double muc = act ? a.mu[col] : 0.0;
+    int off[16];  // column t of row l sits at l * SW + off[l & 15]
+#pragma unroll
+    for (int k = 0; k < 16; ++k) off[k] = pk_swz(t, k);
+    for (int b = 0; b < nblk; ++b) {
+      const int s = b & (NB - 1);
+      const int Lb = (int)min((int64_t)L, a.steps - (int64_t)b * L);
+      const double* rb = rows + (size_t)s * L * SW;
+      const double* dd = dl + (b & 3) * L;
+      const double* ee = d2 + (b & 3) * L;
+      const int ws = (b + 1) & (NW - 1);
+      // the block's column goes to registers before delta_b is known (slot released at once)
+      double xr[L];
+      if (!mbar_test(&full[s], (uint32_t)((b / NB) & 1))) mbar_spin(&full[s], (uint32_t)((b / NB) & 1));
+      const bool dok = mbar_test(&dready[b & 3], (uint32_t)((b >> 2) & 1));  // answer arrives under the loads
+#pragma unroll
+      for (int l = 0; l < L; ++l) xr[l] = rb[l * SW + off[l & 15]];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[s]);
+      if (t == 0) chain_trace(a.prof, cr, b, 6);
+      if (!dok) mbar_spin(&dready[b & 3], (uint32_t)((b >> 2) & 1));
+      if (t == 0) chain_trace(a.prof, cr, b, 4);
+      // rows past Lb (the tail block of an epoch) are zero rows with delta = 0.
+      // One pass for both rank-L updates (8 independent chains).
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+      for (int l = 0; l < L; l += 4) {
+        const double4 dq = *reinterpret_cast<const double4*>(dd + l);
+        const double4 eq = *reinterpret_cast<const double4*>(ee + l);
+        u0 = fma(dq.x, xr[l], u0); u1 = fma(dq.y, xr[l + 1], u1);
+        u2 = fma(dq.z, xr[l + 2], u2); u3 = fma(dq.w, xr[l + 3], u3);
+        v0 = fma(eq.x, xr[l], v0); v1 = fma(eq.y, xr[l + 1], v1);
+        v2 = fma(eq.z, xr[l + 2], v2); v3 = fma(eq.w, xr[l + 3], v3);
+      }
+      const double u = (u0 + u1) + (u2 + u3);
+      const double wn = w - a.eta * u - a.eta * (double)Lb * muc;
+      wsm[ws * SW + t] = wn;  // w_{b+1}
+      __syncwarp();
+      if (t == 0) chain_trace(a.prof, cr, b, 5);
+      if (lane == 0) mbar_arrive_local(&wready[ws]);
+      const double vv = (v0 + v1) + (v2 + v3);
+      S += (double)Lb * w - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
+      w = wn;
     }
     if (act) {
       a.state[col] = w;
