@@ -506,6 +506,15 @@ def warm_library(sk, configs, ctx):
     wprob = sk.preconditioned_components(wp, sk.build_sketched(wsv, 1e-3))
     sk.svrg_solve(wprob, sk.SvrgConfig(2, 1 << 20, configs.step_size(wprob.max_row_sq()), 1), None,
                   sk.reference_minimum(wp).minimum)
+    # every inner-loop geometry (chain slice widths 32 / 64 / 128 / 256, both storage types): the
+    # first launch of a kernel instantiation loads its code (CUDA lazy loading, tens of ms)
+    for d in (1024, 2048, 4096):
+        for dt in ("f64", "f32"):
+            gd = sk.DataMatrix.generate(sk.SynthSpec(4096, d, dt, 9, 0, 0.0, False, 0.1), ctx)
+            gp = sk.RidgeProblem(gd, gd.labels(), 1e-3)
+            gsv = sk.block_lanczos(sk.scaled_design(gp), sk.LanczosConfig(8, 0.5, 1, 2))
+            gprob = sk.preconditioned_components(gp, sk.build_sketched(gsv, 1e-3))
+            sk.svrg_solve(gprob, sk.SvrgConfig(1, 8192, configs.step_size(gprob.max_row_sq()), 1), np.zeros(d))
     ctx.synchronize()
 
 

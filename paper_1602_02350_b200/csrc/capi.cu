@@ -249,9 +249,10 @@ template <class T, int VEC, int TR, int NT>
 void launch_fullgrad_nt(Ctx& c, FgPlan& p, int64_t ntiles, const T* X, int64_t ld, int64_t n, const double* y,
                         const double* w, double* part_g, double* part_loss, bool plan_only) {
   const K9Knobs& kn = k9_knobs();
-  if (kn.impl != 2) {
+  const size_t tile = (size_t)ld * sizeof(T) * TR;
+  // two tiles must fit the bulk-copy ring (fp64 rows beyond ~3600 columns do not: register-staged kernel)
+  if (kn.impl != 2 && 2 * tile <= (size_t)227 * 1024) {
     auto kern = fullgrad_tma_kernel<T, VEC, TR, NT>;
-    const size_t tile = (size_t)ld * sizeof(T) * TR;
     // 2 CTAs/SM at <= 256 threads (96 KB rings), 1 CTA/SM with a ~200 KB ring at 512
     const size_t budget = (size_t)(getenv("SKR_K9_SMEM_KB") ? kn.smem_kb : (NT >= 512 ? 200 : 96)) * 1024;
     const int stages = (int)std::max<size_t>(2, std::min<size_t>(16, budget / tile));

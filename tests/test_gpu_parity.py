@@ -151,6 +151,22 @@ def test_identity_preconditioner(O):
     assert pg.strong_convexity() == lam
 
 
+def test_full_gradient_wide_fp64_rows(O):
+    # fp64 rows of 4096 columns: two 4-row tiles exceed the bulk-copy ring, so the pass takes the
+    # register-staged kernel; the widest inner-loop geometry (256-column slices, 16-step blocks) too
+    X, y, lam, _ = small_problem(n=96, d=4096)
+    po = O.problem(X, y, lam)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam),
+                                      sk.Preconditioner.identity(4096, lam))
+    w = np.random.default_rng(5).standard_normal(4096)
+    assert rel(pg.full_gradient(w), po.full_gradient(w)) < 1e-12
+    eta = configs.step_size(po.scalars()[2])
+    want = po.svrg(2, 300, eta, 7)
+    got = sk.svrg_solve(pg, sk.SvrgConfig(2, 300, eta, 7), np.zeros(4096))
+    assert rel(np.array([r.objective for r in got.trace]), want.trace) < 1e-10
+    assert rel(got.iterate, want.iterate) < 1e-8
+
+
 def test_full_gradient_is_mean_of_components():
     # test_ridge.cpp:167-181
     X, y, lam, k = small_problem(n=60, d=12, k=3)
