@@ -341,6 +341,27 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
     // per-lane fragment geometry: row r8 = lane >> 2 of an 8-row tile, k index t4 = lane & 3
     const int r8 = lane >> 2, t4 = lane & 3;
     const int la = 8 * mt + r8;  // A row (block b)
+    // B operand of n-tile q: element (row, column j) at boff[q] + (j ^ bxor[q]); lanes with
+    // bok[q] false feed zeros.  No branch inside the product loop: a conditional mma.sync
+    // costs a WARPSYNC and serialises the tiles (the first version ran the FP64 pipe at a third
+    // of this).  Tiles of blocks that are not in this launch (nprev < q) multiply stale but
+    // finite-or-not data into accumulators the epilogue never reads.
+    int boff[NJ], bxor[NJ];
+    bool bok[NJ];
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      const int nt = nb + STEP * q;
+      if (nt < NTN - 1) {
+        const int rr = 8 * nt + r8;
+        boff[q] = rr * SW;
+        bxor[q] = (rr % L) & 15;
+        bok[q] = true;
+      } else {
+        boff[q] = NRB * SW + (r8 < 2 ? r8 : 0) * SW;
+        bxor[q] = 0;
+        bok[q] = nt == NTN - 1 && r8 < 2;
+      }
+    }
     for (int s = 0; s < CS; ++s) {
       if (tid == 0 && s + nstg - 1 < CS) issue(s + nstg - 1);
       const int slot = (int)(waited % (uint32_t)nstg);
@@ -349,23 +370,20 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
       const double* st = stg + (size_t)slot * stage_d;
       const double* arow = st + (size_t)la * SW;
       const int ax = la & 15;
+#pragma unroll 2
       for (int g16 = 0; g16 < SW; g16 += 16) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int j = g16 + c + 4 * t4;  // this lane's column of the k-step {c, c+4, c+8, c+12}
           const double a = arow[j ^ ax];
+          double bv[NJ];
 #pragma unroll
           for (int q = 0; q < NJ; ++q) {
-            const int nt = nb + STEP * q;
-            if (nt < NTN - 1) {
-              const int rr = 8 * nt + r8, lb = rr % L;
-              if (rr / L <= nprev)  // warp-uniform: a tile covers rows of one block (L % 8 == 0)
-                dmma_884(acc[q][0], acc[q][1], a, st[(size_t)rr * SW + (j ^ (lb & 15))]);
-            } else if (nt == NTN - 1) {
-              const double bv = r8 < 2 ? st[(size_t)NRB * SW + (size_t)r8 * SW + j] : 0.0;
-              dmma_884(acc[q][0], acc[q][1], a, bv);
-            }
+            bv[q] = 0.0;
+            if (bok[q]) bv[q] = st[boff[q] + (j ^ bxor[q])];
           }
+#pragma unroll
+          for (int q = 0; q < NJ; ++q) dmma_884(acc[q][0], acc[q][1], a, bv[q]);
         }
       }
       __syncthreads();  // the slot may be refilled
@@ -388,15 +406,28 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
       }
     }
     __syncthreads();
-    // T = I + eta C G_strict (unit lower); column j of T^{-1} by forward substitution (thread j)
+    // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward substitution; a column
+    // only depends on itself, so PARTS = 256 / L lanes of one warp share column j (each sums the
+    // k2 = j + part (mod PARTS) terms of a row, xor-shuffle reduction) and no block barrier is
+    // needed between rows (one thread per column took ~15 K cycles per block with 7 warps idle).
+    {
+      constexpr int PARTS = 256 / L;
+      const int j = tid / PARTS, part = tid % PARTS;
+      for (int i = part; i < L; i += PARTS) Ti[i * (L + 1) + j] = i == j ? 1.0 : 0.0;
+      __syncwarp();
+      const int jmin = (tid & ~31) / PARTS;  // lowest column of this warp
+      for (int i = jmin + 1; i < L; ++i) {
+        double sacc = 0.0;
+        if (i > j)
+          for (int k2 = j + part; k2 < i; k2 += PARTS) sacc = fma(res[i * RS + k2], Ti[k2 * (L + 1) + j], sacc);
+#pragma unroll
+        for (int o = PARTS / 2; o >= 1; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (i > j && part == 0) Ti[i * (L + 1) + j] = -eta * cvec[i] * sacc;
+        __syncwarp();
+      }
+    }
     if (tid < L) {
       const int j = tid;
-      for (int i = 0; i < L; ++i) Ti[i * (L + 1) + j] = i == j ? 1.0 : 0.0;
-      for (int i = j + 1; i < L; ++i) {
-        double sacc = 0.0;
-        for (int k2 = j; k2 < i; ++k2) sacc = fma(res[i * RS + k2], Ti[k2 * (L + 1) + j], sacc);
-        Ti[i * (L + 1) + j] = -eta * cvec[i] * sacc;
-      }
       // p_j = eta j e_j + b_j (0-based j), + eta L nprev e_j: the dots of this block were taken nprev blocks early
       pv[j] = eta * (double)(j + L * nprev) * res[j * RS + NRB] + res[j * RS + NRB + 1];
     }
@@ -959,7 +990,10 @@ template <int SW, int L>
 struct Chain7Cfg {
   static constexpr int NUW = SW / 32;
   static constexpr int NDW = SW * L / 1024;
-  static constexpr int NT = 32 * (NDW + NUW + 6);  // + sender, postA, postB, chain, rows producer, matrix producer
+  // each 32-column group of the update is shared by two warps (half the block's rows each): the
+  // update warps' occupancy per block (~130 instructions at ~6-8 cycles each on a lone warp) set
+  // the chain's period
+  static constexpr int NT = 32 * (NDW + 2 * NUW + 6);  // + sender, postA, postB, chain, rows producer, matrix producer
   // ring depths are powers of two and block counters 32-bit: the 64-bit % 3, % 6 of the first
   // version cost every role ~300 cycles of dependent integer arithmetic per block
   static constexpr int NB = SW * L * 8 <= 16384 ? 8 : 4;
@@ -969,7 +1003,7 @@ struct Chain7Cfg {
   static constexpr int NW = 4;    // w slices: w_b in slot b % 4 (>= 3)
   static constexpr size_t smem() {
     return sizeof(double) * ((size_t)NB * L * SW + (size_t)NMX * MXW + (size_t)NPS * 16 * L + 17 * L +
-                             4 * NDW * L + NW * SW) +
+                             4 * NDW * L + NW * SW + 2 * SW) +
            sizeof(uint64_t) * (2 * NB + 2 * NMX + NPS + 4 + 4 + NW + 4 + 4) + 128;
   }
 };
@@ -1023,7 +1057,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
   using Cf = Chain7Cfg<SW, L>;
   constexpr int NUW = Cf::NUW, NDW = Cf::NDW, NB = Cf::NB, NMX = Cf::NMX, MXW = Cf::MXW, NPS = Cf::NPS;
   constexpr int NW = Cf::NW;
-  constexpr int WU0 = NDW, WSN = NDW + NUW, WPA = WSN + 1, WPB = WSN + 2, WCH = WSN + 3, WPR = WSN + 4, WPM = WSN + 5;
+  constexpr int WU0 = NDW, WSN = NDW + 2 * NUW, WPA = WSN + 1, WPB = WSN + 2, WCH = WSN + 3, WPR = WSN + 4, WPM = WSN + 5;
   constexpr int HALVES = 32 / L, KPL = L / HALVES;
   static_assert(L == 16 || L == 32, "lanes = rows in the dots");
   static_assert(SW >= 32 && SW % 32 == 0, "slice width");
@@ -1038,7 +1072,8 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
   double* abuf = sbuf + 4 * L;                                  // [L] a~_b (postB)
   double* dpart = abuf + L;                                     // [4][NDW][L] dot warps' partials
   double* wsm = dpart + 4 * NDW * L;                            // [NW][SW] w slice: w_b in slot b % NW
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + NW * SW);  // [NB]
+  double* ubuf = wsm + NW * SW;                                 // [SW][2] second half's partial (u, v)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ubuf + 2 * SW);  // [NB]
   uint64_t* empty = full + NB;                                  // [NB]
   uint64_t* mx_full = empty + NB;                               // [NMX]
   uint64_t* mx_empty = mx_full + NMX;                           // [NMX]
@@ -1058,7 +1093,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
   if (tid == 0) {
     for (int q = 0; q < NB; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&empty[q], NUW + NDW);
+      mbar_init(&empty[q], 2 * NUW + NDW);
     }
     for (int q = 0; q < NMX; ++q) {
       mbar_init(&mx_full[q], 1);
@@ -1243,8 +1278,12 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
       }
     }
   } else {
-    // ---------------- update warps: thread t owns column slice0 + t ----------------
-    const int t = tid - 32 * WU0;
+    // ---------------- update warps: column slice0 + t, rows [hh L/2, (hh + 1) L/2) ----------------
+    // warps 2g and 2g + 1 share the 32 columns of group g; the second hands its partial sums to
+    // the first (named barrier 1 + g), which finishes w_{b+1} and the running sum
+    constexpr int LH = L / 2;
+    const int uw = warp - WU0, g = uw >> 1, hh = uw & 1;
+    const int t = 32 * g + lane;
     const int64_t col = slice0 + t;
     const bool act = col < a.ld;
     double w = act ? a.state[col] : 0.0;
@@ -1256,44 +1295,53 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
     for (int b = 0; b < nblk; ++b) {
       const int s = b & (NB - 1);
       const int Lb = (int)min((int64_t)L, a.steps - (int64_t)b * L);
-      const double* rb = rows + (size_t)s * L * SW;
-      const double* dd = dl + (b & 3) * L;
-      const double* ee = d2 + (b & 3) * L;
+      const double* rb = rows + (size_t)s * L * SW + (size_t)hh * LH * SW;
+      const double* dd = dl + (b & 3) * L + hh * LH;
+      const double* ee = d2 + (b & 3) * L + hh * LH;
       const int ws = (b + 1) & (NW - 1);
       // the block's column goes to registers before delta_b is known (slot released at once)
-      double xr[L];
+      double xr[LH];
       if (!mbar_test(&full[s], (uint32_t)((b / NB) & 1))) mbar_spin(&full[s], (uint32_t)((b / NB) & 1));
       const bool dok = mbar_test(&dready[b & 3], (uint32_t)((b >> 2) & 1));  // answer arrives under the loads
 #pragma unroll
-      for (int l = 0; l < L; ++l) xr[l] = rb[l * SW + off[l & 15]];
+      for (int l = 0; l < LH; ++l) xr[l] = rb[l * SW + off[(hh * LH + l) & 15]];
       __syncwarp();
       if (lane == 0) mbar_arrive_local(&empty[s]);
-      if (t == 0) chain_trace(a.prof, cr, b, 6);
+      if (uw == 0 && lane == 0) chain_trace(a.prof, cr, b, 6);
       if (!dok) mbar_spin(&dready[b & 3], (uint32_t)((b >> 2) & 1));
-      if (t == 0) chain_trace(a.prof, cr, b, 4);
-      // rows past Lb (the tail block of an epoch) are zero rows with delta = 0.
-      // One pass for both rank-L updates (8 independent chains).
-      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      if (uw == 0 && lane == 0) chain_trace(a.prof, cr, b, 4);
+      // rows past Lb (the tail block of an epoch) are zero rows with delta = 0
+      double u0 = 0.0, u1 = 0.0, v0 = 0.0, v1 = 0.0;
 #pragma unroll
-      for (int l = 0; l < L; l += 4) {
+      for (int l = 0; l < LH; l += 4) {
         const double4 dq = *reinterpret_cast<const double4*>(dd + l);
         const double4 eq = *reinterpret_cast<const double4*>(ee + l);
         u0 = fma(dq.x, xr[l], u0); u1 = fma(dq.y, xr[l + 1], u1);
-        u2 = fma(dq.z, xr[l + 2], u2); u3 = fma(dq.w, xr[l + 3], u3);
+        u0 = fma(dq.z, xr[l + 2], u0); u1 = fma(dq.w, xr[l + 3], u1);
         v0 = fma(eq.x, xr[l], v0); v1 = fma(eq.y, xr[l + 1], v1);
-        v2 = fma(eq.z, xr[l + 2], v2); v3 = fma(eq.w, xr[l + 3], v3);
+        v0 = fma(eq.z, xr[l + 2], v0); v1 = fma(eq.w, xr[l + 3], v1);
       }
-      const double u = (u0 + u1) + (u2 + u3);
-      const double wn = w - a.eta * u - a.eta * (double)Lb * muc;
-      wsm[ws * SW + t] = wn;  // w_{b+1}
-      __syncwarp();
-      if (t == 0) chain_trace(a.prof, cr, b, 5);
-      if (lane == 0) mbar_arrive_local(&wready[ws]);
-      const double vv = (v0 + v1) + (v2 + v3);
-      S += (double)Lb * w - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
-      w = wn;
+      double u = u0 + u1, vv = v0 + v1;
+      if (hh == 1) {
+        *reinterpret_cast<double2*>(ubuf + 2 * t) = make_double2(u, vv);
+        named_bar(1 + g, 64);  // partials visible to the first warp ...
+        named_bar(1 + g, 64);  // ... and read before the next block overwrites them
+      } else {
+        named_bar(1 + g, 64);
+        const double2 o = *reinterpret_cast<const double2*>(ubuf + 2 * t);
+        named_bar(1 + g, 64);
+        u += o.x;
+        vv += o.y;
+        const double wn = w - a.eta * u - a.eta * (double)Lb * muc;
+        wsm[ws * SW + t] = wn;  // w_{b+1}
+        __syncwarp();
+        if (uw == 0 && lane == 0) chain_trace(a.prof, cr, b, 5);
+        if (lane == 0) mbar_arrive_local(&wready[ws]);
+        S += (double)Lb * w - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
+        w = wn;
+      }
     }
-    if (act) {
+    if (act && hh == 0) {
       a.state[col] = w;
       a.state[a.ld + col] = S;
     }
