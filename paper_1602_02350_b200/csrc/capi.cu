@@ -985,13 +985,10 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     p->s_pk.alloc(2 * pkchunk, c.stream);
     p->s_pk.zero();
   }
-  auto prep = sstep_prep_kernel<T, L>;
   auto pack = sstep_pack_kernel<T, L>;
   auto gram = sstep_gram_kernel<L, 2>;
   auto chain = sstep_chain_kernel<SW, L>;
-  constexpr size_t prep_smem = sstep_prep_smem<L>();
-  // PREP v2 (PACK + GRAM): ring of nstg stages of one column slice of the staged blocks
-  static const bool prep_v1 = getenv("SKR_PREP_V1") != nullptr;
+  // PACK + GRAM: ring of nstg stages of one column slice of the staged blocks
   using GC = GramCfg<L, 2>;
   const size_t gstage = GC::stage_bytes(SW);
   const int nstg = (int)std::max<size_t>(2, std::min<size_t>(std::min<size_t>(4, (size_t)CS), (200 * 1024) / gstage));
@@ -1004,7 +1001,6 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
   static_assert(Cf::smem() <= 227 * 1024, "chain shared memory");
   constexpr size_t chain_smem = 227 * 1024;
   configure_once((const void*)chain, [&] {
-    SKR_CUDA(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
     SKR_CUDA(cudaFuncSetAttribute(gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chain_smem));
     SKR_CUDA(cudaFuncSetAttribute(chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1037,18 +1033,12 @@ void run_sstep_t(skr_problem* p, const double* snap, const double* mu, const int
     const int64_t nblk = (steps + L - 1) / L;
     if (chunk >= 2) SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_chain[b], 0));  // chain(i-2) done with buffer b
     const int64_t pgrid = c.prep_cap > 0 ? std::min<int64_t>(nblk, c.prep_cap) : nblk;
-    if (prep_v1) {
-      prep<<<(unsigned)pgrid, 256, prep_smem, c.aux>>>(rows, idx + s0, steps, p->inv_nq.get(), p->data_coef,
-                                                       p->reg_coef, mu, snap, eta, Mb, pb, Xb, pkb, pg);
-      SKR_LAUNCHED(&c);
-    } else {
-      pack<<<(unsigned)pgrid, 256, 0, c.aux>>>(rows, idx + s0, steps, pkb, pg);
-      SKR_LAUNCHED(&c);
-      gram<<<(unsigned)pgrid, 256, gram_smem, c.aux>>>(pkb, pg, nstg, idx + s0, steps, p->n_global, p->inv_nq.get(),
-                                                       p->data_coef, p->reg_coef, p->s_vec.get(),
-                                                       p->s_vec.get() + vw, ld, eta, Mb, pb, Xb, nullptr);
-      SKR_LAUNCHED(&c);
-    }
+    pack<<<(unsigned)pgrid, 256, 0, c.aux>>>(rows, idx + s0, steps, pkb, pg);
+    SKR_LAUNCHED(&c);
+    gram<<<(unsigned)pgrid, 256, gram_smem, c.aux>>>(pkb, pg, nstg, idx + s0, steps, p->n_global, p->inv_nq.get(),
+                                                     p->data_coef, p->reg_coef, p->s_vec.get(), p->s_vec.get() + vw,
+                                                     ld, eta, Mb, pb, Xb, nullptr);
+    SKR_LAUNCHED(&c);
     SKR_CUDA(cudaEventRecord(c.ev_prep[b], c.aux));
     SKR_CUDA(cudaStreamWaitEvent(c.stream, c.ev_prep[b], 0));
     ChainArgs ca{pkb, steps, Mb, pb, Xb, mu, ld, eta, p->s_state.get(), chunk == 0 ? dprof : nullptr};

@@ -63,147 +63,10 @@ struct PackGeom {
 __host__ __device__ __forceinline__ int pk_swz(int j, int l) { return j ^ (l & 15); }
 
 // ---------------------------------------------------------------------------
-// PREP: one CTA (256 threads, 8 warps) per block of L (16 or 32) steps.  One
-// FP64 tensor-core (DMMA m8n8k4) product of the block's rows against the staged
-// rows [R_b; R_{b-1}; mu; wbar] gives G = R_b R_b^T, X = R_b R_{b-1}^T
-// (look-ahead), e = R_b mu and b = R_b wbar in one pass over the rows (column
-// chunks of 32, register-prefetched one chunk ahead); the same pass writes the
-// block's rows (fp64) to the packed buffer.  Then M = (I + eta C G_strict)^{-1} C
-// by forward substitution.  Outputs: Mout[b] (L x L, stored TRANSPOSED:
-// Mout[b][j*L + i] = M[i][j]), pout[b] (L), Xout[b] (transposed, blocks > 0 of
-// the launch), pk.  Padded steps (beyond `steps`) get c_l = 0, so delta_l = 0
-// there, and zero rows.
-template <class T, int L>
-__global__ void __launch_bounds__(256)
-sstep_prep_kernel(SstepRows R, const int64_t* __restrict__ idx, int64_t steps, const double* __restrict__ inv_nq,
-                  double data_coef, double reg_coef, const double* __restrict__ mu,
-                  const double* __restrict__ wbar, double eta, double* __restrict__ Mout,
-                  double* __restrict__ pout, double* __restrict__ Xout, double* __restrict__ pk, PackGeom pg) {
-  static_assert(L == 16 || L == 32, "L = 16 or 32");
-  constexpr int KC = 32, SP = KC + 4;         // staged columns per chunk, padded row stride (conflict-free frags)
-  constexpr int NR = 2 * L + 8;               // staged rows: block b, block b-1, mu, wbar, zero pad
-  constexpr int NTN = NR / 8;                 // n-tiles
-  constexpr int MT = L / 8;                   // m-tiles
-  constexpr int STEP = 8 / MT;                // warps per m-tile
-  constexpr int NJ = (NTN + STEP - 1) / STEP; // n-tiles per warp
-  constexpr int PER = NR * KC / 256;          // staged elements per thread per chunk
-  static_assert(NR * KC % 256 == 0, "staging split");
-  constexpr int RS = NR + 1;                  // result row stride
-  extern __shared__ double dyn[];
-  double* st = dyn;                           // [NR][SP] staging, then [L][RS] results
-  double (*Xs)[L + 1] = reinterpret_cast<double (*)[L + 1]>(dyn + NR * SP);  // column j of T^{-1}
-  __shared__ double cvec[L];
-  __shared__ int64_t ridx[2 * L];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // grid-strided over the chunk's blocks: a capped grid (skr_ctx_set_prep_cap) leaves
-  // SMs to concurrent chains (eta-grid lanes)
-  const int64_t nblk = (steps + L - 1) / L;
-  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int64_t t0 = (int64_t)blk * L;
-    const bool look = blk > 0;  // the previous block of this launch exists (and is full)
-    if (tid < L) {
-      const int64_t t = t0 + tid;
-      const int64_t i = t < steps ? idx[t] : -1;
-      ridx[tid] = i;
-      ridx[L + tid] = look ? idx[t0 - L + tid] : -1;
-      cvec[tid] = i < 0 ? 0.0 : (i < R.n ? data_coef : reg_coef) * inv_nq[i];
-    }
-    __syncthreads();
-    auto fetch = [&](int64_t c0, double (&v)[PER]) {
-  #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int e = tid + q * 256, r = e / KC;
-        const int64_t col = c0 + e % KC;
-        double x = 0.0;
-        if (col < R.d) {
-          if (r < 2 * L) {
-            const int64_t i = ridx[r];
-            if (i >= 0) x = row_elem<T>(R, i, col);
-          } else if (r == 2 * L) {
-            x = mu[col];
-          } else if (r == 2 * L + 1) {
-            x = wbar[col];
-          }
-        }
-        v[q] = x;
-      }
-    };
-    const int mt = warp % MT, nb = warp / MT;  // m-tile; n-tiles nb, nb + STEP, ...
-    double acc[NJ][2] = {};
-    double v[PER];
-    fetch(0, v);
-    double* pkb = pk + (size_t)blk * pg.cs * L * pg.sw;
-    for (int64_t c0 = 0; c0 < R.d; c0 += KC) {
-      __syncthreads();
-  #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int e = tid + q * 256, r = e / KC;
-        st[r * SP + e % KC] = v[q];
-        const int64_t col = c0 + e % KC;
-        if (r < L && col < R.d)  // the block's rows, packed per chain-CTA slice (swizzled, see pk_swz)
-          pkb[((col / pg.sw) * L + r) * pg.sw + pk_swz((int)(col % pg.sw), r)] = v[q];
-      }
-      __syncthreads();
-      if (c0 + KC < R.d) fetch(c0 + KC, v);  // next chunk in flight during the products
-  #pragma unroll
-      for (int k4 = 0; k4 < KC; k4 += 4) {
-        const double a = st[(8 * mt + (lane >> 2)) * SP + k4 + (lane & 3)];
-  #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const int nt = nb + STEP * j;
-          if (nt < NTN) dmma_884(acc[j][0], acc[j][1], a, st[(8 * nt + (lane >> 2)) * SP + k4 + (lane & 3)]);
-        }
-      }
-    }
-    __syncthreads();
-    double* res = st;  // res[i*RS + n]: n < L: G, L..2L-1: X, 2L: e, 2L+1: b
-  #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int nt = nb + STEP * j;
-      if (nt < NTN) {
-        const int i = 8 * mt + (lane >> 2), n = 8 * nt + 2 * (lane & 3);
-        res[i * RS + n] = acc[j][0];
-        res[i * RS + n + 1] = acc[j][1];
-      }
-    }
-    __syncthreads();
-    if (look) {  // X = R_b R_{b-1}^T stored transposed: Xt[j*L + i] = X[i][j]
-      double* Xb = Xout + (int64_t)blk * L * L;
-      for (int e = tid; e < L * L; e += blockDim.x) Xb[e] = res[(e % L) * RS + L + e / L];
-    }
-    // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward
-    // substitution (thread j), then M = T^{-1} C  (M[i][j] = Tinv[i][j] c_j).
-    double* Mb = Mout + (int64_t)blk * L * L;
-    if (tid < L) {
-      const int j = tid;
-      for (int i = 0; i < L; ++i) Xs[i][j] = i == j ? 1.0 : 0.0;
-      for (int i = j + 1; i < L; ++i) {
-        double s = 0.0;
-        for (int k2 = j; k2 < i; ++k2) s = fma(res[i * RS + k2], Xs[k2][j], s);
-        Xs[i][j] = -eta * cvec[i] * s;
-      }
-      // p_j = eta (j-1) e_j + b_j (1-based), + eta L e_j when a_b is formed by look-ahead
-      pout[(int64_t)blk * L + j] = eta * (double)(look ? j + L : j) * res[j * RS + 2 * L] + res[j * RS + 2 * L + 1];
-    }
-    __syncthreads();
-    for (int e = tid; e < L * L; e += blockDim.x) {  // stored transposed: Mt[j][i] = M[i][j]
-      const int j = e / L, i = e % L;
-      Mb[e] = Xs[i][j] * cvec[j];
-    }
-    __syncthreads();  // shared staging / results are reused by the next block
-  }
-}
-
-template <int L>
-constexpr size_t sstep_prep_smem() {
-  return sizeof(double) * ((2 * L + 8) * (32 + 4) + L * (L + 1));
-}
-
-// ---------------------------------------------------------------------------
-// PREP v2 = PACK + GRAM (round 2).  The one-kernel PREP above issues one
-// dependent gather per 32-column chunk (64-128 global round trips per block,
-// ~5 B/clk/SM in flight): 0.81 ms per 1024 blocks at c3, as long as the chain
-// it is supposed to hide behind.  v2 splits it:
+// PREP = PACK + GRAM (round 2).  Round 1's one-kernel PREP issued one dependent
+// gather per 32-column chunk (64-128 global round trips per block, ~5 B/clk/SM in
+// flight): 0.81 ms per 1024 blocks at c3, as long as the chain it is supposed to
+// hide behind.  Now:
 //  * PACK (all SMs, many independent 16-byte loads in flight): gathers every
 //    sampled row ONCE, widens it to fp64 and writes it to the packed buffer
 //    pk[block][chain CTA][l][SW] (the layout the chain's bulk copies want);
@@ -989,7 +852,8 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
 template <int SW, int L>
 struct Chain7Cfg {
   static constexpr int NUW = SW / 32;
-  static constexpr int NDW = SW * L / 1024;
+  static constexpr int DSPLIT = 1;                    // dot lanes take 32 / DSPLIT columns (2 at SW = 64 was slower: 21.8 vs 20.4 ns at c5)
+  static constexpr int NDW = SW * L / 1024 * DSPLIT;
   // each 32-column group of the update is shared by two warps (half the block's rows each): the
   // update warps' occupancy per block (~130 instructions at ~6-8 cycles each on a lone warp) set
   // the chain's period
@@ -1240,7 +1104,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
     }
   } else if (warp < NDW) {
     // ---------------- dot warps: a~_bb = R_bb w_{bb-2}, lanes = rows ----------------
-    constexpr int NCOL = 32;
+    constexpr int NCOL = 32 / Cf::DSPLIT;
     static_assert(NDW * HALVES * NCOL == SW, "dot warps cover the slice");
     const int l = lane % L;
     const int c0 = (warp * HALVES + lane / L) * NCOL;
