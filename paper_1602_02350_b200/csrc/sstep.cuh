@@ -23,11 +23,13 @@
 // p'_b = p_b + eta L e_b for every block but the first of a launch, whose a_0 is
 // computed directly.
 //
-// Row staging (v2): PREP, which reads every sampled row anyway, also writes the
-// block's rows widened to fp64 into a PACKED buffer laid out per CTA slice,
-// pk[block][cta][l][SW], so each chain CTA receives its L x SW slice of a block
-// with ONE bulk copy (v1 issued one bulk copy per row slice from two producer
-// warps plus two fp32 -> fp64 widener warps).
+// File map:
+//   PACK + GRAM   the per-block quantities for a chunk of blocks, on all SMs, one chunk ahead of
+//                 the chain: PACK gathers the sampled rows once (widened to fp64) into the packed
+//                 buffer pk[block][cta][l][SW]; GRAM forms R_b [R_b; R_{b-1}; (R_{b-2};) mu; wbar]^T
+//                 on DMMA from the packed tiles and solves for M (and Y_q = eta M X_q, p'');
+//   chain v7      look-ahead depth 3 (the default): see its header below;
+//   chain v3      look-ahead depth 2 (SKR_CHAIN_V3=1, kept for A/B).
 #pragma once
 
 #include <cooperative_groups.h>
