@@ -1122,7 +1122,8 @@ void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const in
   const int64_t vw = (int64_t)CS * SW;
   sstep_padvec_kernel<<<ceil_div(vw, 256), 256, 0, c.stream>>>(mu, snap, p->d, vw, p->s_vec.get());
   SKR_LAUNCHED(&c);
-  const int64_t chunk_steps = kSstepChunkBlocks * L;
+  // chunk sizes ramp 128, 256, 512, 1024, 1024, ... blocks: the first chunk's PACK + GRAM is the
+  // only one the chain cannot hide behind (an epoch of c2 is four full chunks, of c1 half of one)
   SKR_CUDA(cudaEventRecord(c.ev_fork, c.stream));
   SKR_CUDA(cudaStreamWaitEvent(c.aux, c.ev_fork, 0));
   if (getenv("SKR_DEBUG_CHAIN") && !dprof) {
@@ -1130,7 +1131,10 @@ void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const in
     SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
   }
   int64_t chunk = 0;
-  for (int64_t s0 = 0; s0 < m; s0 += chunk_steps, ++chunk) {
+  for (int64_t s0 = 0, chunk_steps = 0; s0 < m; s0 += chunk_steps, ++chunk) {
+    static const bool ramp = getenv("SKR_K10_NO_RAMP") == nullptr;
+    chunk_steps = (ramp ? std::min<int64_t>(kSstepChunkBlocks, (int64_t)128 << std::min<int64_t>(chunk, 3))
+                        : kSstepChunkBlocks) * L;
     const int b = (int)(chunk & 1);
     double* MXb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * MXW;
     double* pkb = p->s_pk.get() + (size_t)b * pkchunk;

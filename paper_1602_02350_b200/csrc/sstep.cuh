@@ -854,7 +854,9 @@ __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(Cha
 template <int SW, int L>
 struct Chain7Cfg {
   static constexpr int NUW = SW / 32;
-  static constexpr int DSPLIT = 1;                    // dot lanes take 32 / DSPLIT columns (2 at SW = 64 was slower: 21.8 vs 20.4 ns at c5)
+  // dot lanes take 32 / DSPLIT columns: 2 at SW = 256 (c4 53.7 -> 52.4 ns); at SW = 64 it was slower
+  // (c5 20.4 -> 21.8 ns: more warps on the same shared-memory pipe), at SW = 128 no change
+  static constexpr int DSPLIT = SW >= 256 ? 2 : 1;
   static constexpr int NDW = SW * L / 1024 * DSPLIT;
   // each 32-column group of the update is shared by two warps (half the block's rows each): the
   // update warps' occupancy per block (~130 instructions at ~6-8 cycles each on a lone warp) set
