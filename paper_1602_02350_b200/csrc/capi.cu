@@ -964,7 +964,8 @@ void run_epoch_t(Ctx& c, int64_t ld, const EpochArgs& a) {
 }
 
 // K10 s-step: prep (all SMs) + chain (one cluster) per chunk of blocks.
-constexpr int64_t kSstepChunkBlocks = 1024;  // blocks per prep/chain launch pair (double-buffered)
+constexpr int64_t kSstepChunkBlocks = 1024;  // blocks per prep/chain launch pair (double-buffered), chain v3
+constexpr int64_t kSstepChunkBlocksV7 = 1024;  // 4096: c4 58.5 -> 57 ns but c3 28.7 -> 29.6, c2 24.3 -> 26.2
 static unsigned long long* dprof = nullptr;  // SKR_DEBUG_CHAIN phase counters
 
 template <class T, int SW, int L>
@@ -1090,10 +1091,15 @@ void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const in
   if (CS > 16) raise(SKR_EDIM, "svrg: dimension too large for the s-step inner loop (d > 4096)");
   constexpr int MXW = MX7<L>::W;
   if (p->s_state.n < (size_t)3 * ld) p->s_state.alloc(3 * ld, c.stream);
-  const size_t mneed = (size_t)2 * kSstepChunkBlocks * MXW;
-  const size_t pkchunk = (size_t)kSstepChunkBlocks * CS * L * SW;
+  // chunk = blocks per PACK / GRAM / chain launch triple (double-buffered).  Every chunk boundary
+  // drains and refills the chain's three-block pipeline and pays a cluster launch (~5 % of the
+  // epoch at 1024 blocks; larger chunks did not pay, see kSstepChunkBlocksV7); the workspaces follow
+  // the epoch length, so small problems do not allocate and zero 1024-block buffers.
+  const int64_t chunk_cap = std::min<int64_t>(kSstepChunkBlocksV7, std::max<int64_t>(128, (m + L - 1) / L));
+  const size_t mneed = (size_t)2 * chunk_cap * MXW;
+  const size_t pkchunk = (size_t)chunk_cap * CS * L * SW;
   if (p->s_M.n < mneed) p->s_M.alloc(mneed, c.stream);
-  if (p->s_pk.n != 2 * pkchunk) {  // zero once: the padding columns past d are never written
+  if (p->s_pk.n < 2 * pkchunk) {  // zero once: the padding columns past d are never written
     p->s_pk.alloc(2 * pkchunk, c.stream);
     p->s_pk.zero();
   }
@@ -1133,10 +1139,9 @@ void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const in
   int64_t chunk = 0;
   for (int64_t s0 = 0, chunk_steps = 0; s0 < m; s0 += chunk_steps, ++chunk) {
     static const bool ramp = getenv("SKR_K10_NO_RAMP") == nullptr;
-    chunk_steps = (ramp ? std::min<int64_t>(kSstepChunkBlocks, (int64_t)128 << std::min<int64_t>(chunk, 3))
-                        : kSstepChunkBlocks) * L;
+    chunk_steps = (ramp ? std::min<int64_t>(chunk_cap, (int64_t)128 << std::min<int64_t>(chunk, 5)) : chunk_cap) * L;
     const int b = (int)(chunk & 1);
-    double* MXb = p->s_M.get() + (size_t)b * kSstepChunkBlocks * MXW;
+    double* MXb = p->s_M.get() + (size_t)b * chunk_cap * MXW;
     double* pkb = p->s_pk.get() + (size_t)b * pkchunk;
     const int64_t steps = std::min(chunk_steps, m - s0);
     const int64_t nblk = (steps + L - 1) / L;

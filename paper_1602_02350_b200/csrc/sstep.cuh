@@ -144,8 +144,8 @@ struct GramCfg {
   static constexpr int NRB = DEPTH * L;          // staged block rows
   static constexpr int NTN = NRB / 8 + 1;        // n-tiles: block rows, then [mu; wbar; 0...]
   static constexpr int MT = L / 8;               // m-tiles
-  static constexpr int STEP = 8 / MT;            // warps per m-tile
-  static constexpr int NJ = (NTN + STEP - 1) / STEP;
+  static constexpr int STEP = 8 / MT;            // warps per m-tile: they split the k-steps, each takes every n-tile
+  static constexpr int NJ = NTN;
   static constexpr int RS = NRB + 3;             // result row stride (odd: conflict-free column reads)
   static constexpr size_t stage_bytes(int sw) { return sizeof(double) * ((size_t)NRB * sw + 2 * sw); }
   static constexpr size_t epi_bytes() { return sizeof(double) * ((size_t)L * RS + 3 * (size_t)L * (L + 1) + L); }
@@ -171,7 +171,7 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
   const size_t stage_d = (size_t)NRB * SW + 2 * SW;  // doubles per stage
   double* stg = reinterpret_cast<double*>(gsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mt = warp % MT, nb = warp / MT;
+  const int mt = warp % MT, kpart = warp / MT;  // m-tile; this warp's share of the k-steps (k-step c of a 16-column group)
   const int64_t nblk = (steps + L - 1) / L;
   if (tid == 0) {
     for (int s = 0; s < 4; ++s) mbar_init(&full[s], 1);
@@ -215,16 +215,15 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
     bool bok[NJ];
 #pragma unroll
     for (int q = 0; q < NJ; ++q) {
-      const int nt = nb + STEP * q;
-      if (nt < NTN - 1) {
-        const int rr = 8 * nt + r8;
+      if (q < NTN - 1) {
+        const int rr = 8 * q + r8;
         boff[q] = rr * SW;
         bxor[q] = (rr % L) & 15;
         bok[q] = true;
-      } else {
+      } else {  // [mu; wbar; zero rows]
         boff[q] = NRB * SW + (r8 < 2 ? r8 : 0) * SW;
         bxor[q] = 0;
-        bok[q] = nt == NTN - 1 && r8 < 2;
+        bok[q] = r8 < 2;
       }
     }
     for (int s = 0; s < CS; ++s) {
@@ -235,10 +234,14 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
       const double* st = stg + (size_t)slot * stage_d;
       const double* arow = st + (size_t)la * SW;
       const int ax = la & 15;
+      // the STEP warps of an m-tile take the k-steps c = kpart, kpart + STEP, .. of every 16-column
+      // group and every n-tile (one A fragment per NTN products; no padding tile); their partial
+      // accumulators are summed in warp order below
 #pragma unroll 2
       for (int g16 = 0; g16 < SW; g16 += 16) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int cc = 0; cc < 4 / STEP; ++cc) {
+          const int c = kpart + STEP * cc;
           const int j = g16 + c + 4 * t4;  // this lane's column of the k-step {c, c+4, c+8, c+12}
           const double a = arow[j ^ ax];
           double bv[NJ];
@@ -259,18 +262,24 @@ sstep_gram_kernel(const double* __restrict__ pk, PackGeom pg, int nstg, const in
     double* W1 = Ti + (size_t)L * (L + 1);               // [L][L+1] scratch (Y1)
     double* W2 = W1 + (size_t)L * (L + 1);               // [L][L+1] scratch (Y2)
     double* pv = W2 + (size_t)L * (L + 1);               // [L]
+    for (int kp = 0; kp < STEP; ++kp) {  // fixed order: deterministic
+      if (kpart == kp) {
 #pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-      const int nt = nb + STEP * q;
-      if (nt < NTN) {
-        const int i = 8 * mt + r8, n = 8 * nt + 2 * t4;
-        if (n < RS - 1) {
-          res[i * RS + n] = acc[q][0];
-          res[i * RS + n + 1] = acc[q][1];
+        for (int q = 0; q < NJ; ++q) {
+          const int i = 8 * mt + r8, n = 8 * q + 2 * t4;
+          if (n < RS - 1) {
+            if (kp == 0) {
+              res[i * RS + n] = acc[q][0];
+              res[i * RS + n + 1] = acc[q][1];
+            } else {
+              res[i * RS + n] += acc[q][0];
+              res[i * RS + n + 1] += acc[q][1];
+            }
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     // T = I + eta C G_strict (unit lower).  Column j of T^{-1} by forward substitution; a column
     // only depends on itself, so PARTS = 256 / L lanes of one warp share column j (each sums the
     // k2 = j + part (mod PARTS) terms of a row, xor-shuffle reduction) and no block barrier is
