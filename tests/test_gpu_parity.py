@@ -151,6 +151,22 @@ def test_identity_preconditioner(O):
     assert pg.strong_convexity() == lam
 
 
+@pytest.mark.parametrize("n,d,m", [(40, 1, 7), (40, 17, 1), (50, 33, 31), (50, 33, 32), (50, 33, 33), (64, 100, 65),
+                                   (80, 513, 96), (48, 1000, 200), (40, 1500, 97), (40, 2049, 70)])
+def test_inner_loop_edge_shapes(O, n, d, m):
+    """The s-step inner loop at the corners of its geometry: one to three blocks per launch (the
+    look-ahead has no predecessors there), epoch lengths around the block size, 1 .. 16 CTAs per
+    cluster, row lengths that are not multiples of the slice width."""
+    X, y, lam, _ = small_problem(n=n, d=d)
+    po = O.problem(X, y, lam)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam), sk.Preconditioner.identity(d, lam))
+    eta = configs.step_size(po.scalars()[2])
+    want = po.svrg(3, m, eta, 11)
+    got = sk.svrg_solve(pg, sk.SvrgConfig(3, m, eta, 11), np.zeros(d))
+    assert rel(np.array([r.objective for r in got.trace]), want.trace) < 1e-10
+    assert rel(got.iterate, want.iterate) < 1e-8
+
+
 def test_full_gradient_wide_fp64_rows(O):
     # fp64 rows of 4096 columns: two 4-row tiles exceed the bulk-copy ring, so the pass takes the
     # register-staged kernel; the widest inner-loop geometry (256-column slices, 16-step blocks) too
