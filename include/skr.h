@@ -72,6 +72,12 @@ int skr_shard_rows(int64_t n, int world, int rank, int64_t* row0, int64_t* n_loc
 int skr_shard_layout(const int64_t* counts, int world, int rank, int64_t* n_global, int64_t* row0);
 int skr_ctx_destroy(skr_ctx* ctx);
 int skr_ctx_synchronize(skr_ctx* ctx);
+/* Buffers of 1 GiB and more are parked on release for the next request of the
+ * same size (cudaFree of a multi-GiB mapping stalls the host); at most 40 GiB per
+ * GPU, given back whenever an allocation would otherwise fail and on
+ * skr_ctx_destroy.  skr_ctx_trim returns them to the driver now (bytes_released
+ * may be NULL). */
+int skr_ctx_trim(skr_ctx* ctx, int64_t* bytes_released);
 void* skr_ctx_stream(skr_ctx* ctx); /* cudaStream_t the context orders work on */
 /* number of this library's kernel launches so far on the context */
 int64_t skr_ctx_kernel_launches(const skr_ctx* ctx);

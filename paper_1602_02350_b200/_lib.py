@@ -46,6 +46,7 @@ SIGNATURES = {
     "skr_shard_layout": (cint, [i64ptr, cint, cint, P(i64), P(i64)]),
     "skr_ctx_destroy": (cint, [vp]),
     "skr_ctx_synchronize": (cint, [vp]),
+    "skr_ctx_trim": (cint, [vp, P(i64)]),
     "skr_ctx_stream": (vp, [vp]),
     "skr_ctx_kernel_launches": (i64, [vp]),
     "skr_ctx_profile": (cint, [vp, cint]),

@@ -1695,7 +1695,17 @@ int skr_ctx_destroy(skr_ctx* ctx) {
     }
     cudaStreamDestroy(ctx->c.aux);
     cudaStreamDestroy(ctx->c.stream);
+    BigPark::get().trim();
     delete ctx;
+  });
+}
+
+int skr_ctx_trim(skr_ctx* ctx, int64_t* bytes_released) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    c.sync();
+    const size_t b = BigPark::get().trim();
+    if (bytes_released) *bytes_released = (int64_t)b;
   });
 }
 
@@ -2576,6 +2586,7 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
       // memory budget: the replica of all ng rows of X~ (the sequential inner loop
       // reads any sampled row) on top of this rank's X and X~ shards
       size_t free_b = 0, total_b = 0;
+      BigPark::get().trim();  // parked buffers are free memory for this purpose
       SKR_CUDA(cudaMemGetInfo(&free_b, &total_b));
       const size_t need = (size_t)ng * row_bytes + (size_t)ng * sizeof(double) + (256ull << 20);
       if (need > free_b)

@@ -100,16 +100,100 @@ inline NcclApi& nccl() {
 // Buffers of >= 1 GiB bypass the stream-ordered pool: growing the pool maps
 // memory at ~17 GB/s on B200 (3.8 s for 64 GiB) while cudaMalloc maps 64 GiB in
 // ~5 ms (profiles/alloc_probe.py).  A direct buffer is released after an
-// explicit synchronisation of its stream (every queued use on it has finished);
-// big buffers are never freed inside a graph capture (they outlive the graphs).
+// explicit synchronisation of its stream (every queued use on it has finished),
+// so it can be handed to any stream afterwards; big buffers are never freed
+// inside a graph capture (they outlive the graphs).
+//
+// Released direct buffers are parked per device and handed back to the next
+// request of the same size (the Lanczos products' T / split operands, X~ of a
+// rebuilt problem, the packed rows of the inner loop): cudaFree of a multi-GiB
+// mapping stalls the host for up to ~90 ms at irregular times
+// (profiles/lanczos_variance.py: c3 sketch 0.145 s of device work took
+// 0.15-0.38 s of wall time).  The park holds at most kBigParkCap bytes per
+// device (oldest out first) and is emptied when any allocation runs out of
+// memory (the request is retried once), by skr_ctx_trim and by skr_ctx_destroy.
 constexpr size_t kDirectAllocBytes = size_t(1) << 30;
+constexpr size_t kBigParkCap = size_t(40) << 30;
+struct BigPark {
+  struct Block { int dev; size_t bytes; void* p; };
+  std::mutex mu;
+  std::vector<Block> blocks;  // oldest first
+  static BigPark& get() {
+    static BigPark* park = new BigPark;  // never destroyed: no CUDA calls from static destructors
+    return *park;
+  }
+  static int device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+  }
+  void* take(size_t bytes) {
+    const int dev = device();
+    std::lock_guard<std::mutex> g(mu);
+    for (size_t i = blocks.size(); i-- > 0;)
+      if (blocks[i].dev == dev && blocks[i].bytes == bytes) {
+        void* p = blocks[i].p;
+        blocks.erase(blocks.begin() + i);
+        return p;
+      }
+    return nullptr;
+  }
+  void put(void* p, size_t bytes) {
+    const int dev = device();
+    std::vector<void*> drop;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (bytes > kBigParkCap) {
+        drop.push_back(p);
+      } else {
+        blocks.push_back({dev, bytes, p});
+        size_t held = 0;
+        for (const Block& b : blocks) held += b.dev == dev ? b.bytes : 0;
+        for (size_t i = 0; i < blocks.size() && held > kBigParkCap;)
+          if (blocks[i].dev == dev) {
+            held -= blocks[i].bytes;
+            drop.push_back(blocks[i].p);
+            blocks.erase(blocks.begin() + i);
+          } else {
+            ++i;
+          }
+      }
+    }
+    for (void* q : drop) cudaFree(q);
+  }
+  size_t trim() {  // frees every parked block of the current device
+    const int dev = device();
+    std::vector<void*> drop;
+    size_t bytes = 0;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      for (size_t i = 0; i < blocks.size();)
+        if (blocks[i].dev == dev) {
+          bytes += blocks[i].bytes;
+          drop.push_back(blocks[i].p);
+          blocks.erase(blocks.begin() + i);
+        } else {
+          ++i;
+        }
+    }
+    for (void* q : drop) cudaFree(q);
+    return bytes;
+  }
+};
 inline cudaError_t dev_malloc(void** p, size_t bytes, cudaStream_t s) {
-  return bytes >= kDirectAllocBytes ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, s);
+  const bool direct = bytes >= kDirectAllocBytes;
+  if (direct && (*p = BigPark::get().take(bytes)) != nullptr) return cudaSuccess;
+  cudaError_t e = direct ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, s);
+  if (e == cudaErrorMemoryAllocation && BigPark::get().trim() > 0) {
+    cudaGetLastError();  // the failed attempt is not sticky; clear it and retry with the park emptied
+    e = direct ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, s);
+  }
+  return e;
 }
 inline void dev_free(void* p, size_t bytes, cudaStream_t s) {
   if (bytes >= kDirectAllocBytes) {
     cudaStreamSynchronize(s);
-    cudaFree(p);
+    BigPark::get().put(p, bytes);
   } else {
     cudaFreeAsync(p, s);
   }

@@ -113,6 +113,12 @@ class Context:
         """Enable (and reset) CUDA-event timing of the hot kernels."""
         _check(_lib.load().skr_ctx_profile(self.h, int(enable)))
 
+    def trim(self) -> int:
+        """Return the parked >= 1 GiB buffers to the driver; bytes released (skr_ctx_trim)."""
+        out = i64()
+        _check(_lib.load().skr_ctx_trim(self.h, C.byref(out)))
+        return int(out.value)
+
     def set_prep_cap(self, ctas: int):
         """Cap the inner loop's PREP grid (0 = uncapped); see skr_ctx_set_prep_cap."""
         _check(_lib.load().skr_ctx_set_prep_cap(self.h, int(ctas)))

@@ -814,3 +814,21 @@ def test_prep_cap_grid_strided_identical():
     ctx.set_prep_cap(0)
     for r in runs[1:]:
         assert np.array_equal(np.asarray(r.iterate), np.asarray(runs[0].iterate))
+
+
+def test_parked_big_buffers_are_reused_and_trimmed():
+    """Buffers of >= 1 GiB are parked on release and handed to the next request of the
+    same size (skr.h: skr_ctx_trim): the results of a problem built on a reused buffer
+    are bitwise those of the first build, and trim returns the parked bytes once."""
+    ctx = sk.Context(0)
+    ctx.trim()
+    spec = sk.SynthSpec(1 << 17, 2048, "f32", 5, 0, 0.0, False, 0.1)  # 1 GiB of fp32 rows
+    w = np.linspace(-1.0, 1.0, 2048)
+    vals = []
+    for _ in range(2):
+        data = sk.DataMatrix.generate(spec, ctx)
+        vals.append(sk.objective(sk.RidgeProblem(data, data.labels(), 1e-4), w))
+        del data
+    assert vals[0] == vals[1]
+    assert ctx.trim() >= 1 << 30
+    assert ctx.trim() == 0
