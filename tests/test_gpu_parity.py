@@ -832,3 +832,23 @@ def test_parked_big_buffers_are_reused_and_trimmed():
     assert vals[0] == vals[1]
     assert ctx.trim() >= 1 << 30
     assert ctx.trim() == 0
+
+
+def test_parked_buffers_are_given_back_when_memory_runs_out():
+    """A request larger than the free memory left beside the parked buffers succeeds: the
+    park is emptied and the allocation retried (common.cuh dev_malloc)."""
+    import torch
+    ctx = sk.Context(0)
+    ctx.trim()
+    row = 2048 * 4
+    parked = 8 << 30
+    data = sk.DataMatrix.generate(sk.SynthSpec(parked // row, 2048, "f32", 1, 0, 0.0, False, 0.1), ctx)
+    del data  # 8 GiB parked
+    ctx.synchronize()
+    free_now, _ = torch.cuda.mem_get_info(0)
+    want = free_now + parked // 2  # does not fit beside the park, fits once it is emptied
+    big = sk.DataMatrix.generate(sk.SynthSpec(want // row, 2048, "f32", 2, 0, 0.0, False, 0.1), ctx)
+    assert big.n_local == want // row
+    assert np.isfinite(big.labels()[-1])
+    del big  # larger than the park's cap: freed directly
+    assert ctx.trim() == 0
