@@ -75,8 +75,9 @@ int skr_ctx_synchronize(skr_ctx* ctx);
 /* Buffers of 1 GiB and more are parked on release for the next request of the
  * same size (cudaFree of a multi-GiB mapping stalls the host); at most 40 GiB per
  * GPU, given back whenever an allocation would otherwise fail and on
- * skr_ctx_destroy.  skr_ctx_trim returns them to the driver now (bytes_released
- * may be NULL). */
+ * skr_ctx_destroy.  skr_ctx_trim returns them to the driver now, together with the
+ * unused part of the device's stream-ordered pool; bytes_released (may be NULL)
+ * counts the parked buffers. */
 int skr_ctx_trim(skr_ctx* ctx, int64_t* bytes_released);
 void* skr_ctx_stream(skr_ctx* ctx); /* cudaStream_t the context orders work on */
 /* number of this library's kernel launches so far on the context */

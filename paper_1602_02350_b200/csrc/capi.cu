@@ -210,7 +210,9 @@ void shard_layout(Ctx& c, int64_t n_local, int64_t* n_global, int64_t* row0,
   if (counts) *counts = all;
 }
 
-std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d) {
+// zero = false: the caller overwrites every element (only legal when ld == d: no padding
+// columns, which every kernel expects to read as zeros).
+std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d, bool zero = true) {
   auto st = std::make_shared<Storage>();
   st->dtype = dtype;
   st->n = n;
@@ -220,7 +222,7 @@ std::shared_ptr<Storage> new_storage(Ctx& c, int dtype, int64_t n, int64_t d) {
   const size_t bytes = (size_t)std::max<int64_t>(n, 1) * st->ld * dtype_size(dtype);
   st->bytes = bytes;
   SKR_CUDA(dev_malloc(&st->ptr, bytes, c.stream));
-  SKR_CUDA(cudaMemsetAsync(st->ptr, 0, bytes, c.stream));
+  if (zero || st->ld != d || n < 1) SKR_CUDA(cudaMemsetAsync(st->ptr, 0, bytes, c.stream));
   return st;
 }
 
@@ -1705,6 +1707,10 @@ int skr_ctx_trim(skr_ctx* ctx, int64_t* bytes_released) {
     Ctx& c = C_(ctx);
     c.sync();
     const size_t b = BigPark::get().trim();
+    cudaMemPool_t pool;  // the unused part of the stream-ordered pool goes back as well
+    SKR_CUDA(cudaDeviceGetDefaultMemPool(&pool, c.device));
+    SKR_CUDA(cudaStreamSynchronize(c.aux));
+    SKR_CUDA(cudaMemPoolTrimTo(pool, 0));
     if (bytes_released) *bytes_released = (int64_t)b;
   });
 }
@@ -2542,7 +2548,7 @@ int skr_problem_create(skr_ctx* ctx, const skr_data* X, const double* y, double 
     if (!S.sparse) DISPATCH_DTYPE(S.dtype, T, {
       const T* Xp = static_cast<const T*>(S.ptr);
       if (k > 0) {
-        auto xt = new_storage(c, S.dtype, n, d);
+        auto xt = new_storage(c, S.dtype, n, d, /*zero=*/false);  // the X~ product writes all n x d elements
         scale_cols_kernel<<<std::min<unsigned>(ceil_div(n * k, 256), 65535u), 256, 0, c.stream>>>(
             P.get(), n, k, p->D.get(), p->c);
         SKR_LAUNCHED(&c);

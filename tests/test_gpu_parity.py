@@ -9,6 +9,7 @@ agrees to ~1e-12 relative (parallel reductions reassociate); the BASELINE gates
 are 1e-6 (fp64) / 1e-3 (fp32) on Ritz values and 1e-8 / 1e-5 on L(w^).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -836,19 +837,29 @@ def test_parked_big_buffers_are_reused_and_trimmed():
 
 def test_parked_buffers_are_given_back_when_memory_runs_out():
     """A request larger than the free memory left beside the parked buffers succeeds: the
-    park is emptied and the allocation retried (common.cuh dev_malloc)."""
-    import torch
-    ctx = sk.Context(0)
-    ctx.trim()
-    row = 2048 * 4
-    parked = 8 << 30
-    data = sk.DataMatrix.generate(sk.SynthSpec(parked // row, 2048, "f32", 1, 0, 0.0, False, 0.1), ctx)
-    del data  # 8 GiB parked
-    ctx.synchronize()
-    free_now, _ = torch.cuda.mem_get_info(0)
-    want = free_now + parked // 2  # does not fit beside the park, fits once it is emptied
-    big = sk.DataMatrix.generate(sk.SynthSpec(want // row, 2048, "f32", 2, 0, 0.0, False, 0.1), ctx)
-    assert big.n_local == want // row
-    assert np.isfinite(big.labels()[-1])
-    del big  # larger than the park's cap: freed directly
-    assert ctx.trim() == 0
+    park is emptied and the allocation retried (common.cuh dev_malloc).  Runs in a fresh
+    process, whose stream-ordered pool holds nothing that the driver could reclaim instead."""
+    import subprocess
+    import sys
+    script = r"""
+import sys
+sys.path.insert(0, %r)
+import numpy as np, torch
+from paper_1602_02350_b200 import skridge as sk
+ctx = sk.Context(0)
+row, parked = 2048 * 4, 8 << 30
+data = sk.DataMatrix.generate(sk.SynthSpec(parked // row, 2048, "f32", 1, 0, 0.0, False, 0.1), ctx)
+del data  # 8 GiB parked
+ctx.synchronize()
+free_now, _ = torch.cuda.mem_get_info(0)
+want = free_now + parked // 2  # does not fit beside the park, fits once it is emptied
+big = sk.DataMatrix.generate(sk.SynthSpec(want // row, 2048, "f32", 2, 0, 0.0, False, 0.1), ctx)
+assert big.n_local == want // row
+assert np.isfinite(big.labels()[-1])
+del big  # larger than the park's cap: freed directly
+ctx.trim()
+assert torch.cuda.mem_get_info(0)[0] >= free_now + parked  # everything is back with the driver
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
