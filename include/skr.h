@@ -73,7 +73,7 @@ int skr_shard_layout(const int64_t* counts, int world, int rank, int64_t* n_glob
 int skr_ctx_destroy(skr_ctx* ctx);
 int skr_ctx_synchronize(skr_ctx* ctx);
 /* Buffers of 1 GiB and more are parked on release for the next request of the
- * same size (cudaFree of a multi-GiB mapping stalls the host); at most 40 GiB per
+ * same size (cudaFree of a multi-GiB mapping stalls the host); at most 80 GiB per
  * GPU, given back whenever an allocation would otherwise fail and on
  * skr_ctx_destroy.  skr_ctx_trim returns them to the driver now, together with the
  * unused part of the device's stream-ordered pool; bytes_released (may be NULL)
@@ -218,6 +218,11 @@ int skr_svrg_until(skr_problem* p, const skr_svrg_config* cfg, const double* w0,
                    double* w_out, skr_epoch_record* trace, int64_t* epochs_done);
 /* the index stream skr_svrg would draw (test hook; `count` steps from seed) */
 int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out);
+/* make_cumulative_weights (svrg.cpp:90-106) on the device for a host table beta[N] (>= 0):
+ * cum[i] = the reference's sequential fp64 running sum of beta_i / total (cum[N-1] = 1),
+ * *total = its sequential sum.  sequential = 0: the block-scan form (what the solver
+ * uses); 1: the one-thread chains.  Both are bit-identical to the reference loop. */
+int skr_cumulative_weights(skr_ctx* ctx, const double* beta, int64_t N, int sequential, double* cum, double* total);
 /* NormalSampler(seed).uniform() x count from the device mt19937_64 (test hook) */
 int skr_mt_uniforms(skr_ctx* ctx, uint64_t seed, int64_t count, double* out);
 /* tcgen05 3xTF32 GEMM check: C (M x N fp64) = A (M x K fp32) . B (N x K fp32)^T (test hook) */

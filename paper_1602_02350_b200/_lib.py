@@ -47,6 +47,7 @@ SIGNATURES = {
     "skr_ctx_destroy": (cint, [vp]),
     "skr_ctx_synchronize": (cint, [vp]),
     "skr_ctx_trim": (cint, [vp, P(i64)]),
+    "skr_cumulative_weights": (cint, [vp, dptr, i64, cint, dptr, P(f64)]),
     "skr_ctx_stream": (vp, [vp]),
     "skr_ctx_kernel_launches": (i64, [vp]),
     "skr_ctx_profile": (cint, [vp, cint]),

@@ -567,6 +567,30 @@ void problem_fullgrad(skr_problem* p, const double* w, double* mu, double* obj) 
   fullgrad_sums(c, p->dtype, p->xt->ptr, p->ld, p->n, p->y.get(), w, p->part_g, p->part_loss, p->sums, &fin);
 }
 
+// make_cumulative_weights (svrg.cpp:90-106) on one CTA: the block-scan form of the two
+// sequential fp64 sums (cumulative_exact_kernel, bit-identical) or, with SKR_CUM_SEQ=1 /
+// sequential = true, the one-thread chains.  The chains are latency-bound: with reserve_sm
+// the CTA takes its SM's whole shared memory so that no GEMM CTA of a concurrent X~
+// product shares its issue slots.
+void launch_cumulative(Ctx& c, cudaStream_t s, const double* beta, int64_t N, double* cum, double* total,
+                       bool reserve_sm, bool sequential = false) {
+  static const bool seq_env = getenv("SKR_CUM_SEQ") != nullptr;
+  constexpr int kReserve = 180 * 1024;
+  if (sequential || seq_env) {
+    configure_once((const void*)cumulative_kernel, [&] {
+      SKR_CUDA(cudaFuncSetAttribute(cumulative_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kReserve));
+    });
+    cumulative_kernel<<<1, 512, reserve_sm ? kReserve : 0, s>>>(beta, N, cum, total);
+  } else {
+    configure_once((const void*)cumulative_exact_kernel, [&] {
+      SKR_CUDA(cudaFuncSetAttribute(cumulative_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kReserve));
+    });
+    const int smem = reserve_sm ? kReserve : CE_TILE * (int)sizeof(double);
+    cumulative_exact_kernel<<<1, CE_T, smem, s>>>(beta, N, cum, total);
+  }
+  SKR_LAUNCHED(&c);
+}
+
 // Exact sampling tables (svrg.cpp:90-106, :165-172), built once per problem.
 // Sampling tables (svrg.cpp:90-106, :167-172) on the side stream as soon as the
 // beta table is final; ensure_tables makes the main stream wait for them.
@@ -579,14 +603,7 @@ void start_tables_async(skr_problem* p) {
   if (!p->ev_tables) SKR_CUDA(cudaEventCreateWithFlags(&p->ev_tables, cudaEventDisableTiming));
   SKR_CUDA(cudaEventRecord(p->ev_tables, c.stream));  // the betas and the buffers above
   SKR_CUDA(cudaStreamWaitEvent(c.aux, p->ev_tables, 0));
-  // the two dependent chains are latency-bound: the CTA reserves its SM's shared memory
-  // (unused) so no GEMM CTA of the concurrent X~ product shares its issue slots
-  constexpr int kCumSmem = 180 * 1024;  // + its 32 KB of static tiles
-  configure_once((const void*)cumulative_kernel, [&] {
-    SKR_CUDA(cudaFuncSetAttribute(cumulative_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCumSmem));
-  });
-  cumulative_kernel<<<1, 512, kCumSmem, c.aux>>>(p->betas.get(), N, p->cum.get(), p->total.get());
-  SKR_LAUNCHED(&c);
+  launch_cumulative(c, c.aux, p->betas.get(), N, p->cum.get(), p->total.get(), /*reserve_sm=*/true);
   inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.aux>>>(p->betas.get(), N, p->total.get(),
                                                                                p->inv_nq.get());
   SKR_LAUNCHED(&c);
@@ -608,8 +625,7 @@ void ensure_tables(skr_problem* p) {
   p->cum.alloc(N, c.stream);
   p->inv_nq.alloc(N, c.stream);
   p->total.alloc(1, c.stream);
-  cumulative_kernel<<<1, 512, 0, c.stream>>>(p->betas.get(), N, p->cum.get(), p->total.get());
-  SKR_LAUNCHED(&c);
+  launch_cumulative(c, c.stream, p->betas.get(), N, p->cum.get(), p->total.get(), false);
   inv_nq_kernel<<<std::min<unsigned>(ceil_div(N, 256), 4096), 256, 0, c.stream>>>(p->betas.get(), N, p->total.get(),
                                                                                   p->inv_nq.get());
   SKR_LAUNCHED(&c);
@@ -2815,6 +2831,19 @@ int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) 
     c.sync();
     if (mu) std::memcpy(mu, p->io_host + ld, sizeof(double) * d);
     if (obj) *obj = p->io_host[2 * ld];
+  });
+}
+
+int skr_cumulative_weights(skr_ctx* ctx, const double* beta, int64_t N, int sequential, double* cum, double* total) {
+  return guard([&] {
+    Ctx& c = C_(ctx);
+    if (!beta || !cum || N < 1) raise(SKR_EPARAM, "cumulative_weights: empty table");
+    DBuf<double> db(N, c.stream), dc(N, c.stream), dt(1, c.stream);
+    SKR_CUDA(cudaMemcpyAsync(db.get(), beta, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
+    launch_cumulative(c, c.stream, db.get(), N, dc.get(), dt.get(), false, sequential != 0);
+    SKR_CUDA(cudaMemcpyAsync(cum, dc.get(), sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+    if (total) SKR_CUDA(cudaMemcpyAsync(total, dt.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
   });
 }
 

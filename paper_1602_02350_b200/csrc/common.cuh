@@ -109,11 +109,17 @@ inline NcclApi& nccl() {
 // rebuilt problem, the packed rows of the inner loop): cudaFree of a multi-GiB
 // mapping stalls the host for up to ~90 ms at irregular times
 // (profiles/lanczos_variance.py: c3 sketch 0.145 s of device work took
-// 0.15-0.38 s of wall time).  The park holds at most kBigParkCap bytes per
+// 0.15-0.38 s of wall time).  The park holds at most big_park_cap() bytes per
 // device (oldest out first) and is emptied when any allocation runs out of
 // memory (the request is retried once), by skr_ctx_trim and by skr_ctx_destroy.
 constexpr size_t kDirectAllocBytes = size_t(1) << 30;
-constexpr size_t kBigParkCap = size_t(40) << 30;
+inline size_t big_park_cap() {  // bytes parked per device at most (SKR_PARK_GIB, default 80; 0: no park)
+  static const size_t cap = [] {
+    const char* e = getenv("SKR_PARK_GIB");
+    return (size_t)(e ? std::max(0, atoi(e)) : 80) << 30;
+  }();
+  return cap;
+}
 struct BigPark {
   struct Block { int dev; size_t bytes; void* p; };
   std::mutex mu;
@@ -143,13 +149,13 @@ struct BigPark {
     std::vector<void*> drop;
     {
       std::lock_guard<std::mutex> g(mu);
-      if (bytes > kBigParkCap) {
+      if (bytes > big_park_cap()) {
         drop.push_back(p);
       } else {
         blocks.push_back({dev, bytes, p});
         size_t held = 0;
         for (const Block& b : blocks) held += b.dev == dev ? b.bytes : 0;
-        for (size_t i = 0; i < blocks.size() && held > kBigParkCap;)
+        for (size_t i = 0; i < blocks.size() && held > big_park_cap();)
           if (blocks[i].dev == dev) {
             held -= blocks[i].bytes;
             drop.push_back(blocks[i].p);

@@ -828,6 +828,18 @@ def mt_uniforms(seed: int, count: int, ctx: Context | None = None) -> np.ndarray
     return out
 
 
+def make_cumulative_weights(beta, sequential: bool = False, ctx: Context | None = None):
+    """svrg.cpp:90-106 on the device: (cum, total) of the sampling weights, bit-identical to the
+    reference's sequential fp64 loops (block-scan form, or the one-thread chains)."""
+    ctx = ctx or default_context()
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    if beta.size == 0:
+        raise InputError("make_cumulative_weights: empty table")
+    cum, tot = np.empty(beta.size), f64()
+    _check(_lib.load().skr_cumulative_weights(ctx.h, beta, beta.size, int(sequential), cum, C.byref(tot)))
+    return cum, tot.value
+
+
 def gaussian_matrix(rows: int, cols: int, seed: int, ctx: Context | None = None) -> np.ndarray:
     """random.cpp:28-41 on the device; returns (rows, cols)."""
     ctx = ctx or default_context()

@@ -863,3 +863,42 @@ print("ok")
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def _cum_reference(beta):
+    """svrg.cpp:90-106 in numpy: np.add.accumulate is the same sequential fp64 loop."""
+    total = np.add.accumulate(beta)[-1]
+    cum = np.add.accumulate(beta / total)
+    cum[-1] = 1.0
+    return cum, total
+
+
+@pytest.mark.parametrize("case", ["uniform", "lognormal", "ties", "zeros", "wide", "tiny", "one"])
+def test_cumulative_weights_block_scan_is_bitwise_sequential(case):
+    """The block-scan form of make_cumulative_weights (integer prefix sums inside a binade;
+    ties, binade changes and zero starts summed in index order) against the one-thread chains
+    and the sequential numpy loop: every entry bit for bit."""
+    rng = np.random.default_rng(11)
+    if case == "uniform":      # the c5 shape: equal-ish weights, ~1 tie expected per 2^24 entries
+        beta = rng.uniform(0.5, 1.5, 3_000_001)
+    elif case == "lognormal":  # 12 orders of magnitude
+        beta = np.exp(rng.normal(0.0, 4.0, 1_000_003))
+    elif case == "ties":       # few mantissa bits: x / ulp(S) hits fraction 1/2 all the time
+        beta = rng.integers(1, 8, 262_147).astype(np.float64) * 2.0 ** rng.integers(-30, 3, 262_147)
+    elif case == "zeros":      # leading and interleaved zeros (S = 0 start, delta = 0 steps)
+        beta = rng.uniform(0.0, 1.0, 70_001)
+        beta[:5000] = 0.0
+        beta[rng.integers(0, beta.size, 20_000)] = 0.0
+        beta[-1] = 0.25
+    elif case == "wide":       # operands far above the running sum (binade jumps of many steps)
+        beta = rng.uniform(0.0, 1.0, 50_000)
+        beta[::997] *= 2.0 ** 40
+    elif case == "tiny":
+        beta = rng.uniform(0.1, 1.0, 7)
+    else:
+        beta = np.array([3.5])
+    ref_cum, ref_total = _cum_reference(beta)
+    for sequential in (True, False):
+        cum, total = sk.make_cumulative_weights(beta, sequential=sequential)
+        assert total == ref_total
+        assert np.array_equal(cum, ref_cum), (case, sequential, int(np.argmax(cum != ref_cum)))
