@@ -1203,6 +1203,9 @@ void run_sstep7_t(skr_problem* p, const double* snap, const double* mu, const in
               "delta seen %lld, w out %lld\n",
               kTraceB0 + k, (long long)(e[0] - b0), (long long)(e[1] - b0), (long long)(e[7] - b0), (long long)(e[2] - b0),
               (long long)(e[3] - b0), (long long)(e[6] - b0), (long long)(e[4] - b0), (long long)(e[5] - b0));
+      const unsigned long long* f = h + 80 + 4 * k;
+      fprintf(stderr, "[skr]             dot warp 0 at its loop top %lld, last dot warp done %lld, last column group's w out %lld\n",
+              (long long)(f[0] - b0), (long long)(f[1] - b0), (long long)(f[2] - b0));
     }
     SKR_CUDA(cudaMemset(dprof, 0, 128 * sizeof(unsigned long long)));
   }

@@ -503,6 +503,12 @@ __device__ __forceinline__ void chain_trace(unsigned long long* prof, int cr, in
   if (prof && cr == 0 && b >= kTraceB0 && b < kTraceB0 + kTraceN) prof[16 + 8 * (b - kTraceB0) + e] = t;
 }
 
+// four more events per traced block: prof[80 + 4 * k + e]
+__device__ __forceinline__ void chain_trace2(unsigned long long* prof, int cr, int64_t b, int e) {
+  const unsigned long long t = clock64();
+  if (prof && cr == 0 && b >= kTraceB0 && b < kTraceB0 + kTraceN) prof[80 + 4 * (b - kTraceB0) + e] = t;
+}
+
 template <int SW, int L>
 __global__ void __launch_bounds__(ChainCfg<SW, L>::NT, 1) sstep_chain_kernel(ChainArgs a) {
   using Cf = ChainCfg<SW, L>;
@@ -1127,6 +1133,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
     for (int bb = 0; bb < nblk; ++bb) {
       const int s = bb & (NB - 1);
       const int wi = bb >= 2 ? bb - 2 : 0;  // w_{wi}
+      if (warp == 0 && lane == 0) chain_trace2(a.prof, cr, bb, 0);  // loop top (before the waits)
       const bool fok = mbar_test(&full[s], (uint32_t)((bb / NB) & 1));
       if (wi >= 1) mbar_spin(&wready[wi & (NW - 1)], (uint32_t)(((wi - 1) / NW) & 1));  // slot's k-th phase (slot 0: w_NW first)
       if (!fok) mbar_spin(&full[s], (uint32_t)((bb / NB) & 1));
@@ -1152,6 +1159,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
       if (lane == 0) {
         mbar_arrive_local(&dotdone[bb & 3]);
         if (warp == 0) chain_trace(a.prof, cr, bb, 1);
+        if (warp == NDW - 1) chain_trace2(a.prof, cr, bb, 1);  // last dot warp done
       }
     }
   } else {
@@ -1213,6 +1221,7 @@ __global__ void __launch_bounds__(Chain7Cfg<SW, L>::NT, 1) sstep_chain7_kernel(C
         wsm[ws * SW + t] = wn;  // w_{b+1}
         __syncwarp();
         if (uw == 0 && lane == 0) chain_trace(a.prof, cr, b, 5);
+        if (uw == 2 * NUW - 2 && lane == 0) chain_trace2(a.prof, cr, b, 2);  // last column group's w out
         if (lane == 0) mbar_arrive_local(&wready[ws]);
         S += (double)Lb * w - a.eta * vv - a.eta * muc * (0.5 * (double)Lb * (double)(Lb + 1));
         w = wn;
