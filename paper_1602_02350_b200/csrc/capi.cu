@@ -311,6 +311,18 @@ FgPlan run_fullgrad_tiles(Ctx& c, int64_t ld, int64_t n, const T* X, const doubl
   int pow2 = 32;
   while (pow2 < nt) pow2 *= 2;
   if (pow2 > 512) raise(SKR_EDIM, "full gradient: dimension too large for the fused pass (d > 4096)");
+  // fp32 rows of more than 2048 columns (c4): 16 columns per thread and 2-row tiles keep the
+  // CTA at 256 threads, so two CTAs per SM hide each other's per-tile block reduction
+  // (512 threads, one CTA per SM: 5.7 TB/s at d = 4096)
+  if constexpr (sizeof(T) == 4) {
+    static const bool wide_off = getenv("SKR_K9_WIDE512") != nullptr;
+    if (pow2 == 512 && env_vec == 0 && !wide_off && ld % 16 == 0 && (ld + 15) / 16 <= 256) {
+      p.nt = 256;
+      p.bytes = 16 * (int)sizeof(T);
+      launch_fullgrad_nt<T, 16, 2, 256>(c, p, (n + 1) / 2, X, ld, n, y, w, part_g, part_loss, plan_only);
+      return p;
+    }
+  }
   p.nt = pow2;
   p.bytes = vec * (int)sizeof(T);
   if (vec == 8) launch_fullgrad_v<T, 8, 4>(c, p, ld, n, X, y, w, part_g, part_loss, plan_only);

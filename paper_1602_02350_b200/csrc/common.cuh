@@ -319,7 +319,7 @@ void configure_once(const void* kernel, F&& set) {
 }
 
 // Resident CTAs per SM of `kernel` at (threads, smem), raising its dynamic
-// shared-memory limit first; cached per (kernel, device, threads, smem) under a lock.
+// shared-memory limit first (never lowering it); cached per (kernel, device, threads, smem) under a lock.
 inline int resident_ctas(const void* kernel, int threads, size_t smem) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
@@ -329,7 +329,14 @@ inline int resident_ctas(const void* kernel, int threads, size_t smem) {
   auto key = std::make_tuple(kernel, dev, threads, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024) SKR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the attribute is the kernel's limit, not a per-launch value: only ever raise it (a later,
+  // smaller request must not lower it under a cached larger launch size)
+  static std::map<std::pair<const void*, int>, size_t> limit;
+  size_t& lim = limit[std::make_pair(kernel, dev)];
+  if (smem > 48 * 1024 && smem > lim) {
+    SKR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lim = smem;
+  }
   int per_sm = 0;
   SKR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
   per_sm = std::max(per_sm, 1);

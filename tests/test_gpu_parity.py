@@ -184,6 +184,20 @@ def test_full_gradient_wide_fp64_rows(O):
     assert rel(got.iterate, want.iterate) < 1e-8
 
 
+@pytest.mark.parametrize("d", [4096, 3000, 2064])
+def test_full_gradient_wide_fp32_rows(O, d):
+    # fp32 rows of more than 2048 columns (c4's shape) take the 256-thread tile kernel with 16
+    # columns per thread and 2-row tiles; n odd: the last tile holds one row; d = 3000 / 2064:
+    # threads past the row end, ld padded to 3008 / 2064
+    X, y, lam, _ = small_problem(n=97, d=d, dtype=np.float32)
+    Xd = X.astype(np.float64)
+    po = O.problem(Xd, y, lam)
+    pg = sk.preconditioned_components(sk.RidgeProblem(sk.DataMatrix(X), y, lam), sk.Preconditioner.identity(d, lam))
+    w = np.random.default_rng(5).standard_normal(d)
+    assert rel(pg.full_gradient(w), po.full_gradient(w)) < 1e-12
+    assert abs(pg.objective(w) - po.objective(w)) < 1e-12 * abs(po.objective(w))
+
+
 def test_full_gradient_is_mean_of_components():
     # test_ridge.cpp:167-181
     X, y, lam, k = small_problem(n=60, d=12, k=3)
@@ -874,7 +888,7 @@ def _cum_reference(beta):
 
 
 @pytest.mark.parametrize("case", ["uniform", "lognormal", "ties", "zeros", "wide", "tiny", "one"])
-def test_cumulative_weights_block_scan_is_bitwise_sequential(case):
+def test_cumulative_weights_block_scan_is_bitwise_sequential(O, case):
     """The block-scan form of make_cumulative_weights (integer prefix sums inside a binade;
     ties, binade changes and zero starts summed in index order) against the one-thread chains
     and the sequential numpy loop: every entry bit for bit."""
@@ -898,6 +912,7 @@ def test_cumulative_weights_block_scan_is_bitwise_sequential(case):
     else:
         beta = np.array([3.5])
     ref_cum, ref_total = _cum_reference(beta)
+    assert np.array_equal(O.cumulative_weights(beta), ref_cum)  # the oracle's make_cumulative_weights
     for sequential in (True, False):
         cum, total = sk.make_cumulative_weights(beta, sequential=sequential)
         assert total == ref_total
