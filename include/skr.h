@@ -221,7 +221,9 @@ int skr_index_stream(skr_problem* p, uint64_t seed, int64_t count, int64_t* out)
 /* make_cumulative_weights (svrg.cpp:90-106) on the device for a host table beta[N] (>= 0):
  * cum[i] = the reference's sequential fp64 running sum of beta_i / total (cum[N-1] = 1),
  * *total = its sequential sum.  sequential = 0: the block-scan form (what the solver
- * uses); 1: the one-thread chains.  Both are bit-identical to the reference loop. */
+ * uses); 1: the one-thread chains.  Both are bit-identical to the reference loop.
+ * SKR_EINPUT with the reference's messages for an empty table, a negative (or NaN)
+ * weight and a zero total. */
 int skr_cumulative_weights(skr_ctx* ctx, const double* beta, int64_t N, int sequential, double* cum, double* total);
 /* NormalSampler(seed).uniform() x count from the device mt19937_64 (test hook) */
 int skr_mt_uniforms(skr_ctx* ctx, uint64_t seed, int64_t count, double* out);

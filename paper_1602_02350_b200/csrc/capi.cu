@@ -2852,13 +2852,19 @@ int skr_full_gradient(skr_problem* p, const double* w, double* mu, double* obj) 
 int skr_cumulative_weights(skr_ctx* ctx, const double* beta, int64_t N, int sequential, double* cum, double* total) {
   return guard([&] {
     Ctx& c = C_(ctx);
-    if (!beta || !cum || N < 1) raise(SKR_EPARAM, "cumulative_weights: empty table");
+    // the reference's checks and messages (svrg.cpp:91-97)
+    if (!beta || !cum || N < 1) raise(SKR_EINPUT, "sampling: no weights");
+    for (int64_t i = 0; i < N; ++i)
+      if (!(beta[i] >= 0.0)) raise(SKR_EINPUT, "sampling: negative weight");
     DBuf<double> db(N, c.stream), dc(N, c.stream), dt(1, c.stream);
     SKR_CUDA(cudaMemcpyAsync(db.get(), beta, sizeof(double) * N, cudaMemcpyHostToDevice, c.stream));
     launch_cumulative(c, c.stream, db.get(), N, dc.get(), dt.get(), false, sequential != 0);
     SKR_CUDA(cudaMemcpyAsync(cum, dc.get(), sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
-    if (total) SKR_CUDA(cudaMemcpyAsync(total, dt.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    double tot = 0.0;
+    SKR_CUDA(cudaMemcpyAsync(&tot, dt.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    if (!(tot > 0.0)) raise(SKR_EINPUT, "sampling: zero total weight");
+    if (total) *total = tot;
   });
 }
 

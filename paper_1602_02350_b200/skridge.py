@@ -834,7 +834,7 @@ def make_cumulative_weights(beta, sequential: bool = False, ctx: Context | None 
     ctx = ctx or default_context()
     beta = np.ascontiguousarray(beta, dtype=np.float64)
     if beta.size == 0:
-        raise InputError("make_cumulative_weights: empty table")
+        raise InputError("sampling: no weights")
     cum, tot = np.empty(beta.size), f64()
     _check(_lib.load().skr_cumulative_weights(ctx.h, beta, beta.size, int(sequential), cum, C.byref(tot)))
     return cum, tot.value

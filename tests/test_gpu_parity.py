@@ -917,3 +917,14 @@ def test_cumulative_weights_block_scan_is_bitwise_sequential(O, case):
         cum, total = sk.make_cumulative_weights(beta, sequential=sequential)
         assert total == ref_total
         assert np.array_equal(cum, ref_cum), (case, sequential, int(np.argmax(cum != ref_cum)))
+
+
+def test_cumulative_weights_errors_are_the_references(O):
+    # svrg.cpp:91-97: empty table, negative (or NaN) weight, zero total
+    for bad, msg in ((np.zeros(0), "no weights"), (np.array([1.0, -0.5, 2.0]), "negative weight"),
+                     (np.array([1.0, np.nan]), "negative weight"), (np.zeros(5), "zero total weight")):
+        with pytest.raises(sk.InputError, match=msg):
+            sk.make_cumulative_weights(bad)
+        if bad.size:
+            with pytest.raises(oracle.OracleError, match=msg):
+                O.cumulative_weights(bad)
