@@ -855,6 +855,7 @@ def test_parked_buffers_are_given_back_when_memory_runs_out():
     process, whose stream-ordered pool holds nothing that the driver could reclaim instead."""
     import subprocess
     import sys
+    sk.Context(0).trim()  # this process's own parked buffers and pool go back first: the child needs room
     script = r"""
 import sys
 sys.path.insert(0, %r)
